@@ -1,0 +1,166 @@
+/*
+ * lomo_b200.h -- C-ABI of the B200 (sm_100a) LOMO fused-update hot path.
+ *
+ * This is the drop-in boundary for the per-parameter hook body of the
+ * reference `fusedtrain` (CPU/numpy, /root/reference/pkg/src/fusedtrain):
+ *
+ *   reference (file:line)                               replaced by
+ *   --------------------------------------------------  --------------------------
+ *   optim.py:52-54   apply_update(param, g, lr)          lomo_fused_update  (K1)
+ *   tensor.py:74-81  Tensor.assign (write-back)          K1 store (RNE to dtype)
+ *   tensor.py:30-38  round_through_half                  K1 store (cvt.rn.f16.*)
+ *   optim.py:126-128 LOMO hook (update, CONSUME)         K1, state=NULL-equivalent
+ *   stabilize.py:82-86,168-173 clip_by_value in hook     K1 clip_value > 0
+ *   stabilize.py:193-200 probe_hook (overflow, sumsq)    lomo_probe         (K2)
+ *   stabilize.py:204-213 norm / clip-coef decision       lomo_finalize_norm (K3a)
+ *   stabilize.py:155-159 _skip -> LossScaler.on_overflow K3a (on device)
+ *   stabilize.py:115-127 LossScaler.on_overflow/on_clean K3a / lomo_scaler_on_clean (K3b)
+ *   stabilize.py:217-224 update_hook (unscale,clip,coef) K1 with LOMO_USE_SCALE|LOMO_USE_COEF
+ *   optim.py:63-65   _require_finite(loss)               lomo_begin_step (device flag)
+ *   tape.py:330-405  Tape.backward/_deliver hook call    torch post-accumulate-grad hook
+ *                                                         (host side)
+ *
+ * Conventions
+ *   - Every entry point is asynchronous on `stream` (a cudaStream_t passed as
+ *     void*), never synchronises the host, never allocates, and returns 0 on
+ *     success or a positive cudaError_t / negative LOMO_E* code.  No C++
+ *     exception crosses this boundary.
+ *   - `p` and `g` are device pointers to `n` contiguous elements of `dtype`.
+ *     The update is in place on `p`; `g` is read once.  Any alignment works;
+ *     16-byte-aligned p/g with equal misalignment take the 128-bit path.
+ *   - The device-resident step state (`lomo_state` + per-slot sum-of-squares
+ *     partials + K2 scratch) is one block of lomo_state_bytes(nslots) bytes
+ *     owned by the caller (allocated with the framework's allocator).
+ */
+#ifndef LOMO_B200_H
+#define LOMO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOMO_ABI_VERSION 1
+
+/* storage dtype of p and g (reference: Precision, tensor.py:19-21;
+ * FULL == float64 storage, HALF_EMULATED == binary16; bf16 is new). */
+typedef enum {
+  LOMO_F32 = 0,
+  LOMO_F16 = 1,
+  LOMO_BF16 = 2,
+  LOMO_F64 = 3
+} lomo_dtype;
+
+/* arithmetic width of the update.  F64 reproduces the reference's full-width
+ * arithmetic (optim.py:9-13) and rounds f64 -> storage directly (bit-exact with
+ * numpy's float64 -> float16 cast); F32 is the fp32-math hot path. */
+typedef enum {
+  LOMO_MATH_F32 = 0,
+  LOMO_MATH_F64 = 1
+} lomo_math;
+
+/* flags for lomo_fused_update / lomo_probe */
+#define LOMO_USE_SCALE 0x1u /* g *= state->inv_scale  (stabilize.py:218)           */
+#define LOMO_USE_COEF 0x2u  /* g *= state->clip_coef  (stabilize.py:221-222)       */
+#define LOMO_USE_SKIP 0x4u  /* no-op when state->skip (stabilize.py:204-205,       */
+                            /*                          optim.py:63-65)            */
+
+#define LOMO_E_ARG (-1)     /* invalid argument (null pointer, n < 0, bad dtype)   */
+#define LOMO_E_SLOT (-2)    /* slot outside [0, nslots)                            */
+
+/* Device-resident step state.  Layout is part of the ABI (host code may view
+ * individual fields, e.g. `scale` to multiply the loss on device). */
+typedef struct lomo_state {
+  double scale;          /*   0: dynamic loss scale, power of two (stabilize.py:106) */
+  double inv_scale;      /*   8: 1/scale (exact)                                     */
+  double min_scale;      /*  16                                                      */
+  double max_scale;      /*  24                                                      */
+  double clip_coef;      /*  32: min(1, max_norm/N) or 1 (stabilize.py:212-213)      */
+  double total_norm;     /*  40: N of the last finalize                              */
+  double sumsq_total;    /*  48: sum over slots, in slot order                       */
+  double max_norm;       /*  56: config (<= 0: no norm clip)                         */
+  int32_t growth_interval; /* 64                                                     */
+  int32_t clean_steps;   /*  68: stabilize.py:110                                    */
+  int32_t overflow;      /*  72: non-finite grad (K2) or loss (begin_step) seen      */
+  int32_t skip;          /*  76: this step is dropped; K1 with LOMO_USE_SKIP no-ops  */
+  int32_t underflow;     /*  80: on_overflow would go below min_scale (fatal)        */
+  int32_t nslots;        /*  84                                                      */
+  int32_t steps_applied; /*  88                                                      */
+  int32_t steps_skipped; /*  92                                                      */
+  uint32_t ticket;       /*  96: K2 last-block ticket (internal)                     */
+  int32_t has_scaler;    /* 100                                                      */
+  float scale_f32;       /* 104: scale as fp32 (exact: power of two), for loss*scale */
+  int32_t reserved[5];   /* 108..127                                                 */
+  /* followed by: double sumsq[nslots]; double scratch[LOMO_MAX_PROBE_BLOCKS]; */
+} lomo_state;
+
+#define LOMO_MAX_PROBE_BLOCKS 4096
+
+/* 128-byte host snapshot of the state header (lomo_read_status). */
+typedef lomo_state lomo_status;
+
+/* ---- library / state management ------------------------------------- */
+int lomo_abi_version(void);
+size_t lomo_state_bytes(int nslots);
+/* Initialise a state block (device memory).  scale <= 0 => no loss scaler
+ * (scale = 1).  max_norm <= 0 => no global-norm clip. */
+int lomo_state_init(void* state, int nslots, double scale, int growth_interval,
+                    double min_scale, double max_scale, double max_norm,
+                    void* stream);
+/* Start of a step: clear overflow/skip/underflow and the slot partials; if
+ * `loss` is non-NULL, set overflow+skip when it is non-finite
+ * (optim.py:63-65 / stabilize.py:185-189). */
+int lomo_begin_step(void* state, const void* loss, int loss_dtype, void* stream);
+/* Copy the 128-byte header to host memory `out` (async on `stream`; the
+ * caller synchronises before reading -- the one host sync per step). */
+int lomo_read_status(const void* state, lomo_status* out, void* stream);
+
+/* ---- K1: fused update ------------------------------------------------ */
+/* p <- round_dtype(p*(1-lr*wd) - lr * coef * clip(g * inv_scale, +-clip_value))
+ *   clip_value <= 0 : no value clip;  weight_decay == 0 : reference semantics
+ *   (the reference LOMO has no weight decay, optim.py:52-54). */
+int lomo_fused_update(void* p, const void* g, int64_t n, int dtype, int math,
+                      double lr, double clip_value, double weight_decay,
+                      unsigned flags, const void* state, void* stream);
+
+/* Multi-tensor K1: one launch over `ntensors` (p, g, n) triples whose pointer
+ * tables live in DEVICE memory (coalesced small tensors; same dtype/math). */
+int lomo_fused_update_multi(void* const* p_table, const void* const* g_table,
+                            const int64_t* n_table, int ntensors, int64_t max_n,
+                            int dtype, int math, double lr, double clip_value,
+                            double weight_decay, unsigned flags,
+                            const void* state, void* stream);
+
+/* ---- K2: probe (two-pass pass 1) --------------------------------------- */
+/* sumsq[slot] = sum((g * inv_scale)^2) (deterministic: fixed-order f64 tree);
+ * state->overflow |= any(!isfinite(g)).  flags: LOMO_USE_SCALE. */
+int lomo_probe(const void* g, int64_t n, int dtype, int slot, unsigned flags,
+               void* state, void* stream);
+
+/* ---- K3: finalisers (single CTA) --------------------------------------- */
+/* K3a: total = sum(sumsq[0..nslots)) in slot order; N = sqrt(total);
+ * skip = overflow || (max_norm > 0 && !isfinite(N)); coef per
+ * stabilize.py:209-213; on skip, LossScaler.on_overflow on device. */
+int lomo_finalize_norm(void* state, void* stream);
+/* K3b: LossScaler.on_clean on device when the step was applied. */
+int lomo_scaler_on_clean(void* state, void* stream);
+/* Sharded mode (ZeRO-3 shards, one rank per GPU):
+ * lomo_local_norm_partial writes {sum(sumsq slots in slot order), overflow}
+ * of THIS rank into out2_dev[0..1] (it is what the all-gather exchanges);
+ * lomo_finalize_norm_ranks takes the gathered [world][2] rows and runs K3a's
+ * decision on the rank-ordered sum (deterministic across ranks). */
+int lomo_local_norm_partial(const void* state, double* out2_dev, void* stream);
+int lomo_finalize_norm_ranks(void* state, const double* parts_dev, int world,
+                             void* stream);
+
+/* Number of SMs the library sized its grids for (device of the current
+ * context); 0 if no device. */
+int lomo_num_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOMO_B200_H */

@@ -1,0 +1,129 @@
+"""ctypes binding of the C-ABI in include/lomo_b200.h (liblomo_b200.so).
+
+There is no fallback: if the shared library is missing or a CUDA device is
+absent, every compute entry point raises.  The library is built in-tree by
+``__graft_entry__.build()`` (nvcc, -gencode arch=compute_100a,code=sm_100a).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import NativeError
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "_native" / "liblomo_b200.so"
+
+# lomo_dtype (include/lomo_b200.h)
+F32, F16, BF16, F64 = 0, 1, 2, 3
+MATH_F32, MATH_F64 = 0, 1
+USE_SCALE, USE_COEF, USE_SKIP = 0x1, 0x2, 0x4
+MAX_PROBE_BLOCKS = 4096
+ABI_VERSION = 1
+
+# every symbol the header declares (checked by tests/test_native_abi.py)
+EXPORTS = (
+    "lomo_abi_version",
+    "lomo_state_bytes",
+    "lomo_state_init",
+    "lomo_begin_step",
+    "lomo_read_status",
+    "lomo_fused_update",
+    "lomo_fused_update_multi",
+    "lomo_probe",
+    "lomo_finalize_norm",
+    "lomo_scaler_on_clean",
+    "lomo_local_norm_partial",
+    "lomo_finalize_norm_ranks",
+    "lomo_num_sms",
+)
+
+
+class LomoStatus(ctypes.Structure):
+    """Host mirror of ``lomo_state`` (128 bytes, include/lomo_b200.h)."""
+
+    _fields_ = [
+        ("scale", ctypes.c_double),
+        ("inv_scale", ctypes.c_double),
+        ("min_scale", ctypes.c_double),
+        ("max_scale", ctypes.c_double),
+        ("clip_coef", ctypes.c_double),
+        ("total_norm", ctypes.c_double),
+        ("sumsq_total", ctypes.c_double),
+        ("max_norm", ctypes.c_double),
+        ("growth_interval", ctypes.c_int32),
+        ("clean_steps", ctypes.c_int32),
+        ("overflow", ctypes.c_int32),
+        ("skip", ctypes.c_int32),
+        ("underflow", ctypes.c_int32),
+        ("nslots", ctypes.c_int32),
+        ("steps_applied", ctypes.c_int32),
+        ("steps_skipped", ctypes.c_int32),
+        ("ticket", ctypes.c_uint32),
+        ("has_scaler", ctypes.c_int32),
+        ("scale_f32", ctypes.c_float),
+        ("reserved", ctypes.c_int32 * 5),
+    ]
+
+
+assert ctypes.sizeof(LomoStatus) == 128
+STATE_HEADER_BYTES = 128
+SCALE_F32_OFFSET = LomoStatus.scale_f32.offset
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int
+_dbl = ctypes.c_double
+_u32 = ctypes.c_uint
+
+_SIGS = {
+    "lomo_abi_version": (_i32, []),
+    "lomo_state_bytes": (ctypes.c_size_t, [_i32]),
+    "lomo_state_init": (_i32, [_vp, _i32, _dbl, _i32, _dbl, _dbl, _dbl, _vp]),
+    "lomo_begin_step": (_i32, [_vp, _vp, _i32, _vp]),
+    "lomo_read_status": (_i32, [_vp, ctypes.POINTER(LomoStatus), _vp]),
+    "lomo_fused_update": (_i32, [_vp, _vp, _i64, _i32, _i32, _dbl, _dbl, _dbl, _u32, _vp, _vp]),
+    "lomo_fused_update_multi": (
+        _i32, [_vp, _vp, _vp, _i32, _i64, _i32, _i32, _dbl, _dbl, _dbl, _u32, _vp, _vp]),
+    "lomo_probe": (_i32, [_vp, _i64, _i32, _i32, _u32, _vp, _vp]),
+    "lomo_finalize_norm": (_i32, [_vp, _vp]),
+    "lomo_scaler_on_clean": (_i32, [_vp, _vp]),
+    "lomo_local_norm_partial": (_i32, [_vp, _vp, _vp]),
+    "lomo_finalize_norm_ranks": (_i32, [_vp, _vp, _i32, _vp]),
+    "lomo_num_sms": (_i32, []),
+}
+
+_LIB = None
+
+
+def load() -> ctypes.CDLL:
+    """Load liblomo_b200.so once; raise loudly if it was not built."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = Path(os.environ.get("LOMO_B200_LIB", LIB_PATH))
+    if not path.exists():
+        raise NativeError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the fused-update path)"
+        )
+    lib = ctypes.CDLL(str(path))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.lomo_abi_version() != ABI_VERSION:
+        raise NativeError(f"ABI version mismatch: {lib.lomo_abi_version()} != {ABI_VERSION}")
+    _LIB = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise NativeError(f"{what} failed with status {rc}")
+
+
+def state_bytes(nslots: int) -> int:
+    # pure arithmetic restated so it works without loading (must equal the C side)
+    return STATE_HEADER_BYTES + 8 * (int(nslots) + MAX_PROBE_BLOCKS)

@@ -1,0 +1,816 @@
+// lomo_kernels.cu -- sm_100a kernels behind include/lomo_b200.h.
+//
+// K1  lomo_fused_update        p <- round(p - lr * coef * clip(g * inv_scale))
+//     reference: optim.py:52-54 (apply_update), tensor.py:30-38,74-81 (write-back
+//     rounding), stabilize.py:163-176 (value clip hook), stabilize.py:215-224
+//     (update_hook).  HBM-bound streaming kernel, 6 B/elem at 16-bit storage.
+// K2  lomo_probe               sumsq[slot] = sum((g*inv_scale)^2), overflow flag
+//     reference: stabilize.py:190-200 (probe_hook).  2 B/elem at 16-bit.
+// K3a lomo_finalize_norm       N, clip coef, skip, LossScaler.on_overflow
+//     reference: stabilize.py:201-213, 94-127, 155-159.
+// K3b lomo_scaler_on_clean     LossScaler.on_clean (stabilize.py:123-127, :228-229)
+//
+// Design notes:
+//  * Each launch processes ONE tensor as it arrives from autograd (the LOMO
+//    contract: a gradient is consumed the moment it exists, tape.py:387-405).
+//  * 128-bit LDG/STG: g is read through the non-coherent path with
+//    L1::no_allocate (read exactly once), p is read and written with
+//    streaming hints; every CTA owns one contiguous, equally sized chunk of
+//    the tensor so all CTAs finish together (no grid-stride tail).
+//  * Grid = min(work, #SM x resident CTAs/SM) (queried once per device).
+//  * Determinism: K2 reduces per thread (fixed element order), per warp
+//    (xor shuffles), per CTA (fixed warp order) and across CTAs by a
+//    last-CTA finish over scratch[] in index order -- no float atomics.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lomo_b200.h"
+
+namespace lomo_k {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;  // 16-byte vectors in flight per thread per operand
+
+// --------------------------------------------------------------------------
+// device info (grid sizing)
+// --------------------------------------------------------------------------
+struct DevInfo {
+  int sms = 0;
+};
+
+DevInfo g_dev[64];
+
+const DevInfo& dev_info() {
+  int d = 0;
+  cudaGetDevice(&d);
+  DevInfo& di = g_dev[d & 63];
+  if (di.sms == 0) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+    di.sms = sms > 0 ? sms : 148;
+  }
+  return di;
+}
+
+// --------------------------------------------------------------------------
+// 128-bit memory ops with cache hints
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld_stream_ro(const void* ptr) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_stream_rw(const void* ptr) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr));
+  return r;
+}
+__device__ __forceinline__ void st_stream(void* ptr, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// --------------------------------------------------------------------------
+// storage <-> math conversions
+// --------------------------------------------------------------------------
+template <typename T>
+struct St;
+template <>
+struct St<float> {
+  static constexpr int kDtype = LOMO_F32;
+};
+template <>
+struct St<double> {
+  static constexpr int kDtype = LOMO_F64;
+};
+template <>
+struct St<__half> {
+  static constexpr int kDtype = LOMO_F16;
+};
+template <>
+struct St<__nv_bfloat16> {
+  static constexpr int kDtype = LOMO_BF16;
+};
+
+template <typename M, typename T>
+__device__ __forceinline__ M to_m(T v);
+template <>
+__device__ __forceinline__ float to_m<float, float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_m<float, double>(double v) { return (float)v; }
+template <>
+__device__ __forceinline__ float to_m<float, __half>(__half v) { return __half2float(v); }
+template <>
+__device__ __forceinline__ float to_m<float, __nv_bfloat16>(__nv_bfloat16 v) {
+  return __bfloat162float(v);
+}
+template <>
+__device__ __forceinline__ double to_m<double, float>(float v) { return (double)v; }
+template <>
+__device__ __forceinline__ double to_m<double, double>(double v) { return v; }
+template <>
+__device__ __forceinline__ double to_m<double, __half>(__half v) {
+  return (double)__half2float(v);  // exact
+}
+template <>
+__device__ __forceinline__ double to_m<double, __nv_bfloat16>(__nv_bfloat16 v) {
+  return (double)__bfloat162float(v);  // exact
+}
+
+// Round-to-nearest-even store, overflow to +-inf (tensor.py:30-38 for f16;
+// the bf16 rule is this framework's restatement, see oracle/lomo_oracle.py).
+template <typename T, typename M>
+__device__ __forceinline__ T from_m(M v);
+template <>
+__device__ __forceinline__ float from_m<float, float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float from_m<float, double>(double v) { return __double2float_rn(v); }
+template <>
+__device__ __forceinline__ double from_m<double, float>(float v) { return (double)v; }
+template <>
+__device__ __forceinline__ double from_m<double, double>(double v) { return v; }
+template <>
+__device__ __forceinline__ __half from_m<__half, float>(float v) { return __float2half_rn(v); }
+template <>
+__device__ __forceinline__ __half from_m<__half, double>(double v) {
+  __half r;
+  asm("cvt.rn.f16.f64 %0, %1;" : "=h"(*reinterpret_cast<unsigned short*>(&r)) : "d"(v));
+  return r;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_m<__nv_bfloat16, float>(float v) {
+  return __float2bfloat16_rn(v);
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_m<__nv_bfloat16, double>(double v) {
+  __nv_bfloat16 r;
+  asm("cvt.rn.bf16.f64 %0, %1;" : "=h"(*reinterpret_cast<unsigned short*>(&r)) : "d"(v));
+  return r;
+}
+
+// --------------------------------------------------------------------------
+// the per-element update (stabilize.py:217-224 then optim.py:52-54)
+// --------------------------------------------------------------------------
+template <typename M>
+struct UpdArgs {
+  M lr;         // learning rate (held in M: fp32 constant in F32 mode)
+  M clip;       // > 0: value clip threshold
+  M decay;      // 1 - lr*wd (only used when has_wd)
+  M inv_scale;  // 1 / loss scale (exact power of two)
+  M coef;       // global-norm clip coefficient
+  bool use_scale, use_coef, use_clip, has_wd;
+};
+
+// NaN-propagating clamp (np.clip semantics: NaN stays NaN).
+template <typename M>
+__device__ __forceinline__ M clamp_nan(M g, M c) {
+  return g < -c ? -c : (g > c ? c : g);
+}
+
+__device__ __forceinline__ float upd_elem(float p, float g, const UpdArgs<float>& a) {
+  if (a.use_scale) g = g * a.inv_scale;
+  if (a.use_clip) g = clamp_nan(g, a.clip);
+  if (a.use_coef) g = g * a.coef;
+  if (a.has_wd) p = p * a.decay;
+  return __fmaf_rn(-a.lr, g, p);  // one rounding of p - lr*g
+}
+
+__device__ __forceinline__ double upd_elem(double p, double g, const UpdArgs<double>& a) {
+  // exactly the reference's float64 sequence: g/scale (exact for a power of
+  // two), clip, *norm_scale, then p - (lr*g) with two roundings (no FMA).
+  if (a.use_scale) g = __dmul_rn(g, a.inv_scale);
+  if (a.use_clip) g = clamp_nan(g, a.clip);
+  if (a.use_coef) g = __dmul_rn(g, a.coef);
+  if (a.has_wd) p = __dmul_rn(p, a.decay);
+  return __dsub_rn(p, __dmul_rn(a.lr, g));
+}
+
+template <typename T>
+union Vec16 {
+  uint4 u;
+  T e[16 / sizeof(T)];
+};
+
+template <typename T, typename M>
+__device__ __forceinline__ uint4 upd_vec(const uint4& pv, const uint4& gv,
+                                         const UpdArgs<M>& a) {
+  Vec16<T> P, G, O;
+  P.u = pv;
+  G.u = gv;
+#pragma unroll
+  for (int k = 0; k < (int)(16 / sizeof(T)); ++k) {
+    M r = upd_elem(to_m<M>(P.e[k]), to_m<M>(G.e[k]), a);
+    O.e[k] = from_m<T, M>(r);
+  }
+  return O.u;
+}
+
+template <typename M>
+__device__ __forceinline__ bool load_args(UpdArgs<M>& a, unsigned flags,
+                                          const lomo_state* st) {
+  if (st != nullptr) {
+    if ((flags & LOMO_USE_SKIP) && *((volatile const int32_t*)&st->skip)) return false;
+    if (flags & LOMO_USE_SCALE) a.inv_scale = (M)st->inv_scale;
+    if (flags & LOMO_USE_COEF) a.coef = (M)st->clip_coef;
+  }
+  return true;
+}
+
+// Vector body: `nvec` 16-byte vectors starting at p/g (16-B aligned), plus
+// scalar head/tail elements handled by CTA 0.
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k1_update(T* __restrict__ p, const T* __restrict__ g, int64_t n, int head,
+              int64_t nvec, UpdArgs<M> a, unsigned flags, const lomo_state* st) {
+  constexpr int V = 16 / sizeof(T);
+  if (!load_args(a, flags, st)) return;
+
+  // scalar head (before the first aligned vector) and tail
+  if (blockIdx.x == 0) {
+    const int64_t tail0 = head + nvec * V;
+    const int64_t ntail = n - tail0;
+    for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
+      const int64_t e = i < head ? i : tail0 + (i - head);
+      p[e] = from_m<T, M>(upd_elem(to_m<M>(p[e]), to_m<M>(g[e]), a));
+    }
+  }
+
+  // contiguous equal chunks per CTA, strided by CTA width inside the chunk
+  const int64_t chunk = (nvec + gridDim.x - 1) / gridDim.x;
+  const int64_t beg = (int64_t)blockIdx.x * chunk;
+  const int64_t end = min(beg + chunk, nvec);
+  uint4* pv = reinterpret_cast<uint4*>(p + head);
+  const uint4* gv = reinterpret_cast<const uint4*>(g + head);
+
+  for (int64_t base = beg + threadIdx.x; base < end; base += (int64_t)kThreads * kUnroll) {
+    uint4 P[kUnroll], G[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < end) {
+        G[u] = ld_stream_ro(gv + i);
+        P[u] = ld_stream_rw(pv + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < end) st_stream(pv + i, upd_vec<T, M>(P[u], G[u], a));
+    }
+  }
+}
+
+// Fallback when p and g have different 16-byte misalignment: scalar, still
+// coalesced (consecutive threads touch consecutive elements).
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k1_update_scalar(T* __restrict__ p, const T* __restrict__ g, int64_t n, UpdArgs<M> a,
+                     unsigned flags, const lomo_state* st) {
+  if (!load_args(a, flags, st)) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = from_m<T, M>(upd_elem(to_m<M>(p[i]), to_m<M>(g[i]), a));
+}
+
+// Multi-tensor variant: blockIdx.y selects the tensor (small tensors coalesced
+// into one launch).  Element-wise scalar path with 16-byte vectors when both
+// pointers are 16-B aligned.
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k1_update_multi(T* const* __restrict__ pt, const T* const* __restrict__ gt,
+                    const int64_t* __restrict__ nt, UpdArgs<M> a, unsigned flags,
+                    const lomo_state* st) {
+  constexpr int V = 16 / sizeof(T);
+  if (!load_args(a, flags, st)) return;
+  T* p = pt[blockIdx.y];
+  const T* g = gt[blockIdx.y];
+  const int64_t n = nt[blockIdx.y];
+  const bool aligned = ((((uintptr_t)p) | ((uintptr_t)g)) & 15) == 0;
+  const int64_t nvec = aligned ? n / V : 0;
+  uint4* pv = reinterpret_cast<uint4*>(p);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x)
+    st_stream(pv + i, upd_vec<T, M>(ld_stream_rw(pv + i), ld_stream_ro(gv + i), a));
+  for (int64_t i = nvec * V + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = from_m<T, M>(upd_elem(to_m<M>(p[i]), to_m<M>(g[i]), a));
+}
+
+// --------------------------------------------------------------------------
+// K2: probe -- deterministic sum of squares + non-finite flag
+// --------------------------------------------------------------------------
+__device__ __forceinline__ lomo_state* hdr(void* s) { return reinterpret_cast<lomo_state*>(s); }
+__device__ __forceinline__ double* slots_of(lomo_state* s) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(s) + sizeof(lomo_state));
+}
+__device__ __forceinline__ double* scratch_of(lomo_state* s) {
+  return slots_of(s) + s->nslots;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fixed-order CTA reduction; result valid in thread 0
+__device__ __forceinline__ double block_sum(double v, double* sm) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r += sm[i];
+  }
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ bool is_fin(float x) { return fabsf(x) <= 3.402823466e38f; }
+__device__ __forceinline__ bool is_fin(double x) { return fabs(x) <= 1.7976931348623157e308; }
+
+// per-vector partial: squares (exact for 16-bit storage) summed in the math
+// type, then accumulated across vectors in f64.
+template <typename T, typename M>
+__device__ __forceinline__ double vec_sumsq(const uint4& gv, M inv_scale, bool use_scale,
+                                            bool& bad) {
+  Vec16<T> G;
+  G.u = gv;
+  M acc = 0;
+#pragma unroll
+  for (int k = 0; k < (int)(16 / sizeof(T)); ++k) {
+    M x = to_m<M>(G.e[k]);
+    bad |= !is_fin(x);
+    if (use_scale) x = x * inv_scale;
+    acc = fma(x, x, acc);
+  }
+  return (double)acc;
+}
+
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k2_probe(const T* __restrict__ g, int64_t n, int head, int64_t nvec, int slot,
+             unsigned flags, void* state) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ double sm[kThreads / 32];
+  __shared__ bool am_last;
+  lomo_state* st = hdr(state);
+  const bool use_scale = (flags & LOMO_USE_SCALE) != 0;
+  const M inv_scale = use_scale ? (M)st->inv_scale : (M)1;
+
+  double acc = 0.0;
+  bool bad = false;
+  if (blockIdx.x == 0) {
+    const int64_t tail0 = head + nvec * V;
+    const int64_t ntail = n - tail0;
+    for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
+      const int64_t e = i < head ? i : tail0 + (i - head);
+      M x = to_m<M>(g[e]);
+      bad |= !is_fin(x);
+      if (use_scale) x = x * inv_scale;
+      acc += (double)x * (double)x;
+    }
+  }
+  const int64_t chunk = (nvec + gridDim.x - 1) / gridDim.x;
+  const int64_t beg = (int64_t)blockIdx.x * chunk;
+  const int64_t end = min(beg + chunk, nvec);
+  const uint4* gv = reinterpret_cast<const uint4*>(g + head);
+  for (int64_t base = beg + threadIdx.x; base < end; base += (int64_t)kThreads * kUnroll) {
+    uint4 G[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < end) G[u] = ld_stream_ro(gv + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = base + (int64_t)u * kThreads;
+      if (i < end) acc += vec_sumsq<T, M>(G[u], inv_scale, use_scale, bad);
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
+
+  const double bsum = block_sum(acc, sm);
+  double* scratch = scratch_of(st);
+  if (threadIdx.x == 0) {
+    scratch[blockIdx.x] = bsum;
+    __threadfence();
+    const unsigned t = atomicAdd(&st->ticket, 1u);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  // last CTA: fixed-order reduction of the per-CTA partials
+  double r = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += kThreads)
+    r += ((volatile double*)scratch)[i];
+  r = block_sum(r, sm);
+  if (threadIdx.x == 0) {
+    slots_of(st)[slot] = r;
+    st->ticket = 0;
+  }
+}
+
+// --------------------------------------------------------------------------
+// K3 + bookkeeping kernels (single CTA)
+// --------------------------------------------------------------------------
+__device__ void scaler_on_overflow(lomo_state* st) {
+  // stabilize.py:115-121
+  if (!st->has_scaler) return;
+  if (st->scale / 2.0 < st->min_scale) {
+    st->underflow = 1;
+    return;
+  }
+  st->scale = st->scale / 2.0;
+  st->inv_scale = 1.0 / st->scale;
+  st->scale_f32 = (float)st->scale;
+  st->clean_steps = 0;
+}
+
+__device__ void decide(lomo_state* st, double total) {
+  // stabilize.py:201-213
+  st->sumsq_total = total;
+  const double N = sqrt(total);
+  st->total_norm = N;
+  const bool norm_clip = st->max_norm > 0.0;
+  bool skip = st->overflow != 0;
+  double coef = 1.0;
+  if (!skip && norm_clip) {
+    if (!isfinite(N)) {
+      skip = true;
+    } else if (N > 0.0) {
+      coef = fmin(1.0, st->max_norm / N);
+    }
+  }
+  st->clip_coef = coef;
+  st->skip = skip ? 1 : 0;
+  if (skip) {
+    st->steps_skipped += 1;
+    scaler_on_overflow(st);  // _skip, stabilize.py:155-159
+  }
+}
+
+__global__ void k3_finalize(void* state) {
+  if (threadIdx.x != 0) return;
+  lomo_state* st = hdr(state);
+  const double* s = slots_of(st);
+  double total = 0.0;
+  for (int i = 0; i < st->nslots; ++i) total += s[i];  // delivery (slot) order
+  decide(st, total);
+}
+
+__global__ void k3_finalize_ranks(void* state, const double* parts, int world) {
+  if (threadIdx.x != 0) return;
+  lomo_state* st = hdr(state);
+  double total = 0.0;
+  int ovf = st->overflow;
+  for (int r = 0; r < world; ++r) {  // rank order: identical on every rank
+    total += parts[2 * r];
+    ovf |= parts[2 * r + 1] != 0.0;
+  }
+  st->overflow = ovf;
+  decide(st, total);
+}
+
+__global__ void k3_local_partial(const void* state, double* out2) {
+  if (threadIdx.x != 0) return;
+  lomo_state* st = hdr(const_cast<void*>(state));
+  const double* s = slots_of(st);
+  double total = 0.0;
+  for (int i = 0; i < st->nslots; ++i) total += s[i];
+  out2[0] = total;
+  out2[1] = st->overflow ? 1.0 : 0.0;
+}
+
+__global__ void k3_on_clean(void* state) {
+  if (threadIdx.x != 0) return;
+  lomo_state* st = hdr(state);
+  if (st->skip) return;
+  st->steps_applied += 1;
+  if (!st->has_scaler) return;
+  // stabilize.py:123-127
+  st->clean_steps += 1;
+  if (st->clean_steps >= st->growth_interval) {
+    st->scale = fmin(st->scale * 2.0, st->max_scale);
+    st->inv_scale = 1.0 / st->scale;
+    st->scale_f32 = (float)st->scale;
+    st->clean_steps = 0;
+  }
+}
+
+__global__ void k_state_init(void* state, int nslots, double scale, int growth_interval,
+                             double min_scale, double max_scale, double max_norm) {
+  lomo_state* st = hdr(state);
+  if (threadIdx.x == 0) {
+    const bool has = scale > 0.0;
+    st->has_scaler = has ? 1 : 0;
+    st->scale = has ? scale : 1.0;
+    st->inv_scale = 1.0 / st->scale;
+    st->scale_f32 = (float)st->scale;
+    st->min_scale = min_scale;
+    st->max_scale = max_scale;
+    st->clip_coef = 1.0;
+    st->total_norm = 0.0;
+    st->sumsq_total = 0.0;
+    st->max_norm = max_norm;
+    st->growth_interval = growth_interval;
+    st->clean_steps = 0;
+    st->overflow = 0;
+    st->skip = 0;
+    st->underflow = 0;
+    st->nslots = nslots;
+    st->steps_applied = 0;
+    st->steps_skipped = 0;
+    st->ticket = 0;
+    for (int i = 0; i < 5; ++i) st->reserved[i] = 0;
+  }
+  double* s = reinterpret_cast<double*>(reinterpret_cast<char*>(state) + sizeof(lomo_state));
+  for (int i = threadIdx.x; i < nslots + LOMO_MAX_PROBE_BLOCKS; i += blockDim.x) s[i] = 0.0;
+}
+
+__device__ __forceinline__ bool loss_finite(const void* loss, int dt) {
+  switch (dt) {
+    case LOMO_F32: return isfinite(*(const float*)loss);
+    case LOMO_F64: return isfinite(*(const double*)loss);
+    case LOMO_F16: return isfinite(__half2float(*(const __half*)loss));
+    case LOMO_BF16: return isfinite(__bfloat162float(*(const __nv_bfloat16*)loss));
+  }
+  return true;
+}
+
+__global__ void k_begin_step(void* state, const void* loss, int loss_dtype) {
+  lomo_state* st = hdr(state);
+  const int ns = st->nslots;
+  double* s = slots_of(st);
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) s[i] = 0.0;
+  if (threadIdx.x == 0) {
+    st->overflow = 0;
+    st->skip = 0;
+    st->underflow = 0;
+    st->clip_coef = 1.0;
+    st->ticket = 0;
+    if (loss != nullptr && !loss_finite(loss, loss_dtype)) {
+      st->overflow = 1;  // optim.py:63-65 / stabilize.py:188-189
+      st->skip = 1;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// host-side launch helpers
+// --------------------------------------------------------------------------
+inline int dtype_size(int dt) {
+  switch (dt) {
+    case LOMO_F32: return 4;
+    case LOMO_F16: return 2;
+    case LOMO_BF16: return 2;
+    case LOMO_F64: return 8;
+  }
+  return 0;
+}
+
+// resident CTAs per SM for one kernel instantiation (queried once)
+template <typename K>
+int occupancy(K kernel) {
+  static int occ = 0;
+  if (occ == 0) {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, kThreads, 0) != cudaSuccess ||
+        o < 1) {
+      cudaGetLastError();
+      o = 1;
+    }
+    occ = o;
+  }
+  return occ;
+}
+
+inline int grid_for(int64_t nvec_per_thread_units, int occ) {
+  const DevInfo& di = dev_info();
+  const int64_t cap = (int64_t)di.sms * occ;
+  int64_t want = (nvec_per_thread_units + kThreads - 1) / kThreads;
+  if (want < 1) want = 1;
+  return (int)(want < cap ? want : cap);
+}
+
+template <typename M>
+UpdArgs<M> make_args(double lr, double clip_value, double weight_decay, unsigned flags) {
+  UpdArgs<M> a;
+  a.lr = (M)lr;
+  a.clip = (M)(clip_value > 0 ? clip_value : 0);
+  a.decay = (M)(1.0 - lr * weight_decay);
+  a.inv_scale = (M)1;
+  a.coef = (M)1;
+  a.use_scale = (flags & LOMO_USE_SCALE) != 0;
+  a.use_coef = (flags & LOMO_USE_COEF) != 0;
+  a.use_clip = clip_value > 0;
+  a.has_wd = weight_decay != 0.0;
+  return a;
+}
+
+template <typename T, typename M>
+int launch_update(void* p_, const void* g_, int64_t n, double lr, double clip, double wd,
+                  unsigned flags, const void* state, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  T* p = static_cast<T*>(p_);
+  const T* g = static_cast<const T*>(g_);
+  const lomo_state* st = static_cast<const lomo_state*>(state);
+  UpdArgs<M> a = make_args<M>(lr, clip, wd, flags);
+  const uintptr_t pa = (uintptr_t)p, ga = (uintptr_t)g;
+  if ((pa & 15) == (ga & 15) && (pa % sizeof(T)) == 0) {
+    int head = (int)(((16 - (pa & 15)) & 15) / sizeof(T));
+    if (head > n) head = (int)n;
+    const int64_t nvec = (n - head) / V;
+    const int grid = grid_for(nvec > 0 ? (nvec + kUnroll - 1) / kUnroll : 1,
+                              occupancy(k1_update<T, M>));
+    k1_update<T, M><<<grid, kThreads, 0, s>>>(p, g, n, head, nvec, a, flags, st);
+  } else {
+    const int grid = grid_for((n + 3) / 4, occupancy(k1_update_scalar<T, M>));
+    k1_update_scalar<T, M><<<grid, kThreads, 0, s>>>(p, g, n, a, flags, st);
+  }
+  return (int)cudaGetLastError();
+}
+
+template <typename T, typename M>
+int launch_update_multi(void* const* pt, const void* const* gt, const int64_t* nt, int ntens,
+                        int64_t max_n, double lr, double clip, double wd, unsigned flags,
+                        const void* state, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  UpdArgs<M> a = make_args<M>(lr, clip, wd, flags);
+  const int64_t units = (max_n + V - 1) / V;
+  int gx = (int)((units + kThreads - 1) / kThreads);
+  if (gx < 1) gx = 1;
+  if (gx > 64) gx = 64;
+  dim3 grid(gx, ntens);
+  k1_update_multi<T, M><<<grid, kThreads, 0, s>>>(
+      reinterpret_cast<T* const*>(pt), reinterpret_cast<const T* const*>(gt), nt, a, flags,
+      static_cast<const lomo_state*>(state));
+  return (int)cudaGetLastError();
+}
+
+template <typename T, typename M>
+int launch_probe(const void* g_, int64_t n, int slot, unsigned flags, void* state,
+                 cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  const T* g = static_cast<const T*>(g_);
+  const uintptr_t ga = (uintptr_t)g;
+  if ((ga % sizeof(T)) != 0) return LOMO_E_ARG;
+  int head = (int)(((16 - (ga & 15)) & 15) / sizeof(T));
+  if (head > n) head = (int)n;
+  const int64_t nvec = (n - head) / V;
+  int grid = grid_for(nvec > 0 ? (nvec + kUnroll - 1) / kUnroll : 1, occupancy(k2_probe<T, M>));
+  if (grid > LOMO_MAX_PROBE_BLOCKS) grid = LOMO_MAX_PROBE_BLOCKS;
+  k2_probe<T, M><<<grid, kThreads, 0, s>>>(g, n, head, nvec, slot, flags, state);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace lomo_k
+using namespace lomo_k;
+
+// ==========================================================================
+// C ABI
+// ==========================================================================
+extern "C" {
+
+int lomo_abi_version(void) { return LOMO_ABI_VERSION; }
+
+size_t lomo_state_bytes(int nslots) {
+  if (nslots < 0) nslots = 0;
+  return sizeof(lomo_state) + sizeof(double) * ((size_t)nslots + LOMO_MAX_PROBE_BLOCKS);
+}
+
+int lomo_num_sms(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return 0;
+  }
+  return dev_info().sms;
+}
+
+int lomo_state_init(void* state, int nslots, double scale, int growth_interval,
+                    double min_scale, double max_scale, double max_norm, void* stream) {
+  if (state == nullptr || nslots < 0 || growth_interval < 1) return LOMO_E_ARG;
+  k_state_init<<<1, 256, 0, (cudaStream_t)stream>>>(state, nslots, scale, growth_interval,
+                                                     min_scale, max_scale, max_norm);
+  return (int)cudaGetLastError();
+}
+
+int lomo_begin_step(void* state, const void* loss, int loss_dtype, void* stream) {
+  if (state == nullptr) return LOMO_E_ARG;
+  if (loss != nullptr && dtype_size(loss_dtype) == 0) return LOMO_E_ARG;
+  k_begin_step<<<1, 256, 0, (cudaStream_t)stream>>>(state, loss, loss_dtype);
+  return (int)cudaGetLastError();
+}
+
+int lomo_read_status(const void* state, lomo_status* out, void* stream) {
+  if (state == nullptr || out == nullptr) return LOMO_E_ARG;
+  return (int)cudaMemcpyAsync(out, state, sizeof(lomo_status), cudaMemcpyDeviceToHost,
+                              (cudaStream_t)stream);
+}
+
+int lomo_fused_update(void* p, const void* g, int64_t n, int dtype, int math, double lr,
+                      double clip_value, double weight_decay, unsigned flags,
+                      const void* state, void* stream) {
+  if (n < 0) return LOMO_E_ARG;
+  if (n == 0) return 0;
+  if (p == nullptr || g == nullptr) return LOMO_E_ARG;
+  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP)) && state == nullptr)
+    return LOMO_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool f64 = math == LOMO_MATH_F64;
+  if (math != LOMO_MATH_F32 && math != LOMO_MATH_F64) return LOMO_E_ARG;
+  switch (dtype) {
+    case LOMO_F16:
+      return f64 ? launch_update<__half, double>(p, g, n, lr, clip_value, weight_decay, flags, state, s)
+                 : launch_update<__half, float>(p, g, n, lr, clip_value, weight_decay, flags, state, s);
+    case LOMO_BF16:
+      return f64 ? launch_update<__nv_bfloat16, double>(p, g, n, lr, clip_value, weight_decay, flags, state, s)
+                 : launch_update<__nv_bfloat16, float>(p, g, n, lr, clip_value, weight_decay, flags, state, s);
+    case LOMO_F32:
+      return f64 ? launch_update<float, double>(p, g, n, lr, clip_value, weight_decay, flags, state, s)
+                 : launch_update<float, float>(p, g, n, lr, clip_value, weight_decay, flags, state, s);
+    case LOMO_F64:
+      // f64 storage always computes in f64
+      return launch_update<double, double>(p, g, n, lr, clip_value, weight_decay, flags, state, s);
+  }
+  return LOMO_E_ARG;
+}
+
+int lomo_fused_update_multi(void* const* p_table, const void* const* g_table,
+                            const int64_t* n_table, int ntensors, int64_t max_n, int dtype,
+                            int math, double lr, double clip_value, double weight_decay,
+                            unsigned flags, const void* state, void* stream) {
+  if (ntensors < 0 || max_n < 0) return LOMO_E_ARG;
+  if (ntensors == 0 || max_n == 0) return 0;
+  if (p_table == nullptr || g_table == nullptr || n_table == nullptr) return LOMO_E_ARG;
+  if (ntensors > 65535) return LOMO_E_ARG;
+  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP)) && state == nullptr)
+    return LOMO_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool f64 = math == LOMO_MATH_F64;
+  if (math != LOMO_MATH_F32 && math != LOMO_MATH_F64) return LOMO_E_ARG;
+#define LOMO_MULTI(T, M) \
+  launch_update_multi<T, M>(p_table, g_table, n_table, ntensors, max_n, lr, clip_value, weight_decay, flags, state, s)
+  switch (dtype) {
+    case LOMO_F16: return f64 ? LOMO_MULTI(__half, double) : LOMO_MULTI(__half, float);
+    case LOMO_BF16: return f64 ? LOMO_MULTI(__nv_bfloat16, double) : LOMO_MULTI(__nv_bfloat16, float);
+    case LOMO_F32: return f64 ? LOMO_MULTI(float, double) : LOMO_MULTI(float, float);
+    case LOMO_F64: return LOMO_MULTI(double, double);
+  }
+#undef LOMO_MULTI
+  return LOMO_E_ARG;
+}
+
+int lomo_probe(const void* g, int64_t n, int dtype, int slot, unsigned flags, void* state,
+               void* stream) {
+  if (state == nullptr || n < 0) return LOMO_E_ARG;
+  if (slot < 0) return LOMO_E_SLOT;
+  if (n > 0 && g == nullptr) return LOMO_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) return 0;
+  switch (dtype) {
+    case LOMO_F16: return launch_probe<__half, float>(g, n, slot, flags, state, s);
+    case LOMO_BF16: return launch_probe<__nv_bfloat16, float>(g, n, slot, flags, state, s);
+    case LOMO_F32: return launch_probe<float, double>(g, n, slot, flags, state, s);
+    case LOMO_F64: return launch_probe<double, double>(g, n, slot, flags, state, s);
+  }
+  return LOMO_E_ARG;
+}
+
+int lomo_finalize_norm(void* state, void* stream) {
+  if (state == nullptr) return LOMO_E_ARG;
+  k3_finalize<<<1, 32, 0, (cudaStream_t)stream>>>(state);
+  return (int)cudaGetLastError();
+}
+
+int lomo_scaler_on_clean(void* state, void* stream) {
+  if (state == nullptr) return LOMO_E_ARG;
+  k3_on_clean<<<1, 32, 0, (cudaStream_t)stream>>>(state);
+  return (int)cudaGetLastError();
+}
+
+int lomo_local_norm_partial(const void* state, double* out2_dev, void* stream) {
+  if (state == nullptr || out2_dev == nullptr) return LOMO_E_ARG;
+  k3_local_partial<<<1, 32, 0, (cudaStream_t)stream>>>(state, out2_dev);
+  return (int)cudaGetLastError();
+}
+
+int lomo_finalize_norm_ranks(void* state, const double* parts_dev, int world, void* stream) {
+  if (state == nullptr || parts_dev == nullptr || world < 1) return LOMO_E_ARG;
+  k3_finalize_ranks<<<1, 32, 0, (cudaStream_t)stream>>>(state, parts_dev, world);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"

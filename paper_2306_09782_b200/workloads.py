@@ -1,0 +1,299 @@
+"""Models and synthetic inputs that drive the fused-update path.
+
+The models are the *callers* of the hot path (autograd produces the
+gradients the hook consumes); they are plain PyTorch and not part of the
+product kernels.
+
+* ``MiniTransformer`` restates the reference's bundled pre-norm decoder
+  (fusedtrain/zoo.py:150-201) op for op -- weights stored ``[in, out]`` and
+  applied as ``x @ W`` (ops.py:58-75), additive sinusoidal positions
+  (ops.py:209-223), RMSNorm ``x / sqrt(mean(x^2) + 1e-5) * s`` (ops.py:228-236),
+  no causal mask (zoo.py:173-178), tanh-GELU gate times up (zoo.py:189-193),
+  untied head, mean cross entropy (ops.py:332-352) -- so config 1 (C1) can be
+  checked against the reference's own run.  ``mini_transformer_init`` draws
+  the initial weights with the reference's RNG sequence (zoo.py:150-224,
+  ``INIT_RANGE`` zoo.py:26) and ``sequence_copy_batch`` its tokens
+  (zoo.py:227-241).
+* ``Llama`` is a LLaMA-1 decoder (RMSNorm, rotary, causal SDPA, SwiGLU, untied
+  head) with random init, for configs 3-5 (7B/13B/65B).
+* ``llama_param_shapes`` lists the 291 (7B) parameter shapes for the
+  fused-update microbench (config 2), in registration order.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+INIT_RANGE = 0.08   # zoo.py:26
+RMSNORM_EPS = 1e-5  # zoo.py:27
+
+
+# ---------------------------------------------------------------------------
+# C1: the reference's mini transformer
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class MiniConfig:
+    layers: int = 2
+    hidden: int = 256
+    heads: int = 4
+    vocab: int = 1024
+    seed: int = 0
+
+    @property
+    def ffn(self) -> int:
+        return 4 * self.hidden  # zoo.py:86-88
+
+
+def round_half_np(x: np.ndarray) -> np.ndarray:
+    """float64 -> binary16 -> float64, RNE, overflow to inf (tensor.py:30-38)."""
+    with np.errstate(over="ignore"):
+        return np.asarray(x, dtype=np.float64).astype(np.float16).astype(np.float64)
+
+
+def mini_transformer_init(cfg: MiniConfig) -> list[tuple[str, np.ndarray]]:
+    """Initial parameters in build (registration) order, float64 (zoo.py:150-201)."""
+    rng = np.random.default_rng(cfg.seed)
+    h, f = cfg.hidden, cfg.ffn
+    uni = lambda *shape: rng.uniform(-INIT_RANGE, INIT_RANGE, shape)
+    out = [("embedding.weight", uni(cfg.vocab, h))]
+    for l in range(cfg.layers):
+        pre = f"block{l}"
+        out.append((f"{pre}.attn_norm.scale", np.ones(h)))
+        for name in ("q", "k", "v"):
+            out.append((f"{pre}.attn.{name}_proj", uni(h, h)))
+        out.append((f"{pre}.attn.out_proj", uni(h, h)))
+        out.append((f"{pre}.ffn_norm.scale", np.ones(h)))
+        out.append((f"{pre}.ffn.gate_proj", uni(h, f)))
+        out.append((f"{pre}.ffn.up_proj", uni(h, f)))
+        out.append((f"{pre}.ffn.down_proj", uni(f, h)))
+    out.append(("final_norm.scale", np.ones(h)))
+    out.append(("head.weight", uni(h, cfg.vocab)))
+    return out
+
+
+def sequence_copy_batch(dataset_seed: int, step: int, batch: int, seq_len: int,
+                        vocab: int) -> np.ndarray:
+    """Token ids for (dataset_seed, step); targets are the ids (zoo.py:227-241)."""
+    rng = np.random.default_rng([dataset_seed, step])
+    return rng.integers(0, vocab, (batch, seq_len))
+
+
+def sinusoidal_table(seq_len: int, width: int) -> np.ndarray:
+    """ops.py:209-215."""
+    pos = np.arange(seq_len, dtype=np.float64)[:, None]
+    idx = np.arange(width, dtype=np.float64)[None, :]
+    angle = pos / np.power(10000.0, 2.0 * np.floor(idx / 2.0) / width)
+    return np.where(idx % 2 == 0, np.sin(angle), np.cos(angle))
+
+
+def _op(x: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
+    """Round an op output to the storage dtype (tape.py:286-289 / :377)."""
+    return x if x.dtype == dtype else x.to(dtype)
+
+
+class MiniTransformer(nn.Module):
+    """zoo._build_mini_transformer in torch; every op's output is rounded to
+    the parameter dtype, nonlinear ops compute in fp32 (or fp64 for fp64)."""
+
+    def __init__(self, cfg: MiniConfig, dtype: torch.dtype = torch.float32,
+                 device: str | torch.device = "cuda",
+                 init: list[tuple[str, np.ndarray]] | None = None):
+        super().__init__()
+        self.cfg = cfg
+        self.dtype = dtype
+        init = init if init is not None else mini_transformer_init(cfg)
+        self._names = []
+        for name, arr in init:
+            if dtype in (torch.float16,):
+                arr = round_half_np(arr)  # Tensor(data, HALF) rounds at build (tensor.py:44-46)
+            t = torch.tensor(arr, dtype=torch.float64).to(dtype=dtype, device=device)
+            self.register_parameter(name.replace(".", "__"), nn.Parameter(t))
+            self._names.append(name)
+        self.inner = torch.float64 if dtype == torch.float64 else torch.float32
+
+    def param(self, name: str) -> nn.Parameter:
+        return getattr(self, name.replace(".", "__"))
+
+    def named_reference_parameters(self):
+        for name in self._names:
+            yield name, self.param(name)
+
+    def _rmsnorm(self, x, s):
+        xi, si = x.to(self.inner), s.to(self.inner)
+        r = torch.sqrt(torch.mean(xi * xi, dim=-1, keepdim=True) + RMSNORM_EPS)
+        return _op(xi / r * si, self.dtype)
+
+    def _gelu(self, x):
+        xi = x.to(self.inner)
+        c = math.sqrt(2.0 / math.pi)
+        return _op(0.5 * xi * (1.0 + torch.tanh(c * (xi + 0.044715 * xi ** 3))), self.dtype)
+
+    def forward(self, ids: torch.Tensor) -> torch.Tensor:
+        cfg, dt = self.cfg, self.dtype
+        b, s = ids.shape
+        h, nh = cfg.hidden, cfg.heads
+        dh = h // nh
+        pos = torch.tensor(sinusoidal_table(s, h), dtype=self.inner, device=ids.device)
+        x = F.embedding(ids, self.param("embedding.weight"))
+        x = _op(x.to(self.inner) + pos, dt)
+        for l in range(cfg.layers):
+            pre = f"block{l}"
+            a = self._rmsnorm(x, self.param(f"{pre}.attn_norm.scale"))
+            heads = []
+            for nm in ("q", "k", "v"):
+                y = a @ self.param(f"{pre}.attn.{nm}_proj")
+                heads.append(y.view(b, s, nh, dh).transpose(1, 2))
+            q, k, v = heads
+            scores = _op((q @ k.transpose(-1, -2)).to(self.inner) * (1.0 / math.sqrt(dh)), dt)
+            probs = _op(torch.softmax(scores.to(self.inner), dim=-1), dt)
+            ctx = (probs @ v).transpose(1, 2).reshape(b, s, h)
+            x = x + ctx @ self.param(f"{pre}.attn.out_proj")
+            y = self._rmsnorm(x, self.param(f"{pre}.ffn_norm.scale"))
+            gated = self._gelu(y @ self.param(f"{pre}.ffn.gate_proj")) * \
+                (y @ self.param(f"{pre}.ffn.up_proj"))
+            x = x + gated @ self.param(f"{pre}.ffn.down_proj")
+        xf = self._rmsnorm(x, self.param("final_norm.scale"))
+        return xf @ self.param("head.weight")
+
+
+def mean_cross_entropy(logits: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+    """Mean per-position CE (ops.py:332-352), computed in >= fp32."""
+    inner = torch.float64 if logits.dtype == torch.float64 else torch.float32
+    return F.cross_entropy(logits.reshape(-1, logits.shape[-1]).to(inner), targets.reshape(-1))
+
+
+# ---------------------------------------------------------------------------
+# LLaMA-1 shapes (configs 2-5)
+# ---------------------------------------------------------------------------
+LLAMA = {
+    "7b": dict(hidden=4096, layers=32, heads=32, ffn=11008, vocab=32000),
+    "13b": dict(hidden=5120, layers=40, heads=40, ffn=13824, vocab=32000),
+    "30b": dict(hidden=6656, layers=60, heads=52, ffn=17920, vocab=32000),
+    "65b": dict(hidden=8192, layers=80, heads=64, ffn=22016, vocab=32000),
+}
+
+
+def llama_param_shapes(size: str = "7b") -> list[tuple[str, tuple[int, ...]]]:
+    """All parameter shapes of LLaMA-``size`` in registration order."""
+    c = LLAMA[size]
+    h, f, v = c["hidden"], c["ffn"], c["vocab"]
+    out = [("embed_tokens.weight", (v, h))]
+    for l in range(c["layers"]):
+        p = f"layers.{l}"
+        out += [(f"{p}.input_layernorm.weight", (h,)),
+                (f"{p}.self_attn.q_proj.weight", (h, h)),
+                (f"{p}.self_attn.k_proj.weight", (h, h)),
+                (f"{p}.self_attn.v_proj.weight", (h, h)),
+                (f"{p}.self_attn.o_proj.weight", (h, h)),
+                (f"{p}.post_attention_layernorm.weight", (h,)),
+                (f"{p}.mlp.gate_proj.weight", (f, h)),
+                (f"{p}.mlp.up_proj.weight", (f, h)),
+                (f"{p}.mlp.down_proj.weight", (h, f))]
+    out += [("norm.weight", (h,)), ("lm_head.weight", (v, h))]
+    return out
+
+
+def llama_param_count(size: str = "7b") -> int:
+    return sum(math.prod(s) for _, s in llama_param_shapes(size))
+
+
+class RMSNorm(nn.Module):
+    def __init__(self, h: int, dtype, device):
+        super().__init__()
+        self.weight = nn.Parameter(torch.ones(h, dtype=dtype, device=device))
+
+    def forward(self, x):
+        xf = x.float()
+        y = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + RMSNORM_EPS)
+        return y.to(x.dtype) * self.weight
+
+
+def _linear(h_in: int, h_out: int, dtype, device, std: float) -> nn.Parameter:
+    w = torch.empty(h_out, h_in, dtype=dtype, device=device)
+    w.normal_(0.0, std)
+    return nn.Parameter(w)
+
+
+class LlamaLayer(nn.Module):
+    def __init__(self, h, nh, f, dtype, device, std):
+        super().__init__()
+        self.nh = nh
+        self.input_layernorm = RMSNorm(h, dtype, device)
+        self.q = _linear(h, h, dtype, device, std)
+        self.k = _linear(h, h, dtype, device, std)
+        self.v = _linear(h, h, dtype, device, std)
+        self.o = _linear(h, h, dtype, device, std)
+        self.post_attention_layernorm = RMSNorm(h, dtype, device)
+        self.gate = _linear(h, f, dtype, device, std)
+        self.up = _linear(h, f, dtype, device, std)
+        self.down = _linear(f, h, dtype, device, std)
+
+    def forward(self, x, cos, sin):
+        b, s, h = x.shape
+        nh, dh = self.nh, h // self.nh
+        a = self.input_layernorm(x)
+        q = F.linear(a, self.q).view(b, s, nh, dh).transpose(1, 2)
+        k = F.linear(a, self.k).view(b, s, nh, dh).transpose(1, 2)
+        v = F.linear(a, self.v).view(b, s, nh, dh).transpose(1, 2)
+        q, k = _rope(q, cos, sin), _rope(k, cos, sin)
+        o = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        x = x + F.linear(o.transpose(1, 2).reshape(b, s, h), self.o)
+        y = self.post_attention_layernorm(x)
+        return x + F.linear(F.silu(F.linear(y, self.gate)) * F.linear(y, self.up), self.down)
+
+
+def _rope(x, cos, sin):
+    x1, x2 = x.chunk(2, dim=-1)
+    return x * cos + torch.cat((-x2, x1), dim=-1) * sin
+
+
+class Llama(nn.Module):
+    """LLaMA-1 decoder, random init N(0, 0.02), parameters in ``dtype``."""
+
+    def __init__(self, size: str = "7b", dtype=torch.float16, device="cuda",
+                 checkpointing: bool = False, layers: int | None = None, seed: int = 0):
+        super().__init__()
+        c = dict(LLAMA[size])
+        if layers is not None:
+            c["layers"] = layers
+        self.cfg = c
+        self.checkpointing = checkpointing
+        h, f, v, nh = c["hidden"], c["ffn"], c["vocab"], c["heads"]
+        g = torch.cuda.manual_seed(seed) if str(device).startswith("cuda") else None
+        std = 0.02
+        self.embed_tokens = nn.Parameter(torch.empty(v, h, dtype=dtype, device=device).normal_(0, std))
+        self.layers = nn.ModuleList(LlamaLayer(h, nh, f, dtype, device, std)
+                                    for _ in range(c["layers"]))
+        self.norm = RMSNorm(h, dtype, device)
+        self.lm_head = nn.Parameter(torch.empty(v, h, dtype=dtype, device=device).normal_(0, std))
+        self._rope_cache = {}
+
+    def _cos_sin(self, s, device, dtype):
+        key = (s, device, dtype)
+        if key not in self._rope_cache:
+            dh = self.cfg["hidden"] // self.cfg["heads"]
+            inv = 1.0 / (10000 ** (torch.arange(0, dh, 2, device=device, dtype=torch.float32) / dh))
+            t = torch.arange(s, device=device, dtype=torch.float32)
+            fr = torch.outer(t, inv)
+            emb = torch.cat((fr, fr), dim=-1)
+            self._rope_cache[key] = (emb.cos().to(dtype), emb.sin().to(dtype))
+        return self._rope_cache[key]
+
+    def forward(self, ids):
+        x = F.embedding(ids, self.embed_tokens)
+        cos, sin = self._cos_sin(ids.shape[1], ids.device, x.dtype)
+        for layer in self.layers:
+            if self.checkpointing and self.training:
+                x = torch.utils.checkpoint.checkpoint(layer, x, cos, sin, use_reentrant=False)
+            else:
+                x = layer(x, cos, sin)
+        return F.linear(self.norm(x), self.lm_head)
+
+    def loss(self, ids, targets):
+        logits = self(ids)
+        return F.cross_entropy(logits.view(-1, logits.shape[-1]).float(), targets.view(-1))

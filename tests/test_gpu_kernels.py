@@ -1,0 +1,416 @@
+"""GPU parity of the sm_100a kernels (K1/K2/K3) against the CPU oracle and the
+reference's own recorded behaviour (tests/golden/hook_cases.*), through the C-ABI.
+
+Tolerances (stated here, north star): f64 arithmetic mode is bit-exact
+against the float64 oracle (the reference's own arithmetic, optim.py:9-13)
+except where a global-norm coefficient enters (our deterministic f64
+reduction order differs from BLAS ddot: <= 1 ulp); f32 arithmetic mode is
+within 1 ulp per element of the oracle (north star: 2 ulp) with the
+mismatch fraction reported.  Overflow-skip and clip decisions: identical.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import lomo_oracle as O
+from conftest import case_arrays
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import gpu_util as U
+    from paper_2306_09782_b200 import _lib
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    torch.cuda.set_device(0)
+
+
+PRECS = ["half", "bf16", "f32"]
+
+
+def _expected(p, g, prec, lr=0.05, clip=None, inv_scale=None, coef=None, wd=0.0):
+    """The reference hook arithmetic (stabilize.py:217-224, optim.py:52-54) in f64."""
+    g = np.asarray(g, np.float64)
+    p = np.asarray(p, np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        if inv_scale is not None:
+            g = g * inv_scale
+        if clip is not None:
+            g = np.clip(g, -clip, clip)
+        if coef is not None:
+            g = g * coef
+        if wd:
+            p = p * (1.0 - lr * wd)
+        return O.round_to(p - lr * g, prec)
+
+
+def _draw(n, prec, rng, gscale=1e-3):
+    p = O.round_to(rng.uniform(-0.08, 0.08, n), prec)
+    g = O.round_to(rng.normal(0, gscale, n), prec)
+    return p, g
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 4095, 4096, 4097, (1 << 20) + 3])
+@pytest.mark.parametrize("offset", [0, 3])
+def test_k1_plain_update_f64_math_bit_exact(prec, n, offset):
+    rng = np.random.default_rng(n + offset)
+    p0, g0 = _draw(n, prec, rng)
+    dt = U.TORCH_DT[prec]
+    p, g = U.to_dev(p0, dt, offset), U.to_dev(g0, dt, offset)
+    U.fused_update(p, g, math="f64")
+    got = p.double().cpu().numpy()
+    assert np.array_equal(got, _expected(p0, g0, prec))
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("n", [5, 4097, 3 * (1 << 20) + 1])
+def test_k1_plain_update_f32_math_within_one_ulp(prec, n):
+    rng = np.random.default_rng(n)
+    p0, g0 = _draw(n, prec, rng)
+    dt = U.TORCH_DT[prec]
+    p, g = U.to_dev(p0, dt), U.to_dev(g0, dt)
+    U.fused_update(p, g, math="f32")
+    want = U.to_dev(_expected(p0, g0, prec), dt)
+    d = U.ulp_diff(p, want)
+    frac = (d > 0).float().mean().item()
+    print(f"{prec} n={n}: max ulp {d.max().item()}, mismatch fraction {frac:.2e}")
+    assert d.max().item() <= 1
+
+
+def test_k1_misaligned_pair_takes_scalar_path_and_matches():
+    rng = np.random.default_rng(1)
+    n = 100001
+    p0, g0 = _draw(n, "half", rng)
+    p, g = U.to_dev(p0, torch.float16, 1), U.to_dev(g0, torch.float16, 4)
+    U.fused_update(p, g, math="f64")
+    assert np.array_equal(p.double().cpu().numpy(), _expected(p0, g0, "half"))
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("math_mode", ["f64", "f32"])
+def test_k1_all_stages(prec, math_mode):
+    """unscale -> value clip -> coef -> weight decay -> update, flags from state."""
+    rng = np.random.default_rng(7)
+    n = 1 << 18
+    scale = 2.0 ** 12
+    p0 = O.round_to(rng.uniform(-0.08, 0.08, n), prec)
+    g0 = O.round_to(rng.normal(0, 1e-3, n) * scale, prec)
+    dt = U.TORCH_DT[prec]
+    st = U.State(1, scale=scale)
+    coef = 0.731
+    st.write_header(clip_coef=coef)
+    for wd in (0.0, 0.1):
+        p, g = U.to_dev(p0, dt), U.to_dev(g0, dt)
+        U.fused_update(p, g, math=math_mode, clip=1.5e-3, wd=wd,
+                       flags=_lib.USE_SCALE | _lib.USE_COEF | _lib.USE_SKIP, state=st)
+        want = U.to_dev(_expected(p0, g0, prec, clip=1.5e-3, inv_scale=1 / scale, coef=coef,
+                                  wd=wd), dt)
+        d = U.ulp_diff(p, want)
+        if math_mode == "f64":
+            assert d.max().item() == 0, (wd, d.max().item())
+        else:
+            assert d.max().item() <= 1, (wd, d.max().item())
+
+
+def test_k1_skip_flag_is_a_noop():
+    rng = np.random.default_rng(3)
+    p0, g0 = _draw(50000, "half", rng)
+    p, g = U.to_dev(p0, torch.float16), U.to_dev(g0, torch.float16)
+    st = U.State(1)
+    st.write_header(skip=1)
+    U.fused_update(p, g, flags=_lib.USE_SKIP, state=st)
+    assert np.array_equal(p.double().cpu().numpy(), p0)
+    U.fused_update(p, g, flags=0, state=st)  # without USE_SKIP it applies
+    assert not np.array_equal(p.double().cpu().numpy(), p0)
+
+
+def test_k1_value_clip_propagates_nan_and_kat():
+    # stabilize.py:82-86 KAT [1.3, 0.8] @ 1.0 -> [1.0, 0.8]; np.clip keeps NaN
+    p = torch.zeros(4, dtype=torch.float64, device="cuda")
+    g = torch.tensor([1.3, 0.8, -2.5, float("nan")], dtype=torch.float64, device="cuda")
+    U.fused_update(p, g, math="f64", lr=1.0, clip=1.0)
+    got = p.cpu().numpy()
+    assert np.array_equal(got[:3], [-1.0, -0.8, 1.0]) and np.isnan(got[3])
+
+
+def test_k1_scalar_kat():
+    # test_optim.py:25-36: w=2, x=3, t=0 -> g=18, lr=0.1 -> w'=0.2
+    p = torch.tensor([2.0], dtype=torch.float64, device="cuda")
+    g = torch.tensor([18.0], dtype=torch.float64, device="cuda")
+    U.fused_update(p, g, math="f64", lr=0.1)
+    assert p.item() == 2.0 - 0.1 * 18.0
+
+
+def test_k1_zero_lr_and_empty():
+    rng = np.random.default_rng(9)
+    p0, g0 = _draw(1000, "bf16", rng)
+    p, g = U.to_dev(p0, torch.bfloat16), U.to_dev(g0, torch.bfloat16)
+    U.fused_update(p, g, lr=0.0)
+    assert np.array_equal(p.double().cpu().numpy(), p0)
+    e = torch.empty(0, dtype=torch.bfloat16, device="cuda")
+    U.fused_update(e, e)
+
+
+def test_k1_fp16_overflow_to_inf_on_store():
+    p = torch.tensor([65504.0, -65504.0, 1.0], dtype=torch.float16, device="cuda")
+    g = torch.tensor([-1000.0, 1000.0, 0.0], dtype=torch.float16, device="cuda")
+    U.fused_update(p, g, math="f64", lr=1.0)
+    assert p[0].item() == math.inf and p[1].item() == -math.inf and p[2].item() == 1.0
+
+
+def test_k1_f64_math_rounds_directly_not_through_fp32():
+    """f64 -> f16 must be ONE rounding (numpy's cast, tensor.py:38).  On 1M
+    random updates a double rounding through fp32 differs somewhere; the
+    device result must match the direct rounding everywhere."""
+    rng = np.random.default_rng(99)
+    n = 1 << 20
+    rng.uniform(size=3 * n)  # (same draws as the probe that found such cases)
+    p0 = O.round_to(rng.uniform(-2.0, 2.0, n), "half")
+    g0 = O.round_to(rng.normal(0, 0.3, n), "half")
+    exact = p0 - 0.0123 * g0
+    direct = O.round_through_half(exact)
+    double = O.round_through_half(exact.astype(np.float32).astype(np.float64))
+    assert (direct != double).sum() > 0  # the test has power
+    p, g = U.to_dev(p0, torch.float16), U.to_dev(g0, torch.float16)
+    U.fused_update(p, g, math="f64", lr=0.0123)
+    assert np.array_equal(p.double().cpu().numpy(), direct)
+
+
+# --- K2 probe ----------------------------------------------------------------
+
+@pytest.mark.parametrize("prec", ["half", "bf16", "f32", "full"])
+@pytest.mark.parametrize("n", [1, 9, 4096, 1000003, 4096 * 11008])
+def test_k2_sumsq_and_determinism(prec, n):
+    rng = np.random.default_rng(n)
+    scale = 1024.0 if prec in ("half", "bf16") else 1.0
+    g0 = O.round_to(rng.normal(0, 1e-3, n) * scale, prec)
+    g = U.to_dev(g0, U.TORCH_DT[prec], offset=n % 5)
+    st = U.State(2, scale=scale if scale != 1.0 else 0.0)
+    flags = _lib.USE_SCALE if scale != 1.0 else 0
+    st.begin()
+    st.probe(g, 0, flags)
+    st.probe(g, 1, flags)
+    s = st.slots(2)
+    ovf, want = O.probe([g0], scale, True)
+    assert not ovf and st.status().overflow == 0
+    assert s[0] == s[1]  # deterministic, run to run
+    tol = 1e-12 if prec in ("f32", "full") else 2e-6
+    assert abs(s[0] - want) <= tol * want, (s[0], want)
+
+
+@pytest.mark.parametrize("prec", ["half", "bf16", "f32"])
+@pytest.mark.parametrize("pos", ["head", "middle", "tail"])
+@pytest.mark.parametrize("bad", [math.inf, -math.inf, math.nan])
+def test_k2_overflow_flag(prec, pos, bad):
+    n = 100003
+    g0 = np.full(n, 1e-3)
+    idx = {"head": 0, "middle": n // 2, "tail": n - 1}[pos]
+    g0[idx] = bad
+    g = U.to_dev(O.round_to(g0, prec), U.TORCH_DT[prec], offset=1)
+    st = U.State(1)
+    st.begin()
+    st.probe(g, 0, 0)
+    assert st.status().overflow == 1
+
+
+def test_k2_large_finite_fp16_does_not_flag():
+    g = torch.full((4097,), 65504.0, dtype=torch.float16, device="cuda")
+    st = U.State(1)
+    st.begin()
+    st.probe(g, 0, 0)
+    status = st.status()
+    assert status.overflow == 0
+    assert st.slots(1)[0] == 4097 * 65504.0 ** 2
+
+
+# --- K3 ------------------------------------------------------------------------
+
+def test_k3_scaler_replay_matches_reference_fixture():
+    import json
+    from conftest import GOLDEN
+    seqs = json.loads((GOLDEN / "scaler_replay.json").read_text())
+    inf = torch.tensor(float("inf"), device="cuda")
+    zero = torch.tensor(0.5, device="cuda")
+    for s in seqs[:120]:
+        st = U.State(1, scale=2.0 ** 6, growth=s["growth"], min_scale=1.0, max_scale=2.0 ** 10)
+        trace = []
+        for ok in s["outcomes"]:
+            st.begin(zero if ok else inf)  # a non-finite loss forces the overflow path
+            st.finalize()
+            st.on_clean()
+            h = st.status()
+            if h.underflow:
+                trace.append(None)
+                break
+            assert h.skip == (0 if ok else 1)
+            trace.append(h.scale)
+            assert h.scale_f32 == h.scale and h.inv_scale == 1.0 / h.scale
+        assert trace == s["trace"]
+
+
+def test_k3_norm_decision():
+    g = torch.full((10000,), 0.01, dtype=torch.float64, device="cuda")  # N = 1.0
+    for max_norm, coef in ((0.5, 0.5), (2.0, 1.0)):
+        st = U.State(3, max_norm=max_norm)
+        st.begin()
+        st.probe(g, 0, 0)
+        st.probe(g, 2, 0)  # slot 1 unused -> stays 0 (begin_step zeroes it)
+        st.finalize()
+        h = st.status()
+        assert abs(h.total_norm - math.sqrt(2.0)) < 1e-12
+        assert h.clip_coef == min(1.0, max_norm / h.total_norm)
+        assert h.skip == 0
+    # zero gradients: N = 0 -> coef 1 (stabilize.py:212)
+    st = U.State(1, max_norm=1.0)
+    st.begin()
+    st.probe(torch.zeros(100, dtype=torch.float32, device="cuda"), 0, 0)
+    st.finalize()
+    assert st.status().clip_coef == 1.0
+
+
+def test_k3_rank_combination_is_rank_ordered():
+    st = U.State(1, max_norm=1.0)
+    parts = torch.tensor([[0.25, 0.0], [0.5, 0.0], [0.25, 0.0]], dtype=torch.float64,
+                         device="cuda")
+    st.begin()
+    _lib.check(U.lib().lomo_finalize_norm_ranks(st.ptr, parts.data_ptr(), 3, U.stream()), "r")
+    h = st.status()
+    assert h.sumsq_total == 1.0 and h.clip_coef == 1.0 and h.skip == 0
+    parts[1, 1] = 1.0  # one rank saw a non-finite gradient
+    st.begin()
+    _lib.check(U.lib().lomo_finalize_norm_ranks(st.ptr, parts.data_ptr(), 3, U.stream()), "r")
+    assert st.status().skip == 1
+
+
+def test_multi_tensor_update_matches_single():
+    rng = np.random.default_rng(12)
+    sizes = [4096, 4096, 17, 4096 * 3 + 5]
+    ps = [_draw(n, "bf16", rng) for n in sizes]
+    P = [U.to_dev(p, torch.bfloat16) for p, _ in ps]
+    G = [U.to_dev(g, torch.bfloat16) for _, g in ps]
+    pt = torch.tensor([t.data_ptr() for t in P], dtype=torch.int64, device="cuda")
+    gt = torch.tensor([t.data_ptr() for t in G], dtype=torch.int64, device="cuda")
+    nt = torch.tensor(sizes, dtype=torch.int64, device="cuda")
+    _lib.check(U.lib().lomo_fused_update_multi(pt.data_ptr(), gt.data_ptr(), nt.data_ptr(),
+                                               len(sizes), max(sizes), _lib.BF16, _lib.MATH_F64,
+                                               0.05, 0.0, 0.0, 0, None, U.stream()), "multi")
+    for t, (p0, g0) in zip(P, ps):
+        assert np.array_equal(t.double().cpu().numpy(), _expected(p0, g0, "bf16"))
+
+
+# --- reference hook cases, replayed through the C-ABI ------------------------------
+
+def _device_case(case, arrays, nshapes, prec, math_mode):
+    p, g = case_arrays(arrays, case["name"], nshapes)
+    dt = U.TORCH_DT[prec]
+    P = [U.to_dev(O.round_to(x, prec), dt) for x in p[0]]
+    sc, clip = case["scaler"], case["clip"]
+    two = sc is not None or (clip is not None and clip["kind"] == "by_global_norm")
+    thresh = clip["threshold"] if clip and clip["kind"] == "by_value" else 0.0
+    max_norm = clip["max_norm"] if clip and clip["kind"] == "by_global_norm" else 0.0
+    st = U.State(nshapes, scale=case["init_scale"] or 0.0,
+                 growth=sc["growth_interval"] if sc else 1,
+                 min_scale=sc["min_scale"] if sc else 1.0,
+                 max_scale=sc["max_scale"] if sc else 1.0, max_norm=max_norm)
+    outs, scales, results = [], [], []
+    for k in range(case["steps"]):
+        scale = st.status().scale
+        loss = torch.tensor(case["losses"][k], dtype=torch.float32, device="cuda")
+        st.begin(loss)
+        delivered = [U.to_dev(O.round_to(x * scale, prec), dt) for x in g[k]]
+        order = list(reversed(range(nshapes)))  # delivery order (tape.py:350-360)
+        if two:
+            for slot, i in enumerate(order):
+                st.probe(delivered[i], slot, _lib.USE_SCALE if sc else 0)
+            st.finalize()
+            h = st.status()
+            if h.underflow:
+                outs.append("underflow")
+            elif h.skip:
+                outs.append("skipped_overflow")
+            else:
+                flags = _lib.USE_SKIP | (_lib.USE_SCALE if sc else 0) | \
+                    (_lib.USE_COEF if max_norm > 0 else 0)
+                for i in order:
+                    U.fused_update(P[i], delivered[i], math=math_mode, lr=case["lr"],
+                                   clip=thresh, flags=flags, state=st)
+                st.on_clean()
+                outs.append("applied")
+        else:
+            for i in order:
+                U.fused_update(P[i], delivered[i], math=math_mode, lr=case["lr"], clip=thresh,
+                               flags=_lib.USE_SKIP, state=st)
+            st.on_clean()
+            outs.append("nonfinite_loss" if st.status().skip else "applied")
+        scales.append(st.status().scale if sc else None)
+        results.append([t.clone() for t in P])
+    return outs, scales, results, p
+
+
+@pytest.mark.parametrize("math_mode", ["f64", "f32"])
+def test_reference_hook_cases_replayed_on_device(hook_cases, math_mode):
+    meta, arrays = hook_cases
+    nshapes = len(meta["shapes"])
+    worst = {}
+    for case in meta["cases"]:
+        prec = case["precision"]
+        outs, scales, results, p = _device_case(case, arrays, nshapes, prec, math_mode)
+        want = [o if not o.startswith("underflow") else "underflow" for o in case["outcomes"]]
+        assert outs == want, case["name"]                     # decisions: bit-exact
+        if case["scaler"] is not None:
+            assert scales == case["scales"], case["name"]
+        norm = case["clip"] is not None and case["clip"]["kind"] == "by_global_norm"
+        dt = U.TORCH_DT[prec]
+        for k in range(case["steps"]):
+            for i in range(nshapes):
+                ref = U.to_dev(p[k + 1][i], dt)
+                d = U.ulp_diff(results[k][i], ref).max().item()
+                worst[case["name"]] = max(worst.get(case["name"], 0), d)
+                if math_mode == "f64" and not norm:
+                    assert d == 0, (case["name"], k, i, d)
+                else:
+                    assert d <= 1, (case["name"], k, i, d)
+    print(math_mode, "max ulp per case:", worst)
+
+
+@pytest.mark.parametrize("math_mode", ["f64", "f32"])
+def test_bf16_cases_match_oracle(hook_cases, math_mode):
+    """bf16 has no reference: the oracle's bf16 restatement is the target."""
+    meta, arrays = hook_cases
+    nshapes = len(meta["shapes"])
+    for case in meta["cases"]:
+        if case["precision"] != "half" or case["name"].startswith("nonfinite"):
+            continue
+        c = dict(case)
+        outs, scales, results, _ = _device_case(c, arrays, nshapes, "bf16", math_mode)
+        # oracle replay in bf16
+        p, g = case_arrays(arrays, case["name"], nshapes)
+        params = [O.round_to(x, "bf16") for x in p[0]]
+        sc = case["scaler"]
+        scaler = O.LossScaler(case["init_scale"], sc["growth_interval"], sc["min_scale"],
+                              sc["max_scale"]) if sc else None
+        clip = case["clip"]
+        max_norm = clip["max_norm"] if clip and clip["kind"] == "by_global_norm" else None
+        thresh = clip["threshold"] if clip and clip["kind"] == "by_value" else None
+        for k in range(case["steps"]):
+            if scaler is not None or max_norm is not None:
+                params, out, _, _ = O.two_pass_step(params, g[k], case["lr"], "bf16", scaler,
+                                                    max_norm, thresh)
+                out = {"applied": "applied", "skipped": "skipped_overflow",
+                       "underflow": "underflow"}[out]
+            else:
+                params = [O.value_clip_update(pp, O.round_to(gg, "bf16"), case["lr"], thresh,
+                                              "bf16") for pp, gg in zip(params, g[k])]
+                out = "applied"
+            assert outs[k] == out, (case["name"], k)
+            for i in range(nshapes):
+                d = U.ulp_diff(results[k][i], U.to_dev(params[i], torch.bfloat16)).max().item()
+                assert d <= (0 if math_mode == "f64" and max_norm is None else 1), \
+                    (case["name"], k, i, d)

@@ -1,0 +1,258 @@
+"""End-to-end parity of the LOMO optimizer (autograd hooks -> C-ABI -> K1/K2/K3)
+on config 1 (the reference's mini transformer), against fixtures recorded from
+the reference itself (tests/golden/c1.*), plus the protocol invariants of
+fusedtrain's tests (test_optim.py, test_stabilize.py, test_acceptance.py).
+
+Tolerances (stated): fp32 storage -- per-step loss rel 1e-5 and final
+parameters normwise-relative 1e-5 (north star "fp32 rel 1e-5"); fp64
+storage + f64 math -- loss rel 1e-10, parameters abs 1e-12; fp16 -- every
+overflow-skip / clip decision and the loss-scale trajectory identical, the
+element error reported as max/mean ulp and bounded below.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2306_09782_b200 import (LOMO, ClipMode, LossScaler, NonFiniteLossError, Stabilizer,
+                                   StepOutcome, TapeStateError)
+from paper_2306_09782_b200.workloads import (MiniConfig, MiniTransformer, mean_cross_entropy,
+                                             sequence_copy_batch)
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    torch.cuda.set_device(0)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+
+
+C1 = MiniConfig(layers=2, hidden=256, heads=4, vocab=1024, seed=0)
+
+
+def _tokens(step):
+    return torch.from_numpy(sequence_copy_batch(0, step, 4, 128, 1024)).cuda()
+
+
+def _run_c1(dtype, opt_kwargs, steps=10, math_mode="f32"):
+    model = MiniTransformer(C1, dtype=dtype, device="cuda")
+    opt = LOMO(model, lr=0.05, math=math_mode, **opt_kwargs)
+    losses, outcomes, scales = [], [], []
+    for step in range(steps):
+        ids = _tokens(step)
+        loss = opt.step(lambda: mean_cross_entropy(model(ids), ids), 0.05)
+        losses.append(loss)
+        outcomes.append(opt.last_outcome.value if opt.last_outcome else "applied")
+        scales.append(opt.loss_scale)
+    return model, opt, losses, outcomes, scales
+
+
+def _sampled(model, c1_arrays, key):
+    out = {}
+    for name, p in model.named_reference_parameters():
+        idx = torch.from_numpy(c1_arrays[f"{key}/{name}/idx"]).cuda()
+        out[name] = (p.detach().reshape(-1)[idx].double().cpu().numpy(),
+                     c1_arrays[f"{key}/{name}/val"])
+    return out
+
+
+def test_c1_fixture_A_fp32(c1_meta, c1_arrays):
+    model, opt, losses, _, _ = _run_c1(torch.float32, {})
+    want = c1_meta["A"]["losses"]
+    for got, ref in zip(losses, want):
+        assert abs(got - ref) <= 1e-5 * abs(ref), (got, ref)
+    worst = 0.0
+    for name, (got, ref) in _sampled(model, c1_arrays, "A").items():
+        rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        worst = max(worst, rel)
+        assert rel <= 1e-5, (name, rel)
+    print(f"fixture A fp32: worst normwise rel {worst:.2e}, "
+          f"max |dloss|/loss {max(abs(a - b) / b for a, b in zip(losses, want)):.2e}")
+
+
+def test_c1_fixture_A_fp64_f64_math(c1_meta, c1_arrays):
+    model, _, losses, _, _ = _run_c1(torch.float64, {}, math_mode="f64")
+    for got, ref in zip(losses, c1_meta["A"]["losses"]):
+        assert abs(got - ref) <= 1e-10 * abs(ref), (got, ref)
+    worst = 0.0
+    for name, (got, ref) in _sampled(model, c1_arrays, "A").items():
+        worst = max(worst, float(np.max(np.abs(got - ref))))
+    assert worst <= 1e-12, worst
+    print(f"fixture A fp64: max abs param error {worst:.2e}")
+
+
+def _ulps16(got, ref):
+    g = got.astype(np.float16).view(np.int16).astype(np.int64)
+    r = ref.astype(np.float16).view(np.int16).astype(np.int64)
+    g = np.where(g < 0, -(1 << 15) - g, g)
+    r = np.where(r < 0, -(1 << 15) - r, r)
+    return np.abs(g - r)
+
+
+@pytest.mark.parametrize("key,scaler", [("B", LossScaler(2.0 ** 16, 2)),
+                                        ("C", LossScaler(2.0 ** 24, 2, max_scale=2.0 ** 24))])
+@pytest.mark.parametrize("math_mode", ["f32", "f64"])
+def test_c1_fixture_fp16_two_pass(c1_meta, c1_arrays, key, scaler, math_mode):
+    stab = Stabilizer(ClipMode.by_global_norm(1.0), scaler)
+    model, opt, losses, outcomes, scales = _run_c1(torch.float16, {"stabilizer": stab},
+                                                   math_mode=math_mode)
+    ref = c1_meta[key]
+    assert outcomes == ref["outcomes"]                        # skip decisions: exact
+    assert [math.log2(s) for s in scales] == ref["log2_scale"]  # scaler trajectory: exact
+    u = np.concatenate([_ulps16(g, r) for g, r in _sampled(model, c1_arrays, key).values()])
+    rel = max(abs(a - b) / abs(b) for a, b in zip(losses, ref["losses"]) if math.isfinite(b))
+    print(f"fixture {key} fp16 ({math_mode} math): max ulp {u.max()}, mean ulp {u.mean():.4f}, "
+          f">2ulp fraction {(u > 2).mean():.2e}, max loss rel {rel:.2e}")
+    assert rel < 5e-3
+    assert u.mean() < 0.25 and u.max() <= 64
+
+
+def test_lomo_equals_sgd_bit_exact_fp64():
+    """test_optim.py:59-71 / criterion 1: fused update == materialise-then-SGD."""
+    torch.use_deterministic_algorithms(True, warn_only=True)
+    try:
+        cfg = MiniConfig(layers=2, hidden=64, heads=4, vocab=128, seed=3)
+        fused = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+        plain = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+        opt = LOMO(fused, lr=0.05, math="f64")
+        for step in range(10):
+            ids = torch.from_numpy(sequence_copy_batch(4, step, 4, 16, 128)).cuda()
+            lf = opt.step(lambda: mean_cross_entropy(fused(ids), ids), 0.05)
+            lp = mean_cross_entropy(plain(ids), ids)
+            lp.backward()
+            with torch.no_grad():
+                for p in plain.parameters():
+                    p.copy_(p - 0.05 * p.grad)  # two roundings, like optim.py:54
+                    p.grad = None
+            assert lf == lp.item()
+        for a, b in zip(fused.parameters(), plain.parameters()):
+            assert torch.equal(a, b)
+    finally:
+        torch.use_deterministic_algorithms(False)
+
+
+def test_two_pass_with_huge_max_norm_equals_plain_step():
+    """test_stabilize.py:85-91."""
+    cfg = MiniConfig(layers=1, hidden=64, heads=2, vocab=128, seed=1)
+    a = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+    b = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+    oa = LOMO(a, lr=0.05, clip_grad_norm=1e9, math="f64")
+    ob = LOMO(b, lr=0.05, math="f64")
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 2, 16, 128)).cuda()
+    oa.step(lambda: mean_cross_entropy(a(ids), ids), 0.05)
+    ob.step(lambda: mean_cross_entropy(b(ids), ids), 0.05)
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)
+
+
+def test_gradient_peak_is_one_tensor():
+    """test_optim.py:74-91: never two parameter gradients alive at once."""
+    cfg = MiniConfig(layers=2, hidden=128, heads=4, vocab=512, seed=0)
+    model = MiniTransformer(cfg, dtype=torch.float16, device="cuda")
+    params = list(model.parameters())
+    alive = []
+
+    def checker(p):
+        alive.append(sum(q.grad is not None for q in params))
+    for p in params:
+        p.register_post_accumulate_grad_hook(checker)   # runs before LOMO's hook
+    opt = LOMO(model, lr=0.05)
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 2, 32, 512)).cuda()
+    opt.step(lambda: mean_cross_entropy(model(ids), ids), 0.05)
+    assert alive and max(alive) == 1 and len(alive) == len(params)
+    assert all(p.grad is None for p in params)
+    assert opt.state_nbytes() == 0
+
+
+def test_gradient_memory_peak_vs_retained_grads():
+    cfg = MiniConfig(layers=4, hidden=512, heads=8, vocab=8192, seed=0)
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 1, 8, 8192)).cuda()
+    sizes = []
+
+    def peak_delta(use_lomo):
+        model = MiniTransformer(cfg, dtype=torch.float16, device="cuda")
+        sizes[:] = [p.numel() * 2 for p in model.parameters()]
+        opt = LOMO(model, lr=0.05) if use_lomo else None
+        loss = mean_cross_entropy(model(ids), ids)
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        if use_lomo:
+            opt.fused_backward(loss, 0.05)
+        else:
+            loss.backward()
+        torch.cuda.synchronize()
+        return torch.cuda.max_memory_allocated() - base
+    lomo, sgd = peak_delta(True), peak_delta(False)
+    total, largest = sum(sizes), max(sizes)
+    print(f"peak grad-phase delta: LOMO {lomo / 2**20:.1f} MiB, retained {sgd / 2**20:.1f} MiB, "
+          f"largest tensor {largest / 2**20:.1f} MiB, all grads {total / 2**20:.1f} MiB")
+    assert sgd >= total
+    assert lomo <= sgd - (total - largest) + (4 << 20)
+
+
+def test_non_finite_loss_aborts_without_touching_params():
+    """test_optim.py:162-170."""
+    cfg = MiniConfig(layers=1, hidden=64, heads=2, vocab=128, seed=0)
+    model = MiniTransformer(cfg, dtype=torch.float32, device="cuda")
+    before = [p.detach().clone() for p in model.parameters()]
+    opt = LOMO(model, lr=0.05)
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 2, 8, 128)).cuda()
+    with pytest.raises(NonFiniteLossError):
+        opt.step(lambda: mean_cross_entropy(model(ids), ids) * float("inf"), 0.05)
+    for a, b in zip(before, model.parameters()):
+        assert torch.equal(a, b)
+    # the optimizer keeps working afterwards
+    opt.step(lambda: mean_cross_entropy(model(ids), ids), 0.05)
+    assert not all(torch.equal(a, b) for a, b in zip(before, model.parameters()))
+
+
+def test_overflow_skip_leaves_params_byte_identical_and_halves_scale():
+    """test_stabilize.py:233-240 / criterion 6."""
+    cfg = MiniConfig(layers=1, hidden=64, heads=2, vocab=128, seed=0)
+    model = MiniTransformer(cfg, dtype=torch.float16, device="cuda")
+    before = [p.detach().clone() for p in model.parameters()]
+    opt = LOMO(model, lr=0.05, stabilizer=Stabilizer(
+        ClipMode.none(), LossScaler(2.0 ** 24, max_scale=2.0 ** 24)))
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 2, 8, 128)).cuda()
+    opt.step(lambda: mean_cross_entropy(model(ids), ids) * 1e4, 0.05)
+    assert opt.last_outcome is StepOutcome.SKIPPED_OVERFLOW
+    assert opt.loss_scale == 2.0 ** 23
+    for a, b in zip(before, model.parameters()):
+        assert torch.equal(a, b)
+
+
+def test_fused_backward_requires_grad_norm_in_two_pass_mode():
+    cfg = MiniConfig(layers=1, hidden=32, heads=2, vocab=64, seed=0)
+    model = MiniTransformer(cfg, dtype=torch.float32, device="cuda")
+    opt = LOMO(model, lr=0.05, clip_grad_norm=1.0)
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 2, 8, 64)).cuda()
+    loss = mean_cross_entropy(model(ids), ids)
+    with pytest.raises(TapeStateError):
+        opt.fused_backward(loss, 0.05)
+    norm = opt.grad_norm(loss)
+    assert norm is not None and norm > 0
+    opt.fused_backward(loss, 0.05)
+    assert opt.last_outcome is StepOutcome.APPLIED
+
+
+def test_recompute_forward_equals_retained_graph():
+    cfg = MiniConfig(layers=1, hidden=64, heads=2, vocab=128, seed=2)
+    a = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+    b = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+    stab = lambda: Stabilizer(ClipMode.by_global_norm(0.05), LossScaler(2.0 ** 8, 2))
+    oa = LOMO(a, lr=0.05, stabilizer=stab(), math="f64")
+    ob = LOMO(b, lr=0.05, stabilizer=stab(), math="f64")
+    for step in range(3):
+        ids = torch.from_numpy(sequence_copy_batch(1, step, 2, 16, 128)).cuda()
+        la = oa.step(lambda: mean_cross_entropy(a(ids), ids), 0.05)
+        lb = ob.step(lambda: mean_cross_entropy(b(ids), ids), 0.05, recompute_forward=True)
+        assert la == lb
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)

@@ -1,0 +1,102 @@
+"""Host-side logic on CPU: configuration mirrors, the C1 restatement's init and
+tokens against the reference's recorded digests, hook delivery order."""
+import hashlib
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2306_09782_b200 import ClipMode, ConfigError, LossScaler, Stabilizer
+from paper_2306_09782_b200.workloads import (MiniConfig, MiniTransformer, llama_param_count,
+                                             llama_param_shapes, mean_cross_entropy,
+                                             mini_transformer_init, round_half_np,
+                                             sequence_copy_batch)
+
+
+# --- stabilize.py validation mirror (test_stabilize.py:57-61,153-155,190-194) ----
+
+def test_clip_threshold_must_be_positive():
+    with pytest.raises(ConfigError):
+        ClipMode.by_value(0.0)
+    with pytest.raises(ConfigError):
+        ClipMode.by_value(-1.0)
+    with pytest.raises(ConfigError):
+        ClipMode.by_global_norm(0.0)
+
+
+def test_scale_must_be_power_of_two():
+    with pytest.raises(ConfigError):
+        LossScaler(scale=1000.0)
+    with pytest.raises(ConfigError):
+        LossScaler(scale=2.0 ** 30, max_scale=2.0 ** 24)
+    with pytest.raises(ConfigError):
+        LossScaler(growth_interval=0)
+
+
+def test_grouped_does_not_combine_with_scaler():
+    with pytest.raises(ConfigError):
+        Stabilizer(ClipMode.by_group_norm(1.0, 1), LossScaler())
+
+
+def test_pass_counts():
+    assert Stabilizer(ClipMode.by_value(0.5)).backward_passes_per_step == 1
+    assert Stabilizer(ClipMode.by_global_norm(1.0)).backward_passes_per_step == 2
+    assert Stabilizer(ClipMode.none(), LossScaler()).backward_passes_per_step == 2
+    assert Stabilizer(ClipMode.by_global_norm(1.0), LossScaler()).backward_passes_per_step == 2
+
+
+# --- C1 restatement pinned to the reference run ---------------------------------
+
+def _digest(named):
+    h = hashlib.sha256()  # zoo.py:124-129
+    for name, arr in named:
+        h.update(name.encode())
+        h.update(np.ascontiguousarray(arr, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+def test_c1_init_matches_reference_digest(c1_meta):
+    init = mini_transformer_init(MiniConfig())
+    assert _digest(init) == c1_meta["A"]["init_digest"]
+    assert _digest([(n, round_half_np(a)) for n, a in init]) == c1_meta["B"]["init_digest"]
+    assert [n for n, _ in init] == c1_meta["A"]["names"]
+
+
+def test_c1_tokens_match_reference(c1_meta):
+    ids = sequence_copy_batch(0, 0, 4, 128, 1024)
+    assert hashlib.sha256(np.ascontiguousarray(ids).tobytes()).hexdigest() == \
+        c1_meta["tokens_step0_sha256"]
+
+
+def test_slot_order_is_reference_delivery_order(c1_meta):
+    """LOMO slots = reverse registration order == the reference tape's delivery
+    order (tape.py:350-360), so the norm sums in the reference's order."""
+    names = [n for n, _ in mini_transformer_init(MiniConfig())]
+    assert list(reversed(names)) == c1_meta["delivery_order"]
+
+
+def test_c1_first_loss_on_cpu_fp64(c1_meta):
+    model = MiniTransformer(MiniConfig(), dtype=torch.float64, device="cpu")
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 4, 128, 1024))
+    loss = mean_cross_entropy(model(ids), ids).item()
+    assert abs(loss - c1_meta["A"]["losses"][0]) < 1e-12
+
+
+def test_torch_hooks_fire_once_per_parameter_on_cpu():
+    model = MiniTransformer(MiniConfig(layers=1, hidden=32, heads=2, vocab=64), torch.float64,
+                            "cpu")
+    fired = []
+    for name, p in model.named_reference_parameters():
+        p.register_post_accumulate_grad_hook(lambda t, n=name: fired.append(n))
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 2, 8, 64))
+    mean_cross_entropy(model(ids), ids).backward()
+    assert sorted(fired) == sorted(n for n, _ in model.named_reference_parameters())
+    assert len(fired) == len(set(fired))
+
+
+def test_llama_shapes():
+    assert llama_param_count("7b") == 6_738_415_616   # test_estimate.py:18-21
+    assert len(llama_param_shapes("7b")) == 291
+    assert llama_param_count("13b") == 13_015_864_320
+    assert llama_param_count("65b") == 65_285_660_672

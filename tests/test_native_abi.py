@@ -1,0 +1,83 @@
+"""The C-ABI library loads on a CPU-only host and exports exactly what
+include/lomo_b200.h declares (no compute calls without a GPU)."""
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from conftest import ROOT
+from paper_2306_09782_b200 import _lib
+
+HEADER = ROOT / "include" / "lomo_b200.h"
+
+
+def _declared():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t)\s+(lomo_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declarations_match_binding():
+    assert _declared() == sorted(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (lomo_\w+)", out))
+    assert set(_declared()) <= exported
+
+
+def test_abi_version_and_state_size():
+    lib = _lib.load()
+    assert lib.lomo_abi_version() == _lib.ABI_VERSION
+    for n in (0, 1, 291, 5000):
+        assert lib.lomo_state_bytes(n) == _lib.state_bytes(n)
+
+
+def test_argument_errors_need_no_gpu():
+    lib = _lib.load()
+    assert lib.lomo_fused_update(None, None, -1, 1, 0, 0.1, 0.0, 0.0, 0, None, None) == -1
+    assert lib.lomo_fused_update(None, None, 0, 1, 0, 0.1, 0.0, 0.0, 0, None, None) == 0
+    assert lib.lomo_fused_update(None, None, 5, 1, 0, 0.1, 0.0, 0.0, 0, None, None) == -1
+    # state-dependent flags without a state
+    assert lib.lomo_fused_update(1, 1, 5, 1, 0, 0.1, 0.0, 0.0, _lib.USE_SKIP, None, None) == -1
+    assert lib.lomo_probe(None, 10, 1, 0, 0, None, None) == -1
+    assert lib.lomo_probe(None, 10, 1, -1, 0, 1, None) == -2
+    assert lib.lomo_finalize_norm(None, None) == -1
+    assert lib.lomo_state_init(None, 1, 1.0, 1, 1.0, 1.0, 0.0, None) == -1
+    assert lib.lomo_finalize_norm_ranks(1, None, 2, None) == -1
+
+
+def test_status_struct_layout_matches_c(tmp_path):
+    """offsetof() of every lomo_state field, compiled from the header by gcc."""
+    fields = [f for f, _ in _lib.LomoStatus._fields_]
+    src = tmp_path / "off.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "lomo_b200.h"\n'
+                   "int main(void){\n" +
+                   "".join(f'printf("{f} %zu\\n", offsetof(lomo_state, {f}));\n' for f in fields) +
+                   'printf("sizeof %zu\\n", sizeof(lomo_state));\nreturn 0;}\n')
+    exe = tmp_path / "off"
+    subprocess.run(["gcc", f"-I{ROOT / 'include'}", str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True,
+                                                       text=True).stdout.splitlines())
+    for f in fields:
+        assert int(got[f]) == getattr(_lib.LomoStatus, f).offset, f
+    assert int(got["sizeof"]) == ctypes.sizeof(_lib.LomoStatus) == 128
+
+
+def test_product_path_has_no_cpu_fallback():
+    import torch
+    from paper_2306_09782_b200 import LOMO, ConfigError
+    m = torch.nn.Linear(4, 4)
+    with pytest.raises(ConfigError):
+        LOMO(m, lr=0.1)  # CPU parameters: refused, never silently updated on the host
+
+
+def test_package_does_not_import_the_oracle():
+    for p in (ROOT / "paper_2306_09782_b200").rglob("*.py"):
+        assert "lomo_oracle" not in p.read_text(), p
