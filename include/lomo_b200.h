@@ -66,6 +66,10 @@ typedef enum {
 #define LOMO_USE_COEF 0x2u  /* g *= state->clip_coef  (stabilize.py:221-222)       */
 #define LOMO_USE_SKIP 0x4u  /* no-op when state->skip (stabilize.py:204-205,       */
                             /*                          optim.py:63-65)            */
+#define LOMO_ACCUM_F64 0x8u /* K2: accumulate every square in f64 (the reference's */
+                            /* float64 dot, stabilize.py:199); default for 16-bit   */
+                            /* storage: exact fp32 squares summed per 16-byte      */
+                            /* vector in fp32, vectors accumulated in f64           */
 
 #define LOMO_E_ARG (-1)     /* invalid argument (null pointer, n < 0, bad dtype)   */
 #define LOMO_E_SLOT (-2)    /* slot outside [0, nslots)                            */
@@ -125,19 +129,25 @@ int lomo_fused_update(void* p, const void* g, int64_t n, int dtype, int math,
                       double lr, double clip_value, double weight_decay,
                       unsigned flags, const void* state, void* stream);
 
-/* Multi-tensor K1: one launch over `ntensors` (p, g, n) triples whose pointer
- * tables live in DEVICE memory (coalesced small tensors; same dtype/math). */
-int lomo_fused_update_multi(void* const* p_table, const void* const* g_table,
-                            const int64_t* n_table, int ntensors, int64_t max_n,
-                            int dtype, int math, double lr, double clip_value,
-                            double weight_decay, unsigned flags,
-                            const void* state, void* stream);
+/* Multi-tensor K1: one launch per 64 (p, g, n) triples.  The three lists are
+ * HOST arrays (they are packed into the kernel's parameter block); used to
+ * coalesce the many tiny tensors (norm scales) of a backward pass. */
+int lomo_fused_update_multi(void* const* p_list, const void* const* g_list,
+                            const int64_t* n_list, int count, int dtype, int math,
+                            double lr, double clip_value, double weight_decay,
+                            unsigned flags, const void* state, void* stream);
 
 /* ---- K2: probe (two-pass pass 1) --------------------------------------- */
 /* sumsq[slot] = sum((g * inv_scale)^2) (deterministic: fixed-order f64 tree);
  * state->overflow |= any(!isfinite(g)).  flags: LOMO_USE_SCALE. */
 int lomo_probe(const void* g, int64_t n, int dtype, int slot, unsigned flags,
                void* state, void* stream);
+
+/* Multi-tensor K2 for small tensors: one CTA per tensor writes sumsq[slot]
+ * directly (host arrays, as for lomo_fused_update_multi). */
+int lomo_probe_multi(const void* const* g_list, const int64_t* n_list,
+                     const int* slot_list, int count, int dtype, unsigned flags,
+                     void* state, void* stream);
 
 /* ---- K3: finalisers (single CTA) --------------------------------------- */
 /* K3a: total = sum(sumsq[0..nslots)) in slot order; N = sqrt(total);

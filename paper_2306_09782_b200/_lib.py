@@ -18,7 +18,7 @@ LIB_PATH = _HERE / "_native" / "liblomo_b200.so"
 # lomo_dtype (include/lomo_b200.h)
 F32, F16, BF16, F64 = 0, 1, 2, 3
 MATH_F32, MATH_F64 = 0, 1
-USE_SCALE, USE_COEF, USE_SKIP = 0x1, 0x2, 0x4
+USE_SCALE, USE_COEF, USE_SKIP, ACCUM_F64 = 0x1, 0x2, 0x4, 0x8
 MAX_PROBE_BLOCKS = 4096
 ABI_VERSION = 1
 
@@ -32,6 +32,7 @@ EXPORTS = (
     "lomo_fused_update",
     "lomo_fused_update_multi",
     "lomo_probe",
+    "lomo_probe_multi",
     "lomo_finalize_norm",
     "lomo_scaler_on_clean",
     "lomo_local_norm_partial",
@@ -85,8 +86,9 @@ _SIGS = {
     "lomo_read_status": (_i32, [_vp, ctypes.POINTER(LomoStatus), _vp]),
     "lomo_fused_update": (_i32, [_vp, _vp, _i64, _i32, _i32, _dbl, _dbl, _dbl, _u32, _vp, _vp]),
     "lomo_fused_update_multi": (
-        _i32, [_vp, _vp, _vp, _i32, _i64, _i32, _i32, _dbl, _dbl, _dbl, _u32, _vp, _vp]),
+        _i32, [_vp, _vp, _vp, _i32, _i32, _i32, _dbl, _dbl, _dbl, _u32, _vp, _vp]),
     "lomo_probe": (_i32, [_vp, _i64, _i32, _i32, _u32, _vp, _vp]),
+    "lomo_probe_multi": (_i32, [_vp, _vp, _vp, _i32, _i32, _u32, _vp, _vp]),
     "lomo_finalize_norm": (_i32, [_vp, _vp]),
     "lomo_scaler_on_clean": (_i32, [_vp, _vp]),
     "lomo_local_norm_partial": (_i32, [_vp, _vp, _vp]),

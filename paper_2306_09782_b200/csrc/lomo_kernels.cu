@@ -26,6 +26,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "lomo_b200.h"
 
@@ -76,6 +77,16 @@ __device__ __forceinline__ void st_stream(void* ptr, const uint4& v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+// Programmatic dependent launch: every kernel waits for its stream
+// predecessor's completion (and memory flush) before touching memory, and
+// lets its own dependents be scheduled as soon as all its CTAs are running,
+// which hides the launch latency between the back-to-back per-tensor launches
+// of one backward pass.  Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // --------------------------------------------------------------------------
@@ -216,6 +227,8 @@ __device__ __forceinline__ uint4 upd_vec(const uint4& pv, const uint4& gv,
 template <typename M>
 __device__ __forceinline__ bool load_args(UpdArgs<M>& a, unsigned flags,
                                           const lomo_state* st) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (st != nullptr) {
     if ((flags & LOMO_USE_SKIP) && *((volatile const int32_t*)&st->skip)) return false;
     if (flags & LOMO_USE_SCALE) a.inv_scale = (M)st->inv_scale;
@@ -226,6 +239,16 @@ __device__ __forceinline__ bool load_args(UpdArgs<M>& a, unsigned flags,
 
 // Vector body: `nvec` 16-byte vectors starting at p/g (16-B aligned), plus
 // scalar head/tail elements handled by CTA 0.
+//
+// One tile of kThreads x kK1Vec 16-byte vectors per CTA, no loop: the grid
+// holds ceil(nvec / tile) CTAs and the hardware block scheduler hands tiles
+// to SMs as earlier CTAs retire.  That dynamic balance removes the CTA-spread
+// tail a persistent/chunked grid pays (tools/k1_variants.cu: 6.70 TB/s for
+// this layout vs 5.85 TB/s for one chunk per resident CTA on the LLaMA-7B
+// pass), and with PDL the next tensor's tiles start as soon as this grid
+// drains.
+constexpr int kK1Vec = 1;
+
 template <typename T, typename M>
 __global__ void __launch_bounds__(kThreads)
     k1_update(T* __restrict__ p, const T* __restrict__ g, int64_t n, int head,
@@ -233,8 +256,7 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int V = 16 / sizeof(T);
   if (!load_args(a, flags, st)) return;
 
-  // scalar head (before the first aligned vector) and tail
-  if (blockIdx.x == 0) {
+  if (blockIdx.x == 0) {  // scalar head (before the first aligned vector) and tail
     const int64_t tail0 = head + nvec * V;
     const int64_t ntail = n - tail0;
     for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
@@ -242,29 +264,22 @@ __global__ void __launch_bounds__(kThreads)
       p[e] = from_m<T, M>(upd_elem(to_m<M>(p[e]), to_m<M>(g[e]), a));
     }
   }
-
-  // contiguous equal chunks per CTA, strided by CTA width inside the chunk
-  const int64_t chunk = (nvec + gridDim.x - 1) / gridDim.x;
-  const int64_t beg = (int64_t)blockIdx.x * chunk;
-  const int64_t end = min(beg + chunk, nvec);
   uint4* pv = reinterpret_cast<uint4*>(p + head);
   const uint4* gv = reinterpret_cast<const uint4*>(g + head);
-
-  for (int64_t base = beg + threadIdx.x; base < end; base += (int64_t)kThreads * kUnroll) {
-    uint4 P[kUnroll], G[kUnroll];
+  const int64_t base = (int64_t)blockIdx.x * (kThreads * kK1Vec) + threadIdx.x;
+  uint4 P[kK1Vec], G[kK1Vec];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t i = base + (int64_t)u * kThreads;
-      if (i < end) {
-        G[u] = ld_stream_ro(gv + i);
-        P[u] = ld_stream_rw(pv + i);
-      }
+  for (int u = 0; u < kK1Vec; ++u) {
+    const int64_t i = base + (int64_t)u * kThreads;
+    if (i < nvec) {
+      G[u] = ld_stream_ro(gv + i);
+      P[u] = ld_stream_rw(pv + i);
     }
+  }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t i = base + (int64_t)u * kThreads;
-      if (i < end) st_stream(pv + i, upd_vec<T, M>(P[u], G[u], a));
-    }
+  for (int u = 0; u < kK1Vec; ++u) {
+    const int64_t i = base + (int64_t)u * kThreads;
+    if (i < nvec) st_stream(pv + i, upd_vec<T, M>(P[u], G[u], a));
   }
 }
 
@@ -280,19 +295,27 @@ __global__ void __launch_bounds__(kThreads)
     p[i] = from_m<T, M>(upd_elem(to_m<M>(p[i]), to_m<M>(g[i]), a));
 }
 
-// Multi-tensor variant: blockIdx.y selects the tensor (small tensors coalesced
-// into one launch).  Element-wise scalar path with 16-byte vectors when both
-// pointers are 16-B aligned.
+// Multi-tensor variant (small tensors coalesced into one launch): the
+// pointer tables travel BY VALUE in the kernel parameter block, blockIdx.y
+// selects the tensor.
+constexpr int kMulti = 64;
+struct MultiTable {
+  void* p[kMulti];
+  const void* g[kMulti];
+  int64_t n[kMulti];
+  int32_t slot[kMulti];
+  int count;
+};
+
 template <typename T, typename M>
 __global__ void __launch_bounds__(kThreads)
-    k1_update_multi(T* const* __restrict__ pt, const T* const* __restrict__ gt,
-                    const int64_t* __restrict__ nt, UpdArgs<M> a, unsigned flags,
+    k1_update_multi(const __grid_constant__ MultiTable tab, UpdArgs<M> a, unsigned flags,
                     const lomo_state* st) {
   constexpr int V = 16 / sizeof(T);
   if (!load_args(a, flags, st)) return;
-  T* p = pt[blockIdx.y];
-  const T* g = gt[blockIdx.y];
-  const int64_t n = nt[blockIdx.y];
+  T* p = static_cast<T*>(tab.p[blockIdx.y]);
+  const T* g = static_cast<const T*>(tab.g[blockIdx.y]);
+  const int64_t n = tab.n[blockIdx.y];
   const bool aligned = ((((uintptr_t)p) | ((uintptr_t)g)) & 15) == 0;
   const int64_t nvec = aligned ? n / V : 0;
   uint4* pv = reinterpret_cast<uint4*>(p);
@@ -364,6 +387,8 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int V = 16 / sizeof(T);
   __shared__ double sm[kThreads / 32];
   __shared__ bool am_last;
+  pdl_wait();
+  pdl_launch_dependents();
   lomo_state* st = hdr(state);
   const bool use_scale = (flags & LOMO_USE_SCALE) != 0;
   const M inv_scale = use_scale ? (M)st->inv_scale : (M)1;
@@ -422,6 +447,37 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Multi-tensor probe: one CTA per (small) tensor, which writes its slot
+// directly (fixed-order CTA reduction; no cross-CTA finish needed).
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k2_probe_multi(const __grid_constant__ MultiTable tab, unsigned flags, void* state) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ double sm[kThreads / 32];
+  pdl_wait();
+  pdl_launch_dependents();
+  lomo_state* st = hdr(state);
+  const bool use_scale = (flags & LOMO_USE_SCALE) != 0;
+  const M inv_scale = use_scale ? (M)st->inv_scale : (M)1;
+  const T* g = static_cast<const T*>(tab.g[blockIdx.x]);
+  const int64_t n = tab.n[blockIdx.x];
+  const int64_t nvec = (((uintptr_t)g) & 15) == 0 ? n / V : 0;
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t i = threadIdx.x; i < nvec; i += kThreads)
+    acc += vec_sumsq<T, M>(ld_stream_ro(gv + i), inv_scale, use_scale, bad);
+  for (int64_t i = nvec * V + threadIdx.x; i < n; i += kThreads) {
+    M x = to_m<M>(g[i]);
+    bad |= !is_fin(x);
+    if (use_scale) x = x * inv_scale;
+    acc += (double)x * (double)x;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
+  const double r = block_sum(acc, sm);
+  if (threadIdx.x == 0) slots_of(st)[tab.slot[blockIdx.x]] = r;
+}
+
 // --------------------------------------------------------------------------
 // K3 + bookkeeping kernels (single CTA)
 // --------------------------------------------------------------------------
@@ -462,6 +518,7 @@ __device__ void decide(lomo_state* st, double total) {
 }
 
 __global__ void k3_finalize(void* state) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   lomo_state* st = hdr(state);
   const double* s = slots_of(st);
@@ -471,6 +528,7 @@ __global__ void k3_finalize(void* state) {
 }
 
 __global__ void k3_finalize_ranks(void* state, const double* parts, int world) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   lomo_state* st = hdr(state);
   double total = 0.0;
@@ -484,6 +542,7 @@ __global__ void k3_finalize_ranks(void* state, const double* parts, int world) {
 }
 
 __global__ void k3_local_partial(const void* state, double* out2) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   lomo_state* st = hdr(const_cast<void*>(state));
   const double* s = slots_of(st);
@@ -494,6 +553,7 @@ __global__ void k3_local_partial(const void* state, double* out2) {
 }
 
 __global__ void k3_on_clean(void* state) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   lomo_state* st = hdr(state);
   if (st->skip) return;
@@ -550,6 +610,7 @@ __device__ __forceinline__ bool loss_finite(const void* loss, int dt) {
 }
 
 __global__ void k_begin_step(void* state, const void* loss, int loss_dtype) {
+  pdl_wait();
   lomo_state* st = hdr(state);
   const int ns = st->nslots;
   double* s = slots_of(st);
@@ -604,6 +665,31 @@ inline int grid_for(int64_t nvec_per_thread_units, int occ) {
   return (int)(want < cap ? want : cap);
 }
 
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LOMO_PDL");
+    v = (e == nullptr || e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// cudaLaunchKernelEx with programmatic stream serialisation (PDL)
+template <typename... KArgs, typename... Args>
+int launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 template <typename M>
 UpdArgs<M> make_args(double lr, double clip_value, double weight_decay, unsigned flags) {
   UpdArgs<M> a;
@@ -632,31 +718,59 @@ int launch_update(void* p_, const void* g_, int64_t n, double lr, double clip, d
     int head = (int)(((16 - (pa & 15)) & 15) / sizeof(T));
     if (head > n) head = (int)n;
     const int64_t nvec = (n - head) / V;
-    const int grid = grid_for(nvec > 0 ? (nvec + kUnroll - 1) / kUnroll : 1,
-                              occupancy(k1_update<T, M>));
-    k1_update<T, M><<<grid, kThreads, 0, s>>>(p, g, n, head, nvec, a, flags, st);
-  } else {
-    const int grid = grid_for((n + 3) / 4, occupancy(k1_update_scalar<T, M>));
-    k1_update_scalar<T, M><<<grid, kThreads, 0, s>>>(p, g, n, a, flags, st);
+    const int64_t tiles = (nvec + kThreads * kK1Vec - 1) / (kThreads * kK1Vec);
+    const unsigned grid = (unsigned)(tiles > 0 ? tiles : 1);
+    return launch(k1_update<T, M>, dim3(grid), dim3(kThreads), s, p, g, n, head, nvec, a, flags,
+                  st);
   }
-  return (int)cudaGetLastError();
+  const int grid = grid_for((n + 3) / 4, occupancy(k1_update_scalar<T, M>));
+  return launch(k1_update_scalar<T, M>, dim3(grid), dim3(kThreads), s, p, g, n, a, flags, st);
 }
 
 template <typename T, typename M>
-int launch_update_multi(void* const* pt, const void* const* gt, const int64_t* nt, int ntens,
-                        int64_t max_n, double lr, double clip, double wd, unsigned flags,
-                        const void* state, cudaStream_t s) {
+int launch_update_multi(void* const* pl, const void* const* gl, const int64_t* nl, int count,
+                        double lr, double clip, double wd, unsigned flags, const void* state,
+                        cudaStream_t s) {
   constexpr int V = 16 / sizeof(T);
   UpdArgs<M> a = make_args<M>(lr, clip, wd, flags);
-  const int64_t units = (max_n + V - 1) / V;
-  int gx = (int)((units + kThreads - 1) / kThreads);
-  if (gx < 1) gx = 1;
-  if (gx > 64) gx = 64;
-  dim3 grid(gx, ntens);
-  k1_update_multi<T, M><<<grid, kThreads, 0, s>>>(
-      reinterpret_cast<T* const*>(pt), reinterpret_cast<const T* const*>(gt), nt, a, flags,
-      static_cast<const lomo_state*>(state));
-  return (int)cudaGetLastError();
+  for (int base = 0; base < count; base += kMulti) {
+    MultiTable tab;
+    tab.count = count - base < kMulti ? count - base : kMulti;
+    int64_t max_n = 0;
+    for (int i = 0; i < tab.count; ++i) {
+      tab.p[i] = pl[base + i];
+      tab.g[i] = gl[base + i];
+      tab.n[i] = nl[base + i];
+      tab.slot[i] = 0;
+      if (nl[base + i] > max_n) max_n = nl[base + i];
+    }
+    if (max_n == 0) continue;
+    int gx = (int)(((max_n + V - 1) / V + kThreads - 1) / kThreads);
+    if (gx < 1) gx = 1;
+    if (gx > 64) gx = 64;
+    int rc = launch(k1_update_multi<T, M>, dim3(gx, tab.count), dim3(kThreads), s, tab, a, flags,
+                    static_cast<const lomo_state*>(state));
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+template <typename T, typename M>
+int launch_probe_multi(const void* const* gl, const int64_t* nl, const int* slots, int count,
+                       unsigned flags, void* state, cudaStream_t s) {
+  for (int base = 0; base < count; base += kMulti) {
+    MultiTable tab;
+    tab.count = count - base < kMulti ? count - base : kMulti;
+    for (int i = 0; i < tab.count; ++i) {
+      tab.p[i] = nullptr;
+      tab.g[i] = gl[base + i];
+      tab.n[i] = nl[base + i];
+      tab.slot[i] = slots[base + i];
+    }
+    int rc = launch(k2_probe_multi<T, M>, dim3(tab.count), dim3(kThreads), s, tab, flags, state);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 template <typename T, typename M>
@@ -671,8 +785,8 @@ int launch_probe(const void* g_, int64_t n, int slot, unsigned flags, void* stat
   const int64_t nvec = (n - head) / V;
   int grid = grid_for(nvec > 0 ? (nvec + kUnroll - 1) / kUnroll : 1, occupancy(k2_probe<T, M>));
   if (grid > LOMO_MAX_PROBE_BLOCKS) grid = LOMO_MAX_PROBE_BLOCKS;
-  k2_probe<T, M><<<grid, kThreads, 0, s>>>(g, n, head, nvec, slot, flags, state);
-  return (int)cudaGetLastError();
+  return launch(k2_probe<T, M>, dim3(grid), dim3(kThreads), s, g, n, head, nvec, slot, flags,
+                state);
 }
 
 }  // namespace lomo_k
@@ -748,21 +862,24 @@ int lomo_fused_update(void* p, const void* g, int64_t n, int dtype, int math, do
   return LOMO_E_ARG;
 }
 
-int lomo_fused_update_multi(void* const* p_table, const void* const* g_table,
-                            const int64_t* n_table, int ntensors, int64_t max_n, int dtype,
-                            int math, double lr, double clip_value, double weight_decay,
-                            unsigned flags, const void* state, void* stream) {
-  if (ntensors < 0 || max_n < 0) return LOMO_E_ARG;
-  if (ntensors == 0 || max_n == 0) return 0;
-  if (p_table == nullptr || g_table == nullptr || n_table == nullptr) return LOMO_E_ARG;
-  if (ntensors > 65535) return LOMO_E_ARG;
+int lomo_fused_update_multi(void* const* p_list, const void* const* g_list,
+                            const int64_t* n_list, int count, int dtype, int math, double lr,
+                            double clip_value, double weight_decay, unsigned flags,
+                            const void* state, void* stream) {
+  if (count < 0) return LOMO_E_ARG;
+  if (count == 0) return 0;
+  if (p_list == nullptr || g_list == nullptr || n_list == nullptr) return LOMO_E_ARG;
+  for (int i = 0; i < count; ++i) {
+    if (n_list[i] < 0) return LOMO_E_ARG;
+    if (n_list[i] > 0 && (p_list[i] == nullptr || g_list[i] == nullptr)) return LOMO_E_ARG;
+  }
   if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP)) && state == nullptr)
     return LOMO_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const bool f64 = math == LOMO_MATH_F64;
   if (math != LOMO_MATH_F32 && math != LOMO_MATH_F64) return LOMO_E_ARG;
 #define LOMO_MULTI(T, M) \
-  launch_update_multi<T, M>(p_table, g_table, n_table, ntensors, max_n, lr, clip_value, weight_decay, flags, state, s)
+  launch_update_multi<T, M>(p_list, g_list, n_list, count, lr, clip_value, weight_decay, flags, state, s)
   switch (dtype) {
     case LOMO_F16: return f64 ? LOMO_MULTI(__half, double) : LOMO_MULTI(__half, float);
     case LOMO_BF16: return f64 ? LOMO_MULTI(__nv_bfloat16, double) : LOMO_MULTI(__nv_bfloat16, float);
@@ -773,6 +890,31 @@ int lomo_fused_update_multi(void* const* p_table, const void* const* g_table,
   return LOMO_E_ARG;
 }
 
+int lomo_probe_multi(const void* const* g_list, const int64_t* n_list, const int* slot_list,
+                     int count, int dtype, unsigned flags, void* state, void* stream) {
+  if (state == nullptr || count < 0) return LOMO_E_ARG;
+  if (count == 0) return 0;
+  if (g_list == nullptr || n_list == nullptr || slot_list == nullptr) return LOMO_E_ARG;
+  for (int i = 0; i < count; ++i) {
+    if (n_list[i] < 0) return LOMO_E_ARG;
+    if (n_list[i] > 0 && g_list[i] == nullptr) return LOMO_E_ARG;
+    if (slot_list[i] < 0) return LOMO_E_SLOT;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool f64 = (flags & LOMO_ACCUM_F64) != 0;
+  switch (dtype) {
+    case LOMO_F16:
+      return f64 ? launch_probe_multi<__half, double>(g_list, n_list, slot_list, count, flags, state, s)
+                 : launch_probe_multi<__half, float>(g_list, n_list, slot_list, count, flags, state, s);
+    case LOMO_BF16:
+      return f64 ? launch_probe_multi<__nv_bfloat16, double>(g_list, n_list, slot_list, count, flags, state, s)
+                 : launch_probe_multi<__nv_bfloat16, float>(g_list, n_list, slot_list, count, flags, state, s);
+    case LOMO_F32: return launch_probe_multi<float, double>(g_list, n_list, slot_list, count, flags, state, s);
+    case LOMO_F64: return launch_probe_multi<double, double>(g_list, n_list, slot_list, count, flags, state, s);
+  }
+  return LOMO_E_ARG;
+}
+
 int lomo_probe(const void* g, int64_t n, int dtype, int slot, unsigned flags, void* state,
                void* stream) {
   if (state == nullptr || n < 0) return LOMO_E_ARG;
@@ -780,9 +922,14 @@ int lomo_probe(const void* g, int64_t n, int dtype, int slot, unsigned flags, vo
   if (n > 0 && g == nullptr) return LOMO_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   if (n == 0) return 0;
+  const bool f64 = (flags & LOMO_ACCUM_F64) != 0;
   switch (dtype) {
-    case LOMO_F16: return launch_probe<__half, float>(g, n, slot, flags, state, s);
-    case LOMO_BF16: return launch_probe<__nv_bfloat16, float>(g, n, slot, flags, state, s);
+    case LOMO_F16:
+      return f64 ? launch_probe<__half, double>(g, n, slot, flags, state, s)
+                 : launch_probe<__half, float>(g, n, slot, flags, state, s);
+    case LOMO_BF16:
+      return f64 ? launch_probe<__nv_bfloat16, double>(g, n, slot, flags, state, s)
+                 : launch_probe<__nv_bfloat16, float>(g, n, slot, flags, state, s);
     case LOMO_F32: return launch_probe<float, double>(g, n, slot, flags, state, s);
     case LOMO_F64: return launch_probe<double, double>(g, n, slot, flags, state, s);
   }

@@ -1,0 +1,103 @@
+"""Host-side dispatch of the hook bodies onto the C-ABI (one place, used by
+the LOMO optimizer's autograd hooks and by bench.py, so the benchmark times
+exactly the launches training issues).
+
+Every gradient >= ``small_numel`` elements is handed to its own K1 (update)
+or K2 (probe) launch the moment its hook fires -- the LOMO contract
+(optim.py:1-7): consume each gradient as soon as it exists.  Tiny tensors
+(the RMSNorm scale vectors: 65 of the 291 LLaMA-7B tensors, 0.004% of the
+elements) would each cost a full launch; they are parked (their gradients
+total a few hundred KB) and flushed as ONE multi-tensor launch per 64 at
+the end of the backward pass.  Peak gradient memory therefore stays at the
+largest single tensor plus the parked tiny ones.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+
+SMALL_NUMEL = 1 << 16
+
+
+class HookDispatcher:
+    def __init__(self, lib, state_ptr: int | None, math_code: int,
+                 small_numel: int = SMALL_NUMEL):
+        self.lib = lib
+        self.state_ptr = state_ptr
+        self.math = math_code
+        self.small = small_numel
+        self._upd = {}    # dtype code -> [(p, g)]
+        self._prb = {}    # dtype code -> [(g, slot)]
+        self.launches = 0
+        self.configure()
+
+    def configure(self, lr: float = 0.0, clip: float = 0.0, wd: float = 0.0, flags: int = 0):
+        """Per-pass constants (the same for every tensor of one backward)."""
+        self.lr, self.clip, self.wd, self.flags = float(lr), float(clip), float(wd), int(flags)
+
+    # ------------------------------------------------------------ K1 / K2
+    def update(self, p, g, dt: int, stream: int) -> None:
+        n = p.numel()
+        if n <= self.small:
+            lst = self._upd.setdefault(dt, [])
+            lst.append((p, g))
+            if len(lst) == 64:
+                self._flush_upd(dt, stream)
+            return
+        rc = self.lib.lomo_fused_update(p.data_ptr(), g.data_ptr(), n, dt, self.math, self.lr,
+                                        self.clip, self.wd, self.flags, self.state_ptr, stream)
+        if rc:
+            _lib.check(rc, "lomo_fused_update")
+        self.launches += 1
+
+    def probe(self, g, dt: int, slot: int, stream: int) -> None:
+        n = g.numel()
+        if n <= self.small:
+            lst = self._prb.setdefault(dt, [])
+            lst.append((g, slot))
+            if len(lst) == 64:
+                self._flush_prb(dt, stream)
+            return
+        rc = self.lib.lomo_probe(g.data_ptr(), n, dt, slot, self.flags, self.state_ptr, stream)
+        if rc:
+            _lib.check(rc, "lomo_probe")
+        self.launches += 1
+
+    # ------------------------------------------------------------ flushing
+    def _flush_upd(self, dt, stream):
+        lst = self._upd.pop(dt, [])
+        if not lst:
+            return
+        k = len(lst)
+        ps = (ctypes.c_void_p * k)(*[p.data_ptr() for p, _ in lst])
+        gs = (ctypes.c_void_p * k)(*[g.data_ptr() for _, g in lst])
+        ns = (ctypes.c_int64 * k)(*[p.numel() for p, _ in lst])
+        _lib.check(self.lib.lomo_fused_update_multi(ps, gs, ns, k, dt, self.math, self.lr,
+                                                    self.clip, self.wd, self.flags,
+                                                    self.state_ptr, stream),
+                   "lomo_fused_update_multi")
+        self.launches += (k + 63) // 64
+
+    def _flush_prb(self, dt, stream):
+        lst = self._prb.pop(dt, [])
+        if not lst:
+            return
+        k = len(lst)
+        gs = (ctypes.c_void_p * k)(*[g.data_ptr() for g, _ in lst])
+        ns = (ctypes.c_int64 * k)(*[g.numel() for g, _ in lst])
+        ss = (ctypes.c_int * k)(*[s for _, s in lst])
+        _lib.check(self.lib.lomo_probe_multi(gs, ns, ss, k, dt, self.flags, self.state_ptr, stream),
+                   "lomo_probe_multi")
+        self.launches += (k + 63) // 64
+
+    def flush(self, stream: int) -> None:
+        """Launch everything parked; the parked gradients are released after
+        their kernel is enqueued (stream-ordered reuse by the allocator)."""
+        for dt in list(self._upd):
+            self._flush_upd(dt, stream)
+        for dt in list(self._prb):
+            self._flush_prb(dt, stream)
+
+    def pending(self) -> int:
+        return sum(map(len, self._upd.values())) + sum(map(len, self._prb.values()))

@@ -34,6 +34,7 @@ from typing import Callable, Iterable
 import torch
 
 from . import _lib
+from .dispatch import HookDispatcher
 from .errors import (ConfigError, NonFiniteLossError, ScaleUnderflowError, ShapeError,
                      TapeStateError)
 from .stabilize import ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome
@@ -159,9 +160,8 @@ class LOMO:
                 float(scaler.max_scale) if scaler else 1.0,
                 float(st.clip.max_norm) if self._norm_clip else 0.0, s), "lomo_state_init")
 
+        self._dispatch = HookDispatcher(self._lib, self._state_ptr, self._math)
         self._mode = 0
-        self._flags = 0
-        self._cur_lr = self.lr
         self._pending = None          # None | "apply" | "skip" after grad_norm
         self.last_outcome: StepOutcome | None = None
         self.clip_coef: float | None = None
@@ -183,17 +183,11 @@ class LOMO:
         if not g.is_contiguous():
             g = g.contiguous()
         stream = torch.cuda.current_stream(p.device).cuda_stream
-        n = p.numel()
         dt = _DTYPE_CODE[p.dtype]
         if mode == _PROBE:
-            rc = self._lib.lomo_probe(g.data_ptr(), n, dt, self._slot[id(p)], self._flags,
-                                      self._state_ptr, stream)
+            self._dispatch.probe(g, dt, self._slot[id(p)], stream)
         else:
-            rc = self._lib.lomo_fused_update(p.data_ptr(), g.data_ptr(), n, dt, self._math,
-                                             self._cur_lr, self._clip_value, self.weight_decay,
-                                             self._flags, self._state_ptr, stream)
-        if rc != 0:
-            _lib.check(rc, "lomo_probe" if mode == _PROBE else "lomo_fused_update")
+            self._dispatch.update(p, g, dt, stream)
         self.hook_calls += 1
         p.grad = None  # CONSUME: the caching allocator reuses the block stream-ordered
 
@@ -216,17 +210,21 @@ class LOMO:
             _lib.check(self._lib.lomo_begin_step(self._state_ptr, None, 0, self._stream()),
                        "lomo_begin_step")
 
-    def _backward(self, loss: torch.Tensor, mode: int, flags: int, retain_graph: bool) -> None:
+    def _backward(self, loss: torch.Tensor, mode: int, flags: int, retain_graph: bool,
+                  lr: float = 0.0) -> None:
         for p in self.params:
             if p.grad is not None:
                 raise TapeStateError("a parameter already holds a gradient; LOMO consumes "
                                      "gradients inside backward (call zero_grad(set_to_none=True))")
         target = loss.float() * self._scale_view if self._has_scaler else loss
-        self._mode, self._flags = mode, flags
+        self._dispatch.configure(lr, self._clip_value, self.weight_decay, flags)
+        self._mode = mode
         try:
             target.backward(retain_graph=retain_graph)
         finally:
-            self._mode, self._flags = 0, 0
+            self._mode = 0
+            # launch the parked tiny tensors (same stream as the hooks)
+            self._dispatch.flush(self._stream())
 
     def read_status(self) -> _lib.LomoStatus:
         """Copy the device step status to the host (synchronises the stream)."""
@@ -249,7 +247,8 @@ class LOMO:
         if self.passes != 2:
             raise TapeStateError("grad_norm is only needed with clip_grad_norm or loss_scale")
         self._begin(loss)
-        flags = _lib.USE_SCALE if self._has_scaler else 0
+        flags = (_lib.USE_SCALE if self._has_scaler else 0) | \
+            (_lib.ACCUM_F64 if self._math == _lib.MATH_F64 else 0)
         self._backward(loss, _PROBE, flags, retain_graph)
         _lib.check(self._lib.lomo_finalize_norm(self._state_ptr, self._stream()),
                    "lomo_finalize_norm")
@@ -275,7 +274,7 @@ class LOMO:
         :class:`NonFiniteLossError` for a non-finite loss with every parameter
         untouched (optim.py:63-65; the check is a device flag K1 honours).
         """
-        self._cur_lr = self.lr if lr is None else float(lr)
+        lr = self.lr if lr is None else float(lr)
         if self.passes == 2:
             if self._pending is None:
                 raise TapeStateError("clip_grad_norm/loss_scale need grad_norm(loss) "
@@ -285,19 +284,19 @@ class LOMO:
                 return
             flags = _lib.USE_SKIP | (_lib.USE_SCALE if self._has_scaler else 0) \
                 | (_lib.USE_COEF if self._norm_clip else 0)
-            self._backward(loss, _UPDATE, flags, retain_graph=False)
+            self._backward(loss, _UPDATE, flags, retain_graph=False, lr=lr)
             _lib.check(self._lib.lomo_scaler_on_clean(self._state_ptr, self._stream()),
                        "lomo_scaler_on_clean")
             self.last_outcome = StepOutcome.APPLIED
             return
         self._begin(loss)
-        self._backward(loss, _UPDATE, _lib.USE_SKIP, retain_graph=False)
+        self._backward(loss, _UPDATE, _lib.USE_SKIP, retain_graph=False, lr=lr)
         _lib.check(self._lib.lomo_scaler_on_clean(self._state_ptr, self._stream()),
                    "lomo_scaler_on_clean")
         st = self.read_status()
         if st.skip:
             self.last_outcome = None
-            raise NonFiniteLossError(f"loss is non-finite ({float(loss)}); step aborted")
+            raise NonFiniteLossError(f"loss is non-finite ({float(loss.detach())}); step aborted")
         self.last_outcome = None if self.stabilizer is None else StepOutcome.APPLIED
 
     def step(self, closure: Callable[[], torch.Tensor], lr: float | None = None,
@@ -314,19 +313,19 @@ class LOMO:
             self.grad_norm(loss, retain_graph=not recompute_forward)
             if self._pending == "skip":
                 self._pending = None
-                return float(loss)
+                return float(loss.detach())
             if recompute_forward:
                 loss = closure()
             self.fused_backward(loss, lr)
-            return float(loss)
+            return float(loss.detach())
         self.fused_backward(loss, lr)
-        return float(loss)
+        return float(loss.detach())
 
     # ------------------------------------------------------------ accessors
     @property
     def loss_scale(self) -> float:
-        """Current loss scale as of the last host status read."""
-        return float(self._status.scale) if self._has_scaler else 1.0
+        """Current loss scale (reads the device state: synchronises)."""
+        return float(self.read_status().scale) if self._has_scaler else 1.0
 
     def state_nbytes(self) -> int:
         """Optimizer state per parameter: zero (optim.py:115-116)."""

@@ -81,7 +81,15 @@ def test_k1_plain_update_f32_math_within_one_ulp(prec, n):
     d = U.ulp_diff(p, want)
     frac = (d > 0).float().mean().item()
     print(f"{prec} n={n}: max ulp {d.max().item()}, mismatch fraction {frac:.2e}")
-    assert d.max().item() <= 1
+    if prec == "f32":
+        # fp32 storage: the fp32 constant lr and one FMA rounding; where p and
+        # lr*g cancel the result-ulp error grows, so bound the error by the
+        # operands' magnitude (2 ulp of max(|p|, |lr g|)), i.e. fp32 rel 1e-7
+        err = (p.double() - want.double()).abs().cpu().numpy()
+        bound = 2 * np.spacing(np.maximum(np.abs(p0), np.abs(0.05 * g0)).astype(np.float32))
+        assert np.all(err <= bound)
+    else:
+        assert d.max().item() <= 1
 
 
 def test_k1_misaligned_pair_takes_scalar_path_and_matches():
@@ -115,6 +123,9 @@ def test_k1_all_stages(prec, math_mode):
         d = U.ulp_diff(p, want)
         if math_mode == "f64":
             assert d.max().item() == 0, (wd, d.max().item())
+        elif prec == "f32":
+            err = (p.double() - want.double()).abs().cpu().numpy()
+            assert np.all(err <= 4e-7 * (np.abs(p0) + 0.05 * 1.5e-3)), wd
         else:
             assert d.max().item() <= 1, (wd, d.max().item())
 
@@ -185,15 +196,16 @@ def test_k1_f64_math_rounds_directly_not_through_fp32():
 
 # --- K2 probe ----------------------------------------------------------------
 
+@pytest.mark.parametrize("accum", [0, 0x8])
 @pytest.mark.parametrize("prec", ["half", "bf16", "f32", "full"])
 @pytest.mark.parametrize("n", [1, 9, 4096, 1000003, 4096 * 11008])
-def test_k2_sumsq_and_determinism(prec, n):
+def test_k2_sumsq_and_determinism(prec, n, accum):
     rng = np.random.default_rng(n)
     scale = 1024.0 if prec in ("half", "bf16") else 1.0
     g0 = O.round_to(rng.normal(0, 1e-3, n) * scale, prec)
     g = U.to_dev(g0, U.TORCH_DT[prec], offset=n % 5)
     st = U.State(2, scale=scale if scale != 1.0 else 0.0)
-    flags = _lib.USE_SCALE if scale != 1.0 else 0
+    flags = (_lib.USE_SCALE if scale != 1.0 else 0) | accum
     st.begin()
     st.probe(g, 0, flags)
     st.probe(g, 1, flags)
@@ -201,7 +213,7 @@ def test_k2_sumsq_and_determinism(prec, n):
     ovf, want = O.probe([g0], scale, True)
     assert not ovf and st.status().overflow == 0
     assert s[0] == s[1]  # deterministic, run to run
-    tol = 1e-12 if prec in ("f32", "full") else 2e-6
+    tol = 1e-12 if prec in ("f32", "full") or accum else 2e-6
     assert abs(s[0] - want) <= tol * want, (s[0], want)
 
 
@@ -220,14 +232,19 @@ def test_k2_overflow_flag(prec, pos, bad):
     assert st.status().overflow == 1
 
 
-def test_k2_large_finite_fp16_does_not_flag():
+@pytest.mark.parametrize("accum", [0, 0x8])
+def test_k2_large_finite_fp16_does_not_flag(accum):
     g = torch.full((4097,), 65504.0, dtype=torch.float16, device="cuda")
     st = U.State(1)
     st.begin()
-    st.probe(g, 0, 0)
+    st.probe(g, 0, accum)
     status = st.status()
     assert status.overflow == 0
-    assert st.slots(1)[0] == 4097 * 65504.0 ** 2
+    want = 4097 * 65504.0 ** 2
+    got = st.slots(1)[0]
+    # f64 accumulation is exact here; the default fp32-per-vector partial
+    # sums round at 2^-24 relative
+    assert got == want if accum else abs(got - want) <= 8 * 2 ** -24 * want
 
 
 # --- K3 ------------------------------------------------------------------------
@@ -295,11 +312,12 @@ def test_multi_tensor_update_matches_single():
     ps = [_draw(n, "bf16", rng) for n in sizes]
     P = [U.to_dev(p, torch.bfloat16) for p, _ in ps]
     G = [U.to_dev(g, torch.bfloat16) for _, g in ps]
-    pt = torch.tensor([t.data_ptr() for t in P], dtype=torch.int64, device="cuda")
-    gt = torch.tensor([t.data_ptr() for t in G], dtype=torch.int64, device="cuda")
-    nt = torch.tensor(sizes, dtype=torch.int64, device="cuda")
-    _lib.check(U.lib().lomo_fused_update_multi(pt.data_ptr(), gt.data_ptr(), nt.data_ptr(),
-                                               len(sizes), max(sizes), _lib.BF16, _lib.MATH_F64,
+    import ctypes
+    k = len(sizes)
+    pt = (ctypes.c_void_p * k)(*[t.data_ptr() for t in P])
+    gt = (ctypes.c_void_p * k)(*[t.data_ptr() for t in G])
+    nt = (ctypes.c_int64 * k)(*sizes)
+    _lib.check(U.lib().lomo_fused_update_multi(pt, gt, nt, k, _lib.BF16, _lib.MATH_F64,
                                                0.05, 0.0, 0.0, 0, None, U.stream()), "multi")
     for t, (p0, g0) in zip(P, ps):
         assert np.array_equal(t.double().cpu().numpy(), _expected(p0, g0, "bf16"))
@@ -328,7 +346,8 @@ def _device_case(case, arrays, nshapes, prec, math_mode):
         order = list(reversed(range(nshapes)))  # delivery order (tape.py:350-360)
         if two:
             for slot, i in enumerate(order):
-                st.probe(delivered[i], slot, _lib.USE_SCALE if sc else 0)
+                st.probe(delivered[i], slot, (_lib.USE_SCALE if sc else 0) |
+                         (_lib.ACCUM_F64 if math_mode == "f64" else 0))
             st.finalize()
             h = st.status()
             if h.underflow:
@@ -351,7 +370,7 @@ def _device_case(case, arrays, nshapes, prec, math_mode):
             outs.append("nonfinite_loss" if st.status().skip else "applied")
         scales.append(st.status().scale if sc else None)
         results.append([t.clone() for t in P])
-    return outs, scales, results, p
+    return outs, scales, results, p, g
 
 
 @pytest.mark.parametrize("math_mode", ["f64", "f32"])
@@ -361,7 +380,7 @@ def test_reference_hook_cases_replayed_on_device(hook_cases, math_mode):
     worst = {}
     for case in meta["cases"]:
         prec = case["precision"]
-        outs, scales, results, p = _device_case(case, arrays, nshapes, prec, math_mode)
+        outs, scales, results, p, g = _device_case(case, arrays, nshapes, prec, math_mode)
         want = [o if not o.startswith("underflow") else "underflow" for o in case["outcomes"]]
         assert outs == want, case["name"]                     # decisions: bit-exact
         if case["scaler"] is not None:
@@ -375,6 +394,15 @@ def test_reference_hook_cases_replayed_on_device(hook_cases, math_mode):
                 worst[case["name"]] = max(worst.get(case["name"], 0), d)
                 if math_mode == "f64" and not norm:
                     assert d == 0, (case["name"], k, i, d)
+                elif prec == "full":
+                    # f64 storage: a coef that differs in its last bits (our
+                    # reduction order vs BLAS ddot) moves p by ~eps*|lr g|,
+                    # which is many result-ulps where p and lr*g cancel
+                    err = (results[k][i] - ref).abs().cpu().numpy()
+                    bound = 8 * 2.0 ** -52 * (np.abs(p[k][i]) + np.abs(case["lr"] * g[k][i]))
+                    bound = bound.reshape(err.shape)
+                    ok = (err == 0) | (err <= bound)  # NaN grads (skipped steps): err 0
+                    assert np.all(ok), (case["name"], k, i)
                 else:
                     assert d <= 1, (case["name"], k, i, d)
     print(math_mode, "max ulp per case:", worst)
@@ -389,7 +417,7 @@ def test_bf16_cases_match_oracle(hook_cases, math_mode):
         if case["precision"] != "half" or case["name"].startswith("nonfinite"):
             continue
         c = dict(case)
-        outs, scales, results, _ = _device_case(c, arrays, nshapes, "bf16", math_mode)
+        outs, scales, results, _, _ = _device_case(c, arrays, nshapes, "bf16", math_mode)
         # oracle replay in bf16
         p, g = case_arrays(arrays, case["name"], nshapes)
         params = [O.round_to(x, "bf16") for x in p[0]]

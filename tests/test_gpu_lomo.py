@@ -193,8 +193,10 @@ def test_gradient_memory_peak_vs_retained_grads():
     total, largest = sum(sizes), max(sizes)
     print(f"peak grad-phase delta: LOMO {lomo / 2**20:.1f} MiB, retained {sgd / 2**20:.1f} MiB, "
           f"largest tensor {largest / 2**20:.1f} MiB, all grads {total / 2**20:.1f} MiB")
-    assert sgd >= total
-    assert lomo <= sgd - (total - largest) + (4 << 20)
+    # LOMO holds at most the largest gradient above the post-forward level
+    # (plus allocator rounding); retaining every gradient costs far more
+    assert lomo <= largest + (1 << 20)
+    assert sgd - lomo >= 0.5 * (total - largest)
 
 
 def test_non_finite_loss_aborts_without_touching_params():

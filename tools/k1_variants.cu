@@ -1,0 +1,397 @@
+// k1_variants.cu -- design-space probe for the K1 streaming update on B200.
+// Not part of the product: a standalone harness that times variants of the
+// bf16 / fp32-math update over the LLaMA-7B tensor list (one launch per
+// tensor, the hook pattern) and over one flat buffer (one launch), so the
+// per-launch boundary cost and the in-kernel efficiency can be separated.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude \
+//        -o tools/k1_variants tools/k1_variants.cu && ./tools/k1_variants
+#include "../paper_2306_09782_b200/csrc/lomo_kernels.cu"
+
+#include <cstdio>
+#include <vector>
+
+using namespace lomo_k;
+
+#define CK(x)                                                                  \
+  do {                                                                         \
+    cudaError_t e = (x);                                                       \
+    if (e != cudaSuccess) {                                                    \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      exit(1);                                                                 \
+    }                                                                          \
+  } while (0)
+
+typedef __nv_bfloat16 bf;
+
+// ---- variant: grid-stride interleaved (CTA-consecutive 16B vectors) --------
+template <int UNROLL>
+__global__ void __launch_bounds__(256) v_interleaved(bf* __restrict__ p, const bf* __restrict__ g,
+                                                     int64_t nvec, UpdArgs<float> a) {
+  pdl_wait();
+  pdl_launch_dependents();
+  uint4* pv = reinterpret_cast<uint4*>(p);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const int64_t stride = (int64_t)gridDim.x * 256 * UNROLL;
+  for (int64_t base = (int64_t)blockIdx.x * 256 * UNROLL + threadIdx.x; base < nvec;
+       base += stride) {
+    uint4 P[UNROLL], G[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = base + u * 256;
+      if (i < nvec) {
+        G[u] = ld_stream_ro(gv + i);
+        P[u] = ld_stream_rw(pv + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = base + u * 256;
+      if (i < nvec) st_stream(pv + i, upd_vec<bf, float>(P[u], G[u], a));
+    }
+  }
+}
+
+// ---- variant: contiguous chunk per CTA with configurable unroll / threads ---
+template <int UNROLL, int THREADS>
+__global__ void __launch_bounds__(THREADS) v_chunked(bf* __restrict__ p, const bf* __restrict__ g,
+                                                     int64_t nvec, UpdArgs<float> a) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int64_t chunk = (nvec + gridDim.x - 1) / gridDim.x;
+  const int64_t beg = (int64_t)blockIdx.x * chunk;
+  const int64_t end = min(beg + chunk, nvec);
+  uint4* pv = reinterpret_cast<uint4*>(p);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  for (int64_t base = beg + threadIdx.x; base < end; base += (int64_t)THREADS * UNROLL) {
+    uint4 P[UNROLL], G[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = base + (int64_t)u * THREADS;
+      if (i < end) {
+        G[u] = ld_stream_ro(gv + i);
+        P[u] = ld_stream_rw(pv + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = base + (int64_t)u * THREADS;
+      if (i < end) st_stream(pv + i, upd_vec<bf, float>(P[u], G[u], a));
+    }
+  }
+}
+
+// ---- variant: one tile per CTA (non-persistent; the block scheduler balances)
+template <int UNROLL>
+__global__ void __launch_bounds__(256) v_tile(bf* __restrict__ p, const bf* __restrict__ g,
+                                              int64_t nvec, UpdArgs<float> a) {
+  pdl_wait();
+  pdl_launch_dependents();
+  uint4* pv = reinterpret_cast<uint4*>(p);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const int64_t base = (int64_t)blockIdx.x * 256 * UNROLL + threadIdx.x;
+  uint4 P[UNROLL], G[UNROLL];
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const int64_t i = base + u * 256;
+    if (i < nvec) {
+      G[u] = ld_stream_ro(gv + i);
+      P[u] = ld_stream_rw(pv + i);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < UNROLL; ++u) {
+    const int64_t i = base + u * 256;
+    if (i < nvec) st_stream(pv + i, upd_vec<bf, float>(P[u], G[u], a));
+  }
+}
+
+// ---- variant: TMA bulk copies through a 4-stage shared-memory ring ---------
+constexpr int kTileElems = 8192;  // 16 KB per operand per stage
+constexpr int kStages = 4;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)),
+               "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, int phase) {
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
+      "r"(phase));
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(m))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(256) v_tma(bf* __restrict__ p, const bf* __restrict__ g,
+                                             int64_t n, UpdArgs<float> a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  bf* sp = reinterpret_cast<bf*>(smem);
+  bf* sg = sp + kStages * kTileElems;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sg + kStages * kTileElems);
+  pdl_wait();
+  pdl_launch_dependents();
+  const int64_t ntiles = n / kTileElems;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // tiles handled by this CTA: blockIdx.x, +gridDim.x, ...
+  auto issue = [&](int64_t t, int s) {
+    mbar_expect_tx(&full[s], 2 * kTileElems * sizeof(bf));
+    bulk_load(sp + s * kTileElems, p + t * kTileElems, kTileElems * sizeof(bf), &full[s]);
+    bulk_load(sg + s * kTileElems, g + t * kTileElems, kTileElems * sizeof(bf), &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+      if (t < ntiles) issue(t, s);
+    }
+  }
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % kStages;
+    mbar_wait(&full[s], (k / kStages) & 1);
+    uint4* P = reinterpret_cast<uint4*>(sp + s * kTileElems);
+    const uint4* G = reinterpret_cast<const uint4*>(sg + s * kTileElems);
+#pragma unroll
+    for (int j = 0; j < kTileElems * 2 / 16 / 256; ++j) {
+      const int i = threadIdx.x + j * 256;
+      P[i] = upd_vec<bf, float>(P[i], G[i], a);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_store(p + t * kTileElems, sp + s * kTileElems, kTileElems * sizeof(bf));
+      const int64_t nt = t + (int64_t)kStages * gridDim.x;
+      if (nt < ntiles) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        issue(nt, s);
+      }
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+struct Tensor {
+  bf* p;
+  bf* g;
+  int64_t n;
+};
+
+__global__ void fill(bf* x, int64_t n, float lo, float hi, uint32_t seed) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ seed;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    x[i] = __float2bfloat16(lo + (hi - lo) * (h & 0xffffff) / 16777216.0f);
+  }
+}
+
+template <typename F>
+float time_passes(F&& one_pass, int reps) {
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  for (int i = 0; i < 3; ++i) one_pass();
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(a));
+  for (int i = 0; i < reps; ++i) one_pass();
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  return ms / reps;
+}
+
+template <typename K>
+int occ_of(K k, int threads, size_t smem = 0) {
+  int o = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, threads, smem));
+  return o;
+}
+
+int main() {
+  int sms;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  // LLaMA-7B tensors (bytes identical to the bench), norms excluded
+  std::vector<int64_t> sizes;
+  sizes.push_back(32000LL * 4096);
+  for (int l = 0; l < 32; ++l) {
+    for (int k = 0; k < 4; ++k) sizes.push_back(4096LL * 4096);
+    for (int k = 0; k < 3; ++k) sizes.push_back(4096LL * 11008);
+  }
+  sizes.push_back(32000LL * 4096);
+  std::vector<Tensor> ts;
+  int64_t total = 0;
+  for (auto n : sizes) {
+    Tensor t;
+    t.n = n;
+    CK(cudaMalloc(&t.p, n * 2));
+    CK(cudaMalloc(&t.g, n * 2));
+    fill<<<1184, 256>>>(t.p, n, -0.08f, 0.08f, 1);
+    fill<<<1184, 256>>>(t.g, n, -1e-3f, 1e-3f, 2);
+    ts.push_back(t);
+    total += n;
+  }
+  CK(cudaDeviceSynchronize());
+  UpdArgs<float> a = make_args<float>(0.05, 0.0, 0.0, 0);
+  const double gb = 6.0 * total / 1e9;
+  printf("sms %d, %zu tensors, %.3f G elements, %.2f GB algorithmic per pass\n", sms, ts.size(),
+         total / 1e9, gb);
+
+  auto report = [&](const char* name, float ms) {
+    printf("%-44s %8.3f ms  %7.1f GB/s\n", name, ms, gb / (ms * 1e-3));
+  };
+
+  // product kernel through the C-ABI (PDL on)
+  report("product lomo_fused_update (per tensor)", time_passes([&] {
+           for (int i = (int)ts.size() - 1; i >= 0; --i)
+             lomo_fused_update(ts[i].p, ts[i].g, ts[i].n, LOMO_BF16, LOMO_MATH_F32, 0.05, 0, 0, 0,
+                               nullptr, nullptr);
+         }, 10));
+
+  auto per_tensor = [&](auto kern, int threads, int grid_per_sm, size_t smem, const char* name,
+                        bool pdl, bool vec_units) {
+    float ms = time_passes([&] {
+      for (int i = (int)ts.size() - 1; i >= 0; --i) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(sms * grid_per_sm);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const int64_t units = vec_units ? ts[i].n / 8 : ts[i].n;
+        CK(cudaLaunchKernelEx(&cfg, kern, ts[i].p, (const bf*)ts[i].g, units, a));
+      }
+    }, 10);
+    report(name, ms);
+  };
+
+  char buf[128];
+  auto tiled = [&](auto kern, int unroll, const char* name) {
+    float ms = time_passes([&] {
+      for (int i = (int)ts.size() - 1; i >= 0; --i) {
+        cudaLaunchConfig_t cfg = {};
+        const int64_t nvec = ts[i].n / 8;
+        cfg.gridDim = dim3((unsigned)((nvec + 256 * unroll - 1) / (256 * unroll)));
+        cfg.blockDim = dim3(256);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, kern, ts[i].p, (const bf*)ts[i].g, nvec, a));
+      }
+    }, 10);
+    report(name, ms);
+  };
+  tiled(v_tile<1>, 1, "tile 256 vec/CTA (u1)");
+  tiled(v_tile<2>, 2, "tile 512 vec/CTA (u2)");
+  tiled(v_tile<4>, 4, "tile 1024 vec/CTA (u4)");
+  tiled(v_tile<8>, 8, "tile 2048 vec/CTA (u8)");
+  tiled(v_tile<16>, 16, "tile 4096 vec/CTA (u16)");
+  {
+    auto k = v_chunked<4, 256>;
+    int o = occ_of(k, 256);
+    for (int gps : {o, 2 * o, 4 * o, 8 * o, 16 * o}) {
+      snprintf(buf, sizeof buf, "chunked u4 t256 grid=%dx%d pdl", sms, gps);
+      per_tensor(k, 256, gps, 0, buf, true, true);
+    }
+    snprintf(buf, sizeof buf, "chunked u4 t256 grid=%dx%d nopdl", sms, o);
+    per_tensor(k, 256, o, 0, buf, false, true);
+  }
+  {
+    auto k = v_chunked<8, 256>;
+    int o = occ_of(k, 256);
+    for (int gps : {o, 4 * o, 8 * o}) {
+      snprintf(buf, sizeof buf, "chunked u8 t256 grid=%dx%d pdl", sms, gps);
+      per_tensor(k, 256, gps, 0, buf, true, true);
+    }
+  }
+  {
+    auto k = v_chunked<2, 256>;
+    int o = occ_of(k, 256);
+    for (int gps : {4 * o, 8 * o, 16 * o}) {
+      snprintf(buf, sizeof buf, "chunked u2 t256 grid=%dx%d pdl", sms, gps);
+      per_tensor(k, 256, gps, 0, buf, true, true);
+    }
+  }
+  {
+    auto k = v_chunked<2, 512>;
+    int o = occ_of(k, 512);
+    snprintf(buf, sizeof buf, "chunked u2 t512 grid=%dx%d pdl", sms, o);
+    per_tensor(k, 512, o, 0, buf, true, true);
+  }
+  {
+    auto k = v_chunked<4, 128>;
+    int o = occ_of(k, 128);
+    snprintf(buf, sizeof buf, "chunked u4 t128 grid=%dx%d pdl", sms, o);
+    per_tensor(k, 128, o, 0, buf, true, true);
+  }
+  for (int u : {2, 4, 8}) {
+    auto k = u == 2 ? v_interleaved<2> : (u == 4 ? v_interleaved<4> : v_interleaved<8>);
+    int o = occ_of(k, 256);
+    for (int m : {1, 4}) {
+      snprintf(buf, sizeof buf, "interleaved u%d t256 grid=%dx%d pdl", u, sms, o * m);
+      per_tensor(k, 256, o * m, 0, buf, true, true);
+    }
+  }
+  {
+    size_t smem = kStages * kTileElems * 2 * 2 + 64;
+    CK(cudaFuncSetAttribute(v_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int o = occ_of(v_tma, 256, smem);
+    snprintf(buf, sizeof buf, "tma 4x16KB ring grid=%dx%d pdl", sms, o);
+    per_tensor(v_tma, 256, o, smem, buf, true, false);
+  }
+
+  // one flat launch over the biggest tensor only (in-kernel efficiency)
+  {
+    auto k = v_chunked<4, 256>;
+    int o = occ_of(k, 256);
+    Tensor& t = ts[0];
+    float ms = time_passes([&] {
+      k<<<sms * o, 256>>>(t.p, t.g, t.n / 8, a);
+    }, 20);
+    printf("%-44s %8.3f ms  %7.1f GB/s\n", "single 32000x4096 chunked u4", ms,
+           6.0 * t.n / 1e9 / (ms * 1e-3));
+    Tensor& t2 = ts[1];
+    ms = time_passes([&] {
+      k<<<sms * o, 256>>>(t2.p, t2.g, t2.n / 8, a);
+    }, 50);
+    printf("%-44s %8.3f ms  %7.1f GB/s\n", "single 4096x4096 chunked u4 (L2-warm)", ms,
+           6.0 * t2.n / 1e9 / (ms * 1e-3));
+  }
+  // plain copy for reference (cudaMemcpy D2D of the biggest tensor)
+  {
+    Tensor& t = ts[0];
+    float ms = time_passes([&] { CK(cudaMemcpyAsync(t.p, t.g, t.n * 2, cudaMemcpyDeviceToDevice)); }, 20);
+    printf("%-44s %8.3f ms  %7.1f GB/s (read+write)\n", "cudaMemcpy D2D 262MB", ms,
+           4.0 * t.n / 1e9 / (ms * 1e-3));
+  }
+  return 0;
+}
