@@ -97,10 +97,14 @@ typedef struct lomo_state {
   int32_t has_scaler;    /* 100                                                      */
   float scale_f32;       /* 104: scale as fp32 (exact: power of two), for loss*scale */
   int32_t reserved[5];   /* 108..127                                                 */
-  /* followed by: double sumsq[nslots]; double scratch[LOMO_MAX_PROBE_BLOCKS]; */
+  /* followed by: double  sumsq[nslots];                      (per-slot totals)
+   *              int32_t nblocks[nslots], padded to 8 bytes;  (K2 CTAs per slot)
+   *              double  partials[nslots][LOMO_PROBE_BLOCKS_PER_SLOT];
+   * K2 writes one partial per CTA (no atomics); K3a reduces each row in CTA
+   * order, then the slots in slot order: deterministic. */
 } lomo_state;
 
-#define LOMO_MAX_PROBE_BLOCKS 4096
+#define LOMO_PROBE_BLOCKS_PER_SLOT 4096
 
 /* 128-byte host snapshot of the state header (lomo_read_status). */
 typedef lomo_state lomo_status;

@@ -19,7 +19,7 @@ LIB_PATH = _HERE / "_native" / "liblomo_b200.so"
 F32, F16, BF16, F64 = 0, 1, 2, 3
 MATH_F32, MATH_F64 = 0, 1
 USE_SCALE, USE_COEF, USE_SKIP, ACCUM_F64 = 0x1, 0x2, 0x4, 0x8
-MAX_PROBE_BLOCKS = 4096
+PROBE_BLOCKS_PER_SLOT = 4096
 ABI_VERSION = 1
 
 # every symbol the header declares (checked by tests/test_native_abi.py)
@@ -128,4 +128,5 @@ def check(rc: int, what: str) -> None:
 
 def state_bytes(nslots: int) -> int:
     # pure arithmetic restated so it works without loading (must equal the C side)
-    return STATE_HEADER_BYTES + 8 * (int(nslots) + MAX_PROBE_BLOCKS)
+    n = int(nslots)
+    return STATE_HEADER_BYTES + 8 * (n + (n + 1) // 2 + n * PROBE_BLOCKS_PER_SLOT)

@@ -26,6 +26,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stddef.h>
 #include <stdlib.h>
 
 #include "lomo_b200.h"
@@ -332,11 +333,20 @@ __global__ void __launch_bounds__(kThreads)
 // K2: probe -- deterministic sum of squares + non-finite flag
 // --------------------------------------------------------------------------
 __device__ __forceinline__ lomo_state* hdr(void* s) { return reinterpret_cast<lomo_state*>(s); }
+// state block layout (include/lomo_b200.h): header | sumsq[nslots] |
+// nblocks[nslots] (int32, padded to 8 B) | partials[nslots][PER_SLOT]
+__host__ __device__ __forceinline__ size_t nblocks_words(int nslots) {
+  return (size_t)(nslots + 1) / 2;  // int32 pairs -> 8-byte words
+}
 __device__ __forceinline__ double* slots_of(lomo_state* s) {
   return reinterpret_cast<double*>(reinterpret_cast<char*>(s) + sizeof(lomo_state));
 }
-__device__ __forceinline__ double* scratch_of(lomo_state* s) {
-  return slots_of(s) + s->nslots;
+__device__ __forceinline__ int32_t* nblocks_of(lomo_state* s) {
+  return reinterpret_cast<int32_t*>(slots_of(s) + s->nslots);
+}
+__device__ __forceinline__ double* partials_of(lomo_state* s, int slot) {
+  return slots_of(s) + s->nslots + nblocks_words(s->nslots) +
+         (size_t)slot * LOMO_PROBE_BLOCKS_PER_SLOT;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -382,11 +392,10 @@ __device__ __forceinline__ double vec_sumsq(const uint4& gv, M inv_scale, bool u
 
 template <typename T, typename M>
 __global__ void __launch_bounds__(kThreads)
-    k2_probe(const T* __restrict__ g, int64_t n, int head, int64_t nvec, int slot,
-             unsigned flags, void* state) {
+    k2_probe(const T* __restrict__ g, int64_t n, int head, int64_t nvec, int64_t per_cta,
+             int slot, unsigned flags, void* state) {
   constexpr int V = 16 / sizeof(T);
   __shared__ double sm[kThreads / 32];
-  __shared__ bool am_last;
   pdl_wait();
   pdl_launch_dependents();
   lomo_state* st = hdr(state);
@@ -406,9 +415,10 @@ __global__ void __launch_bounds__(kThreads)
       acc += (double)x * (double)x;
     }
   }
-  const int64_t chunk = (nvec + gridDim.x - 1) / gridDim.x;
-  const int64_t beg = (int64_t)blockIdx.x * chunk;
-  const int64_t end = min(beg + chunk, nvec);
+  // small fixed tiles (>= 1024 vectors, <= LOMO_MAX_PROBE_BLOCKS CTAs): the
+  // block scheduler balances them across SMs like K1's tiles
+  const int64_t beg = (int64_t)blockIdx.x * per_cta;
+  const int64_t end = min(beg + per_cta, nvec);
   const uint4* gv = reinterpret_cast<const uint4*>(g + head);
   for (int64_t base = beg + threadIdx.x; base < end; base += (int64_t)kThreads * kUnroll) {
     uint4 G[kUnroll];
@@ -425,25 +435,12 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
 
+  // per-CTA partial into this slot's partial row; K3 reduces the row in CTA
+  // order (deterministic, no atomics on the hot path)
   const double bsum = block_sum(acc, sm);
-  double* scratch = scratch_of(st);
   if (threadIdx.x == 0) {
-    scratch[blockIdx.x] = bsum;
-    __threadfence();
-    const unsigned t = atomicAdd(&st->ticket, 1u);
-    am_last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
-  // last CTA: fixed-order reduction of the per-CTA partials
-  double r = 0.0;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += kThreads)
-    r += ((volatile double*)scratch)[i];
-  r = block_sum(r, sm);
-  if (threadIdx.x == 0) {
-    slots_of(st)[slot] = r;
-    st->ticket = 0;
+    partials_of(st, slot)[blockIdx.x] = bsum;
+    if (blockIdx.x == 0) nblocks_of(st)[slot] = (int32_t)gridDim.x;
   }
 }
 
@@ -475,7 +472,10 @@ __global__ void __launch_bounds__(kThreads)
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
   const double r = block_sum(acc, sm);
-  if (threadIdx.x == 0) slots_of(st)[tab.slot[blockIdx.x]] = r;
+  if (threadIdx.x == 0) {
+    slots_of(st)[tab.slot[blockIdx.x]] = r;
+    nblocks_of(st)[tab.slot[blockIdx.x]] = 0;  // reduced in place
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -517,14 +517,44 @@ __device__ void decide(lomo_state* st, double total) {
   }
 }
 
-__global__ void k3_finalize(void* state) {
+// K3a: CTA c reduces slots c, c+grid, ... (each slot's K2 partials in CTA
+// order); the
+// last CTA to finish (ticket) sums the slots in slot (= delivery) order and
+// either decides (mode 0: finalize) or exports {sum, overflow} (mode 1:
+// the sharded-mode local partial).
+__global__ void __launch_bounds__(kThreads) k3_reduce(void* state, int mode, double* out2) {
+  __shared__ double sm[kThreads / 32];
+  __shared__ bool am_last;
   pdl_wait();
-  if (threadIdx.x != 0) return;
   lomo_state* st = hdr(state);
-  const double* s = slots_of(st);
+  for (int s = blockIdx.x; s < st->nslots; s += gridDim.x) {  // CTA-uniform loop
+    const int nb = nblocks_of(st)[s];
+    if (nb > 0) {
+      const double* part = partials_of(st, s);
+      double r = 0.0;
+      for (int i = threadIdx.x; i < nb; i += kThreads) r += part[i];
+      r = block_sum(r, sm);
+      if (threadIdx.x == 0) slots_of(st)[s] = r;
+    }
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(&st->ticket, 1u);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last || threadIdx.x != 0) return;
+  __threadfence();
+  const volatile double* sq = slots_of(st);
   double total = 0.0;
-  for (int i = 0; i < st->nslots; ++i) total += s[i];  // delivery (slot) order
-  decide(st, total);
+  for (int i = 0; i < st->nslots; ++i) total += sq[i];  // delivery (slot) order
+  st->ticket = 0;
+  if (mode == 0) {
+    decide(st, total);
+  } else {
+    out2[0] = total;
+    out2[1] = st->overflow ? 1.0 : 0.0;
+  }
 }
 
 __global__ void k3_finalize_ranks(void* state, const double* parts, int world) {
@@ -539,17 +569,6 @@ __global__ void k3_finalize_ranks(void* state, const double* parts, int world) {
   }
   st->overflow = ovf;
   decide(st, total);
-}
-
-__global__ void k3_local_partial(const void* state, double* out2) {
-  pdl_wait();
-  if (threadIdx.x != 0) return;
-  lomo_state* st = hdr(const_cast<void*>(state));
-  const double* s = slots_of(st);
-  double total = 0.0;
-  for (int i = 0; i < st->nslots; ++i) total += s[i];
-  out2[0] = total;
-  out2[1] = st->overflow ? 1.0 : 0.0;
 }
 
 __global__ void k3_on_clean(void* state) {
@@ -596,7 +615,8 @@ __global__ void k_state_init(void* state, int nslots, double scale, int growth_i
     for (int i = 0; i < 5; ++i) st->reserved[i] = 0;
   }
   double* s = reinterpret_cast<double*>(reinterpret_cast<char*>(state) + sizeof(lomo_state));
-  for (int i = threadIdx.x; i < nslots + LOMO_MAX_PROBE_BLOCKS; i += blockDim.x) s[i] = 0.0;
+  const size_t words = (size_t)nslots + nblocks_words(nslots);  // partials need no init
+  for (size_t i = threadIdx.x; i < words; i += blockDim.x) s[i] = 0.0;
 }
 
 __device__ __forceinline__ bool loss_finite(const void* loss, int dt) {
@@ -614,7 +634,11 @@ __global__ void k_begin_step(void* state, const void* loss, int loss_dtype) {
   lomo_state* st = hdr(state);
   const int ns = st->nslots;
   double* s = slots_of(st);
-  for (int i = threadIdx.x; i < ns; i += blockDim.x) s[i] = 0.0;
+  int32_t* nb = nblocks_of(st);
+  for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+    s[i] = 0.0;
+    nb[i] = 0;
+  }
   if (threadIdx.x == 0) {
     st->overflow = 0;
     st->skip = 0;
@@ -783,10 +807,14 @@ int launch_probe(const void* g_, int64_t n, int slot, unsigned flags, void* stat
   int head = (int)(((16 - (ga & 15)) & 15) / sizeof(T));
   if (head > n) head = (int)n;
   const int64_t nvec = (n - head) / V;
-  int grid = grid_for(nvec > 0 ? (nvec + kUnroll - 1) / kUnroll : 1, occupancy(k2_probe<T, M>));
-  if (grid > LOMO_MAX_PROBE_BLOCKS) grid = LOMO_MAX_PROBE_BLOCKS;
-  return launch(k2_probe<T, M>, dim3(grid), dim3(kThreads), s, g, n, head, nvec, slot, flags,
-                state);
+  const int64_t tile = kThreads * kUnroll;
+  int64_t per_cta = (nvec + LOMO_PROBE_BLOCKS_PER_SLOT - 1) / LOMO_PROBE_BLOCKS_PER_SLOT;
+  per_cta = (per_cta + tile - 1) / tile * tile;
+  if (per_cta < tile) per_cta = tile;
+  int64_t grid = (nvec + per_cta - 1) / per_cta;
+  if (grid < 1) grid = 1;
+  return launch(k2_probe<T, M>, dim3((unsigned)grid), dim3(kThreads), s, g, n, head, nvec,
+                per_cta, slot, flags, state);
 }
 
 }  // namespace lomo_k
@@ -801,7 +829,9 @@ int lomo_abi_version(void) { return LOMO_ABI_VERSION; }
 
 size_t lomo_state_bytes(int nslots) {
   if (nslots < 0) nslots = 0;
-  return sizeof(lomo_state) + sizeof(double) * ((size_t)nslots + LOMO_MAX_PROBE_BLOCKS);
+  return sizeof(lomo_state) +
+         sizeof(double) * ((size_t)nslots + nblocks_words(nslots) +
+                           (size_t)nslots * LOMO_PROBE_BLOCKS_PER_SLOT);
 }
 
 int lomo_num_sms(void) {
@@ -938,7 +968,8 @@ int lomo_probe(const void* g, int64_t n, int dtype, int slot, unsigned flags, vo
 
 int lomo_finalize_norm(void* state, void* stream) {
   if (state == nullptr) return LOMO_E_ARG;
-  k3_finalize<<<1, 32, 0, (cudaStream_t)stream>>>(state);
+  cudaStream_t s = (cudaStream_t)stream;
+  k3_reduce<<<dev_info().sms, kThreads, 0, s>>>(state, 0, nullptr);
   return (int)cudaGetLastError();
 }
 
@@ -950,7 +981,8 @@ int lomo_scaler_on_clean(void* state, void* stream) {
 
 int lomo_local_norm_partial(const void* state, double* out2_dev, void* stream) {
   if (state == nullptr || out2_dev == nullptr) return LOMO_E_ARG;
-  k3_local_partial<<<1, 32, 0, (cudaStream_t)stream>>>(state, out2_dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  k3_reduce<<<dev_info().sms, kThreads, 0, s>>>(const_cast<void*>(state), 1, out2_dev);
   return (int)cudaGetLastError();
 }
 

@@ -90,6 +90,10 @@ class State:
         _lib.check(lib().lomo_scaler_on_clean(self.ptr, stream()), "on_clean")
 
     def slots(self, n) -> np.ndarray:
+        # K2 leaves per-CTA partials; K3's reduction (local-partial mode, which
+        # does not run the decision) folds them into the per-slot sums
+        tmp = torch.zeros(2, dtype=torch.float64, device="cuda")
+        _lib.check(lib().lomo_local_norm_partial(self.ptr, tmp.data_ptr(), stream()), "partial")
         torch.cuda.synchronize()
         return self.buf[128:128 + 8 * n].view(torch.float64).cpu().numpy()
 
