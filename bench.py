@@ -253,7 +253,7 @@ def bench_update(args, rank, world):
     shapes["coalesced_small"] = {"tensors": len(small), "us_per_step": round(1e3 * flush_ms / args.steps, 2)}
     # pass 1 of the two-pass protocol over the same tensors: K2 (2 B/elem)
     st = torch.zeros(_lib.state_bytes(len(P)), dtype=torch.uint8, device="cuda")
-    _lib.check(lib.lomo_state_init(st.data_ptr(), len(P), 1024.0, 16, 1.0, 2.0 ** 24, 1.0,
+    _lib.check(lib.lomo_state_init(st.data_ptr(), len(P), 1024.0, 16, 1.0, 2.0 ** 24, 1.0, 1.0,
                                    stream), "init")
     pdisp = HookDispatcher(lib, st.data_ptr(), _lib.MATH_F32)
     pdisp.configure(flags=_lib.USE_SCALE)

@@ -78,7 +78,7 @@ typedef enum {
  * individual fields, e.g. `scale` to multiply the loss on device). */
 typedef struct lomo_state {
   double scale;          /*   0: dynamic loss scale, power of two (stabilize.py:106) */
-  double inv_scale;      /*   8: 1/scale (exact)                                     */
+  double inv_scale;      /*   8: 1/(scale*grad_div), the factor K1/K2 apply to g       */
   double min_scale;      /*  16                                                      */
   double max_scale;      /*  24                                                      */
   double clip_coef;      /*  32: min(1, max_norm/N) or 1 (stabilize.py:212-213)      */
@@ -96,7 +96,9 @@ typedef struct lomo_state {
   uint32_t ticket;       /*  96: K2 last-block ticket (internal)                     */
   int32_t has_scaler;    /* 100                                                      */
   float scale_f32;       /* 104: scale as fp32 (exact: power of two), for loss*scale */
-  int32_t reserved[5];   /* 108..127                                                 */
+  int32_t pad0;          /* 108                                                      */
+  double grad_div;       /* 112: data-parallel gradient divisor (world size; 1)      */
+  int32_t reserved[2];   /* 120..127                                                 */
   /* followed by: double  sumsq[nslots];                      (per-slot totals)
    *              int32_t nblocks[nslots], padded to 8 bytes;  (K2 CTAs per slot)
    *              double  partials[nslots][LOMO_PROBE_BLOCKS_PER_SLOT];
@@ -113,10 +115,12 @@ typedef lomo_state lomo_status;
 int lomo_abi_version(void);
 size_t lomo_state_bytes(int nslots);
 /* Initialise a state block (device memory).  scale <= 0 => no loss scaler
- * (scale = 1).  max_norm <= 0 => no global-norm clip. */
+ * (scale = 1).  max_norm <= 0 => no global-norm clip.  grad_div <= 0 => 1; in
+ * sharded data-parallel mode it is the world size, so LOMO_USE_SCALE turns the
+ * reduce-scattered SUM of per-rank mean gradients into the global mean. */
 int lomo_state_init(void* state, int nslots, double scale, int growth_interval,
                     double min_scale, double max_scale, double max_norm,
-                    void* stream);
+                    double grad_div, void* stream);
 /* Start of a step: clear overflow/skip/underflow and the slot partials; if
  * `loss` is non-NULL, set overflow+skip when it is non-finite
  * (optim.py:63-65 / stabilize.py:185-189). */

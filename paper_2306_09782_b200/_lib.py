@@ -64,7 +64,9 @@ class LomoStatus(ctypes.Structure):
         ("ticket", ctypes.c_uint32),
         ("has_scaler", ctypes.c_int32),
         ("scale_f32", ctypes.c_float),
-        ("reserved", ctypes.c_int32 * 5),
+        ("pad0", ctypes.c_int32),
+        ("grad_div", ctypes.c_double),
+        ("reserved", ctypes.c_int32 * 2),
     ]
 
 
@@ -81,7 +83,7 @@ _u32 = ctypes.c_uint
 _SIGS = {
     "lomo_abi_version": (_i32, []),
     "lomo_state_bytes": (ctypes.c_size_t, [_i32]),
-    "lomo_state_init": (_i32, [_vp, _i32, _dbl, _i32, _dbl, _dbl, _dbl, _vp]),
+    "lomo_state_init": (_i32, [_vp, _i32, _dbl, _i32, _dbl, _dbl, _dbl, _dbl, _vp]),
     "lomo_begin_step": (_i32, [_vp, _vp, _i32, _vp]),
     "lomo_read_status": (_i32, [_vp, ctypes.POINTER(LomoStatus), _vp]),
     "lomo_fused_update": (_i32, [_vp, _vp, _i64, _i32, _i32, _dbl, _dbl, _dbl, _u32, _vp, _vp]),

@@ -489,7 +489,7 @@ __device__ void scaler_on_overflow(lomo_state* st) {
     return;
   }
   st->scale = st->scale / 2.0;
-  st->inv_scale = 1.0 / st->scale;
+  st->inv_scale = 1.0 / (st->scale * st->grad_div);
   st->scale_f32 = (float)st->scale;
   st->clean_steps = 0;
 }
@@ -582,20 +582,22 @@ __global__ void k3_on_clean(void* state) {
   st->clean_steps += 1;
   if (st->clean_steps >= st->growth_interval) {
     st->scale = fmin(st->scale * 2.0, st->max_scale);
-    st->inv_scale = 1.0 / st->scale;
+    st->inv_scale = 1.0 / (st->scale * st->grad_div);
     st->scale_f32 = (float)st->scale;
     st->clean_steps = 0;
   }
 }
 
 __global__ void k_state_init(void* state, int nslots, double scale, int growth_interval,
-                             double min_scale, double max_scale, double max_norm) {
+                             double min_scale, double max_scale, double max_norm,
+                             double grad_div) {
   lomo_state* st = hdr(state);
   if (threadIdx.x == 0) {
     const bool has = scale > 0.0;
+    st->grad_div = grad_div > 0.0 ? grad_div : 1.0;
     st->has_scaler = has ? 1 : 0;
     st->scale = has ? scale : 1.0;
-    st->inv_scale = 1.0 / st->scale;
+    st->inv_scale = 1.0 / (st->scale * st->grad_div);
     st->scale_f32 = (float)st->scale;
     st->min_scale = min_scale;
     st->max_scale = max_scale;
@@ -612,7 +614,8 @@ __global__ void k_state_init(void* state, int nslots, double scale, int growth_i
     st->steps_applied = 0;
     st->steps_skipped = 0;
     st->ticket = 0;
-    for (int i = 0; i < 5; ++i) st->reserved[i] = 0;
+    st->pad0 = 0;
+    st->reserved[0] = st->reserved[1] = 0;
   }
   double* s = reinterpret_cast<double*>(reinterpret_cast<char*>(state) + sizeof(lomo_state));
   const size_t words = (size_t)nslots + nblocks_words(nslots);  // partials need no init
@@ -844,10 +847,11 @@ int lomo_num_sms(void) {
 }
 
 int lomo_state_init(void* state, int nslots, double scale, int growth_interval,
-                    double min_scale, double max_scale, double max_norm, void* stream) {
+                    double min_scale, double max_scale, double max_norm, double grad_div,
+                    void* stream) {
   if (state == nullptr || nslots < 0 || growth_interval < 1) return LOMO_E_ARG;
   k_state_init<<<1, 256, 0, (cudaStream_t)stream>>>(state, nslots, scale, growth_interval,
-                                                     min_scale, max_scale, max_norm);
+                                                     min_scale, max_scale, max_norm, grad_div);
   return (int)cudaGetLastError();
 }
 

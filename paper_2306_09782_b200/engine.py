@@ -1,0 +1,122 @@
+"""The device side of one optimizer: the lomo_state block plus the hook
+dispatcher, behind a small interface shared by LOMO (one GPU) and
+ShardedLOMO (ZeRO-3 shards).
+
+Every method only enqueues work on the current CUDA stream except
+``read_status`` (the one host sync of a step).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .dispatch import HookDispatcher
+from .errors import ConfigError, ShapeError
+
+DTYPE_CODE = {
+    torch.float32: _lib.F32,
+    torch.float16: _lib.F16,
+    torch.bfloat16: _lib.BF16,
+    torch.float64: _lib.F64,
+}
+MATH_CODE = {"f32": _lib.MATH_F32, "f64": _lib.MATH_F64}
+
+
+def dtype_code(dtype: torch.dtype) -> int:
+    try:
+        return DTYPE_CODE[dtype]
+    except KeyError:
+        raise ConfigError(f"unsupported parameter dtype {dtype}") from None
+
+
+class CudaEngine:
+    """State block + K1/K2/K3 launches for one optimizer on one device.
+
+    Args:
+        device: the CUDA device holding parameters and gradients.
+        nslots: number of norm slots (one per parameter, or per bucket).
+        scaler: LossScaler config or None.
+        max_norm: global-norm clip threshold or None.
+        math: "f32" | "f64".
+        grad_div: data-parallel divisor folded into inv_scale (world size).
+    """
+
+    def __init__(self, device: torch.device, nslots: int, scaler=None,
+                 max_norm: float | None = None, math: str = "f32", grad_div: float = 1.0):
+        if device.type != "cuda":
+            raise ConfigError(f"the fused-update path runs on CUDA devices only (got {device}); "
+                              "there is no CPU path")
+        if math not in MATH_CODE:
+            raise ConfigError(f"math must be 'f32' or 'f64', got {math!r}")
+        self.device = device
+        self.lib = _lib.load()
+        self.math = MATH_CODE[math]
+        self.nslots = int(nslots)
+        self.has_scaler = scaler is not None
+        self.state = torch.zeros(_lib.state_bytes(self.nslots), dtype=torch.uint8, device=device)
+        self.ptr = self.state.data_ptr()
+        off = _lib.SCALE_F32_OFFSET
+        self.scale_view = self.state[off:off + 4].view(torch.float32).view(())
+        self.status = _lib.LomoStatus()
+        with torch.cuda.device(device):
+            _lib.check(self.lib.lomo_state_init(
+                self.ptr, self.nslots,
+                float(scaler.scale) if scaler else 0.0,
+                int(scaler.growth_interval) if scaler else 1,
+                float(scaler.min_scale) if scaler else 1.0,
+                float(scaler.max_scale) if scaler else 1.0,
+                float(max_norm) if max_norm else 0.0, float(grad_div), self.stream()),
+                "lomo_state_init")
+        self.dispatch = HookDispatcher(self.lib, self.ptr, self.math)
+
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    # -- step protocol --------------------------------------------------------
+    def begin(self, loss: torch.Tensor | None) -> None:
+        if loss is None:
+            _lib.check(self.lib.lomo_begin_step(self.ptr, None, 0, self.stream()), "begin")
+            return
+        lt = loss.detach()
+        if lt.numel() != 1:
+            raise ShapeError("backward", f"loss must be a scalar, got {tuple(lt.shape)}")
+        lt = lt.contiguous()
+        self._loss_keep = lt  # alive until the kernel has read it (stream order)
+        _lib.check(self.lib.lomo_begin_step(self.ptr, lt.data_ptr(), dtype_code(lt.dtype),
+                                            self.stream()), "lomo_begin_step")
+
+    def configure(self, lr: float = 0.0, clip: float = 0.0, wd: float = 0.0, flags: int = 0):
+        self.dispatch.configure(lr, clip, wd, flags)
+
+    def probe(self, g: torch.Tensor, slot: int) -> None:
+        self.dispatch.probe(g, DTYPE_CODE[g.dtype], slot, self.stream())
+
+    def update(self, p: torch.Tensor, g: torch.Tensor) -> None:
+        self.dispatch.update(p, g, DTYPE_CODE[p.dtype], self.stream())
+
+    def flush(self) -> None:
+        self.dispatch.flush(self.stream())
+
+    def finalize(self) -> None:
+        _lib.check(self.lib.lomo_finalize_norm(self.ptr, self.stream()), "lomo_finalize_norm")
+
+    def local_partial(self, out2: torch.Tensor) -> None:
+        _lib.check(self.lib.lomo_local_norm_partial(self.ptr, out2.data_ptr(), self.stream()),
+                   "lomo_local_norm_partial")
+
+    def finalize_ranks(self, parts: torch.Tensor) -> None:
+        _lib.check(self.lib.lomo_finalize_norm_ranks(self.ptr, parts.data_ptr(), parts.shape[0],
+                                                     self.stream()), "lomo_finalize_norm_ranks")
+
+    def on_clean(self) -> None:
+        _lib.check(self.lib.lomo_scaler_on_clean(self.ptr, self.stream()), "lomo_scaler_on_clean")
+
+    def read_status(self) -> _lib.LomoStatus:
+        _lib.check(self.lib.lomo_read_status(self.ptr, self.status, self.stream()),
+                   "lomo_read_status")
+        torch.cuda.current_stream(self.device).synchronize()
+        return self.status
+
+    @property
+    def launches(self) -> int:
+        return self.dispatch.launches

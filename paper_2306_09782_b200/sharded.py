@@ -1,0 +1,274 @@
+"""ShardedLOMO: the fused update with ZeRO-3 parameter sharding across the
+GPUs of one box (north star (3)).
+
+* Parameters are grouped into buckets (default: one per decoder layer, i.e.
+  per entry of ``model.layers``, plus one "rest" bucket for the embedding,
+  final norm and head).  A bucket is one flat buffer padded to a multiple of
+  ``8 * world`` elements; rank r permanently owns the contiguous slice
+  ``[r*S, (r+1)*S)`` (``bucket.shard``).  That slice is the authoritative copy
+  of those parameters -- the only one that is ever updated.
+* ZeRO-3 life cycle of a layer bucket: ``all_gather_into_tensor`` into the full
+  buffer before the module's forward, released (storage freed) after it;
+  gathered again before the module's backward, released once its gradients
+  have been reduced.  The rest bucket stays gathered and is refreshed from
+  the updated shards after every applied step.
+* Gradients: each parameter hook copies its gradient into the bucket's flat
+  gradient buffer and drops ``p.grad``; when the last gradient of a bucket
+  arrives, ONE ``reduce_scatter_tensor`` (SUM, NCCL over NVLink) produces this
+  rank's shard of the summed gradient and the fused kernel runs on it:
+  K2 (pass 1: overflow + sum of squares) or K1 (pass 2 / single pass:
+  ``p_shard -= lr * ...``).  The 1/world of the data-parallel mean is folded
+  into the state's ``inv_scale`` (``grad_div``), so clipping sees the mean
+  gradient exactly like the single-GPU reference.
+* Global norm (two-pass mode): each rank reduces its slots (K3, local mode),
+  one ``all_gather`` exchanges ``{sumsq, overflow}`` per rank, and K3a decides
+  on the rank-ordered sum -- the same bits on every rank, no float atomics.
+* Gradient peak: one bucket (flat) instead of one tensor.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.distributed as dist
+
+from .engine import CudaEngine, dtype_code
+from .errors import ConfigError, TapeStateError
+from .lomo import _PROBE, _UPDATE, _Protocol, stabilizer_from_args, trainable_params
+from .stabilize import Stabilizer
+
+
+def _backend(group) -> str:
+    return dist.get_backend(group)
+
+
+def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group) -> None:
+    """out[r*S:(r+1)*S] = inp of rank r (NCCL all_gather_into_tensor)."""
+    if _backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+    else:  # gloo (CPU tests): list form
+        dist.all_gather(list(out.chunk(dist.get_world_size(group))), inp, group=group)
+
+
+def reduce_scatter(out: torch.Tensor, inp: torch.Tensor, group) -> None:
+    """out = (sum over ranks of inp)[rank*S:(rank+1)*S] (NCCL reduce_scatter_tensor)."""
+    if _backend(group) == "nccl":
+        dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=group)
+    else:  # gloo has no reduce_scatter_tensor: all_reduce + slice (CPU tests only)
+        tmp = inp.clone()
+        dist.all_reduce(tmp, group=group)
+        r, w = dist.get_rank(group), dist.get_world_size(group)
+        out.copy_(tmp.chunk(w)[r])
+
+
+class _Bucket:
+    def __init__(self, idx: int, params: list, module, persistent: bool, world: int,
+                 rank: int, group):
+        self.idx = idx
+        self.params = params
+        self.module = module
+        self.persistent = persistent
+        self.group = group
+        dev, dt = params[0].device, params[0].dtype
+        for p in params:
+            if p.dtype != dt or p.device != dev:
+                raise ConfigError("a bucket's parameters must share dtype and device")
+        self.dtype, self.device = dt, dev
+        self.numels = [p.numel() for p in params]
+        self.offsets = [0]
+        for n in self.numels[:-1]:
+            self.offsets.append(self.offsets[-1] + n)
+        total = sum(self.numels)
+        align = 8 * world
+        self.padded = int(math.ceil(total / align) * align)
+        self.S = self.padded // world
+        full = torch.zeros(self.padded, dtype=dt, device=dev)
+        with torch.no_grad():
+            for p, off, n in zip(params, self.offsets, self.numels):
+                full[off:off + n].copy_(p.detach().reshape(-1))
+        dist.broadcast(full, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                       group=group)  # every rank starts from rank 0's weights
+        self.shard = full[rank * self.S:(rank + 1) * self.S].clone()
+        self.full = full
+        self.nbytes = self.padded * full.element_size()
+        for p, off, n in zip(params, self.offsets, self.numels):
+            p.data = full[off:off + n].view(p.shape)
+        self.gathered = True
+        self.dirty = False
+        self.gflat = None
+        self.remaining = len(params)
+        if not persistent:
+            self.release()
+
+    def gather(self) -> None:
+        if self.gathered:
+            return
+        self.full.untyped_storage().resize_(self.nbytes)
+        all_gather_into(self.full, self.shard, self.group)
+        self.gathered = True
+        self.dirty = False
+
+    def release(self) -> None:
+        if self.persistent or not self.gathered:
+            return
+        self.full.untyped_storage().resize_(0)
+        self.gathered = False
+
+
+class ShardedLOMO(_Protocol):
+    """LOMO over ZeRO-3 parameter shards, one process per GPU.
+
+    Same public API as :class:`~paper_2306_09782_b200.LOMO`
+    (``grad_norm``, ``fused_backward``, ``step``); the model must be built
+    identically on every rank (rank 0's weights are broadcast at construction).
+
+    Args:
+        buckets: modules whose parameters form one bucket each (default:
+            ``model.layers``); remaining parameters form a persistent bucket.
+        reshard_after_forward: free each layer bucket's full parameters after
+            its forward (ZeRO-3); False keeps them resident (ZeRO-2-like).
+        process_group: the data-parallel group (default: WORLD).
+    """
+
+    _always_scale = True  # inv_scale carries the 1/world of the data-parallel mean
+
+    def __init__(self, model, lr: float = 1e-3, clip_grad_norm: float | None = None,
+                 loss_scale=None, *, clip_grad_value: float | None = None,
+                 weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
+                 math: str = "f32", buckets=None, reshard_after_forward: bool = True,
+                 process_group=None, _engine=None):
+        if not dist.is_initialized():
+            raise ConfigError("ShardedLOMO needs torch.distributed to be initialised")
+        if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
+            raise ConfigError("pass either a Stabilizer or the clip/loss_scale arguments")
+        st = stabilizer if stabilizer is not None else stabilizer_from_args(
+            clip_grad_norm, clip_grad_value, loss_scale)
+        self._init_protocol(st, lr, weight_decay)
+        self.group = process_group
+        self.world = dist.get_world_size(process_group)
+        self.rank = dist.get_rank(process_group)
+        params = trainable_params(model)
+        for p in params:
+            dtype_code(p.dtype)
+        mods = list(buckets) if buckets is not None else list(getattr(model, "layers", []))
+        assigned: set[int] = set()
+        self.buckets: list[_Bucket] = []
+        for m in mods:
+            ps = [p for p in m.parameters() if p.requires_grad and id(p) not in assigned]
+            if not ps:
+                continue
+            assigned.update(id(p) for p in ps)
+            self.buckets.append(_Bucket(len(self.buckets), ps, m, not reshard_after_forward,
+                                        self.world, self.rank, process_group))
+        rest = [p for p in params if id(p) not in assigned]
+        by_dtype: dict = {}
+        for p in rest:
+            by_dtype.setdefault(p.dtype, []).append(p)
+        for ps in by_dtype.values():
+            self.buckets.append(_Bucket(len(self.buckets), ps, None, True, self.world,
+                                        self.rank, process_group))
+        self._loc = {}
+        for b in self.buckets:
+            for p, off, n in zip(b.params, b.offsets, b.numels):
+                self._loc[id(p)] = (b, off, n)
+        self.params = params
+        self.device = params[0].device
+        self.engine = _engine if _engine is not None else CudaEngine(
+            self.device, len(self.buckets), self.scaler, self.max_norm, math,
+            grad_div=float(self.world))
+        self._mode = 0
+        self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
+        for b in self.buckets:
+            if b.module is None or b.persistent:
+                continue
+            self._handles.append(b.module.register_forward_pre_hook(
+                lambda mod, args, b=b: b.gather()))
+            self._handles.append(b.module.register_forward_hook(
+                lambda mod, args, out, b=b: self._after_forward(b)))
+            self._handles.append(b.module.register_full_backward_pre_hook(
+                lambda mod, gout, b=b: b.gather()))
+        self._handles.append(model.register_forward_pre_hook(lambda mod, args: self._refresh()))
+
+    # ---------------------------------------------------------------- ZeRO-3
+    def _after_forward(self, b: _Bucket) -> None:
+        # keep the parameters while autograd recomputes a checkpointed layer
+        if torch._C._current_graph_task_id() == -1:
+            b.release()
+
+    def _refresh(self) -> None:
+        """Re-gather persistent buckets whose shards were updated."""
+        for b in self.buckets:
+            if b.persistent and b.dirty:
+                all_gather_into(b.full, b.shard, self.group)
+                b.dirty = False
+
+    # ----------------------------------------------------------------- hooks
+    def _hook(self, p: torch.Tensor) -> None:
+        if self._mode == 0 or p.grad is None:
+            return
+        b, off, n = self._loc[id(p)]
+        if b.gflat is None:
+            b.gflat = torch.zeros(b.padded, dtype=b.dtype, device=b.device)
+        b.gflat[off:off + n].copy_(p.grad.reshape(-1))
+        p.grad = None
+        b.remaining -= 1
+        if b.remaining == 0:
+            self._reduce(b)
+
+    def _reduce(self, b: _Bucket) -> None:
+        """One reduce-scatter feeding the fused kernel on this rank's shard."""
+        if b.gflat is None:
+            b.gflat = torch.zeros(b.padded, dtype=b.dtype, device=b.device)
+        gshard = torch.empty(b.S, dtype=b.dtype, device=b.device)
+        reduce_scatter(gshard, b.gflat, self.group)
+        b.gflat = None
+        if self._mode == _PROBE:
+            self.engine.probe(gshard, b.idx)
+        else:
+            self.engine.update(b.shard, gshard)
+            b.dirty = True
+        b.remaining = len(b.params)
+        b.release()
+
+    def _run_backward(self, target: torch.Tensor, mode: int, retain_graph: bool) -> None:
+        self._mode = mode
+        try:
+            target.backward(retain_graph=retain_graph)
+            # parameters that received no gradient: reduce their (zero) buckets
+            # in bucket order -- the same collective order on every rank
+            for b in self.buckets:
+                if b.remaining != len(b.params) or b.gflat is not None:
+                    self._reduce(b)
+        finally:
+            self._mode = 0
+            self.engine.flush()
+
+    def _decide(self) -> None:
+        """K3 local partial -> all_gather of {sumsq, overflow} -> K3a on the
+        rank-ordered sum (identical on every rank)."""
+        part = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self.engine.local_partial(part)
+        parts = torch.empty(self.world * 2, dtype=torch.float64, device=self.device)
+        all_gather_into(parts, part, self.group)
+        self.engine.finalize_ranks(parts.view(self.world, 2))
+
+    def _check_loss(self, loss: torch.Tensor) -> torch.Tensor:
+        """Sum of the per-rank losses: non-finite on every rank if it is on
+        any, so every rank takes the same skip / abort decision."""
+        t = loss.detach().float().reshape(1).clone()
+        dist.all_reduce(t, group=self.group)
+        return t
+
+    def _after_update(self) -> None:
+        self._refresh()
+
+    def remove_hooks(self) -> None:
+        for h in self._handles:
+            h.remove()
+        self._handles = []
+
+    def gather_all(self) -> None:
+        """Materialise every bucket's full parameters (e.g. for evaluation)."""
+        self._refresh()
+        for b in self.buckets:
+            b.gather()

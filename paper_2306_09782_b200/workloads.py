@@ -255,16 +255,19 @@ def _rope(x, cos, sin):
 class Llama(nn.Module):
     """LLaMA-1 decoder, random init N(0, 0.02), parameters in ``dtype``."""
 
-    def __init__(self, size: str = "7b", dtype=torch.float16, device="cuda",
+    def __init__(self, size="7b", dtype=torch.float16, device="cuda",
                  checkpointing: bool = False, layers: int | None = None, seed: int = 0):
         super().__init__()
-        c = dict(LLAMA[size])
+        c = dict(LLAMA[size]) if isinstance(size, str) else dict(size)
         if layers is not None:
             c["layers"] = layers
         self.cfg = c
         self.checkpointing = checkpointing
         h, f, v, nh = c["hidden"], c["ffn"], c["vocab"], c["heads"]
-        g = torch.cuda.manual_seed(seed) if str(device).startswith("cuda") else None
+        if str(device).startswith("cuda"):
+            torch.cuda.manual_seed(seed)
+        else:
+            torch.manual_seed(seed)
         std = 0.02
         self.embed_tokens = nn.Parameter(torch.empty(v, h, dtype=dtype, device=device).normal_(0, std))
         self.layers = nn.ModuleList(LlamaLayer(h, nh, f, dtype, device, std)
@@ -296,4 +299,5 @@ class Llama(nn.Module):
 
     def loss(self, ids, targets):
         logits = self(ids)
-        return F.cross_entropy(logits.view(-1, logits.shape[-1]).float(), targets.view(-1))
+        inner = torch.float64 if logits.dtype == torch.float64 else torch.float32
+        return F.cross_entropy(logits.reshape(-1, logits.shape[-1]).to(inner), targets.reshape(-1))

@@ -55,7 +55,7 @@ class State:
         self.buf = torch.zeros(_lib.state_bytes(nslots), dtype=torch.uint8, device="cuda")
         self.ptr = self.buf.data_ptr()
         _lib.check(lib().lomo_state_init(self.ptr, nslots, scale, growth, min_scale, max_scale,
-                                         max_norm, stream()), "init")
+                                         max_norm, 1.0, stream()), "init")
 
     def status(self) -> _lib.LomoStatus:
         st = _lib.LomoStatus()

@@ -1,0 +1,64 @@
+"""ShardedLOMO on the GPU: the CUDA engine + NCCL collectives in a world of
+one rank (this run has a single B200; world_size 2 host logic is covered by
+tests/test_sharded_gloo.py).  With one rank the reduce-scatter is the
+identity, so ShardedLOMO must reproduce single-GPU LOMO -- one K1 launch per
+bucket shard instead of per tensor, and the global norm summed per bucket."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+
+pytestmark = pytest.mark.gpu
+
+CFG = dict(hidden=128, layers=3, heads=4, ffn=256, vocab=256)
+
+
+@pytest.fixture(scope="module")
+def nccl_world():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("stab_kind", ["plain", "norm_scaler"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_sharded_world1_matches_lomo(nccl_world, stab_kind, dtype):
+    from paper_2306_09782_b200 import LOMO, ClipMode, LossScaler, Stabilizer
+    from paper_2306_09782_b200.sharded import ShardedLOMO
+    from paper_2306_09782_b200.workloads import Llama
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+    def stab():
+        if stab_kind == "plain":
+            return None
+        return Stabilizer(ClipMode.by_global_norm(0.5), LossScaler(2.0 ** 8, 2))
+
+    a = Llama(CFG, dtype=dtype, device="cuda", seed=0)
+    b = Llama(CFG, dtype=dtype, device="cuda", seed=0)
+    oa = LOMO(a, lr=0.05, stabilizer=stab())
+    ob = ShardedLOMO(b, lr=0.05, stabilizer=stab())
+    assert all(not bk.gathered for bk in ob.buckets if bk.module is not None)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for step in range(3):
+        d = torch.randint(0, CFG["vocab"], (2, 33), device="cuda", generator=g)
+        la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+        lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+        assert abs(la - lb) <= 1e-6 * abs(la), (step, la, lb)
+        assert ob.last_outcome == oa.last_outcome
+    ob.gather_all()
+    tol = 1e-6 if dtype == torch.float32 else 1e-2
+    for (n, x), (_, y) in zip(a.named_parameters(), b.named_parameters()):
+        err = (x.float() - y.float()).abs().max().item()
+        assert err <= tol * max(1.0, x.float().abs().max().item()), (n, err)
+    ob.remove_hooks()

@@ -49,7 +49,7 @@ def test_argument_errors_need_no_gpu():
     assert lib.lomo_probe(None, 10, 1, 0, 0, None, None) == -1
     assert lib.lomo_probe(None, 10, 1, -1, 0, 1, None) == -2
     assert lib.lomo_finalize_norm(None, None) == -1
-    assert lib.lomo_state_init(None, 1, 1.0, 1, 1.0, 1.0, 0.0, None) == -1
+    assert lib.lomo_state_init(None, 1, 1.0, 1, 1.0, 1.0, 0.0, 1.0, None) == -1
     assert lib.lomo_finalize_norm_ranks(1, None, 2, None) == -1
 
 
