@@ -26,6 +26,7 @@ Restated functions (reference file:line):
 * ``update_hook``             stabilize.py:215-224 (pass-2 hook)
 * ``LossScaler``              stabilize.py:94-127
 * ``two_pass_step``           stabilize.py:180-230 over pre-computed gradients
+* ``grouped_step``            stabilize.py:234-274 (single-pass grouped clipping)
 * ``update_pass_threads``     the CPU baseline: apply_update over many tensors
                               on all host cores (numpy releases the GIL)
 """
@@ -200,6 +201,46 @@ def two_pass_step(params, grads_unscaled, lr, precision, scaler: LossScaler | No
     if scaler is not None:
         scaler.on_clean()
     return out, "applied", total, coef
+
+
+def grouped_step(params, grads, layers, lr, precision, max_norm, window):
+    """Stabilizer._grouped_step (stabilize.py:234-274): one pass; gradients are
+    retained per window of ``window`` adjacent layers (group = layer // window,
+    tape delivery order = reverse build order); each group is clipped by its own
+    norm, a group with a non-finite norm is dropped alone.  ``params``,
+    ``grads`` and ``layers`` are in build order; grads are delivered rounded to
+    the storage precision.  Returns (new_params, outcome)."""
+    out = [np.asarray(p, dtype=np.float64) for p in params]
+    delivered = [round_to(g, precision) for g in grads]
+    skipped = False
+    buffered: list[int] = []
+    cur = None
+
+    def flush():
+        nonlocal skipped
+        if not buffered:
+            return
+        sq = 0.0
+        for i in buffered:
+            flat = delivered[i].ravel()
+            sq += float(np.dot(flat, flat))
+        norm = math.sqrt(sq)
+        if not math.isfinite(norm):
+            skipped = True
+        else:
+            factor = min(1.0, max_norm / norm) if norm > 0.0 else 1.0
+            for i in buffered:
+                out[i] = apply_update(out[i], delivered[i] * factor, lr, precision)
+        buffered.clear()
+
+    for i in reversed(range(len(params))):
+        group = layers[i] // window
+        if cur is not None and group != cur:
+            flush()
+        cur = group
+        buffered.append(i)
+    flush()
+    return out, ("skipped" if skipped else "applied")
 
 
 # --- CPU baseline --------------------------------------------------------------

@@ -8,11 +8,12 @@ unscale, overflow detection, clipping, weight decay and ``p -= lr*g``.
 """
 from .errors import (ConfigError, FusedTrainError, NativeError, NonFiniteLossError,
                      ScaleUnderflowError, ShapeError, TapeStateError)
+from .grouped import GroupedLOMO
 from .lomo import LOMO, lomo_step
 from .stabilize import ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome
 
 __all__ = [
-    "LOMO", "lomo_step", "ClipKind", "ClipMode", "LossScaler", "Stabilizer", "StepOutcome",
+    "LOMO", "GroupedLOMO", "lomo_step", "ClipKind", "ClipMode", "LossScaler", "Stabilizer", "StepOutcome",
     "ConfigError", "FusedTrainError", "NativeError", "NonFiniteLossError",
     "ScaleUnderflowError", "ShapeError", "TapeStateError",
 ]

@@ -65,7 +65,10 @@ class FakeTape:
             with np.errstate(over="ignore", invalid="ignore"):
                 t = Tensor(g * s, self.precision)  # rounded per precision (tape.py:377,394)
             d = hook(p, t)
-            assert d is Disposition.CONSUME
+            if d is Disposition.RETAIN:        # tape.py:402-403
+                p.grad_slot = t
+            else:
+                assert d is Disposition.CONSUME
 
 
 class FakeModel:
@@ -128,7 +131,7 @@ def run_case(name, precision, stab_factory, steps, lr, rng, losses=None, big_ste
             arrays[f"{name}/p{k + 1}_{i}"] = p.value.data.copy()
     if stab is not None:
         rec["clip"] = {"kind": stab.clip.kind.value, "threshold": stab.clip.threshold,
-                       "max_norm": stab.clip.max_norm}
+                       "max_norm": stab.clip.max_norm, "window": stab.clip.window}
         sc = stab.scaler
         rec["scaler"] = None if sc is None else {
             "growth_interval": sc.growth_interval, "min_scale": sc.min_scale,
@@ -162,6 +165,13 @@ def hook_cases():
              {"losses": [float("nan"), 0.5]}),
             (f"nan_grad_2pass_{prec}", prec,
              lambda: Stabilizer(ClipMode.by_global_norm(0.08)), 2, 0.05, {"nan_step": 0}),
+            # single-pass grouped clipping (stabilize.py:234-274), layer = index
+            (f"grouped_w1_{prec}", prec,
+             lambda: Stabilizer(ClipMode.by_group_norm(0.03, 1)), 3, 0.05, {}),
+            (f"grouped_w2_{prec}", prec,
+             lambda: Stabilizer(ClipMode.by_group_norm(0.03, 2)), 3, 0.05, {}),
+            (f"grouped_nan_{prec}", prec,
+             lambda: Stabilizer(ClipMode.by_group_norm(0.03, 2)), 2, 0.05, {"nan_step": 0}),
         ]
     specs += [
         ("overflow_half", "half",

@@ -338,13 +338,34 @@ def _device_case(case, arrays, nshapes, prec, math_mode):
                  min_scale=sc["min_scale"] if sc else 1.0,
                  max_scale=sc["max_scale"] if sc else 1.0, max_norm=max_norm)
     outs, scales, results = [], [], []
+    grouped = clip is not None and clip["kind"] == "by_group_norm"
+    if grouped:
+        st = U.State(nshapes, max_norm=clip["max_norm"])
     for k in range(case["steps"]):
         scale = st.status().scale
         loss = torch.tensor(case["losses"][k], dtype=torch.float32, device="cuda")
         st.begin(loss)
         delivered = [U.to_dev(O.round_to(x * scale, prec), dt) for x in g[k]]
         order = list(reversed(range(nshapes)))  # delivery order (tape.py:350-360)
-        if two:
+        if grouped:
+            # stabilize.py:234-274: per group (layer // window): K2 -> K3a -> K1
+            skipped0 = st.status().steps_skipped
+            groups = []
+            for i in order:
+                if groups and groups[-1][0] == i // clip["window"]:
+                    groups[-1][1].append(i)
+                else:
+                    groups.append((i // clip["window"], [i]))
+            for _, members in groups:
+                st.begin()
+                for slot, i in enumerate(members):
+                    st.probe(delivered[i], slot, _lib.ACCUM_F64 if math_mode == "f64" else 0)
+                st.finalize()
+                for i in members:
+                    U.fused_update(P[i], delivered[i], math=math_mode, lr=case["lr"],
+                                   flags=_lib.USE_SKIP | _lib.USE_COEF, state=st)
+            outs.append("skipped_overflow" if st.status().steps_skipped > skipped0 else "applied")
+        elif two:
             for slot, i in enumerate(order):
                 st.probe(delivered[i], slot, (_lib.USE_SCALE if sc else 0) |
                          (_lib.ACCUM_F64 if math_mode == "f64" else 0))
@@ -385,7 +406,8 @@ def test_reference_hook_cases_replayed_on_device(hook_cases, math_mode):
         assert outs == want, case["name"]                     # decisions: bit-exact
         if case["scaler"] is not None:
             assert scales == case["scales"], case["name"]
-        norm = case["clip"] is not None and case["clip"]["kind"] == "by_global_norm"
+        norm = case["clip"] is not None and case["clip"]["kind"] in ("by_global_norm",
+                                                                      "by_group_norm")
         dt = U.TORCH_DT[prec]
         for k in range(case["steps"]):
             for i in range(nshapes):
@@ -427,8 +449,14 @@ def test_bf16_cases_match_oracle(hook_cases, math_mode):
         clip = case["clip"]
         max_norm = clip["max_norm"] if clip and clip["kind"] == "by_global_norm" else None
         thresh = clip["threshold"] if clip and clip["kind"] == "by_value" else None
+        grouped = clip is not None and clip["kind"] == "by_group_norm"
         for k in range(case["steps"]):
-            if scaler is not None or max_norm is not None:
+            if grouped:
+                params, out = O.grouped_step(params, g[k], list(range(nshapes)), case["lr"],
+                                             "bf16", clip["max_norm"], clip["window"])
+                out = "applied" if out == "applied" else "skipped_overflow"
+                max_norm = clip["max_norm"]
+            elif scaler is not None or max_norm is not None:
                 params, out, _, _ = O.two_pass_step(params, g[k], case["lr"], "bf16", scaler,
                                                     max_norm, thresh)
                 out = {"applied": "applied", "skipped": "skipped_overflow",

@@ -258,3 +258,52 @@ def test_recompute_forward_equals_retained_graph():
         assert la == lb
     for x, y in zip(a.parameters(), b.parameters()):
         assert torch.equal(x, y)
+
+
+# --- grouped-norm clipping (stabilize.py:234-274) ------------------------------
+
+def test_grouped_single_group_equals_two_pass_bit_exact():
+    """test_stabilize.py:115-121: window covering every layer == global clip."""
+    from paper_2306_09782_b200 import GroupedLOMO
+    cfg = MiniConfig(layers=2, hidden=64, heads=2, vocab=128, seed=5)
+    a = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+    b = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+    oa = GroupedLOMO(a, lr=0.05, max_norm=0.05, window=99, math="f64")
+    ob = LOMO(b, lr=0.05, clip_grad_norm=0.05, math="f64")
+    for step in range(3):
+        ids = torch.from_numpy(sequence_copy_batch(2, step, 2, 16, 128)).cuda()
+        oa.step(lambda: mean_cross_entropy(a(ids), ids), 0.05)
+        ob.step(lambda: mean_cross_entropy(b(ids), ids), 0.05)
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)
+
+
+def test_grouped_window_one_matches_per_group_reference():
+    """test_stabilize.py:124-141: every layer clipped by its own norm."""
+    from paper_2306_09782_b200 import GroupedLOMO
+    from paper_2306_09782_b200.grouped import infer_layers
+    cfg = MiniConfig(layers=2, hidden=64, heads=2, vocab=128, seed=6)
+    a = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+    ref = MiniTransformer(cfg, dtype=torch.float64, device="cuda")
+    layers = infer_layers(ref)
+    opt = GroupedLOMO(a, lr=0.05, max_norm=0.02, window=1, math="f64")
+    ids = torch.from_numpy(sequence_copy_batch(3, 0, 2, 16, 128)).cuda()
+    opt.step(lambda: mean_cross_entropy(a(ids), ids), 0.05)
+    mean_cross_entropy(ref(ids), ids).backward()
+    groups = {}
+    for p in ref.parameters():
+        groups.setdefault(layers[id(p)], []).append(p)
+    factors = set()
+    with torch.no_grad():
+        for ps in groups.values():
+            n = torch.sqrt(sum((p.grad.double() ** 2).sum() for p in ps)).item()
+            f = min(1.0, 0.02 / n) if n > 0 else 1.0
+            factors.add(f)
+            for p in ps:
+                p.copy_(p - 0.05 * (p.grad * f))
+    assert len(factors) > 1  # groups really got different factors
+    for x, y in zip(a.parameters(), ref.parameters()):
+        assert torch.allclose(x, y, rtol=0, atol=1e-15)
+    assert opt.last_outcome is StepOutcome.APPLIED
+    largest_group = max(sum(p.numel() * 8 for p in ps) for ps in groups.values())
+    assert opt.peak_group_grads <= largest_group  # gradient peak = largest group

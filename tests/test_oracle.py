@@ -85,9 +85,14 @@ def _replay_case(meta_case, arrays, nshapes, precision_override=None):
     two_pass = scaler is not None or (clip and clip["kind"] == "by_global_norm")
     threshold = clip["threshold"] if clip and clip["kind"] == "by_value" else None
     max_norm = clip["max_norm"] if clip and clip["kind"] == "by_global_norm" else None
+    grouped = clip is not None and clip["kind"] == "by_group_norm"
     for k in range(meta_case["steps"]):
         loss = meta_case["losses"][k]
-        if two_pass:
+        if grouped:
+            params, out = O.grouped_step(params, g[k], list(range(nshapes)), meta_case["lr"],
+                                         prec, clip["max_norm"], clip["window"])
+            outs.append("applied" if out == "applied" else "skipped_overflow")
+        elif two_pass:
             if not math.isfinite(loss):
                 ok = scaler.on_overflow() if scaler else True
                 outs.append("skipped_overflow" if ok else "underflow")
