@@ -307,3 +307,36 @@ def test_grouped_window_one_matches_per_group_reference():
     assert opt.last_outcome is StepOutcome.APPLIED
     largest_group = max(sum(p.numel() * 8 for p in ps) for ps in groups.values())
     assert opt.peak_group_grads <= largest_group  # gradient peak = largest group
+
+
+# --- per-layer activation checkpointing (tape.py:224-250, criterion 8) ----------
+
+@pytest.mark.parametrize("two_pass", [False, True])
+def test_checkpointing_is_transparent(two_pass):
+    """test_acceptance.py:220-246: same bits with and without per-layer
+    checkpointing; the recompute runs each layer's forward at most once more."""
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=64, layers=3, heads=4, ffn=128, vocab=128)
+    torch.use_deterministic_algorithms(True, warn_only=True)
+    try:
+        a = Llama(cfg, dtype=torch.float64, device="cuda", seed=0, checkpointing=False)
+        b = Llama(cfg, dtype=torch.float64, device="cuda", seed=0, checkpointing=True)
+        calls = {"n": 0}
+        for layer in b.layers:
+            layer.register_forward_pre_hook(lambda m, a_: calls.__setitem__("n", calls["n"] + 1))
+        kw = dict(clip_grad_norm=0.5, loss_scale=2.0 ** 8) if two_pass else {}
+        oa = LOMO(a, lr=0.05, math="f64", **kw)
+        ob = LOMO(b, lr=0.05, math="f64", **kw)
+        g = torch.Generator(device="cuda").manual_seed(3)
+        for step in range(3):
+            d = torch.randint(0, 128, (2, 17), device="cuda", generator=g)
+            la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+            lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+            assert la == lb
+        for x, y in zip(a.parameters(), b.parameters()):
+            assert torch.equal(x, y)
+        passes = 2 if two_pass else 1
+        # forward once + one recompute per backward pass, per layer
+        assert calls["n"] == 3 * 3 * (1 + passes)
+    finally:
+        torch.use_deterministic_algorithms(False)

@@ -62,3 +62,24 @@ def test_sharded_world1_matches_lomo(nccl_world, stab_kind, dtype):
         err = (x.float() - y.float()).abs().max().item()
         assert err <= tol * max(1.0, x.float().abs().max().item()), (n, err)
     ob.remove_hooks()
+
+
+def test_sharded_with_checkpointing_world1(nccl_world):
+    """ZeRO-3 gather/release interleaved with the per-layer recompute."""
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.sharded import ShardedLOMO
+    from paper_2306_09782_b200.workloads import Llama
+    a = Llama(CFG, dtype=torch.float32, device="cuda", seed=0, checkpointing=True)
+    b = Llama(CFG, dtype=torch.float32, device="cuda", seed=0, checkpointing=True)
+    oa = LOMO(a, lr=0.05, clip_grad_norm=0.5)
+    ob = ShardedLOMO(b, lr=0.05, clip_grad_norm=0.5)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    for step in range(2):
+        d = torch.randint(0, CFG["vocab"], (2, 17), device="cuda", generator=g)
+        la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+        lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+        assert abs(la - lb) <= 1e-5 * abs(la)
+    ob.gather_all()
+    for (n, x), (_, y) in zip(a.named_parameters(), b.named_parameters()):
+        assert (x - y).abs().max().item() <= 1e-5, n
+    ob.remove_hooks()
