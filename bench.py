@@ -215,10 +215,12 @@ def bench_update(args, rank, world):
     launches = 0
     with ClockSampler(torch.cuda.current_device()) as clk:
         _barrier(world)
+        t0 = time.perf_counter()
         start.record()
         for _ in range(args.steps):
             launches += run_update_pass(disp, P, G, dt_code, stream)
         end.record()
+        host_ms = (time.perf_counter() - t0) * 1e3 / args.steps
         _barrier(world)
     ms_local = start.elapsed_time(end)
     ms = _max_over_ranks(ms_local, world)
@@ -267,13 +269,16 @@ def bench_update(args, rank, world):
     for _ in range(args.warmup):
         probe_pass()
     torch.cuda.synchronize()
+    t0 = time.perf_counter()
     start.record()
     for _ in range(args.steps):
         probe_pass()
     end.record()
+    host_probe_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     torch.cuda.synchronize()
     probe_ms = start.elapsed_time(end) / args.steps
     probe = {"gbs": round(2 * elems / (probe_ms * 1e-3) / 1e9, 1), "ms_per_pass": round(probe_ms, 4),
+             "host_ms_per_pass": round(host_probe_ms, 3),
              "algorithmic_bytes_per_elem": 2,
              "what": "K2 sum-of-squares + overflow flag over every gradient, + begin/finalize (K3a)"}
     # the exact-arithmetic mode (f64 math, direct rounding) on the same pass
@@ -292,7 +297,8 @@ def bench_update(args, rank, world):
            "ms_per_pass": round(f64_ms, 4)}
     del P, G
     torch.cuda.empty_cache()
-    return {"gbs": gbs, "ms": ms / args.steps, "probe": probe, "f64_math": f64, "elems_per_rank": elems, "total_elems": total_elems,
+    return {"gbs": gbs, "ms": ms / args.steps, "probe": probe, "f64_math": f64,
+            "host_ms": host_ms, "elems_per_rank": elems, "total_elems": total_elems,
             "launches": launches, "clocks": clk.summary(), "kernel_gbs": achieved,
             "kernel_ms_per_step": ksum_ms / args.steps, "shapes": shapes}
 
@@ -383,47 +389,116 @@ def bench_e2e(args, rank, world):
 
 
 def bench_train(args, rank, world):
-    """Config 3: LLaMA-7B fp16 LOMO, dynamic loss scale + two-pass clip."""
+    """Config 3: LLaMA-7B fp16 LOMO, dynamic loss scale + two-pass clip.
+
+    Timed twice on the same model: the strict LOMO schedule (each hook
+    launches on the autograd stream, one gradient alive) and ``overlap=True``
+    (hook kernels on a side stream, overlapping the remaining backward)."""
     import torch
     from paper_2306_09782_b200 import LOMO, LossScaler
     from paper_2306_09782_b200.workloads import Llama
     torch.cuda.reset_peak_memory_stats()
-    model = Llama("7b", dtype=torch.float16, device="cuda", checkpointing=False)
+    model = Llama("7b", dtype=torch.float16, device="cuda", checkpointing=args.ckpt)
     model.train()
-    opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
-               loss_scale=LossScaler(2.0 ** 10, growth_interval=16))
+    params_bytes = sum(p.numel() * p.element_size() for p in model.parameters())
+    largest = max(p.numel() * p.element_size() for p in model.parameters())
     seq, batch = args.seq, args.batch
     gen = torch.Generator(device="cuda").manual_seed(0)
+    data = [torch.randint(0, 32000, (batch, seq + 1), device="cuda", generator=gen)
+            for _ in range(4)]
+    out = {"model": "llama-7b (random init N(0,0.02)), fp16 params, no master copy",
+           "seq_len": seq, "batch": batch, "steps": args.train_steps, "passes_per_step": 2,
+           "clip_grad_norm": 1.0, "activation_checkpointing": bool(args.ckpt),
+           "paper_tgs_rtx3090": 769.92}
+    for overlap in (False, True):
+        opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
+                   loss_scale=LossScaler(2.0 ** 10, growth_interval=16), overlap=overlap)
+
+        def step(k):
+            d = data[k % len(data)]
+            return opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
+
+        for k in range(args.train_warmup):
+            step(k)
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        losses, outcomes = [], []
+        start.record()
+        for k in range(args.train_steps):
+            losses.append(step(k))
+            outcomes.append(opt.last_outcome.value)
+        end.record()
+        torch.cuda.synchronize()
+        ms = start.elapsed_time(end) / args.train_steps
+        key = "overlap" if overlap else "strict"
+        out[key] = {"tokens_per_s": round(batch * seq / (ms * 1e-3), 1), "ms_per_step": round(ms, 2),
+                    "peak_mem_gib": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
+                    "loss_scale_final": opt.loss_scale, "outcomes": outcomes,
+                    "losses": [round(x, 4) for x in losses]}
+        opt.remove_hooks()
+        del opt
+    out["tokens_per_s"] = out["strict"]["tokens_per_s"]
+    out["ms_per_step"] = out["strict"]["ms_per_step"]
+    out["memory_gib"] = {
+        "params": round(params_bytes / 2 ** 30, 2), "largest_gradient": round(largest / 2 ** 30, 3),
+        "optimizer_state": 0.0,
+        "lomo_state_block_mib": round(len(list(model.parameters())) * 4096 * 8 / 2 ** 20, 1),
+        "peak_allocated": out["strict"]["peak_mem_gib"],
+        "paper_table1_lomo_row": {"params": 12.55, "gradients": 0.24, "optimizer_states": 0.0}}
+    del model
+    torch.cuda.empty_cache()
+    return out
+
+
+def bench_train_sharded(args, rank, world):
+    """Configs 4/5: LLaMA-13B (or 65B with per-layer activation checkpointing)
+    with ZeRO-3 parameter shards over ``world`` GPUs; each bucket's gradients
+    are reduce-scattered with NCCL and each rank runs the fused update on its
+    shard (ShardedLOMO).  Every rank trains on its own seq x batch tokens, so
+    tokens/s is the whole-job sum."""
+    import torch
+    from paper_2306_09782_b200 import LossScaler
+    from paper_2306_09782_b200.sharded import ShardedLOMO
+    from paper_2306_09782_b200.workloads import Llama
+    size = args.sharded_model
+    ckpt = args.ckpt or size == "65b"
+    model = Llama(size, dtype=torch.float16, device="cuda", checkpointing=ckpt)
+    model.train()
+    opt = ShardedLOMO(model, lr=1e-3, clip_grad_norm=1.0,
+                      loss_scale=LossScaler(2.0 ** 10, growth_interval=16))
+    torch.cuda.empty_cache()
+    seq, batch = args.seq, args.batch
+    gen = torch.Generator(device="cuda").manual_seed(rank)
     data = [torch.randint(0, 32000, (batch, seq + 1), device="cuda", generator=gen)
             for _ in range(4)]
 
     def step(k):
         d = data[k % len(data)]
-        ids, tgt = d[:, :-1], d[:, 1:]
-        return opt.step(lambda: model.loss(ids, tgt), 1e-3)
+        return opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
 
     for k in range(args.train_warmup):
         step(k)
-    torch.cuda.synchronize()
+    _barrier(world)
+    torch.cuda.reset_peak_memory_stats()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    losses, outcomes = [], []
     start.record()
+    outcomes = []
     for k in range(args.train_steps):
-        losses.append(step(k))
+        step(k)
         outcomes.append(opt.last_outcome.value)
     end.record()
-    torch.cuda.synchronize()
-    ms = start.elapsed_time(end) / args.train_steps
-    peak = torch.cuda.max_memory_allocated() / 1e9
-    out = {"model": "llama-7b (random init N(0,0.02)), fp16 params, no master copy",
-           "tokens_per_s": round(batch * seq / (ms * 1e-3), 1), "ms_per_step": round(ms, 2),
-           "seq_len": seq, "batch": batch, "steps": args.train_steps, "passes_per_step": 2,
-           "clip_grad_norm": 1.0, "loss_scale_final": opt.loss_scale,
-           "outcomes": outcomes, "losses": [round(x, 4) for x in losses],
-           "peak_mem_gb": round(peak, 2),
-           "paper_tgs_rtx3090": 769.92}
+    _barrier(world)
+    ms = _max_over_ranks(start.elapsed_time(end), world) / args.train_steps
+    out = {"model": f"llama-{size} (random init), fp16, ZeRO-3 shards over {world} GPUs",
+           "tokens_per_s": round(world * batch * seq / (ms * 1e-3), 1),
+           "tokens_per_gpu_per_s": round(batch * seq / (ms * 1e-3), 1),
+           "ms_per_step": round(ms, 2), "seq_len": seq, "batch_per_rank": batch,
+           "activation_checkpointing": ckpt, "passes_per_step": 2, "outcomes": outcomes,
+           "peak_mem_gib_rank0": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
+           "paper_tgs_rtx3090": {"13b": 66.19, "30b": 11.61, "65b": 4.93}.get(size)}
     opt.remove_hooks()
-    del model, opt
+    del opt, model
     torch.cuda.empty_cache()
     return out
 
@@ -478,6 +553,9 @@ def main():
     ap.add_argument("--train-warmup", type=int, default=3)
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--ckpt", action="store_true", help="per-layer activation checkpointing")
+    ap.add_argument("--sharded-model", default="13b", choices=["7b", "13b", "30b", "65b"],
+                    help="model of the N>1 sharded train leg (config 4: 13b, config 5: 65b)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -512,8 +590,9 @@ def main():
     tr = _traffic()
     e2e = None if args.no_e2e else bench_e2e(args, rank, world)
     train = None
-    if not args.no_train and world == 1:
-        train = bench_train(args, rank, world)
+    if not args.no_train:
+        train = bench_train(args, rank, world) if world == 1 else \
+            bench_train_sharded(args, rank, world)
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cb = cpu_baseline()
@@ -542,6 +621,7 @@ def main():
                                    "on one stream, bracketed by CUDA events; achieved = 6 B/elem x "
                                    "elements / their time",
                          "avg_launch_us": round(1e3 * up["ms"] / (up["launches"] / args.steps), 2),
+                         "host_ms_per_pass": round(up["host_ms"], 3),
                          "per_shape_instrumented": up["shapes"],
                          "per_shape_note": "per-launch event pairs (separate replay) break the PDL "
                                            "overlap, so these per-shape rates understate the pass"},

@@ -34,7 +34,7 @@
 namespace lomo_k {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;  // 16-byte vectors in flight per thread per operand
+constexpr int kUnroll = 8;  // K2: 16-byte loads in flight per thread (tools/k1_variants.cu)
 
 // --------------------------------------------------------------------------
 // device info (grid sizing)
@@ -415,8 +415,8 @@ __global__ void __launch_bounds__(kThreads)
       acc += (double)x * (double)x;
     }
   }
-  // small fixed tiles (>= 1024 vectors, <= LOMO_MAX_PROBE_BLOCKS CTAs): the
-  // block scheduler balances them across SMs like K1's tiles
+  // small fixed tiles (>= 2048 vectors = 32 KB, <= LOMO_PROBE_BLOCKS_PER_SLOT
+  // CTAs): the block scheduler balances them across SMs like K1's tiles
   const int64_t beg = (int64_t)blockIdx.x * per_cta;
   const int64_t end = min(beg + per_cta, nvec);
   const uint4* gv = reinterpret_cast<const uint4*>(g + head);

@@ -21,8 +21,20 @@ SMALL_NUMEL = 1 << 16
 
 
 class HookDispatcher:
+    """Per-pass launcher of K1/K2 for the hooks.
+
+    ``side_stream``: when given, every launch goes to that stream after an
+    event recorded on the hook's (autograd) stream -- the update of parameter
+    i then overlaps the backward of the layers below it on the main stream.
+    The gradient's block is protected with ``record_stream`` so the caching
+    allocator cannot hand it out before the kernel has read it; the caller
+    joins the side stream after backward (``join``).  Gradient lifetime grows
+    from "until the launch" to "until the kernel ran", so more than one
+    gradient can be alive -- hence opt-in.
+    """
+
     def __init__(self, lib, state_ptr: int | None, math_code: int,
-                 small_numel: int = SMALL_NUMEL):
+                 small_numel: int = SMALL_NUMEL, side_stream=None):
         self.lib = lib
         self.state_ptr = state_ptr
         self.math = math_code
@@ -30,7 +42,31 @@ class HookDispatcher:
         self._upd = {}    # dtype code -> [(p, g)]
         self._prb = {}    # dtype code -> [(g, slot)]
         self.launches = 0
+        self.side = side_stream
+        if side_stream is not None:
+            import torch
+            self._events = [torch.cuda.Event() for _ in range(32)]
+            self._ev = 0
         self.configure()
+
+    def _route(self, stream: int, tensors) -> int:
+        """The stream to launch on (the hook's, or the side stream)."""
+        if self.side is None:
+            return stream
+        import torch
+        ev = self._events[self._ev]
+        self._ev = (self._ev + 1) % len(self._events)
+        ev.record(torch.cuda.current_stream())
+        self.side.wait_event(ev)
+        for t in tensors:
+            t.record_stream(self.side)
+        return self.side.cuda_stream
+
+    def join(self) -> None:
+        """Make the current stream wait for everything launched on the side stream."""
+        if self.side is not None:
+            import torch
+            torch.cuda.current_stream().wait_stream(self.side)
 
     def configure(self, lr: float = 0.0, clip: float = 0.0, wd: float = 0.0, flags: int = 0):
         """Per-pass constants (the same for every tensor of one backward)."""
@@ -45,6 +81,7 @@ class HookDispatcher:
             if len(lst) == 64:
                 self._flush_upd(dt, stream)
             return
+        stream = self._route(stream, (g,))
         rc = self.lib.lomo_fused_update(p.data_ptr(), g.data_ptr(), n, dt, self.math, self.lr,
                                         self.clip, self.wd, self.flags, self.state_ptr, stream)
         if rc:
@@ -59,6 +96,7 @@ class HookDispatcher:
             if len(lst) == 64:
                 self._flush_prb(dt, stream)
             return
+        stream = self._route(stream, (g,))
         rc = self.lib.lomo_probe(g.data_ptr(), n, dt, slot, self.flags, self.state_ptr, stream)
         if rc:
             _lib.check(rc, "lomo_probe")
@@ -70,6 +108,7 @@ class HookDispatcher:
         if not lst:
             return
         k = len(lst)
+        stream = self._route(stream, [g for _, g in lst])
         ps = (ctypes.c_void_p * k)(*[p.data_ptr() for p, _ in lst])
         gs = (ctypes.c_void_p * k)(*[g.data_ptr() for _, g in lst])
         ns = (ctypes.c_int64 * k)(*[p.numel() for p, _ in lst])
@@ -84,6 +123,7 @@ class HookDispatcher:
         if not lst:
             return
         k = len(lst)
+        stream = self._route(stream, [g for g, _ in lst])
         gs = (ctypes.c_void_p * k)(*[g.data_ptr() for g, _ in lst])
         ns = (ctypes.c_int64 * k)(*[g.numel() for g, _ in lst])
         ss = (ctypes.c_int * k)(*[s for _, s in lst])
@@ -98,6 +138,7 @@ class HookDispatcher:
             self._flush_upd(dt, stream)
         for dt in list(self._prb):
             self._flush_prb(dt, stream)
+        self.join()
 
     def pending(self) -> int:
         return sum(map(len, self._upd.values())) + sum(map(len, self._prb.values()))

@@ -22,6 +22,13 @@ DTYPE_CODE = {
 MATH_CODE = {"f32": _lib.MATH_F32, "f64": _lib.MATH_F64}
 
 
+try:
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover - older torch
+    def _raw_stream(idx):
+        return torch.cuda.current_stream(idx).cuda_stream
+
+
 def dtype_code(dtype: torch.dtype) -> int:
     try:
         return DTYPE_CODE[dtype]
@@ -39,16 +46,20 @@ class CudaEngine:
         max_norm: global-norm clip threshold or None.
         math: "f32" | "f64".
         grad_div: data-parallel divisor folded into inv_scale (world size).
+        overlap: run K1/K2 on a side stream, overlapping the backward GEMMs
+            (see HookDispatcher).
     """
 
     def __init__(self, device: torch.device, nslots: int, scaler=None,
-                 max_norm: float | None = None, math: str = "f32", grad_div: float = 1.0):
+                 max_norm: float | None = None, math: str = "f32", grad_div: float = 1.0,
+                 overlap: bool = False):
         if device.type != "cuda":
             raise ConfigError(f"the fused-update path runs on CUDA devices only (got {device}); "
                               "there is no CPU path")
         if math not in MATH_CODE:
             raise ConfigError(f"math must be 'f32' or 'f64', got {math!r}")
         self.device = device
+        self._dev_idx = device.index if device.index is not None else torch.cuda.current_device()
         self.lib = _lib.load()
         self.math = MATH_CODE[math]
         self.nslots = int(nslots)
@@ -67,10 +78,12 @@ class CudaEngine:
                 float(scaler.max_scale) if scaler else 1.0,
                 float(max_norm) if max_norm else 0.0, float(grad_div), self.stream()),
                 "lomo_state_init")
-        self.dispatch = HookDispatcher(self.lib, self.ptr, self.math)
+        side = torch.cuda.Stream(device) if overlap else None
+        self.dispatch = HookDispatcher(self.lib, self.ptr, self.math, side_stream=side)
 
     def stream(self) -> int:
-        return torch.cuda.current_stream(self.device).cuda_stream
+        # raw cudaStream_t of the current stream, without building a Stream object
+        return _raw_stream(self._dev_idx)
 
     # -- step protocol --------------------------------------------------------
     def begin(self, loss: torch.Tensor | None) -> None:

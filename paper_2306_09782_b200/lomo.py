@@ -232,12 +232,16 @@ class LOMO(_Protocol):
         stabilizer: alternatively, the reference's :class:`Stabilizer`.
         math: ``"f32"`` (fp32 arithmetic, the hot path) or ``"f64"`` (the
             reference's float64 arithmetic, rounded directly to storage).
+        overlap: launch the hook kernels on a side stream so each update
+            overlaps the rest of the backward (a few gradients may be alive at
+            once instead of one; off by default to keep the reference's
+            one-gradient invariant).
     """
 
     def __init__(self, model, lr: float = 1e-3, clip_grad_norm: float | None = None,
                  loss_scale=None, *, clip_grad_value: float | None = None,
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
-                 math: str = "f32"):
+                 math: str = "f32", overlap: bool = False):
         if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
             raise ConfigError("pass either a Stabilizer or the clip/loss_scale arguments")
         st = stabilizer if stabilizer is not None else stabilizer_from_args(
@@ -256,7 +260,8 @@ class LOMO(_Protocol):
         self.params = uniq
         self.device = dev
         self.math = math
-        self.engine = CudaEngine(dev, len(uniq), self.scaler, self.max_norm, math)
+        self.engine = CudaEngine(dev, len(uniq), self.scaler, self.max_norm, math,
+                                 overlap=overlap)
         # Slot i <-> the i-th parameter in reference delivery order: non-increasing
         # layer, reverse build order within a layer == reverse registration
         # order (tape.py:350-360).  K3a sums the slots in this order (stabilize.py:199).

@@ -86,13 +86,12 @@ class _Bucket:
         with torch.no_grad():
             for p, off, n in zip(params, self.offsets, self.numels):
                 full[off:off + n].copy_(p.detach().reshape(-1))
+                p.data = full[off:off + n].view(p.shape)  # frees the original storage
         dist.broadcast(full, src=dist.get_global_rank(group, 0) if group is not None else 0,
                        group=group)  # every rank starts from rank 0's weights
         self.shard = full[rank * self.S:(rank + 1) * self.S].clone()
         self.full = full
         self.nbytes = self.padded * full.element_size()
-        for p, off, n in zip(params, self.offsets, self.numels):
-            p.data = full[off:off + n].view(p.shape)
         self.gathered = True
         self.dirty = False
         self.gflat = None

@@ -106,6 +106,34 @@ __global__ void __launch_bounds__(256) v_tile(bf* __restrict__ p, const bf* __re
   }
 }
 
+// ---- K2 variant: probe with per-CTA tile of PER vectors, U loads in flight --
+template <int U>
+__global__ void __launch_bounds__(256) v_probe(const bf* __restrict__ g, int64_t nvec,
+                                               int64_t per, double* __restrict__ part) {
+  __shared__ double sm[8];
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const int64_t beg = (int64_t)blockIdx.x * per, end = min(beg + per, nvec);
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t base = beg + threadIdx.x; base < end; base += 256 * U) {
+    uint4 G[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 256;
+      if (i < end) G[u] = ld_stream_ro(gv + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 256;
+      if (i < end) acc += vec_sumsq<bf, float>(G[u], 1.0f, false, bad);
+    }
+  }
+  const double r = block_sum(acc, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = r + (bad ? 1.0 : 0.0);
+}
+
 // ---- variant: TMA bulk copies through a 4-stage shared-memory ring ---------
 constexpr int kTileElems = 8192;  // 16 KB per operand per stage
 constexpr int kStages = 4;
@@ -367,6 +395,42 @@ int main() {
     int o = occ_of(v_tma, 256, smem);
     snprintf(buf, sizeof buf, "tma 4x16KB ring grid=%dx%d pdl", sms, o);
     per_tensor(v_tma, 256, o, smem, buf, true, false);
+  }
+
+  // K2 probe variants (read g only, 2 B/elem)
+  {
+    double* part;
+    CK(cudaMalloc(&part, sizeof(double) * (1 << 20)));
+    const double gbp = 2.0 * total / 1e9;
+    auto probe_pass = [&](auto kern, int64_t min_per, int64_t max_ctas, const char* name) {
+      float ms = time_passes([&] {
+        for (int i = (int)ts.size() - 1; i >= 0; --i) {
+          const int64_t nvec = ts[i].n / 8;
+          int64_t per = (nvec + max_ctas - 1) / max_ctas;
+          per = (per + min_per - 1) / min_per * min_per;
+          if (per < min_per) per = min_per;
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3((unsigned)((nvec + per - 1) / per));
+          cfg.blockDim = dim3(256);
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[0].val.programmaticStreamSerializationAllowed = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          CK(cudaLaunchKernelEx(&cfg, kern, (const bf*)ts[i].g, nvec, per, part));
+        }
+      }, 10);
+      printf("%-44s %8.3f ms  %7.1f GB/s\n", name, ms, gbp / (ms * 1e-3));
+    };
+    probe_pass(v_probe<1>, 256, 1 << 20, "probe 256 vec/CTA u1");
+    probe_pass(v_probe<2>, 512, 1 << 20, "probe 512 vec/CTA u2");
+    probe_pass(v_probe<4>, 1024, 1 << 20, "probe 1024 vec/CTA u4");
+    probe_pass(v_probe<4>, 1024, 4096, "probe >=1024 vec/CTA u4, <=4096 CTAs");
+    probe_pass(v_probe<4>, 2048, 1 << 20, "probe 2048 vec/CTA u4");
+    probe_pass(v_probe<8>, 2048, 1 << 20, "probe 2048 vec/CTA u8");
+    probe_pass(v_probe<8>, 4096, 1 << 20, "probe 4096 vec/CTA u8");
+    probe_pass(v_probe<8>, 8192, 1 << 20, "probe 8192 vec/CTA u8");
+    probe_pass(v_probe<16>, 8192, 1 << 20, "probe 8192 vec/CTA u16");
   }
 
   // one flat launch over the biggest tensor only (in-kernel efficiency)

@@ -1,0 +1,53 @@
+"""Profile one LLaMA-7B LOMO step (config 3) with torch.profiler: GPU time by
+kernel family vs wall time, to see where the step goes.
+
+    python tools/train_profile.py [--seq 1024] [--batch 1] [--layers 32]
+"""
+import argparse
+import sys
+from collections import defaultdict
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+from paper_2306_09782_b200 import LOMO, LossScaler  # noqa: E402
+from paper_2306_09782_b200.workloads import Llama  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--seq", type=int, default=1024)
+ap.add_argument("--batch", type=int, default=1)
+ap.add_argument("--layers", type=int, default=None)
+ap.add_argument("--ckpt", action="store_true")
+a = ap.parse_args()
+torch.cuda.set_device(0)
+model = Llama("7b", dtype=torch.float16, device="cuda", layers=a.layers, checkpointing=a.ckpt)
+opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 10))
+d = torch.randint(0, 32000, (a.batch, a.seq + 1), device="cuda")
+step = lambda: opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
+for _ in range(3):
+    step()
+torch.cuda.synchronize()
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+fam = defaultdict(float)
+total = 0.0
+for e in prof.key_averages():
+    if e.device_type.name != "CUDA":
+        continue
+    t = e.self_device_time_total
+    total += t
+    n = e.key
+    k = ("k1_update" if "k1_update" in n else "k2_probe" if "k2_probe" in n else
+         "k3/begin" if ("k3_" in n or "k_begin" in n) else
+         "gemm" if any(s in n.lower() for s in ("gemm", "sm100", "cutlass", "nvjet", "xmma")) else
+         "attention" if any(s in n.lower() for s in ("flash", "fmha", "attention", "sdpa")) else
+         "elementwise/other")
+    fam[k] += t
+print(f"GPU time per step: {total / 2 / 1e3:.2f} ms")
+for k, v in sorted(fam.items(), key=lambda x: -x[1]):
+    print(f"  {k:20s} {v / 2 / 1e3:8.2f} ms  {100 * v / total:5.1f}%")
+print(prof.key_averages().table(sort_by="self_cuda_time_total", row_limit=25))
