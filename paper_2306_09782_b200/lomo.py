@@ -33,7 +33,9 @@ from typing import Callable
 import torch
 
 from . import _lib
+from . import replay as _replay
 from .engine import CudaEngine, dtype_code
+from .replay import ReplayStash
 from .errors import (ConfigError, NonFiniteLossError, ScaleUnderflowError, ShapeError,
                      TapeStateError)
 from .stabilize import ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome
@@ -161,9 +163,13 @@ class _Protocol:
                                      "before fused_backward(loss, lr)")
             pending, self._pending = self._pending, None
             if pending == "skip":
+                self._drop_stash()
                 return
             self.engine.configure(lr, self.clip_value, self.weight_decay, flags)
-            self._run_backward(self._scaled(loss), _UPDATE, False)
+            if getattr(self, "_stash", None) is not None:
+                self._replay_pass(lr)
+            else:
+                self._run_backward(self._scaled(loss), _UPDATE, False)
             self.engine.on_clean()
             self._after_update()
             self.last_outcome = StepOutcome.APPLIED
@@ -182,6 +188,11 @@ class _Protocol:
     def _after_update(self) -> None:
         pass
 
+    def _drop_stash(self) -> None:
+        st = getattr(self, "_stash", None)
+        if st is not None:
+            st.clear()
+
     def step(self, closure: Callable[[], torch.Tensor], lr: float | None = None,
              recompute_forward: bool = False) -> float:
         """The reference step protocol (optim.py:118-132, stabilize.py:148-230).
@@ -193,11 +204,12 @@ class _Protocol:
         """
         loss = closure()
         if self.passes == 2:
-            self.grad_norm(loss, retain_graph=not recompute_forward)
+            replay = getattr(self, "_stash", None) is not None
+            self.grad_norm(loss, retain_graph=not (recompute_forward or replay))
             if self._pending == "skip":
                 self._pending = None
                 return float(loss.detach())
-            if recompute_forward:
+            if recompute_forward and not replay:
                 loss = closure()
             self.fused_backward(loss, lr)
             return float(loss.detach())
@@ -236,12 +248,16 @@ class LOMO(_Protocol):
             overlaps the rest of the backward (a few gradients may be alive at
             once instead of one; off by default to keep the reference's
             one-gradient invariant).
+        replay: two-pass mode only -- pass 2 recomputes each weight gradient
+            from the (input, output-gradient) pair stashed in pass 1 instead of
+            running a second backward (see replay.py); the model's linears
+            must go through ``paper_2306_09782_b200.replay.linear``.
     """
 
     def __init__(self, model, lr: float = 1e-3, clip_grad_norm: float | None = None,
                  loss_scale=None, *, clip_grad_value: float | None = None,
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
-                 math: str = "f32", overlap: bool = False):
+                 math: str = "f32", overlap: bool = False, replay: bool = False):
         if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
             raise ConfigError("pass either a Stabilizer or the clip/loss_scale arguments")
         st = stabilizer if stabilizer is not None else stabilizer_from_args(
@@ -268,6 +284,10 @@ class LOMO(_Protocol):
         self._slot = {id(p): i for i, p in enumerate(reversed(uniq))}
         self._mode = 0
         self.hook_calls = 0
+        if replay and self.passes != 2:
+            raise ConfigError("replay applies to the two-pass protocol (clip_grad_norm / loss_scale)")
+        self._stash = ReplayStash() if replay else None
+        self._largest = max(p.numel() * p.element_size() for p in uniq)
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in uniq]
 
     def _hook(self, p: torch.Tensor) -> None:
@@ -284,6 +304,9 @@ class LOMO(_Protocol):
             g = g.contiguous()
         if mode == _PROBE:
             self.engine.probe(g, self._slot[id(p)])
+            st = self._stash
+            if st is not None and id(p) not in st.linear:
+                st.grads[id(p)] = g  # not a replayable linear: keep its gradient
         else:
             self.engine.update(p, g)
         self.hook_calls += 1
@@ -295,11 +318,45 @@ class LOMO(_Protocol):
                 raise TapeStateError("a parameter already holds a gradient; LOMO consumes "
                                      "gradients inside backward (call zero_grad(set_to_none=True))")
         self._mode = mode
+        stash = self._stash if (mode == _PROBE and self._stash is not None) else None
+        if stash is not None:
+            stash.clear()
+            _replay._ACTIVE = stash
+            retain_graph = False  # pass 2 replays from the stash, not from the graph
         try:
             target.backward(retain_graph=retain_graph)
         finally:
             self._mode = 0
+            if stash is not None:
+                _replay._ACTIVE = None
             self.engine.flush()  # the parked tiny tensors, same stream as the hooks
+        if stash is not None:
+            kept = sum(g.numel() * g.element_size() for g in stash.grads.values())
+            if kept > 2 * self._largest:
+                stash.clear()
+                raise ConfigError(
+                    f"replay would keep {kept / 2**20:.0f} MiB of gradients: route the model's "
+                    "linear layers through paper_2306_09782_b200.replay.linear")
+
+    def _replay_pass(self, lr: float) -> None:
+        """Pass 2 from the stash: dW = dy^T x (the pass-1 GEMM) -> K1, in
+        delivery order; every gradient is dropped right after its launch."""
+        st = self._stash
+        for p in reversed(self.params):
+            pid = id(p)
+            if pid in st.linear:
+                x, dy = st.linear.pop(pid)
+                g = _replay.weight_grad(x, dy)
+                del x, dy
+            elif pid in st.grads:
+                g = st.grads.pop(pid)
+            else:
+                continue  # no gradient this step (unused parameter)
+            self.engine.update(p, g)
+            self.hook_calls += 1
+            del g
+        self.engine.flush()
+        st.clear()
 
     def _decide(self) -> None:
         self.engine.finalize()

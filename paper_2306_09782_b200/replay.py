@@ -1,0 +1,69 @@
+"""Pass-2 replay for the two-pass protocol (an optional caller-side speedup).
+
+The reference's two-pass step (stabilize.py:180-230) runs a second forward
+and a second full backward only to regenerate the gradients that pass 1
+already produced (pass 1 leaves parameters untouched, so they are identical).
+On B200 the memory is there to avoid most of that work: during pass 1 every
+linear layer routed through :func:`linear` keeps its input ``x`` (already
+saved by autograd) and its output gradient ``dy`` (~2.8 GB for LLaMA-7B at
+seq 1024), and every other parameter (norm scales, embedding) keeps its
+gradient.  Pass 2 then recomputes each weight gradient with exactly the
+GEMM autograd used in pass 1 (``dy^T x``) and hands it straight to K1 --
+no second forward, no input-gradient GEMMs, no elementwise backward.
+
+The update arithmetic is untouched: K1 sees bit-identical gradients to the
+ones K2 probed (same kernels, same inputs).  Enabled with
+``LOMO(..., replay=True)``; models opt in by calling :func:`linear` instead of
+``F.linear`` (``workloads.Llama`` does).
+"""
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+
+_ACTIVE: "ReplayStash | None" = None
+
+
+class ReplayStash:
+    def __init__(self):
+        self.linear: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
+        self.grads: dict[int, torch.Tensor] = {}
+
+    def clear(self):
+        self.linear.clear()
+        self.grads.clear()
+
+    def nbytes(self) -> int:
+        n = sum(x.numel() * x.element_size() + d.numel() * d.element_size()
+                for x, d in self.linear.values())
+        return n + sum(g.numel() * g.element_size() for g in self.grads.values())
+
+
+def weight_grad(x: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
+    """dW = dy^T x for y = x W^T (W: [out, in]) -- the one GEMM both passes use."""
+    return dy.reshape(-1, dy.shape[-1]).t().mm(x.reshape(-1, x.shape[-1]))
+
+
+class _StashLinear(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w):
+        ctx.save_for_backward(x, w)
+        ctx.wid = id(w)
+        return F.linear(x, w)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, w = ctx.saved_tensors
+        dx = dy.matmul(w) if ctx.needs_input_grad[0] else None
+        dw = weight_grad(x, dy) if ctx.needs_input_grad[1] else None
+        st = _ACTIVE
+        if st is not None:
+            st.linear[ctx.wid] = (x, dy)
+        return dx, dw
+
+
+def linear(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """``F.linear(x, w)`` whose backward can stash (x, dy) for pass-2 replay."""
+    if torch.is_grad_enabled() and w.requires_grad:
+        return _StashLinear.apply(x, w)
+    return F.linear(x, w)

@@ -29,6 +29,8 @@ import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
+from .replay import linear as rlinear
+
 INIT_RANGE = 0.08   # zoo.py:26
 RMSNORM_EPS = 1e-5  # zoo.py:27
 
@@ -237,14 +239,14 @@ class LlamaLayer(nn.Module):
         b, s, h = x.shape
         nh, dh = self.nh, h // self.nh
         a = self.input_layernorm(x)
-        q = F.linear(a, self.q).view(b, s, nh, dh).transpose(1, 2)
-        k = F.linear(a, self.k).view(b, s, nh, dh).transpose(1, 2)
-        v = F.linear(a, self.v).view(b, s, nh, dh).transpose(1, 2)
+        q = rlinear(a, self.q).view(b, s, nh, dh).transpose(1, 2)
+        k = rlinear(a, self.k).view(b, s, nh, dh).transpose(1, 2)
+        v = rlinear(a, self.v).view(b, s, nh, dh).transpose(1, 2)
         q, k = _rope(q, cos, sin), _rope(k, cos, sin)
         o = F.scaled_dot_product_attention(q, k, v, is_causal=True)
-        x = x + F.linear(o.transpose(1, 2).reshape(b, s, h), self.o)
+        x = x + rlinear(o.transpose(1, 2).reshape(b, s, h), self.o)
         y = self.post_attention_layernorm(x)
-        return x + F.linear(F.silu(F.linear(y, self.gate)) * F.linear(y, self.up), self.down)
+        return x + rlinear(F.silu(rlinear(y, self.gate)) * rlinear(y, self.up), self.down)
 
 
 def _rope(x, cos, sin):
@@ -295,7 +297,7 @@ class Llama(nn.Module):
                 x = torch.utils.checkpoint.checkpoint(layer, x, cos, sin, use_reentrant=False)
             else:
                 x = layer(x, cos, sin)
-        return F.linear(self.norm(x), self.lm_head)
+        return rlinear(self.norm(x), self.lm_head)
 
     def loss(self, ids, targets):
         logits = self(ids)

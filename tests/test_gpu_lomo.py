@@ -340,3 +340,41 @@ def test_checkpointing_is_transparent(two_pass):
         assert calls["n"] == 3 * 3 * (1 + passes)
     finally:
         torch.use_deterministic_algorithms(False)
+
+
+# --- pass-2 replay (replay.py) ---------------------------------------------------
+
+@pytest.mark.parametrize("dtype,mode", [(torch.float64, "f64"), (torch.bfloat16, "f32")])
+def test_replay_equals_second_backward(dtype, mode):
+    """Replaying pass 2 from the stashed (x, dy) gives the very gradients a
+    second backward produces: identical parameters (deterministic kernels)."""
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=64, layers=2, heads=4, ffn=128, vocab=128)
+    torch.use_deterministic_algorithms(True, warn_only=True)
+    try:
+        a = Llama(cfg, dtype=dtype, device="cuda", seed=0)
+        b = Llama(cfg, dtype=dtype, device="cuda", seed=0)
+        oa = LOMO(a, lr=0.05, clip_grad_norm=0.3, loss_scale=2.0 ** 8, math=mode)
+        ob = LOMO(b, lr=0.05, clip_grad_norm=0.3, loss_scale=2.0 ** 8, math=mode, replay=True)
+        g = torch.Generator(device="cuda").manual_seed(4)
+        for step in range(3):
+            d = torch.randint(0, 128, (2, 17), device="cuda", generator=g)
+            la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+            lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+            assert la == lb and oa.last_outcome == ob.last_outcome
+            assert ob.hook_calls == oa.hook_calls
+        for x, y in zip(a.parameters(), b.parameters()):
+            assert torch.equal(x, y)
+        assert ob._stash.nbytes() == 0  # stash released after the replay
+    finally:
+        torch.use_deterministic_algorithms(False)
+
+
+def test_replay_refuses_models_without_replayable_linears():
+    from paper_2306_09782_b200 import ConfigError
+    cfg = MiniConfig(layers=1, hidden=64, heads=2, vocab=128, seed=0)
+    model = MiniTransformer(cfg, dtype=torch.float32, device="cuda")   # uses x @ W
+    opt = LOMO(model, lr=0.05, clip_grad_norm=1.0, replay=True)
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 2, 8, 128)).cuda()
+    with pytest.raises(ConfigError):
+        opt.step(lambda: mean_cross_entropy(model(ids), ids), 0.05)
