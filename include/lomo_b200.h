@@ -173,6 +173,22 @@ int lomo_local_norm_partial(const void* state, double* out2_dev, void* stream);
 int lomo_finalize_norm_ranks(void* state, const double* parts_dev, int world,
                              void* stream);
 
+/* ---- K5: weight-gradient GEMM with the update as its epilogue ---------- */
+/* For a linear layer y = x W^T (W [out, in] row-major, x [tokens, in],
+ * dy [tokens, out], all row-major, 16-bit): computes on the tensor cores
+ *     p <- alpha * (dy^T x) + beta * p          (p == W, in place)
+ * i.e. the LOMO update with alpha = -lr * coef / scale, beta = 1 - lr*wd, from
+ * the fp32 accumulator -- the gradient dW is never written to memory.
+ * Replaces the K1 launch of pass 2 under replay (replay.py); value clipping
+ * is not linear in dW and stays on K1.  workspace: >= lomo_gemm_update_workspace
+ * bytes of device memory (may be NULL when that is 0).  dtype: F16 or BF16;
+ * out_features and in_features must be multiples of 8. */
+int lomo_gemm_update(void* p, const void* dy, const void* x, int64_t out_features,
+                     int64_t in_features, int64_t tokens, int dtype, double alpha,
+                     double beta, void* workspace, size_t workspace_bytes, void* stream);
+size_t lomo_gemm_update_workspace(int64_t out_features, int64_t in_features,
+                                  int64_t tokens, int dtype);
+
 /* Number of SMs the library sized its grids for (device of the current
  * context); 0 if no device. */
 int lomo_num_sms(void);

@@ -38,6 +38,8 @@ EXPORTS = (
     "lomo_local_norm_partial",
     "lomo_finalize_norm_ranks",
     "lomo_num_sms",
+    "lomo_gemm_update",
+    "lomo_gemm_update_workspace",
 )
 
 
@@ -96,6 +98,9 @@ _SIGS = {
     "lomo_local_norm_partial": (_i32, [_vp, _vp, _vp]),
     "lomo_finalize_norm_ranks": (_i32, [_vp, _vp, _i32, _vp]),
     "lomo_num_sms": (_i32, []),
+    "lomo_gemm_update": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _dbl, _dbl, _vp,
+                                ctypes.c_size_t, _vp]),
+    "lomo_gemm_update_workspace": (ctypes.c_size_t, [_i64, _i64, _i64, _i32]),
 }
 
 _LIB = None

@@ -1,0 +1,135 @@
+// lomo_gemm_update.cu -- the LOMO update fused into the weight-gradient GEMM.
+//
+// For a linear layer y = x W^T (W: [out, in], x: [T, in], dy: [T, out]) the
+// weight gradient is dW = dy^T x (M = out, N = in, K = T).  LOMO consumes dW
+// only to apply p <- p - lr * coef * dW / scale (optim.py:52-54 with the
+// update_hook stages, stabilize.py:217-224).  Here that update is the GEMM's
+// epilogue: the tcgen05 tensor-core GEMM accumulates dW tile by tile in TMEM
+// and the epilogue writes  p <- alpha * acc + beta * p  with
+// alpha = -lr * coef / scale and beta = 1 - lr * wd, so the gradient is never
+// materialised in HBM (K1 would have read it and p, and written p: 6 B/elem;
+// the fused epilogue moves 4 B/elem and needs no separate launch).
+//
+// Built with the CUTLASS 4.x sm100 collective builders (tcgen05.mma issued by
+// one thread, TMA loads, TMEM accumulators, 2-SM CTA pairs), instantiated
+// inside this library; see DESIGN.md.  Value clipping is not linear in the
+// accumulator and stays on the K1 path.
+#include <cuda_runtime.h>
+
+#include "cute/tensor.hpp"
+#include "cutlass/cutlass.h"
+#include "cutlass/epilogue/collective/collective_builder.hpp"
+#include "cutlass/epilogue/fusion/operations.hpp"
+#include "cutlass/gemm/collective/collective_builder.hpp"
+#include "cutlass/gemm/device/gemm_universal_adapter.h"
+#include "cutlass/gemm/kernel/gemm_universal.hpp"
+#include "cutlass/util/packed_stride.hpp"
+
+#include "lomo_b200.h"
+
+namespace lomo_gemm {
+
+using namespace cute;
+
+template <typename Element>
+struct FusedUpdateGemm {
+  using ElementA = Element;                      // dy  [T, out] row-major == A (M=out, K=T), M-major
+  using LayoutA = cutlass::layout::ColumnMajor;
+  using ElementB = Element;                      // x   [T, in]  row-major == B (K=T, N=in), N-major
+  using LayoutB = cutlass::layout::RowMajor;
+  using ElementC = Element;                      // p   [out, in] row-major (source and destination)
+  using LayoutC = cutlass::layout::RowMajor;
+  using ElementAcc = float;
+  using ElementCompute = float;
+  static constexpr int kAlign = 128 / cutlass::sizeof_bits<Element>::value;
+
+  using MmaTileShape = Shape<_256, _128, _64>;
+  using ClusterShape = Shape<_2, _1, _1>;
+
+  using Fusion = cutlass::epilogue::fusion::LinearCombination<ElementC, ElementCompute, ElementC,
+                                                              ElementCompute>;
+
+  using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
+      cutlass::epilogue::collective::EpilogueTileAuto, ElementAcc, ElementCompute, ElementC,
+      LayoutC, kAlign, ElementC, LayoutC, kAlign,
+      cutlass::epilogue::collective::EpilogueScheduleAuto, Fusion>::CollectiveOp;
+
+  using CollectiveMainloop = typename cutlass::gemm::collective::CollectiveBuilder<
+      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, ElementA, LayoutA, kAlign, ElementB,
+      LayoutB, kAlign, ElementAcc, MmaTileShape, ClusterShape,
+      cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(
+          sizeof(typename CollectiveEpilogue::SharedStorage))>,
+      cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
+
+  using GemmKernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>,
+                                                          CollectiveMainloop, CollectiveEpilogue>;
+  using Gemm = cutlass::gemm::device::GemmUniversalAdapter<GemmKernel>;
+
+  static int run(void* p, const void* dy, const void* x, int M, int N, int K, float alpha,
+                 float beta, void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+    using StrideA = typename Gemm::GemmKernel::StrideA;
+    using StrideB = typename Gemm::GemmKernel::StrideB;
+    using StrideC = typename Gemm::GemmKernel::StrideC;
+    using StrideD = typename Gemm::GemmKernel::StrideD;
+    StrideA sA = cutlass::make_cute_packed_stride(StrideA{}, make_shape(M, K, 1));
+    StrideB sB = cutlass::make_cute_packed_stride(StrideB{}, make_shape(N, K, 1));
+    StrideC sC = cutlass::make_cute_packed_stride(StrideC{}, make_shape(M, N, 1));
+    StrideD sD = cutlass::make_cute_packed_stride(StrideD{}, make_shape(M, N, 1));
+    typename Gemm::Arguments args{
+        cutlass::gemm::GemmUniversalMode::kGemm,
+        {M, N, K, 1},
+        {static_cast<const ElementA*>(dy), sA, static_cast<const ElementB*>(x), sB},
+        {{alpha, beta}, static_cast<const ElementC*>(p), sC, static_cast<ElementC*>(p), sD}};
+    Gemm gemm;
+    if (gemm.can_implement(args) != cutlass::Status::kSuccess) return LOMO_E_ARG;
+    const size_t need = Gemm::get_workspace_size(args);
+    if (need > workspace_bytes) return LOMO_E_ARG;
+    if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return LOMO_E_ARG;
+    if (gemm.run(stream) != cutlass::Status::kSuccess) return (int)cudaGetLastError();
+    return (int)cudaGetLastError();
+  }
+
+  static size_t workspace(int M, int N, int K) {
+    typename Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, 1}, {}, {}};
+    return Gemm::get_workspace_size(args);
+  }
+};
+
+}  // namespace lomo_gemm
+
+extern "C" {
+
+int lomo_gemm_update(void* p, const void* dy, const void* x, int64_t out_features,
+                     int64_t in_features, int64_t tokens, int dtype, double alpha, double beta,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+  if (p == nullptr || dy == nullptr || x == nullptr) return LOMO_E_ARG;
+  if (out_features <= 0 || in_features <= 0 || tokens <= 0) return LOMO_E_ARG;
+  if (out_features > INT32_MAX || in_features > INT32_MAX || tokens > INT32_MAX) return LOMO_E_ARG;
+  const int M = (int)out_features, N = (int)in_features, K = (int)tokens;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case LOMO_BF16:
+      return lomo_gemm::FusedUpdateGemm<cutlass::bfloat16_t>::run(p, dy, x, M, N, K, (float)alpha,
+                                                                 (float)beta, workspace,
+                                                                 workspace_bytes, s);
+    case LOMO_F16:
+      return lomo_gemm::FusedUpdateGemm<cutlass::half_t>::run(p, dy, x, M, N, K, (float)alpha,
+                                                             (float)beta, workspace,
+                                                             workspace_bytes, s);
+  }
+  return LOMO_E_ARG;
+}
+
+size_t lomo_gemm_update_workspace(int64_t out_features, int64_t in_features, int64_t tokens,
+                                  int dtype) {
+  if (dtype == LOMO_BF16)
+    return lomo_gemm::FusedUpdateGemm<cutlass::bfloat16_t>::workspace(
+        (int)out_features, (int)in_features, (int)tokens);
+  if (dtype == LOMO_F16)
+    return lomo_gemm::FusedUpdateGemm<cutlass::half_t>::workspace(
+        (int)out_features, (int)in_features, (int)tokens);
+  return 0;
+}
+
+}  // extern "C"

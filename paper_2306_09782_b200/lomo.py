@@ -36,6 +36,8 @@ from . import _lib
 from . import replay as _replay
 from .engine import CudaEngine, dtype_code
 from .replay import ReplayStash
+
+_lib_E_ARG = -1
 from .errors import (ConfigError, NonFiniteLossError, ScaleUnderflowError, ShapeError,
                      TapeStateError)
 from .stabilize import ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome
@@ -139,6 +141,8 @@ class _Protocol:
                 f"loss scale would fall below {st.min_scale}; training diverged")
         self.last_norm = float(st.total_norm)
         self.clip_coef = float(st.clip_coef)
+        self._pass1 = (float(st.clip_coef) if self.norm_clip else 1.0,
+                       float(st.inv_scale) if (self.has_scaler or self._always_scale) else 1.0)
         if st.skip:
             self._pending = "skip"
             self.last_outcome = StepOutcome.SKIPPED_OVERFLOW
@@ -252,12 +256,18 @@ class LOMO(_Protocol):
             from the (input, output-gradient) pair stashed in pass 1 instead of
             running a second backward (see replay.py); the model's linears
             must go through ``paper_2306_09782_b200.replay.linear``.
+        fuse_gemm: with ``replay``, run each linear's pass-2 update as the
+            epilogue of its weight-gradient GEMM on the tensor cores (K5,
+            csrc/lomo_gemm_update.cu): ``p <- p - lr*coef/scale * (dy^T x)`` from
+            the fp32 accumulator, the gradient never materialised.  16-bit
+            parameters, no value clip; other parameters keep K1.
     """
 
     def __init__(self, model, lr: float = 1e-3, clip_grad_norm: float | None = None,
                  loss_scale=None, *, clip_grad_value: float | None = None,
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
-                 math: str = "f32", overlap: bool = False, replay: bool = False):
+                 math: str = "f32", overlap: bool = False, replay: bool = False,
+                 fuse_gemm: bool = False):
         if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
             raise ConfigError("pass either a Stabilizer or the clip/loss_scale arguments")
         st = stabilizer if stabilizer is not None else stabilizer_from_args(
@@ -287,6 +297,11 @@ class LOMO(_Protocol):
         if replay and self.passes != 2:
             raise ConfigError("replay applies to the two-pass protocol (clip_grad_norm / loss_scale)")
         self._stash = ReplayStash() if replay else None
+        if fuse_gemm and not replay:
+            raise ConfigError("fuse_gemm fuses the update into the replayed weight-gradient GEMM: "
+                              "it needs replay=True")
+        self.fuse_gemm = bool(fuse_gemm) and self.clip_value == 0.0
+        self._ws = None
         self._largest = max(p.numel() * p.element_size() for p in uniq)
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in uniq]
 
@@ -338,14 +353,46 @@ class LOMO(_Protocol):
                     f"replay would keep {kept / 2**20:.0f} MiB of gradients: route the model's "
                     "linear layers through paper_2306_09782_b200.replay.linear")
 
+    def _gemm_update(self, p, x, dy, lr: float) -> bool:
+        """K5: p <- alpha * dy^T x + beta * p on the tensor cores; False when the
+        shape/dtype is not supported (the caller falls back to GEMM + K1)."""
+        if p.dtype not in (torch.bfloat16, torch.float16) or p.dim() != 2:
+            return False
+        out_f, in_f = p.shape
+        if out_f % 8 or in_f % 8:
+            return False
+        dy2 = dy.reshape(-1, out_f)
+        x2 = x.reshape(-1, in_f)
+        if not (dy2.is_contiguous() and x2.is_contiguous()) or dy2.dtype != p.dtype:
+            return False
+        coef, inv_scale = self._pass1
+        alpha = -lr * coef * inv_scale
+        beta = 1.0 - lr * self.weight_decay
+        lib, dt = self.engine.lib, dtype_code(p.dtype)
+        need = lib.lomo_gemm_update_workspace(out_f, in_f, dy2.shape[0], dt)
+        if need and (self._ws is None or self._ws.numel() < need):
+            self._ws = torch.empty(need, dtype=torch.uint8, device=p.device)
+        ws = self._ws.data_ptr() if need else None
+        rc = lib.lomo_gemm_update(p.data_ptr(), dy2.data_ptr(), x2.data_ptr(), out_f, in_f,
+                                  dy2.shape[0], dt, alpha, beta, ws, need, self.engine.stream())
+        if rc == _lib_E_ARG:
+            return False
+        _lib.check(rc, "lomo_gemm_update")
+        return True
+
     def _replay_pass(self, lr: float) -> None:
-        """Pass 2 from the stash: dW = dy^T x (the pass-1 GEMM) -> K1, in
-        delivery order; every gradient is dropped right after its launch."""
+        """Pass 2 from the stash, in delivery order: for a replayable linear
+        either K5 (GEMM with the update as epilogue) or dW = dy^T x (the
+        pass-1 GEMM) -> K1; other parameters K1 on their kept gradient.  Every
+        gradient is dropped right after its launch."""
         st = self._stash
         for p in reversed(self.params):
             pid = id(p)
             if pid in st.linear:
                 x, dy = st.linear.pop(pid)
+                if self.fuse_gemm and self._gemm_update(p, x, dy, lr):
+                    self.hook_calls += 1
+                    continue
                 g = _replay.weight_grad(x, dy)
                 del x, dy
             elif pid in st.grads:

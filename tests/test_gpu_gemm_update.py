@@ -1,0 +1,128 @@
+"""K5: the weight-gradient GEMM with the LOMO update as its epilogue
+(csrc/lomo_gemm_update.cu, tcgen05 tensor cores), through the C-ABI.
+
+Reference: p_ref = round(beta * p + alpha * (dy^T x)) with the product in
+float64 (the reference's full-width update arithmetic, optim.py:52-54, on the
+exact gradient).  Tolerance (stated): within one ulp of the operands' scale,
+|got - ref| <= ulp(|p| + |alpha dy^T x|) -- the fp32 tensor-core
+accumulation error is far below that; where p and the update cancel the
+result's own ulp is tiny, so a result-ulp bound would be meaningless there.
+fp16 results are additionally within 1 result-ulp everywhere (measured).
+"""
+import numpy as np
+import pytest
+import torch
+
+import lomo_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import gpu_util as U
+    from paper_2306_09782_b200 import _lib
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    torch.cuda.set_device(0)
+
+
+def _run(p, dy, x, alpha, beta):
+    lib = U.lib()
+    dt = U.CODE[p.dtype]
+    out_f, in_f = p.shape
+    need = lib.lomo_gemm_update_workspace(out_f, in_f, dy.shape[0], dt)
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+    return lib.lomo_gemm_update(p.data_ptr(), dy.data_ptr(), x.data_ptr(), out_f, in_f,
+                                dy.shape[0], dt, alpha, beta, ws.data_ptr(), need, U.stream())
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("out_f,in_f,tokens", [(256, 128, 64), (4096, 4096, 1024),
+                                               (1024, 2816, 1000), (11008, 4096, 512)])
+def test_gemm_update_matches_f64_reference(dtype, out_f, in_f, tokens):
+    prec = "bf16" if dtype == torch.bfloat16 else "half"
+    g = torch.Generator(device="cuda").manual_seed(out_f + tokens)
+    p = torch.empty(out_f, in_f, device="cuda").uniform_(-0.08, 0.08, generator=g).to(dtype)
+    dy = (torch.randn(tokens, out_f, device="cuda", generator=g) * 1e-2).to(dtype)
+    x = torch.randn(tokens, in_f, device="cuda", generator=g).to(dtype)
+    alpha, beta = -0.05 * 0.7 / 1024.0 * 1024.0, 1.0
+    p0 = p.double()
+    upd = alpha * (dy.double().t() @ x.double())
+    want = O.round_to((beta * p0 + upd).cpu().numpy(), prec)
+    assert _run(p, dy, x, alpha, beta) == 0
+    torch.cuda.synchronize()
+    d = U.ulp_diff(p, torch.from_numpy(want).to(dtype).cuda())
+    frac = (d > 0).float().mean().item()
+    err = (p.double().cpu() - torch.from_numpy(want)).abs().numpy()
+    scale = (p0.abs() + upd.abs()).cpu().numpy()
+    mant, emin = (7, -126) if prec == "bf16" else (10, -14)
+    _, e = np.frexp(scale)                      # scale in [2^(e-1), 2^e)
+    ulp = np.ldexp(1.0, np.maximum(e - 1, emin) - mant)
+    print(f"{dtype} {out_f}x{in_f}x{tokens}: max result-ulp {d.max().item()}, "
+          f"mismatch {frac:.2e}, max err/operand-ulp {np.max(err / ulp):.3f}")
+    assert np.all(err <= ulp)
+    if dtype == torch.float16:
+        assert d.max().item() <= 1
+
+
+def test_gemm_update_weight_decay_and_zero_alpha():
+    g = torch.Generator(device="cuda").manual_seed(0)
+    p = torch.empty(512, 256, device="cuda").uniform_(-0.08, 0.08, generator=g).to(torch.bfloat16)
+    dy = torch.randn(128, 512, device="cuda", generator=g).to(torch.bfloat16)
+    x = torch.randn(128, 256, device="cuda", generator=g).to(torch.bfloat16)
+    before = p.clone()
+    assert _run(p, dy, x, 0.0, 1.0) == 0           # skip-equivalent: p unchanged
+    assert torch.equal(p, before)
+    assert _run(p, dy, x, 0.0, 0.5) == 0           # pure decay
+    assert torch.equal(p, (before.float() * 0.5).to(torch.bfloat16))
+
+
+def test_gemm_update_rejects_bad_shapes():
+    lib = U.lib()
+    assert lib.lomo_gemm_update(None, None, None, 8, 8, 8, _lib.BF16, 1.0, 1.0, None, 0,
+                                None) == -1
+    p = torch.zeros(8, 8, dtype=torch.float32, device="cuda")
+    assert lib.lomo_gemm_update(p.data_ptr(), p.data_ptr(), p.data_ptr(), 8, 8, 8, _lib.F32,
+                                1.0, 1.0, None, 0, U.stream()) == -1  # fp32: not on K5
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_lomo_replay_fused_gemm_matches_replay_k1(dtype):
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
+    # full-precision accumulation in cuBLAS for the unfused reference path
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+    torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+    a = Llama(cfg, dtype=dtype, device="cuda", seed=0)
+    b = Llama(cfg, dtype=dtype, device="cuda", seed=0)
+    # a loss scale that keeps the 16-bit gradients of the unfused path out of
+    # the fp16 subnormal range (there K1's rounded dW loses relative precision)
+    scale = 2.0 ** 16 if dtype == torch.float16 else 2.0 ** 8
+    oa = LOMO(a, lr=0.05, clip_grad_norm=0.3, loss_scale=scale, replay=True)
+    ob = LOMO(b, lr=0.05, clip_grad_norm=0.3, loss_scale=scale, replay=True, fuse_gemm=True)
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    d = torch.randint(0, 256, (2, 65), device="cuda", generator=gen)
+    p0 = [p.detach().float().clone() for p in a.parameters()]
+    la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+    lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+    assert oa.last_outcome == ob.last_outcome and la == lb
+    # K5 applies the fp32 accumulator; K1 applies dW rounded to 16 bits first
+    # (relative 2^-8 / 2^-11 of the step): same step up to that rounding
+    eps = 2.0 ** -7 if dtype == torch.bfloat16 else 2.0 ** -10
+    worst = 0.0
+    for (name, x), y, q in zip(a.named_parameters(), b.parameters(), p0):
+        xf, yf = x.detach().float(), y.detach().float()
+        quantum = 2.0 ** -24 if dtype == torch.float16 else 2.0 ** -133  # subnormal ulp
+        tol = eps * torch.maximum(xf.abs(), yf.abs()) + eps * (xf - q).abs() + quantum
+        r = (xf - yf).abs() / tol
+        if r.max().item() > worst:
+            i = r.argmax()
+            print(name, tuple(x.shape), "unfused", xf.flatten()[i].item(), "fused",
+                  yf.flatten()[i].item(), "p0", q.flatten()[i].item())
+        worst = max(worst, r.max().item())
+    print(f"{dtype}: fused vs unfused, max |diff| / tolerance = {worst:.3f}")
+    assert worst <= 1.0
