@@ -43,7 +43,7 @@ struct FusedUpdateGemm {
   using ElementCompute = float;
   static constexpr int kAlign = 128 / cutlass::sizeof_bits<Element>::value;
 
-  using MmaTileShape = Shape<_256, _128, _64>;
+  using MmaTileShape = Shape<_256, _256, _64>;
   using ClusterShape = Shape<_2, _1, _1>;
 
   using Fusion = cutlass::epilogue::fusion::LinearCombination<ElementC, ElementCompute, ElementC,
@@ -81,6 +81,9 @@ struct FusedUpdateGemm {
         {M, N, K, 1},
         {static_cast<const ElementA*>(dy), sA, static_cast<const ElementB*>(x), sB},
         {{alpha, beta}, static_cast<const ElementC*>(p), sC, static_cast<ElementC*>(p), sD}};
+    // persistent tile scheduler sized to the device (epilogue of tile i overlaps
+    // the mainloop of tile i+1 through the double-buffered TMEM accumulator)
+    args.hw_info = hw_info();
     Gemm gemm;
     if (gemm.can_implement(args) != cutlass::Status::kSuccess) return LOMO_E_ARG;
     const size_t need = Gemm::get_workspace_size(args);
@@ -92,7 +95,22 @@ struct FusedUpdateGemm {
 
   static size_t workspace(int M, int N, int K) {
     typename Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, 1}, {}, {}};
+    args.hw_info = hw_info();
     return Gemm::get_workspace_size(args);
+  }
+
+  static cutlass::KernelHardwareInfo hw_info() {
+    static int dev = -1, sms = 0;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d != dev) {
+      sms = cutlass::KernelHardwareInfo::query_device_multiprocessor_count(d);
+      dev = d;
+    }
+    cutlass::KernelHardwareInfo hw;
+    hw.device_id = d;
+    hw.sm_count = sms;
+    return hw;
   }
 };
 
