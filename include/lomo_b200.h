@@ -173,6 +173,23 @@ int lomo_local_norm_partial(const void* state, double* out2_dev, void* stream);
 int lomo_finalize_norm_ranks(void* state, const double* parts_dev, int world,
                              void* stream);
 
+/* ---- K4: reduce-scatter fused with the update (sharded mode) ---------- */
+/* Every rank's flat bucket gradient lives in symmetric (peer-mapped) memory;
+ * peer_bufs_dev is a DEVICE array of the `world` (<= 16) peer base pointers.
+ * Rank r owns elements [offset, offset+n) of the bucket: K4 loads that slice
+ * from every peer over NVLink, sums in rank order (deterministic) and applies
+ * the K1 update to p_shard (n elements) -- or, for the probe, the K2 sum of
+ * squares into `slot` -- without writing the reduced gradient anywhere.
+ * offset*sizeof(dtype) and n*sizeof(dtype) must be multiples of 16.
+ * Replaces NCCL reduce_scatter + K1/K2. */
+int lomo_fused_rs_update(void* p_shard, const void* const* peer_bufs_dev, int world,
+                         int64_t offset, int64_t n, int dtype, int math, double lr,
+                         double clip_value, double weight_decay, unsigned flags,
+                         const void* state, void* stream);
+int lomo_fused_rs_probe(const void* const* peer_bufs_dev, int world, int64_t offset,
+                        int64_t n, int dtype, int slot, unsigned flags, void* state,
+                        void* stream);
+
 /* ---- K5: weight-gradient GEMM with the update as its epilogue ---------- */
 /* For a linear layer y = x W^T (W [out, in] row-major, x [tokens, in],
  * dy [tokens, out], all row-major, 16-bit): computes on the tensor cores

@@ -40,6 +40,8 @@ EXPORTS = (
     "lomo_num_sms",
     "lomo_gemm_update",
     "lomo_gemm_update_workspace",
+    "lomo_fused_rs_update",
+    "lomo_fused_rs_probe",
 )
 
 
@@ -101,6 +103,9 @@ _SIGS = {
     "lomo_gemm_update": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _dbl, _dbl, _vp,
                                 ctypes.c_size_t, _vp]),
     "lomo_gemm_update_workspace": (ctypes.c_size_t, [_i64, _i64, _i64, _i32]),
+    "lomo_fused_rs_update": (_i32, [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _dbl, _dbl, _dbl,
+                                    _u32, _vp, _vp]),
+    "lomo_fused_rs_probe": (_i32, [_vp, _i32, _i64, _i64, _i32, _i32, _u32, _vp, _vp]),
 }
 
 _LIB = None

@@ -479,6 +479,101 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // --------------------------------------------------------------------------
+// K4: reduce-scatter fused with the update / probe over peer memory
+// --------------------------------------------------------------------------
+// Sharded mode: every rank's flat bucket gradient lives in symmetric memory
+// (peer-mapped over NVLink).  Rank r owns [off, off+n) of the bucket; K4 loads
+// that slice from all `world` peers' buffers (P2P loads through NVSwitch),
+// sums in the math type in rank order (deterministic), and feeds the sum
+// straight into the update (K1 arithmetic) or the sum of squares (K2): the
+// reduced gradient is never written to HBM.  Requires 16-byte aligned slices
+// (ShardedLOMO pads buckets to 8*world elements).
+constexpr int kMaxPeers = 16;
+
+template <typename T, typename M>
+__device__ __forceinline__ void peer_sum_vec(const T* const* __restrict__ peers, int world,
+                                             int64_t idx, M (&acc)[16 / sizeof(T)]) {
+  constexpr int V = 16 / sizeof(T);
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = (M)0;
+  uint4 buf[kMaxPeers];
+#pragma unroll
+  for (int r = 0; r < kMaxPeers; ++r)  // all loads in flight before the adds
+    if (r < world) buf[r] = ld_stream_ro(reinterpret_cast<const uint4*>(peers[r]) + idx);
+#pragma unroll
+  for (int r = 0; r < kMaxPeers; ++r) {
+    if (r < world) {
+      Vec16<T> G;
+      G.u = buf[r];
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] += to_m<M>(G.e[k]);
+    }
+  }
+}
+
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k4_rs_update(T* __restrict__ p, const T* const* __restrict__ peers_dev, int world, int64_t off,
+                 int64_t nvec, UpdArgs<M> a, unsigned flags, const lomo_state* st) {
+  constexpr int V = 16 / sizeof(T);
+  if (!load_args(a, flags, st)) return;
+  __shared__ const T* peers[kMaxPeers];
+  if (threadIdx.x < kMaxPeers)
+    peers[threadIdx.x] = threadIdx.x < world ? peers_dev[threadIdx.x] + off : nullptr;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (i >= nvec) return;
+  M g[V];
+  peer_sum_vec<T, M>(peers, world, i, g);
+  uint4* pv = reinterpret_cast<uint4*>(p);
+  Vec16<T> P, O;
+  P.u = ld_stream_rw(pv + i);
+#pragma unroll
+  for (int k = 0; k < V; ++k) O.e[k] = from_m<T, M>(upd_elem(to_m<M>(P.e[k]), g[k], a));
+  st_stream(pv + i, O.u);
+}
+
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k4_rs_probe(const T* const* __restrict__ peers_dev, int world, int64_t off, int64_t nvec,
+                int64_t per_cta, int slot, unsigned flags, void* state) {
+  constexpr int V = 16 / sizeof(T);
+  __shared__ double sm[kThreads / 32];
+  __shared__ const T* peers[kMaxPeers];
+  pdl_wait();
+  pdl_launch_dependents();
+  lomo_state* st = hdr(state);
+  if (threadIdx.x < kMaxPeers)
+    peers[threadIdx.x] = threadIdx.x < world ? peers_dev[threadIdx.x] + off : nullptr;
+  __syncthreads();
+  const bool use_scale = (flags & LOMO_USE_SCALE) != 0;
+  const M inv_scale = use_scale ? (M)st->inv_scale : (M)1;
+  double acc = 0.0;
+  bool bad = false;
+  const int64_t beg = (int64_t)blockIdx.x * per_cta;
+  const int64_t end = min(beg + per_cta, nvec);
+  for (int64_t i = beg + threadIdx.x; i < end; i += kThreads) {
+    M g[V];
+    peer_sum_vec<T, M>(peers, world, i, g);
+    M part = 0;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      M x = g[k];
+      bad |= !is_fin(x);
+      if (use_scale) x = x * inv_scale;
+      part = fma(x, x, part);
+    }
+    acc += (double)part;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
+  const double bsum = block_sum(acc, sm);
+  if (threadIdx.x == 0) {
+    partials_of(st, slot)[blockIdx.x] = bsum;
+    if (blockIdx.x == 0) nblocks_of(st)[slot] = (int32_t)gridDim.x;
+  }
+}
+
+// --------------------------------------------------------------------------
 // K3 + bookkeeping kernels (single CTA)
 // --------------------------------------------------------------------------
 __device__ void scaler_on_overflow(lomo_state* st) {
@@ -820,6 +915,37 @@ int launch_probe(const void* g_, int64_t n, int slot, unsigned flags, void* stat
                 per_cta, slot, flags, state);
 }
 
+template <typename T, typename M>
+int launch_rs_update(void* p, const void* const* peers, int world, int64_t off, int64_t n,
+                     double lr, double clip, double wd, unsigned flags, const void* state,
+                     cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  if (n % V != 0 || (off * (int64_t)sizeof(T)) % 16 != 0 || ((uintptr_t)p & 15) != 0)
+    return LOMO_E_ARG;
+  const int64_t nvec = n / V;
+  UpdArgs<M> a = make_args<M>(lr, clip, wd, flags);
+  const unsigned grid = (unsigned)((nvec + kThreads - 1) / kThreads);
+  return launch(k4_rs_update<T, M>, dim3(grid > 0 ? grid : 1), dim3(kThreads), s,
+                static_cast<T*>(p), reinterpret_cast<const T* const*>(peers), world, off, nvec, a,
+                flags, static_cast<const lomo_state*>(state));
+}
+
+template <typename T, typename M>
+int launch_rs_probe(const void* const* peers, int world, int64_t off, int64_t n, int slot,
+                    unsigned flags, void* state, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  if (n % V != 0 || (off * (int64_t)sizeof(T)) % 16 != 0) return LOMO_E_ARG;
+  const int64_t nvec = n / V;
+  int64_t per_cta = (nvec + LOMO_PROBE_BLOCKS_PER_SLOT - 1) / LOMO_PROBE_BLOCKS_PER_SLOT;
+  per_cta = (per_cta + kThreads - 1) / kThreads * kThreads;
+  if (per_cta < 4 * kThreads) per_cta = 4 * kThreads;
+  int64_t grid = (nvec + per_cta - 1) / per_cta;
+  if (grid < 1) grid = 1;
+  return launch(k4_rs_probe<T, M>, dim3((unsigned)grid), dim3(kThreads), s,
+                reinterpret_cast<const T* const*>(peers), world, off, nvec, per_cta, slot, flags,
+                state);
+}
+
 }  // namespace lomo_k
 using namespace lomo_k;
 
@@ -966,6 +1092,51 @@ int lomo_probe(const void* g, int64_t n, int dtype, int slot, unsigned flags, vo
                  : launch_probe<__nv_bfloat16, float>(g, n, slot, flags, state, s);
     case LOMO_F32: return launch_probe<float, double>(g, n, slot, flags, state, s);
     case LOMO_F64: return launch_probe<double, double>(g, n, slot, flags, state, s);
+  }
+  return LOMO_E_ARG;
+}
+
+int lomo_fused_rs_update(void* p_shard, const void* const* peer_bufs_dev, int world,
+                         int64_t offset, int64_t n, int dtype, int math, double lr,
+                         double clip_value, double weight_decay, unsigned flags,
+                         const void* state, void* stream) {
+  if (n < 0 || offset < 0 || world < 1 || world > kMaxPeers) return LOMO_E_ARG;
+  if (n == 0) return 0;
+  if (p_shard == nullptr || peer_bufs_dev == nullptr) return LOMO_E_ARG;
+  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP)) && state == nullptr)
+    return LOMO_E_ARG;
+  if (math != LOMO_MATH_F32 && math != LOMO_MATH_F64) return LOMO_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool f64 = math == LOMO_MATH_F64;
+#define LOMO_RSU(T, M) \
+  launch_rs_update<T, M>(p_shard, peer_bufs_dev, world, offset, n, lr, clip_value, weight_decay, flags, state, s)
+  switch (dtype) {
+    case LOMO_F16: return f64 ? LOMO_RSU(__half, double) : LOMO_RSU(__half, float);
+    case LOMO_BF16: return f64 ? LOMO_RSU(__nv_bfloat16, double) : LOMO_RSU(__nv_bfloat16, float);
+    case LOMO_F32: return f64 ? LOMO_RSU(float, double) : LOMO_RSU(float, float);
+    case LOMO_F64: return LOMO_RSU(double, double);
+  }
+#undef LOMO_RSU
+  return LOMO_E_ARG;
+}
+
+int lomo_fused_rs_probe(const void* const* peer_bufs_dev, int world, int64_t offset, int64_t n,
+                        int dtype, int slot, unsigned flags, void* state, void* stream) {
+  if (state == nullptr || n < 0 || offset < 0 || world < 1 || world > kMaxPeers) return LOMO_E_ARG;
+  if (slot < 0) return LOMO_E_SLOT;
+  if (n == 0) return 0;
+  if (peer_bufs_dev == nullptr) return LOMO_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool f64 = (flags & LOMO_ACCUM_F64) != 0;
+  switch (dtype) {
+    case LOMO_F16:
+      return f64 ? launch_rs_probe<__half, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s)
+                 : launch_rs_probe<__half, float>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
+    case LOMO_BF16:
+      return f64 ? launch_rs_probe<__nv_bfloat16, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s)
+                 : launch_rs_probe<__nv_bfloat16, float>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
+    case LOMO_F32: return launch_rs_probe<float, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
+    case LOMO_F64: return launch_rs_probe<double, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
   }
   return LOMO_E_ARG;
 }

@@ -110,6 +110,20 @@ class CudaEngine:
     def flush(self) -> None:
         self.dispatch.flush(self.stream())
 
+    # K4: reduce-scatter fused with the update / probe (sharded mode)
+    def rs_update(self, p_shard: torch.Tensor, peers_dev: int, world: int, offset: int) -> None:
+        d = self.dispatch
+        _lib.check(self.lib.lomo_fused_rs_update(
+            p_shard.data_ptr(), peers_dev, world, offset, p_shard.numel(), DTYPE_CODE[p_shard.dtype],
+            self.math, d.lr, d.clip, d.wd, d.flags, self.ptr, self.stream()), "lomo_fused_rs_update")
+
+    def rs_probe(self, peers_dev: int, world: int, offset: int, n: int, dtype: torch.dtype,
+                 slot: int) -> None:
+        d = self.dispatch
+        _lib.check(self.lib.lomo_fused_rs_probe(peers_dev, world, offset, n, DTYPE_CODE[dtype],
+                                                slot, d.flags, self.ptr, self.stream()),
+                   "lomo_fused_rs_probe")
+
     def finalize(self) -> None:
         _lib.check(self.lib.lomo_finalize_norm(self.ptr, self.stream()), "lomo_finalize_norm")
 

@@ -24,6 +24,14 @@ GPUs of one box (north star (3)).
   one ``all_gather`` exchanges ``{sumsq, overflow}`` per rank, and K3a decides
   on the rank-ordered sum -- the same bits on every rank, no float atomics.
 * Gradient peak: one bucket (flat) instead of one tensor.
+* ``fused_rs=True`` (K4): the flat gradient buffers live in symmetric memory
+  (peer-mapped over NVLink, torch symmetric memory); when a bucket is complete
+  every rank runs ONE kernel that loads its slice from all peers' buffers,
+  sums in rank order and applies the update (or the probe) directly -- no
+  reduce-scatter output is ever written.  Two buffers alternate between
+  buckets; a device barrier before the kernel (all peers wrote the bucket) and
+  one before a buffer is refilled (all peers finished reading it) order the
+  ranks.  (Three buffers: autograd can interleave adjacent buckets.)
 """
 from __future__ import annotations
 
@@ -114,6 +122,44 @@ class _Bucket:
         self.gathered = False
 
 
+class _SymmRing:
+    """A few symmetric-memory gradient buffers per dtype.  Autograd can
+    interleave the gradients of adjacent buckets, so a buffer is owned by one
+    open bucket until its K4 launch; reuse waits for a device barrier (every
+    rank finished reading it).  Acquisition order follows the hook order,
+    which is identical on every rank."""
+
+    NBUF = 3
+
+    def __init__(self, numel: int, dtype, device, group):
+        import torch.distributed._symmetric_memory as symm
+        name = (group if group is not None else dist.group.WORLD).group_name
+        self.bufs, self.handles = [], []
+        for _ in range(self.NBUF):
+            t = symm.empty(numel, dtype=dtype, device=device)
+            self.handles.append(symm.rendezvous(t, name))
+            self.bufs.append(t)
+        self.owner = [None] * self.NBUF
+        self.read_pending = [False] * self.NBUF
+        self.k = 0
+
+    def acquire(self, bucket_idx: int) -> int:
+        for _ in range(self.NBUF):
+            k = self.k
+            self.k = (self.k + 1) % self.NBUF
+            if self.owner[k] is None:
+                if self.read_pending[k]:
+                    self.handles[k].barrier(channel=self.NBUF + k)  # peers done reading
+                    self.read_pending[k] = False
+                self.owner[k] = bucket_idx
+                return k
+        raise RuntimeError("more than {} buckets receive gradients at once".format(self.NBUF))
+
+    def release(self, k: int) -> None:
+        self.owner[k] = None
+        self.read_pending[k] = True
+
+
 class ShardedLOMO(_Protocol):
     """LOMO over ZeRO-3 parameter shards, one process per GPU.
 
@@ -127,6 +173,8 @@ class ShardedLOMO(_Protocol):
         reshard_after_forward: free each layer bucket's full parameters after
             its forward (ZeRO-3); False keeps them resident (ZeRO-2-like).
         process_group: the data-parallel group (default: WORLD).
+        fused_rs: K4 -- reduce over peer memory fused with the update instead
+            of NCCL reduce_scatter + K1/K2 (CUDA + NVLink peers only).
     """
 
     _always_scale = True  # inv_scale carries the 1/world of the data-parallel mean
@@ -135,7 +183,7 @@ class ShardedLOMO(_Protocol):
                  loss_scale=None, *, clip_grad_value: float | None = None,
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
                  math: str = "f32", buckets=None, reshard_after_forward: bool = True,
-                 process_group=None, _engine=None):
+                 process_group=None, fused_rs: bool = False, _engine=None):
         if not dist.is_initialized():
             raise ConfigError("ShardedLOMO needs torch.distributed to be initialised")
         if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
@@ -176,6 +224,14 @@ class ShardedLOMO(_Protocol):
             self.device, len(self.buckets), self.scaler, self.max_norm, math,
             grad_div=float(self.world))
         self._mode = 0
+        self.fused_rs = bool(fused_rs)
+        self._rings: dict = {}
+        if self.fused_rs:
+            if self.device.type != "cuda" or self.world > 16:
+                raise ConfigError("fused_rs needs CUDA peers (<= 16 ranks over NVLink)")
+            for dt in {b.dtype for b in self.buckets}:
+                n = max(b.padded for b in self.buckets if b.dtype == dt)
+                self._rings[dt] = _SymmRing(n, dt, self.device, process_group)
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
         for b in self.buckets:
             if b.module is None or b.persistent:
@@ -207,17 +263,43 @@ class ShardedLOMO(_Protocol):
             return
         b, off, n = self._loc[id(p)]
         if b.gflat is None:
-            b.gflat = torch.zeros(b.padded, dtype=b.dtype, device=b.device)
+            self._new_gflat(b)
         b.gflat[off:off + n].copy_(p.grad.reshape(-1))
         p.grad = None
         b.remaining -= 1
         if b.remaining == 0:
             self._reduce(b)
 
+    def _new_gflat(self, b: _Bucket) -> None:
+        if self.fused_rs:
+            ring = self._rings[b.dtype]
+            b.ring_k = ring.acquire(b.idx)
+            b.gflat = ring.bufs[b.ring_k][:b.padded]
+            b.gflat.zero_()
+        else:
+            b.gflat = torch.zeros(b.padded, dtype=b.dtype, device=b.device)
+
     def _reduce(self, b: _Bucket) -> None:
         """One reduce-scatter feeding the fused kernel on this rank's shard."""
         if b.gflat is None:
-            b.gflat = torch.zeros(b.padded, dtype=b.dtype, device=b.device)
+            self._new_gflat(b)
+        if self.fused_rs:
+            # K4: every rank has written the bucket -> reduce over peer memory
+            # fused with the update / probe; nothing is written back
+            ring = self._rings[b.dtype]
+            h = ring.handles[b.ring_k]
+            h.barrier(channel=b.ring_k)  # every rank has written this bucket
+            peers = h.buffer_ptrs_dev
+            if self._mode == _PROBE:
+                self.engine.rs_probe(peers, self.world, self.rank * b.S, b.S, b.dtype, b.idx)
+            else:
+                self.engine.rs_update(b.shard, peers, self.world, self.rank * b.S)
+                b.dirty = True
+            ring.release(b.ring_k)
+            b.gflat = None
+            b.remaining = len(b.params)
+            b.release()
+            return
         gshard = torch.empty(b.S, dtype=b.dtype, device=b.device)
         reduce_scatter(gshard, b.gflat, self.group)
         b.gflat = None

@@ -470,3 +470,54 @@ def test_bf16_cases_match_oracle(hook_cases, math_mode):
                 d = U.ulp_diff(results[k][i], U.to_dev(params[i], torch.bfloat16)).max().item()
                 assert d <= (0 if math_mode == "f64" and max_norm is None else 1), \
                     (case["name"], k, i, d)
+
+
+# --- K4: reduce over peer memory fused with the update / probe -------------------
+
+@pytest.mark.parametrize("prec", ["half", "bf16", "f32"])
+@pytest.mark.parametrize("math_mode", ["f64", "f32"])
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_k4_fused_reduce_update_matches_oracle(prec, math_mode, world):
+    """Peers simulated by `world` buffers on this GPU (the kernel only sees
+    pointers; over NVLink they would be peer-mapped).  Rank 1 of `world` owns
+    the middle slice of a padded bucket."""
+    rng = np.random.default_rng(world)
+    S = 8 * 1000
+    total = S * world
+    dt = U.TORCH_DT[prec]
+    bufs0 = [O.round_to(rng.normal(0, 1e-3, total), prec) for _ in range(world)]
+    bufs = [U.to_dev(b, dt) for b in bufs0]
+    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    rank = 1 if world > 1 else 0
+    off = rank * S
+    p0 = O.round_to(rng.uniform(-0.08, 0.08, S), prec)
+    p = U.to_dev(p0, dt)
+    gsum = np.sum([b[off:off + S] for b in bufs0], axis=0)
+    _lib.check(U.lib().lomo_fused_rs_update(p.data_ptr(), peers.data_ptr(), world, off, S,
+                                            U.CODE[dt], U.MATH[math_mode], 0.05, 0.0, 0.0, 0,
+                                            None, U.stream()), "rs_update")
+    want = U.to_dev(O.apply_update(p0, gsum, 0.05, prec), dt)
+    d = U.ulp_diff(p, want)
+    if math_mode == "f64":
+        assert d.max().item() == 0
+    elif prec != "f32":
+        assert d.max().item() <= 1
+    # probe: sum of squares of the reduced slice
+    st = U.State(2)
+    st.begin()
+    _lib.check(U.lib().lomo_fused_rs_probe(peers.data_ptr(), world, off, S, U.CODE[dt], 1,
+                                           _lib.ACCUM_F64 if math_mode == "f64" else 0, st.ptr,
+                                           U.stream()), "rs_probe")
+    got = st.slots(2)[1]
+    want_sq = float(np.dot(gsum, gsum))
+    assert abs(got - want_sq) <= (1e-12 if math_mode == "f64" else 1e-6) * want_sq
+
+
+def test_k4_rejects_misaligned_slices():
+    b = torch.zeros(64, dtype=torch.bfloat16, device="cuda")
+    peers = torch.tensor([b.data_ptr()], dtype=torch.int64, device="cuda")
+    p = torch.zeros(8, dtype=torch.bfloat16, device="cuda")
+    assert U.lib().lomo_fused_rs_update(p.data_ptr(), peers.data_ptr(), 1, 3, 8, _lib.BF16,
+                                        _lib.MATH_F32, 0.1, 0.0, 0.0, 0, None, U.stream()) == -1
+    assert U.lib().lomo_fused_rs_update(p.data_ptr(), peers.data_ptr(), 17, 0, 8, _lib.BF16,
+                                        _lib.MATH_F32, 0.1, 0.0, 0.0, 0, None, U.stream()) == -1

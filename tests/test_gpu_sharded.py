@@ -83,3 +83,28 @@ def test_sharded_with_checkpointing_world1(nccl_world):
     for (n, x), (_, y) in zip(a.named_parameters(), b.named_parameters()):
         assert (x - y).abs().max().item() <= 1e-5, n
     ob.remove_hooks()
+
+
+@pytest.mark.parametrize("two_pass", [False, True])
+def test_fused_rs_world1_equals_nccl_path(nccl_world, two_pass):
+    """K4 over symmetric memory (world 1: the only peer is this GPU) gives the
+    same parameters as NCCL reduce_scatter + K1/K2."""
+    from paper_2306_09782_b200.sharded import ShardedLOMO
+    from paper_2306_09782_b200.workloads import Llama
+    a = Llama(CFG, dtype=torch.bfloat16, device="cuda", seed=0)
+    b = Llama(CFG, dtype=torch.bfloat16, device="cuda", seed=0)
+    kw = dict(clip_grad_norm=0.5, loss_scale=2.0 ** 8) if two_pass else {}
+    oa = ShardedLOMO(a, lr=0.05, **kw)
+    ob = ShardedLOMO(b, lr=0.05, fused_rs=True, **kw)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for step in range(3):
+        d = torch.randint(0, CFG["vocab"], (2, 33), device="cuda", generator=g)
+        la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+        lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+        assert la == lb
+    oa.gather_all()
+    ob.gather_all()
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)
+    oa.remove_hooks()
+    ob.remove_hooks()
