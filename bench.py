@@ -328,10 +328,11 @@ def bench_e2e(args, rank, world):
     for _, shape in llama_param_shapes("7b"):
         n = math.prod(shape)
         shapes.append((n * (rank + 1)) // world - (n * rank) // world)
-    # device staging: two slots per operand (double buffering)
+    # device staging: NS slots per operand (H2D of tensor i+1.. overlaps K1 / D2H of i)
     maxn = max(shapes)
-    DP = [torch.empty(maxn, dtype=dt, device="cuda") for _ in range(2)]
-    DG = [torch.empty(maxn, dtype=dt, device="cuda") for _ in range(2)]
+    NS = args.e2e_slots
+    DP = [torch.empty(maxn, dtype=dt, device="cuda") for _ in range(NS)]
+    DG = [torch.empty(maxn, dtype=dt, device="cuda") for _ in range(NS)]
     # host buffers (pinned), filled once (generated on the device, copied down)
     gen = torch.Generator(device="cuda").manual_seed(7 + rank)
     HP, HG = [], []
@@ -343,14 +344,14 @@ def bench_e2e(args, rank, world):
         HP.append(hp)
         HG.append(hg)
     h2d, comp, d2h = torch.cuda.Stream(), torch.cuda.current_stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_done = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [torch.cuda.Event() for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(NS)]
+    ev_done = [torch.cuda.Event() for _ in range(NS)]
+    ev_out = [torch.cuda.Event() for _ in range(NS)]
     order = list(range(len(shapes) - 1, -1, -1))
 
     def one_pass():
         for k, i in enumerate(order):
-            s = k & 1
+            s = k % NS
             n = shapes[i]
             with torch.cuda.stream(h2d):
                 h2d.wait_event(ev_out[s])  # slot free (its D2H finished)
@@ -557,6 +558,7 @@ def main():
     ap.add_argument("--dtype", choices=["bf16", "fp16"], default="bf16")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-slots", type=int, default=4, help="device staging slots of the e2e pipeline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--train-warmup", type=int, default=3)

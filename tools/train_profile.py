@@ -19,10 +19,13 @@ ap.add_argument("--seq", type=int, default=1024)
 ap.add_argument("--batch", type=int, default=1)
 ap.add_argument("--layers", type=int, default=None)
 ap.add_argument("--ckpt", action="store_true")
+ap.add_argument("--replay", action="store_true")
+ap.add_argument("--fuse", action="store_true")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 model = Llama("7b", dtype=torch.float16, device="cuda", layers=a.layers, checkpointing=a.ckpt)
-opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 10))
+opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 10),
+           replay=a.replay, fuse_gemm=a.fuse)
 d = torch.randint(0, 32000, (a.batch, a.seq + 1), device="cuda")
 step = lambda: opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
 for _ in range(3):
@@ -35,15 +38,16 @@ with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     torch.cuda.synchronize()
 fam = defaultdict(float)
 total = 0.0
-for e in prof.key_averages():
-    if e.device_type.name != "CUDA":
+for e in prof.events():          # device kernels only (no CPU-op double counting)
+    if e.device_type.name != "CUDA" or e.device_time_total <= 0:
         continue
-    t = e.self_device_time_total
+    t = e.device_time_total
     total += t
-    n = e.key
-    k = ("k1_update" if "k1_update" in n else "k2_probe" if "k2_probe" in n else
-         "k3/begin" if ("k3_" in n or "k_begin" in n) else
-         "gemm" if any(s in n.lower() for s in ("gemm", "sm100", "cutlass", "nvjet", "xmma")) else
+    n = e.name
+    k = ("K1 k1_update" if "k1_update" in n else "K2 k2_probe" if "k2_probe" in n else
+         "K3/begin" if ("k3_" in n or "k_begin" in n) else
+         "K5 fused gemm+update" if "cutlass" in n.lower() or "GemmUniversal" in n else
+         "gemm (cuBLAS)" if any(s in n.lower() for s in ("gemm", "nvjet", "xmma")) else
          "attention" if any(s in n.lower() for s in ("flash", "fmha", "attention", "sdpa")) else
          "elementwise/other")
     fam[k] += t
