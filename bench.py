@@ -461,6 +461,50 @@ def bench_train(args, rank, world):
     return out
 
 
+def bench_memory_table(args):
+    """the paper's Table 1 setting (LLaMA-7B, seq 512 x batch 8,
+    fp16, LOMO) with and without per-layer activation checkpointing, measured
+    from torch.cuda memory stats next to the reference estimator's analytic
+    row (estimate.py:200-218; PAPER.md:193-196)."""
+    import torch
+    from paper_2306_09782_b200 import LOMO, LossScaler
+    from paper_2306_09782_b200.workloads import Llama
+    rows = {}
+    for ac in (False, True):
+        torch.cuda.empty_cache()
+        model = Llama("7b", dtype=torch.float16, device="cuda", checkpointing=ac)
+        model.train()
+        opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 10))
+        d = torch.randint(0, 32000, (8, 513), device="cuda")
+        step = lambda: opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
+        step()
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        step()
+        torch.cuda.synchronize()
+        peak = torch.cuda.max_memory_allocated()
+        params = sum(p.numel() * p.element_size() for p in model.parameters())
+        gib = 2 ** 30
+        rows["ac" if ac else "no_ac"] = {
+            "params_gib": round(params / gib, 2),
+            "step_peak_gib": round(peak / gib, 2),
+            "peak_above_resident_gib": round((peak - base) / gib, 2),
+            "largest_gradient_gib": round(max(p.numel() * p.element_size()
+                                              for p in model.parameters()) / gib, 3),
+            "optimizer_state_gib": 0.0}
+        opt.remove_hooks()
+        del opt, model
+    rows["reference_estimator_lomo_gib"] = {
+        "no_ac": {"params": 12.55, "gradients": 0.24, "optimizer": 0.0, "activations": 45.61,
+                  "total": 59.40},
+        "ac": {"params": 12.55, "gradients": 0.24, "optimizer": 0.0, "activations": 1.79,
+               "total": 14.58},
+        "note": "the estimator counts stored attention scores; SDPA flash attention keeps none"}
+    torch.cuda.empty_cache()
+    return rows
+
+
 def bench_train_sharded(args, rank, world):
     """Configs 4/5: LLaMA-13B (or 65B with per-layer activation checkpointing)
     with ZeRO-3 parameter shards over ``world`` GPUs; each bucket's gradients
@@ -565,6 +609,8 @@ def main():
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--ckpt", action="store_true", help="per-layer activation checkpointing")
+    ap.add_argument("--memory-table", action="store_true",
+                    help="also measure the Table-1 setting (seq 512 x batch 8, AC off/on)")
     ap.add_argument("--sharded-model", default="13b", choices=["7b", "13b", "30b", "65b"],
                     help="model of the N>1 sharded train leg (config 4: 13b, config 5: 65b)")
     args = ap.parse_args()
@@ -604,6 +650,7 @@ def main():
     if not args.no_train:
         train = bench_train(args, rank, world) if world == 1 else \
             bench_train_sharded(args, rank, world)
+    mem_table = bench_memory_table(args) if (args.memory_table and world == 1) else None
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cb = cpu_baseline()
@@ -644,6 +691,8 @@ def main():
             "cpu_baseline": cb,
             "train": train,
         }
+        if mem_table is not None:
+            line["memory_table"] = mem_table
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
