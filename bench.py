@@ -130,9 +130,16 @@ def _dist_init(gpus: int):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
+        # LOMO_BENCH_SHARE_GPU=1 (validation only): every rank on cuda:0 over
+        # gloo, to exercise the N>1 code path on a single-GPU box
+        shared = os.environ.get("LOMO_BENCH_SHARE_GPU") == "1"
+        dev = 0 if shared else local
+        torch.cuda.set_device(dev)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     else:
         torch.cuda.set_device(0)
     return rank, world, local
@@ -517,7 +524,8 @@ def bench_train_sharded(args, rank, world):
     from paper_2306_09782_b200.workloads import Llama
     size = args.sharded_model
     ckpt = args.ckpt or size == "65b"
-    model = Llama(size, dtype=torch.float16, device="cuda", checkpointing=ckpt)
+    spec = dict(hidden=512, layers=4, heads=8, ffn=1408, vocab=32000) if size == "tiny" else size
+    model = Llama(spec, dtype=torch.float16, device="cuda", checkpointing=ckpt)
     model.train()
     opt = ShardedLOMO(model, lr=1e-3, clip_grad_norm=1.0,
                       loss_scale=LossScaler(2.0 ** 10, growth_interval=16))
@@ -611,7 +619,7 @@ def main():
     ap.add_argument("--ckpt", action="store_true", help="per-layer activation checkpointing")
     ap.add_argument("--memory-table", action="store_true",
                     help="also measure the Table-1 setting (seq 512 x batch 8, AC off/on)")
-    ap.add_argument("--sharded-model", default="13b", choices=["7b", "13b", "30b", "65b"],
+    ap.add_argument("--sharded-model", default="13b", choices=["tiny", "7b", "13b", "30b", "65b"],
                     help="model of the N>1 sharded train leg (config 4: 13b, config 5: 65b)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
