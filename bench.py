@@ -653,15 +653,26 @@ def main():
     up = bench_update(args, rank, world)
     peak, peak_src = _peaks()
     tr = _traffic()
-    e2e = None if args.no_e2e else bench_e2e(args, rank, world)
+
+    def optional(fn, *a):
+        """Secondary legs must never cost the headline line: report their error."""
+        try:
+            return fn(*a)
+        except Exception as exc:  # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            torch.cuda.empty_cache()
+            return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
+    e2e = None if args.no_e2e else optional(bench_e2e, args, rank, world)
     train = None
     if not args.no_train:
-        train = bench_train(args, rank, world) if world == 1 else \
-            bench_train_sharded(args, rank, world)
-    mem_table = bench_memory_table(args) if (args.memory_table and world == 1) else None
+        train = optional(bench_train, args, rank, world) if world == 1 else \
+            optional(bench_train_sharded, args, rank, world)
+    mem_table = optional(bench_memory_table, args) if (args.memory_table and world == 1) else None
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cb = cpu_baseline()
+        cb = optional(cpu_baseline)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(up["gbs"], 1), "unit": "GB/s", "n_gpus": world,
