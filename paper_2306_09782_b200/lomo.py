@@ -297,6 +297,8 @@ class LOMO(_Protocol):
         if replay and self.passes != 2:
             raise ConfigError("replay applies to the two-pass protocol (clip_grad_norm / loss_scale)")
         self._stash = ReplayStash() if replay else None
+        self._replay_checked = False
+        self._replay_mismatch: list = []
         if fuse_gemm and not replay:
             raise ConfigError("fuse_gemm fuses the update into the replayed weight-gradient GEMM: "
                               "it needs replay=True")
@@ -320,8 +322,16 @@ class LOMO(_Protocol):
         if mode == _PROBE:
             self.engine.probe(g, self._slot[id(p)])
             st = self._stash
-            if st is not None and id(p) not in st.linear:
-                st.grads[id(p)] = g  # not a replayable linear: keep its gradient
+            if st is not None:
+                if id(p) not in st.linear:
+                    st.grads[id(p)] = g  # not a replayable linear: keep its gradient
+                elif not self._replay_checked:
+                    # first step: the replayed dW must BE the whole gradient
+                    # (a weight tied to another op would also collect that op's
+                    # contribution, which replay would silently drop)
+                    x, dy = st.linear[id(p)]
+                    if not torch.equal(_replay.weight_grad(x, dy), g):
+                        self._replay_mismatch.append(tuple(p.shape))
         else:
             self.engine.update(p, g)
         self.hook_calls += 1
@@ -347,11 +357,19 @@ class LOMO(_Protocol):
             self.engine.flush()  # the parked tiny tensors, same stream as the hooks
         if stash is not None:
             kept = sum(g.numel() * g.element_size() for g in stash.grads.values())
+            bad = None
             if kept > 2 * self._largest:
+                bad = (f"replay would keep {kept / 2**20:.0f} MiB of gradients: route the model's "
+                       "linear layers through paper_2306_09782_b200.replay.linear")
+            elif stash.shared:
+                bad = f"replay: {len(stash.shared)} weight(s) feed more than one linear"
+            elif self._replay_mismatch:
+                bad = (f"replay: weights {self._replay_mismatch[:3]} receive gradient from ops "
+                       "other than their linear (tied weights?)")
+            if bad is not None:
                 stash.clear()
-                raise ConfigError(
-                    f"replay would keep {kept / 2**20:.0f} MiB of gradients: route the model's "
-                    "linear layers through paper_2306_09782_b200.replay.linear")
+                raise ConfigError(bad)
+            self._replay_checked = True
 
     def _gemm_update(self, p, x, dy, lr: float) -> bool:
         """K5: p <- alpha * dy^T x + beta * p on the tensor cores; False when the

@@ -28,10 +28,12 @@ class ReplayStash:
     def __init__(self):
         self.linear: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
         self.grads: dict[int, torch.Tensor] = {}
+        self.shared: set[int] = set()   # weights that fed more than one linear
 
     def clear(self):
         self.linear.clear()
         self.grads.clear()
+        self.shared.clear()
 
     def nbytes(self) -> int:
         n = sum(x.numel() * x.element_size() + d.numel() * d.element_size()
@@ -58,6 +60,8 @@ class _StashLinear(torch.autograd.Function):
         dw = weight_grad(x, dy) if ctx.needs_input_grad[1] else None
         st = _ACTIVE
         if st is not None:
+            if ctx.wid in st.linear:
+                st.shared.add(ctx.wid)
             st.linear[ctx.wid] = (x, dy)
         return dx, dw
 

@@ -378,3 +378,24 @@ def test_replay_refuses_models_without_replayable_linears():
     ids = torch.from_numpy(sequence_copy_batch(0, 0, 2, 8, 128)).cuda()
     with pytest.raises(ConfigError):
         opt.step(lambda: mean_cross_entropy(model(ids), ids), 0.05)
+
+
+def test_replay_refuses_tied_weights():
+    """A weight used by the embedding AND a replayable linear would lose the
+    embedding's contribution under replay: detected on the first step."""
+    from paper_2306_09782_b200 import ConfigError
+    from paper_2306_09782_b200.replay import linear as rlinear
+
+    class Tied(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.emb = torch.nn.Parameter(torch.randn(64, 32, device="cuda") * 0.1)
+
+        def forward(self, ids):
+            return rlinear(torch.nn.functional.embedding(ids, self.emb), self.emb)
+
+    m = Tied()
+    opt = LOMO(m, lr=0.05, clip_grad_norm=1.0, replay=True)
+    ids = torch.randint(0, 64, (2, 8), device="cuda")
+    with pytest.raises(ConfigError):
+        opt.step(lambda: mean_cross_entropy(m(ids), ids), 0.05)
