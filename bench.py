@@ -413,7 +413,9 @@ def bench_train(args, rank, world):
     from paper_2306_09782_b200 import LOMO, LossScaler
     from paper_2306_09782_b200.workloads import Llama
     torch.cuda.reset_peak_memory_stats()
-    model = Llama("7b", dtype=torch.float16, device="cuda", checkpointing=args.ckpt)
+    size = args.train_model
+    ckpt = args.ckpt or size == "65b"
+    model = Llama(size, dtype=torch.float16, device="cuda", checkpointing=ckpt)
     model.train()
     params_bytes = sum(p.numel() * p.element_size() for p in model.parameters())
     largest = max(p.numel() * p.element_size() for p in model.parameters())
@@ -421,11 +423,13 @@ def bench_train(args, rank, world):
     gen = torch.Generator(device="cuda").manual_seed(0)
     data = [torch.randint(0, 32000, (batch, seq + 1), device="cuda", generator=gen)
             for _ in range(4)]
-    out = {"model": "llama-7b (random init N(0,0.02)), fp16 params, no master copy",
+    out = {"model": f"llama-{size} (random init N(0,0.02)), fp16 params, no master copy",
            "seq_len": seq, "batch": batch, "steps": args.train_steps, "passes_per_step": 2,
-           "clip_grad_norm": 1.0, "activation_checkpointing": bool(args.ckpt),
+           "clip_grad_norm": 1.0, "activation_checkpointing": bool(ckpt),
            "paper_tgs_rtx3090": 769.92}
-    for key in ("strict", "replay", "replay_fused_gemm"):
+    variants = ("strict", "replay", "replay_fused_gemm") if not args.train_variants else \
+        tuple(args.train_variants.split(","))
+    for key in variants:
         opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
                    loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
                    replay=key.startswith("replay"), fuse_gemm=key == "replay_fused_gemm")
@@ -453,7 +457,7 @@ def bench_train(args, rank, world):
                     "losses": [round(x, 4) for x in losses]}
         opt.remove_hooks()
         del opt
-    best = max(("strict", "replay", "replay_fused_gemm"), key=lambda k: out[k]["tokens_per_s"])
+    best = max(variants, key=lambda k: out[k]["tokens_per_s"])
     out["tokens_per_s"] = out[best]["tokens_per_s"]
     out["ms_per_step"] = out[best]["ms_per_step"]
     out["headline_variant"] = best
@@ -619,6 +623,10 @@ def main():
     ap.add_argument("--ckpt", action="store_true", help="per-layer activation checkpointing")
     ap.add_argument("--memory-table", action="store_true",
                     help="also measure the Table-1 setting (seq 512 x batch 8, AC off/on)")
+    ap.add_argument("--train-model", default="7b", choices=["7b", "13b", "30b", "65b"],
+                    help="model of the single-GPU train leg (config 3: 7b)")
+    ap.add_argument("--train-variants", default="",
+                    help="comma list of strict,replay,replay_fused_gemm (default: all)")
     ap.add_argument("--sharded-model", default="13b", choices=["tiny", "7b", "13b", "30b", "65b"],
                     help="model of the N>1 sharded train leg (config 4: 13b, config 5: 65b)")
     args = ap.parse_args()
