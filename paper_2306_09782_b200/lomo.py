@@ -35,15 +35,14 @@ import torch
 from . import _lib
 from . import replay as _replay
 from .engine import CudaEngine, dtype_code
-from .replay import ReplayStash
-
-_lib_E_ARG = -1
 from .errors import (ConfigError, NonFiniteLossError, ScaleUnderflowError, ShapeError,
                      TapeStateError)
+from .replay import ReplayStash
 from .stabilize import ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome
 
 _PROBE = 1
 _UPDATE = 2
+_E_ARG = -1  # LOMO_E_ARG (include/lomo_b200.h)
 
 
 def stabilizer_from_args(clip_grad_norm, clip_grad_value, loss_scale) -> Stabilizer | None:
@@ -393,7 +392,7 @@ class LOMO(_Protocol):
         ws = self._ws.data_ptr() if need else None
         rc = lib.lomo_gemm_update(p.data_ptr(), dy2.data_ptr(), x2.data_ptr(), out_f, in_f,
                                   dy2.shape[0], dt, alpha, beta, ws, need, self.engine.stream())
-        if rc == _lib_E_ARG:
+        if rc == _E_ARG:
             return False
         _lib.check(rc, "lomo_gemm_update")
         return True

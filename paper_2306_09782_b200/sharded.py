@@ -41,8 +41,8 @@ import torch
 import torch.distributed as dist
 
 from .engine import CudaEngine, dtype_code
-from .errors import ConfigError, TapeStateError
-from .lomo import _PROBE, _UPDATE, _Protocol, stabilizer_from_args, trainable_params
+from .errors import ConfigError
+from .lomo import _PROBE, _Protocol, stabilizer_from_args, trainable_params
 from .stabilize import Stabilizer
 
 

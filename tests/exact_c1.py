@@ -24,7 +24,6 @@ from __future__ import annotations
 
 import math
 
-import numpy as np
 import torch
 
 from paper_2306_09782_b200.workloads import (MiniConfig, mini_transformer_init, round_half_np,

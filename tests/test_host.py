@@ -1,7 +1,6 @@
 """Host-side logic on CPU: configuration mirrors, the C1 restatement's init and
 tokens against the reference's recorded digests, hook delivery order."""
 import hashlib
-import math
 
 import numpy as np
 import pytest

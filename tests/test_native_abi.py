@@ -3,7 +3,6 @@ include/lomo_b200.h declares (no compute calls without a GPU)."""
 import ctypes
 import re
 import subprocess
-from pathlib import Path
 
 import pytest
 
