@@ -406,7 +406,9 @@ def bench_train(args, rank, world):
     (input, output-gradient) pairs stashed in pass 1 (replay.py) and feeds K1
     without a second backward; ``replay_fused_gemm`` -- replay with each
     linear's update fused into its weight-gradient GEMM on the tensor cores
-    (K5), so pass 2 never materialises a gradient; ``grouped`` -- the paper's
+    (K5), so pass 2 never materialises a gradient; ``replay_fused_gemm_graph``
+    -- the same step captured into two CUDA graphs around the host decision
+    (graphs.py); ``grouped`` -- the paper's
     single-pass alternative (per-layer norm clip, GroupedLOMO), reported beside
     the headline, which is the best two-pass variant (config 3's protocol).  (A side-stream overlap of
     the hook kernels was measured slower -- 8.6k vs 9.1k tok/s -- and is not
@@ -429,10 +431,24 @@ def bench_train(args, rank, world):
            "seq_len": seq, "batch": batch, "steps": args.train_steps, "passes_per_step": 2,
            "clip_grad_norm": 1.0, "activation_checkpointing": bool(ckpt),
            "paper_tgs_rtx3090": 769.92}
-    variants = ("strict", "replay", "replay_fused_gemm", "grouped") if not args.train_variants else \
+    gstep = None
+    variants = ("strict", "replay", "replay_fused_gemm", "replay_fused_gemm_graph", "grouped") \
+        if not args.train_variants else \
         tuple(args.train_variants.split(","))
     for key in variants:
-        if key == "grouped":
+        if key == "replay_fused_gemm_graph":
+            from paper_2306_09782_b200.graphs import GraphedLOMOStep
+            opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
+                       loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
+                       replay=True, fuse_gemm=True)
+            static = data[0].clone()
+            gstep = GraphedLOMOStep(opt, lambda d: model.loss(d[:, :-1], d[:, 1:]), (static,),
+                                    warmup=max(2, args.train_warmup), lr=1e-3)
+
+            def step(k):
+                static.copy_(data[k % len(data)])
+                return gstep.step(1e-3).detach().item()
+        elif key == "grouped":
             # the paper's single-pass alternative (stabilize.py:234-274): clip
             # each decoder layer by its own norm, no loss scaler, one backward
             opt = GroupedLOMO(model, lr=1e-3, max_norm=1.0, window=1)
@@ -441,9 +457,10 @@ def bench_train(args, rank, world):
                        loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
                        replay=key.startswith("replay"), fuse_gemm=key == "replay_fused_gemm")
 
-        def step(k):
-            d = data[k % len(data)]
-            return opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
+        if key != "replay_fused_gemm_graph":
+            def step(k, opt=opt):
+                d = data[k % len(data)]
+                return opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
 
         for k in range(args.train_warmup):
             step(k)
@@ -464,6 +481,8 @@ def bench_train(args, rank, world):
                     "losses": [round(x, 4) for x in losses]}
         opt.remove_hooks()
         del opt
+        step = gstep = None  # noqa: F841  (release the graphs' memory pool)
+        torch.cuda.empty_cache()
     two_pass = [k for k in variants if k != "grouped"]   # the headline: config 3's protocol
     best = max(two_pass or variants, key=lambda k: out[k]["tokens_per_s"])
     out["tokens_per_s"] = out[best]["tokens_per_s"]
@@ -634,7 +653,8 @@ def main():
     ap.add_argument("--train-model", default="7b", choices=["7b", "13b", "30b", "65b"],
                     help="model of the single-GPU train leg (config 3: 7b)")
     ap.add_argument("--train-variants", default="",
-                    help="comma list of strict,replay,replay_fused_gemm,grouped (default: all)")
+                    help="comma list of strict,replay,replay_fused_gemm,replay_fused_gemm_graph,grouped "
+             "(default: all)")
     ap.add_argument("--sharded-model", default="13b", choices=["tiny", "7b", "13b", "30b", "65b"],
                     help="model of the N>1 sharded train leg (config 4: 13b, config 5: 65b)")
     args = ap.parse_args()

@@ -66,6 +66,9 @@ typedef enum {
 #define LOMO_USE_COEF 0x2u  /* g *= state->clip_coef  (stabilize.py:221-222)       */
 #define LOMO_USE_SKIP 0x4u  /* no-op when state->skip (stabilize.py:204-205,       */
                             /*                          optim.py:63-65)            */
+#define LOMO_LR_FROM_STATE 0x10u /* K1: lr = state->lr (set by lomo_set_lr), so a  */
+                                 /* CUDA graph of the step needs no re-capture when */
+                                 /* the schedule changes lr                         */
 #define LOMO_ACCUM_F64 0x8u /* K2: accumulate every square in f64 (the reference's */
                             /* float64 dot, stabilize.py:199); default for 16-bit   */
                             /* storage: exact fp32 squares summed per 16-byte      */
@@ -98,7 +101,7 @@ typedef struct lomo_state {
   float scale_f32;       /* 104: scale as fp32 (exact: power of two), for loss*scale */
   int32_t pad0;          /* 108                                                      */
   double grad_div;       /* 112: data-parallel gradient divisor (world size; 1)      */
-  int32_t reserved[2];   /* 120..127                                                 */
+  double lr;             /* 120: learning rate read under LOMO_LR_FROM_STATE          */
   /* followed by: double  sumsq[nslots];                      (per-slot totals)
    *              int32_t nblocks[nslots], padded to 8 bytes;  (K2 CTAs per slot)
    *              double  partials[nslots][LOMO_PROBE_BLOCKS_PER_SLOT];
@@ -144,6 +147,9 @@ int lomo_fused_update_multi(void* const* p_list, const void* const* g_list,
                             const int64_t* n_list, int count, int dtype, int math,
                             double lr, double clip_value, double weight_decay,
                             unsigned flags, const void* state, void* stream);
+
+/* Set state->lr (a one-thread kernel; launch it outside a captured graph). */
+int lomo_set_lr(void* state, double lr, void* stream);
 
 /* ---- K2: probe (two-pass pass 1) --------------------------------------- */
 /* sumsq[slot] = sum((g * inv_scale)^2) (deterministic: fixed-order f64 tree);
@@ -205,6 +211,17 @@ int lomo_gemm_update(void* p, const void* dy, const void* x, int64_t out_feature
                      double beta, void* workspace, size_t workspace_bytes, void* stream);
 size_t lomo_gemm_update_workspace(int64_t out_features, int64_t in_features,
                                   int64_t tokens, int dtype);
+/* As lomo_gemm_update, with alpha = coefs_dev[0] and beta = coefs_dev[1] read
+ * from device memory at run time (graph-capturable); lomo_update_coefs
+ * computes them on device from the step state:
+ *   alpha = skip ? 0 : -state->lr * [coef] * [inv_scale],  beta = skip ? 1 : 1 - lr*wd
+ * ([x] present when flags has LOMO_USE_COEF / LOMO_USE_SCALE). */
+int lomo_gemm_update_dev(void* p, const void* dy, const void* x, int64_t out_features,
+                         int64_t in_features, int64_t tokens, int dtype,
+                         const float* coefs_dev, void* workspace, size_t workspace_bytes,
+                         void* stream);
+int lomo_update_coefs(const void* state, double weight_decay, unsigned flags,
+                      float* coefs_dev, void* stream);
 
 /* Number of SMs the library sized its grids for (device of the current
  * context); 0 if no device. */

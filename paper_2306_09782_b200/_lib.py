@@ -18,7 +18,7 @@ LIB_PATH = _HERE / "_native" / "liblomo_b200.so"
 # lomo_dtype (include/lomo_b200.h)
 F32, F16, BF16, F64 = 0, 1, 2, 3
 MATH_F32, MATH_F64 = 0, 1
-USE_SCALE, USE_COEF, USE_SKIP, ACCUM_F64 = 0x1, 0x2, 0x4, 0x8
+USE_SCALE, USE_COEF, USE_SKIP, ACCUM_F64, LR_FROM_STATE = 0x1, 0x2, 0x4, 0x8, 0x10
 PROBE_BLOCKS_PER_SLOT = 4096
 ABI_VERSION = 1
 
@@ -42,6 +42,9 @@ EXPORTS = (
     "lomo_gemm_update_workspace",
     "lomo_fused_rs_update",
     "lomo_fused_rs_probe",
+    "lomo_set_lr",
+    "lomo_update_coefs",
+    "lomo_gemm_update_dev",
 )
 
 
@@ -70,7 +73,7 @@ class LomoStatus(ctypes.Structure):
         ("scale_f32", ctypes.c_float),
         ("pad0", ctypes.c_int32),
         ("grad_div", ctypes.c_double),
-        ("reserved", ctypes.c_int32 * 2),
+        ("lr", ctypes.c_double),
     ]
 
 
@@ -106,6 +109,10 @@ _SIGS = {
     "lomo_fused_rs_update": (_i32, [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _dbl, _dbl, _dbl,
                                     _u32, _vp, _vp]),
     "lomo_fused_rs_probe": (_i32, [_vp, _i32, _i64, _i64, _i32, _i32, _u32, _vp, _vp]),
+    "lomo_set_lr": (_i32, [_vp, _dbl, _vp]),
+    "lomo_update_coefs": (_i32, [_vp, _dbl, _u32, _vp, _vp]),
+    "lomo_gemm_update_dev": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp,
+                                    ctypes.c_size_t, _vp]),
 }
 
 _LIB = None

@@ -67,7 +67,8 @@ struct FusedUpdateGemm {
   using Gemm = cutlass::gemm::device::GemmUniversalAdapter<GemmKernel>;
 
   static int run(void* p, const void* dy, const void* x, int M, int N, int K, float alpha,
-                 float beta, void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+                 float beta, const float* coefs_dev, void* workspace, size_t workspace_bytes,
+                 cudaStream_t stream) {
     using StrideA = typename Gemm::GemmKernel::StrideA;
     using StrideB = typename Gemm::GemmKernel::StrideB;
     using StrideC = typename Gemm::GemmKernel::StrideC;
@@ -81,6 +82,10 @@ struct FusedUpdateGemm {
         {M, N, K, 1},
         {static_cast<const ElementA*>(dy), sA, static_cast<const ElementB*>(x), sB},
         {{alpha, beta}, static_cast<const ElementC*>(p), sC, static_cast<ElementC*>(p), sD}};
+    if (coefs_dev != nullptr) {  // alpha/beta read by the epilogue at run time
+      args.epilogue.thread.alpha_ptr = coefs_dev;
+      args.epilogue.thread.beta_ptr = coefs_dev + 1;
+    }
     // persistent tile scheduler sized to the device (epilogue of tile i overlaps
     // the mainloop of tile i+1 through the double-buffered TMEM accumulator)
     args.hw_info = hw_info();
@@ -117,10 +122,14 @@ struct FusedUpdateGemm {
 }  // namespace lomo_gemm
 
 extern "C" {
-
 int lomo_gemm_update(void* p, const void* dy, const void* x, int64_t out_features,
                      int64_t in_features, int64_t tokens, int dtype, double alpha, double beta,
-                     void* workspace, size_t workspace_bytes, void* stream) {
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+static int gemm_update(void* p, const void* dy, const void* x, int64_t out_features,
+                       int64_t in_features, int64_t tokens, int dtype, double alpha, double beta,
+                       const float* coefs_dev, void* workspace, size_t workspace_bytes,
+                       void* stream) {
   if (p == nullptr || dy == nullptr || x == nullptr) return LOMO_E_ARG;
   if (out_features <= 0 || in_features <= 0 || tokens <= 0) return LOMO_E_ARG;
   if (out_features > INT32_MAX || in_features > INT32_MAX || tokens > INT32_MAX) return LOMO_E_ARG;
@@ -128,15 +137,28 @@ int lomo_gemm_update(void* p, const void* dy, const void* x, int64_t out_feature
   cudaStream_t s = (cudaStream_t)stream;
   switch (dtype) {
     case LOMO_BF16:
-      return lomo_gemm::FusedUpdateGemm<cutlass::bfloat16_t>::run(p, dy, x, M, N, K, (float)alpha,
-                                                                 (float)beta, workspace,
-                                                                 workspace_bytes, s);
+      return lomo_gemm::FusedUpdateGemm<cutlass::bfloat16_t>::run(
+          p, dy, x, M, N, K, (float)alpha, (float)beta, coefs_dev, workspace, workspace_bytes, s);
     case LOMO_F16:
-      return lomo_gemm::FusedUpdateGemm<cutlass::half_t>::run(p, dy, x, M, N, K, (float)alpha,
-                                                             (float)beta, workspace,
-                                                             workspace_bytes, s);
+      return lomo_gemm::FusedUpdateGemm<cutlass::half_t>::run(
+          p, dy, x, M, N, K, (float)alpha, (float)beta, coefs_dev, workspace, workspace_bytes, s);
   }
   return LOMO_E_ARG;
+}
+
+int lomo_gemm_update(void* p, const void* dy, const void* x, int64_t out_features,
+                     int64_t in_features, int64_t tokens, int dtype, double alpha, double beta,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+  return gemm_update(p, dy, x, out_features, in_features, tokens, dtype, alpha, beta, nullptr,
+                     workspace, workspace_bytes, stream);
+}
+
+int lomo_gemm_update_dev(void* p, const void* dy, const void* x, int64_t out_features,
+                         int64_t in_features, int64_t tokens, int dtype, const float* coefs_dev,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  if (coefs_dev == nullptr) return LOMO_E_ARG;
+  return gemm_update(p, dy, x, out_features, in_features, tokens, dtype, 0.0, 1.0, coefs_dev,
+                     workspace, workspace_bytes, stream);
 }
 
 size_t lomo_gemm_update_workspace(int64_t out_features, int64_t in_features, int64_t tokens,

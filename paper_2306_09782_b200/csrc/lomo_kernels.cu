@@ -178,6 +178,7 @@ struct UpdArgs {
   M decay;      // 1 - lr*wd (only used when has_wd)
   M inv_scale;  // 1 / loss scale (exact power of two)
   M coef;       // global-norm clip coefficient
+  M wd;         // weight decay (decay recomputed when lr comes from the state)
   bool use_scale, use_coef, use_clip, has_wd;
 };
 
@@ -234,6 +235,10 @@ __device__ __forceinline__ bool load_args(UpdArgs<M>& a, unsigned flags,
     if ((flags & LOMO_USE_SKIP) && *((volatile const int32_t*)&st->skip)) return false;
     if (flags & LOMO_USE_SCALE) a.inv_scale = (M)st->inv_scale;
     if (flags & LOMO_USE_COEF) a.coef = (M)st->clip_coef;
+    if (flags & LOMO_LR_FROM_STATE) {
+      a.lr = (M)st->lr;
+      a.decay = (M)(1.0 - st->lr * (double)a.wd);
+    }
   }
   return true;
 }
@@ -710,11 +715,32 @@ __global__ void k_state_init(void* state, int nslots, double scale, int growth_i
     st->steps_skipped = 0;
     st->ticket = 0;
     st->pad0 = 0;
-    st->reserved[0] = st->reserved[1] = 0;
+    st->lr = 0.0;
   }
   double* s = reinterpret_cast<double*>(reinterpret_cast<char*>(state) + sizeof(lomo_state));
   const size_t words = (size_t)nslots + nblocks_words(nslots);  // partials need no init
   for (size_t i = threadIdx.x; i < words; i += blockDim.x) s[i] = 0.0;
+}
+
+__global__ void k_set_lr(void* state, double lr) {
+  pdl_wait();
+  if (threadIdx.x == 0) hdr(state)->lr = lr;
+}
+
+__global__ void k_update_coefs(const void* state, double wd, unsigned flags, float* out) {
+  pdl_wait();
+  if (threadIdx.x != 0) return;
+  const lomo_state* st = reinterpret_cast<const lomo_state*>(state);
+  if ((flags & LOMO_USE_SKIP) && st->skip) {
+    out[0] = 0.0f;
+    out[1] = 1.0f;
+    return;
+  }
+  double a = -st->lr;
+  if (flags & LOMO_USE_COEF) a *= st->clip_coef;
+  if (flags & LOMO_USE_SCALE) a *= st->inv_scale;
+  out[0] = (float)a;
+  out[1] = (float)(1.0 - st->lr * wd);
 }
 
 __device__ __forceinline__ bool loss_finite(const void* loss, int dt) {
@@ -818,6 +844,7 @@ UpdArgs<M> make_args(double lr, double clip_value, double weight_decay, unsigned
   a.lr = (M)lr;
   a.clip = (M)(clip_value > 0 ? clip_value : 0);
   a.decay = (M)(1.0 - lr * weight_decay);
+  a.wd = (M)weight_decay;
   a.inv_scale = (M)1;
   a.coef = (M)1;
   a.use_scale = (flags & LOMO_USE_SCALE) != 0;
@@ -1094,6 +1121,19 @@ int lomo_probe(const void* g, int64_t n, int dtype, int slot, unsigned flags, vo
     case LOMO_F64: return launch_probe<double, double>(g, n, slot, flags, state, s);
   }
   return LOMO_E_ARG;
+}
+
+int lomo_set_lr(void* state, double lr, void* stream) {
+  if (state == nullptr) return LOMO_E_ARG;
+  k_set_lr<<<1, 32, 0, (cudaStream_t)stream>>>(state, lr);
+  return (int)cudaGetLastError();
+}
+
+int lomo_update_coefs(const void* state, double weight_decay, unsigned flags, float* coefs_dev,
+                      void* stream) {
+  if (state == nullptr || coefs_dev == nullptr) return LOMO_E_ARG;
+  k_update_coefs<<<1, 32, 0, (cudaStream_t)stream>>>(state, weight_decay, flags, coefs_dev);
+  return (int)cudaGetLastError();
 }
 
 int lomo_fused_rs_update(void* p_shard, const void* const* peer_bufs_dev, int world,

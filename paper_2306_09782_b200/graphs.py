@@ -1,0 +1,120 @@
+"""CUDA-graph capture of a whole two-pass LOMO step (replay mode).
+
+A LLaMA-7B step issues ~3,000 kernels -- autograd's, the hook kernels, K5 --
+and at seq 1024 the host cannot launch them as fast as the B200 runs them.
+``GraphedLOMOStep`` captures the step into two CUDA graphs around the one
+host decision of the protocol (stabilize.py:204-205):
+
+* graph 1: forward, ``begin_step`` (loss check), pass-1 backward whose hooks
+  launch K2 and stash (x, dy) for replay, the end-of-backward flush, K3a;
+* host: read the 128-byte status (the one sync) -- skip, underflow, or go;
+* graph 2: ``lomo_update_coefs`` (alpha/beta from the device state), the
+  replayed updates -- K5 with device-side alpha/beta for every linear, K1
+  with ``LOMO_LR_FROM_STATE`` for the rest -- and K3b.
+
+Everything the step reads that changes between steps lives in device memory
+(the batch in static input tensors, loss scale, clip coefficient, skip flag,
+and the learning rate, set with ``lomo_set_lr`` before each replay), so the
+graphs are captured once.  The numerics are those of the eager replay step.
+"""
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import torch
+
+from . import _lib
+from . import replay as _replay
+from .errors import ConfigError, ScaleUnderflowError
+from .lomo import LOMO, _PROBE
+from .stabilize import StepOutcome
+
+
+class GraphedLOMOStep:
+    """Capture ``loss_fn(*static_inputs)`` + the LOMO two-pass replay step.
+
+    Args:
+        opt: a :class:`LOMO` built with ``replay=True`` (``fuse_gemm`` optional)
+            and a two-pass stabiliser (clip_grad_norm and/or loss_scale).
+        loss_fn: the forward, returning the scalar loss.
+        static_inputs: tensors ``loss_fn`` reads; copy each batch into them.
+        warmup: eager steps run before capture (they also perform replay's
+            first-step gradient check).
+        lr: learning rate for the warm-up steps.
+    """
+
+    def __init__(self, opt: LOMO, loss_fn: Callable[..., torch.Tensor],
+                 static_inputs: Sequence[torch.Tensor], warmup: int = 2, lr: float = 1e-3):
+        if not isinstance(opt, LOMO) or opt._stash is None or opt.passes != 2:
+            raise ConfigError("GraphedLOMOStep needs LOMO(..., replay=True) with clip_grad_norm "
+                              "and/or loss_scale")
+        if opt.clip_value:
+            raise ConfigError("value clipping is a single-pass mode; graph it with LOMO directly")
+        self.opt, self.loss_fn, self.inputs = opt, loss_fn, tuple(static_inputs)
+        eng = opt.engine
+        self.coefs = torch.zeros(2, dtype=torch.float32, device=opt.device)
+        side = torch.cuda.Stream(opt.device)
+        side.wait_stream(torch.cuda.current_stream(opt.device))
+        with torch.cuda.stream(side):
+            for _ in range(max(1, warmup)):
+                opt.step(lambda: loss_fn(*self.inputs), lr)
+        torch.cuda.current_stream(opt.device).wait_stream(side)
+        torch.cuda.synchronize(opt.device)
+        if not opt._replay_checked:
+            raise ConfigError("replay's first-step check did not run during warm-up")
+
+        pool = torch.cuda.graph_pool_handle()
+        self.g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g1, pool=pool):
+            self.loss = loss_fn(*self.inputs)
+            eng.begin(self.loss)
+            eng.configure(flags=opt._flags(_PROBE))
+            opt._run_backward(opt._scaled(self.loss), _PROBE, False)
+            opt._decide()
+        self.g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g2, pool=pool):
+            self._capture_pass2()
+        self.steps = 0
+
+    def _capture_pass2(self) -> None:
+        opt, eng = self.opt, self.opt.engine
+        flags = opt._flags(2) | _lib.LR_FROM_STATE
+        _lib.check(eng.lib.lomo_update_coefs(eng.ptr, opt.weight_decay, flags,
+                                             self.coefs.data_ptr(), eng.stream()),
+                   "lomo_update_coefs")
+        eng.configure(0.0, opt.clip_value, opt.weight_decay, flags)
+        st = opt._stash
+        for p in reversed(opt.params):
+            pid = id(p)
+            if pid in st.linear:
+                x, dy = st.linear.pop(pid)
+                if opt.fuse_gemm and opt._gemm_update(p, x, dy, 0.0, coefs=self.coefs):
+                    continue
+                g = _replay.weight_grad(x, dy)
+            elif pid in st.grads:
+                g = st.grads.pop(pid)
+            else:
+                continue
+            eng.update(p, g)
+            del g
+        eng.flush()
+        st.clear()
+        eng.on_clean()
+
+    def step(self, lr: float) -> torch.Tensor:
+        """One captured step; returns the (device) loss tensor of this step."""
+        opt, eng = self.opt, self.opt.engine
+        _lib.check(eng.lib.lomo_set_lr(eng.ptr, float(lr), eng.stream()), "lomo_set_lr")
+        self.g1.replay()
+        st = eng.read_status()          # the one host sync of the step
+        if st.underflow:
+            raise ScaleUnderflowError(
+                f"loss scale would fall below {st.min_scale}; training diverged")
+        opt.last_norm, opt.clip_coef = float(st.total_norm), float(st.clip_coef)
+        if st.skip:
+            opt.last_outcome = StepOutcome.SKIPPED_OVERFLOW
+        else:
+            self.g2.replay()
+            opt.last_outcome = StepOutcome.APPLIED
+        self.steps += 1
+        return self.loss

@@ -370,9 +370,11 @@ class LOMO(_Protocol):
                 raise ConfigError(bad)
             self._replay_checked = True
 
-    def _gemm_update(self, p, x, dy, lr: float) -> bool:
+    def _gemm_update(self, p, x, dy, lr: float, coefs: torch.Tensor | None = None) -> bool:
         """K5: p <- alpha * dy^T x + beta * p on the tensor cores; False when the
-        shape/dtype is not supported (the caller falls back to GEMM + K1)."""
+        shape/dtype is not supported (the caller falls back to GEMM + K1).
+        ``coefs``: a device [alpha, beta] pair (graph capture) instead of host
+        scalars from the pass-1 status."""
         if p.dtype not in (torch.bfloat16, torch.float16) or p.dim() != 2:
             return False
         out_f, in_f = p.shape
@@ -382,16 +384,22 @@ class LOMO(_Protocol):
         x2 = x.reshape(-1, in_f)
         if not (dy2.is_contiguous() and x2.is_contiguous()) or dy2.dtype != p.dtype:
             return False
-        coef, inv_scale = self._pass1
-        alpha = -lr * coef * inv_scale
-        beta = 1.0 - lr * self.weight_decay
         lib, dt = self.engine.lib, dtype_code(p.dtype)
         need = lib.lomo_gemm_update_workspace(out_f, in_f, dy2.shape[0], dt)
         if need and (self._ws is None or self._ws.numel() < need):
             self._ws = torch.empty(need, dtype=torch.uint8, device=p.device)
         ws = self._ws.data_ptr() if need else None
-        rc = lib.lomo_gemm_update(p.data_ptr(), dy2.data_ptr(), x2.data_ptr(), out_f, in_f,
-                                  dy2.shape[0], dt, alpha, beta, ws, need, self.engine.stream())
+        if coefs is not None:
+            rc = lib.lomo_gemm_update_dev(p.data_ptr(), dy2.data_ptr(), x2.data_ptr(), out_f,
+                                          in_f, dy2.shape[0], dt, coefs.data_ptr(), ws, need,
+                                          self.engine.stream())
+        else:
+            coef, inv_scale = self._pass1
+            alpha = -lr * coef * inv_scale
+            beta = 1.0 - lr * self.weight_decay
+            rc = lib.lomo_gemm_update(p.data_ptr(), dy2.data_ptr(), x2.data_ptr(), out_f, in_f,
+                                      dy2.shape[0], dt, alpha, beta, ws, need,
+                                      self.engine.stream())
         if rc == _E_ARG:
             return False
         _lib.check(rc, "lomo_gemm_update")

@@ -126,3 +126,37 @@ def test_lomo_replay_fused_gemm_matches_replay_k1(dtype):
         worst = max(worst, r.max().item())
     print(f"{dtype}: fused vs unfused, max |diff| / tolerance = {worst:.3f}")
     assert worst <= 1.0
+
+
+# --- CUDA-graph capture of the replay step (graphs.py) -----------------------------
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_graphed_step_equals_eager_step(fuse):
+    """The captured two-pass replay step reproduces the eager step exactly
+    (same kernels; alpha/beta and lr read from device memory)."""
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.graphs import GraphedLOMOStep
+    from paper_2306_09782_b200.workloads import Llama
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+    torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+    cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
+    a = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0)
+    b = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0)
+    kw = dict(lr=0.05, clip_grad_norm=0.3, loss_scale=2.0 ** 8, replay=True, fuse_gemm=fuse)
+    oa, ob = LOMO(a, **kw), LOMO(b, **kw)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    data = [torch.randint(0, 256, (2, 65), device="cuda", generator=gen) for _ in range(6)]
+    static = data[0].clone()
+    # the graph object runs 2 eager warm-up steps on data[0]: mirror them on `a`
+    for _ in range(2):
+        oa.step(lambda: a.loss(data[0][:, :-1], data[0][:, 1:]), 0.05)
+    gs = GraphedLOMOStep(ob, lambda d: b.loss(d[:, :-1], d[:, 1:]), (static,), warmup=2, lr=0.05)
+    for k in range(1, 6):
+        lr = 0.05 / k                          # a schedule: lr comes from the state
+        la = oa.step(lambda: a.loss(data[k][:, :-1], data[k][:, 1:]), lr)
+        static.copy_(data[k])
+        lb = gs.step(lr).item()
+        assert oa.last_outcome == ob.last_outcome
+        assert la == lb, (k, la, lb)
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)
