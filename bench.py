@@ -270,12 +270,12 @@ def bench_update(args, rank, world):
     pdisp = HookDispatcher(lib, st.data_ptr(), _lib.MATH_F32)
     pdisp.configure(flags=_lib.USE_SCALE)
 
-    def probe_pass():
-        lib.lomo_begin_step(st.data_ptr(), None, 0, stream)
+    def probe_pass(s=stream):
+        lib.lomo_begin_step(st.data_ptr(), None, 0, s)
         for i in range(len(G) - 1, -1, -1):
-            pdisp.probe(G[i], dt_code, len(G) - 1 - i, stream)
-        pdisp.flush(stream)
-        lib.lomo_finalize_norm(st.data_ptr(), stream)
+            pdisp.probe(G[i], dt_code, len(G) - 1 - i, s)
+        pdisp.flush(s)
+        lib.lomo_finalize_norm(st.data_ptr(), s)
     for _ in range(args.warmup):
         probe_pass()
     torch.cuda.synchronize()
@@ -287,7 +287,30 @@ def bench_update(args, rank, world):
     host_probe_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     torch.cuda.synchronize()
     probe_ms = start.elapsed_time(end) / args.steps
+    # the same launches captured in a CUDA graph (as GraphedLOMOStep runs them):
+    # removes the host launch cost, leaving the kernels' own time
+    def graphed(fn):
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            fn(cap.cuda_stream)
+        torch.cuda.current_stream().wait_stream(cap)
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(args.steps):
+            g.replay()
+        end.record()
+        torch.cuda.synchronize()
+        ms_ = start.elapsed_time(end) / args.steps
+        del g
+        return ms_
+    probe_graph_ms = graphed(probe_pass)
+    upd_graph_ms = graphed(lambda s: run_update_pass(disp, P, G, dt_code, s))
     probe = {"gbs": round(2 * elems / (probe_ms * 1e-3) / 1e9, 1), "ms_per_pass": round(probe_ms, 4),
+             "graphed_gbs": round(2 * elems / (probe_graph_ms * 1e-3) / 1e9, 1),
              "host_ms_per_pass": round(host_probe_ms, 3),
              "algorithmic_bytes_per_elem": 2,
              "what": "K2 sum-of-squares + overflow flag over every gradient, + begin/finalize (K3a)"}
@@ -308,6 +331,7 @@ def bench_update(args, rank, world):
     del P, G
     torch.cuda.empty_cache()
     return {"gbs": gbs, "ms": ms / args.steps, "probe": probe, "f64_math": f64,
+            "graphed_gbs": BYTES_PER_ELEM * elems / (upd_graph_ms * 1e-3) / 1e9,
             "host_ms": host_ms, "elems_per_rank": elems, "total_elems": total_elems,
             "launches": launches, "clocks": clk.summary(), "kernel_gbs": achieved,
             "kernel_ms_per_step": ksum_ms / args.steps, "shapes": shapes}
@@ -736,6 +760,7 @@ def main():
                                    "elements / their time",
                          "avg_launch_us": round(1e3 * up["ms"] / (up["launches"] / args.steps), 2),
                          "host_ms_per_pass": round(up["host_ms"], 3),
+                         "graphed_pass_gbs": round(up["graphed_gbs"], 1),
                          "per_shape_instrumented": up["shapes"],
                          "per_shape_note": "per-launch event pairs (separate replay) break the PDL "
                                            "overlap, so these per-shape rates understate the pass"},

@@ -1,0 +1,54 @@
+/* lomo_workload.h -- fused elementwise kernels of the benchmark decoder.
+ *
+ * These are NOT part of the LOMO update path (include/lomo_b200.h).  They
+ * implement the non-GEMM layers of workloads.Llama -- RMSNorm, rotary
+ * position embedding, SwiGLU -- as one kernel per layer per direction, so
+ * that the config-3 training step (LLaMA-7B) is not
+ * dominated by eager PyTorch's chains of elementwise launches.  Same
+ * conventions as lomo_b200.h: extern "C", plain pointers, async on `stream`,
+ * 0 = ok, LOMO_E_ARG on bad arguments, cudaError_t otherwise.
+ *
+ * Storage dtype: LOMO_F16 or LOMO_BF16 (lomo_dtype); arithmetic in fp32 with
+ * one rounding per output element.  Rows are contiguous, h % 8 == 0.
+ */
+#ifndef LOMO_WORKLOAD_H
+#define LOMO_WORKLOAD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* y[r,:] = round(round(x[r,:] * rstd[r]) * w),  rstd[r] = 1/sqrt(mean(x[r,:]^2) + eps).
+ * rstd (fp32, rows) is saved for the backward.  h <= 8192. */
+int lomo_wl_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows,
+                        int h, int dtype, float eps, void* stream);
+
+/* dx = rstd * (dt - n * mean(dt * n)),  n = x * rstd,  dt = dy * w;
+ * dw = sum_r dy * round(n).  `partial` is fp32 scratch of
+ * lomo_wl_rmsnorm_partial_rows(rows) * h floats (deterministic two-stage
+ * reduction, no atomics). */
+int lomo_wl_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
+                        void* dx, void* dw, float* partial, int64_t rows, int h, int dtype,
+                        void* stream);
+int lomo_wl_rmsnorm_partial_rows(int64_t rows);
+
+/* Rotary embedding of q and k in [rows = b*s, heads, dh] layout, position
+ * = row % seq; cos/sin are [seq, dh] tables in the storage dtype.
+ * direction 0: out = x*cos + rotate_half(x)*sin (forward);
+ * direction 1: the transpose (backward).  q/k may not alias qo/ko. */
+int lomo_wl_rope(const void* q, const void* k, void* qo, void* ko, const void* cos,
+                 const void* sin, int64_t rows, int seq, int heads, int dh, int dtype,
+                 int direction, void* stream);
+
+/* out = silu(g) * u;  backward: dg = dout*u*silu'(g), du = dout*silu(g). */
+int lomo_wl_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, int dtype,
+                       void* stream);
+int lomo_wl_swiglu_bwd(const void* dout, const void* g, const void* u, void* dg, void* du,
+                       int64_t n, int dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOMO_WORKLOAD_H */

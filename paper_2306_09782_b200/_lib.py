@@ -47,6 +47,16 @@ EXPORTS = (
     "lomo_gemm_update_dev",
 )
 
+# include/lomo_workload.h: the benchmark decoder's fused layers (not the LOMO path)
+WL_EXPORTS = (
+    "lomo_wl_rmsnorm_fwd",
+    "lomo_wl_rmsnorm_bwd",
+    "lomo_wl_rmsnorm_partial_rows",
+    "lomo_wl_rope",
+    "lomo_wl_swiglu_fwd",
+    "lomo_wl_swiglu_bwd",
+)
+
 
 class LomoStatus(ctypes.Structure):
     """Host mirror of ``lomo_state`` (128 bytes, include/lomo_b200.h)."""
@@ -113,6 +123,13 @@ _SIGS = {
     "lomo_update_coefs": (_i32, [_vp, _dbl, _u32, _vp, _vp]),
     "lomo_gemm_update_dev": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp,
                                     ctypes.c_size_t, _vp]),
+    "lomo_wl_rmsnorm_fwd": (_i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, ctypes.c_float, _vp]),
+    "lomo_wl_rmsnorm_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp]),
+    "lomo_wl_rmsnorm_partial_rows": (_i32, [_i64]),
+    "lomo_wl_rope": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32,
+                            _vp]),
+    "lomo_wl_swiglu_fwd": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "lomo_wl_swiglu_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
 }
 
 _LIB = None

@@ -226,21 +226,48 @@ __device__ __forceinline__ uint4 upd_vec(const uint4& pv, const uint4& gv,
   return O.u;
 }
 
-template <typename M>
-__device__ __forceinline__ bool load_args(UpdArgs<M>& a, unsigned flags,
-                                          const lomo_state* st) {
+__device__ __forceinline__ void pdl_enter() {
   pdl_wait();
   pdl_launch_dependents();
+}
+
+// Step-state scalars (skip, 1/scale, clip coefficient, lr).  Kernels issue
+// their data loads BEFORE calling this: the loads do not depend on the
+// state, so the state read's L2 latency overlaps them.  Reading the state
+// first put one dependent L2 round trip in front of every CTA's loads --
+// with one 4 KB tile per CTA that cost K1 a third of its bandwidth whenever
+// a state flag was set (9.7 vs 6.2 ms over the LLaMA-7B pass,
+// tools/k1_context.py).
+template <typename M>
+__device__ __forceinline__ bool resolve_args(UpdArgs<M>& a, unsigned flags,
+                                             const lomo_state* st) {
   if (st != nullptr) {
-    if ((flags & LOMO_USE_SKIP) && *((volatile const int32_t*)&st->skip)) return false;
-    if (flags & LOMO_USE_SCALE) a.inv_scale = (M)st->inv_scale;
-    if (flags & LOMO_USE_COEF) a.coef = (M)st->clip_coef;
+    // four independent plain loads from one 128-byte line, all in flight
+    // together (the state was written by an earlier kernel: after the PDL
+    // wait, no volatile/strong access is needed -- a volatile read of `skip`
+    // compiled to LDG.STRONG.SYS and serialised a second round trip)
+    int32_t skip;
+    double inv_scale, coef, lr;
+    asm volatile("ld.global.s32 %0, [%1];" : "=r"(skip) : "l"(&st->skip));
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(inv_scale) : "l"(&st->inv_scale));
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(coef) : "l"(&st->clip_coef));
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(lr) : "l"(&st->lr));
+    if ((flags & LOMO_USE_SKIP) && skip) return false;
+    if (flags & LOMO_USE_SCALE) a.inv_scale = (M)inv_scale;
+    if (flags & LOMO_USE_COEF) a.coef = (M)coef;
     if (flags & LOMO_LR_FROM_STATE) {
-      a.lr = (M)st->lr;
-      a.decay = (M)(1.0 - st->lr * (double)a.wd);
+      a.lr = (M)lr;
+      a.decay = (M)(1.0 - lr * (double)a.wd);
     }
   }
   return true;
+}
+
+template <typename M>
+__device__ __forceinline__ bool load_args(UpdArgs<M>& a, unsigned flags,
+                                          const lomo_state* st) {
+  pdl_enter();
+  return resolve_args(a, flags, st);
 }
 
 // Vector body: `nvec` 16-byte vectors starting at p/g (16-B aligned), plus
@@ -260,16 +287,7 @@ __global__ void __launch_bounds__(kThreads)
     k1_update(T* __restrict__ p, const T* __restrict__ g, int64_t n, int head,
               int64_t nvec, UpdArgs<M> a, unsigned flags, const lomo_state* st) {
   constexpr int V = 16 / sizeof(T);
-  if (!load_args(a, flags, st)) return;
-
-  if (blockIdx.x == 0) {  // scalar head (before the first aligned vector) and tail
-    const int64_t tail0 = head + nvec * V;
-    const int64_t ntail = n - tail0;
-    for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
-      const int64_t e = i < head ? i : tail0 + (i - head);
-      p[e] = from_m<T, M>(upd_elem(to_m<M>(p[e]), to_m<M>(g[e]), a));
-    }
-  }
+  pdl_enter();
   uint4* pv = reinterpret_cast<uint4*>(p + head);
   const uint4* gv = reinterpret_cast<const uint4*>(g + head);
   const int64_t base = (int64_t)blockIdx.x * (kThreads * kK1Vec) + threadIdx.x;
@@ -280,6 +298,16 @@ __global__ void __launch_bounds__(kThreads)
     if (i < nvec) {
       G[u] = ld_stream_ro(gv + i);
       P[u] = ld_stream_rw(pv + i);
+    }
+  }
+  if (!resolve_args(a, flags, st)) return;  // overlaps the loads above
+
+  if (blockIdx.x == 0) {  // scalar head (before the first aligned vector) and tail
+    const int64_t tail0 = head + nvec * V;
+    const int64_t ntail = n - tail0;
+    for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
+      const int64_t e = i < head ? i : tail0 + (i - head);
+      p[e] = from_m<T, M>(upd_elem(to_m<M>(p[e]), to_m<M>(g[e]), a));
     }
   }
 #pragma unroll
@@ -495,16 +523,20 @@ __global__ void __launch_bounds__(kThreads)
 // (ShardedLOMO pads buckets to 8*world elements).
 constexpr int kMaxPeers = 16;
 
-template <typename T, typename M>
-__device__ __forceinline__ void peer_sum_vec(const T* const* __restrict__ peers, int world,
-                                             int64_t idx, M (&acc)[16 / sizeof(T)]) {
-  constexpr int V = 16 / sizeof(T);
-#pragma unroll
-  for (int k = 0; k < V; ++k) acc[k] = (M)0;
-  uint4 buf[kMaxPeers];
+template <typename T>
+__device__ __forceinline__ void peer_load_vec(const T* const* __restrict__ peers, int world,
+                                              int64_t idx, uint4 (&buf)[kMaxPeers]) {
 #pragma unroll
   for (int r = 0; r < kMaxPeers; ++r)  // all loads in flight before the adds
     if (r < world) buf[r] = ld_stream_ro(reinterpret_cast<const uint4*>(peers[r]) + idx);
+}
+
+template <typename T, typename M>
+__device__ __forceinline__ void peer_add_vec(const uint4 (&buf)[kMaxPeers], int world,
+                                             M (&acc)[16 / sizeof(T)]) {
+  constexpr int V = 16 / sizeof(T);
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = (M)0;
 #pragma unroll
   for (int r = 0; r < kMaxPeers; ++r) {
     if (r < world) {
@@ -521,18 +553,21 @@ __global__ void __launch_bounds__(kThreads)
     k4_rs_update(T* __restrict__ p, const T* const* __restrict__ peers_dev, int world, int64_t off,
                  int64_t nvec, UpdArgs<M> a, unsigned flags, const lomo_state* st) {
   constexpr int V = 16 / sizeof(T);
-  if (!load_args(a, flags, st)) return;
+  pdl_enter();
   __shared__ const T* peers[kMaxPeers];
   if (threadIdx.x < kMaxPeers)
     peers[threadIdx.x] = threadIdx.x < world ? peers_dev[threadIdx.x] + off : nullptr;
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (i >= nvec) return;
-  M g[V];
-  peer_sum_vec<T, M>(peers, world, i, g);
+  uint4 buf[kMaxPeers];
+  peer_load_vec<T>(peers, world, i, buf);
   uint4* pv = reinterpret_cast<uint4*>(p);
   Vec16<T> P, O;
   P.u = ld_stream_rw(pv + i);
+  if (!resolve_args(a, flags, st)) return;  // overlaps the loads above
+  M g[V];
+  peer_add_vec<T, M>(buf, world, g);
 #pragma unroll
   for (int k = 0; k < V; ++k) O.e[k] = from_m<T, M>(upd_elem(to_m<M>(P.e[k]), g[k], a));
   st_stream(pv + i, O.u);
@@ -558,8 +593,10 @@ __global__ void __launch_bounds__(kThreads)
   const int64_t beg = (int64_t)blockIdx.x * per_cta;
   const int64_t end = min(beg + per_cta, nvec);
   for (int64_t i = beg + threadIdx.x; i < end; i += kThreads) {
+    uint4 buf[kMaxPeers];
+    peer_load_vec<T>(peers, world, i, buf);
     M g[V];
-    peer_sum_vec<T, M>(peers, world, i, g);
+    peer_add_vec<T, M>(buf, world, g);
     M part = 0;
 #pragma unroll
     for (int k = 0; k < V; ++k) {

@@ -1,0 +1,428 @@
+// Fused elementwise layers of the benchmark decoder (workloads.Llama):
+// RMSNorm, rotary embedding, SwiGLU -- forward and backward, one kernel each.
+//
+// Not on the LOMO update path.  They exist because the config-3 training
+// step (LLaMA-7B, fp16, seq 1024) spent ~1/3 of its GPU time in eager
+// PyTorch's chains of small elementwise kernels around the GEMMs (profiles/
+// r01_summary.md); each layer here is a single HBM pass: 16-byte vector
+// loads/stores, fp32 arithmetic, one rounding per output.  Reductions are
+// fixed-order (no atomics), so results are run-to-run deterministic.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lomo_b200.h"
+#include "lomo_workload.h"
+
+namespace wl {
+
+constexpr int kThreads = 256;
+constexpr int kRmsMaxVec = 4;       // RMSNorm: h <= kThreads * 4 vectors * 8 = 8192
+constexpr int kTargetCtas = 296;    // RMSNorm backward: 2 CTAs per B200 SM
+
+__device__ __forceinline__ float tof(__half x) { return __half2float(x); }
+__device__ __forceinline__ float tof(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T fromf(float x);
+template <> __device__ __forceinline__ __half fromf<__half>(float x) { return __float2half_rn(x); }
+template <> __device__ __forceinline__ __nv_bfloat16 fromf<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+template <typename T> __device__ __forceinline__ float rnd(float x) { return tof(fromf<T>(x)); }
+
+template <typename T>
+union Vec8 {
+  uint4 u;
+  T e[8];
+};
+
+__device__ __forceinline__ uint4 ld_nc(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// fixed-order block sum, result broadcast to every thread
+__device__ __forceinline__ float block_sum(float v, float* sm) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();  // sm reuse across calls
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  float r = 0.f;
+#pragma unroll
+  for (int i = 0; i < kThreads / 32; ++i) r += sm[i];
+  return r;
+}
+
+// ---------------------------------------------------------------- RMSNorm
+template <typename T, int kMaxVec>
+__global__ void __launch_bounds__(kThreads)
+    rms_fwd(const T* __restrict__ x, const T* __restrict__ w, T* __restrict__ y,
+            float* __restrict__ rstd, int h, float eps) {
+  __shared__ float sm[kThreads / 32];
+  const int nv = h / 8;
+  const size_t row = blockIdx.x;
+  const uint4* xv = reinterpret_cast<const uint4*>(x + row * h);
+  Vec8<T> X[kMaxVec];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kThreads;
+    if (i < nv) {
+      X[k].u = ld_nc(xv + i);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss = fmaf(tof(X[k].e[e]), tof(X[k].e[e]), ss);
+    }
+  }
+  const float r = rsqrtf(block_sum(ss, sm) / (float)h + eps);
+  if (threadIdx.x == 0) rstd[row] = r;
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+  uint4* yv = reinterpret_cast<uint4*>(y + row * h);
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kThreads;
+    if (i < nv) {
+      Vec8<T> W, Y;
+      W.u = wv[i];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        Y.e[e] = fromf<T>(rnd<T>(tof(X[k].e[e]) * r) * tof(W.e[e]));
+      yv[i] = Y.u;
+    }
+  }
+}
+
+// one CTA per `rpc` consecutive rows: dx per row, dw partial per CTA
+template <typename T, int kMaxVec>
+__global__ void __launch_bounds__(kThreads)
+    rms_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ w,
+            const float* __restrict__ rstd, T* __restrict__ dx, float* __restrict__ partial,
+            int64_t rows, int h, int rpc) {
+  __shared__ float sm[kThreads / 32];
+  const int nv = h / 8;
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+  float W[kMaxVec][8], DW[kMaxVec][8];
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kThreads;
+    Vec8<T> t;
+    t.u = i < nv ? wv[i] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      W[k][e] = tof(t.e[e]);
+      DW[k][e] = 0.f;
+    }
+  }
+  const int64_t r0 = (int64_t)blockIdx.x * rpc;
+  const int64_t r1 = min(r0 + rpc, rows);
+  for (int64_t row = r0; row < r1; ++row) {
+    const float r = rstd[row];
+    const uint4* xv = reinterpret_cast<const uint4*>(x + row * h);
+    const uint4* dv = reinterpret_cast<const uint4*>(dy + row * h);
+    float N[kMaxVec][8], DT[kMaxVec][8];
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int i = threadIdx.x + k * kThreads;
+      if (i < nv) {
+        Vec8<T> X, D;
+        X.u = ld_nc(xv + i);
+        D.u = ld_nc(dv + i);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float n = tof(X.e[e]) * r;
+          const float d = tof(D.e[e]);
+          N[k][e] = n;
+          DT[k][e] = rnd<T>(d * W[k][e]);            // grad of round(n) * w w.r.t. round(n)
+          DW[k][e] = fmaf(d, rnd<T>(n), DW[k][e]);   // grad w.r.t. w
+          dot = fmaf(DT[k][e], n, dot);
+        }
+      }
+    }
+    const float m = block_sum(dot, sm) / (float)h;
+    uint4* ov = reinterpret_cast<uint4*>(dx + row * h);
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int i = threadIdx.x + k * kThreads;
+      if (i < nv) {
+        Vec8<T> O;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) O.e[e] = fromf<T>(r * (DT[k][e] - N[k][e] * m));
+        ov[i] = O.u;
+      }
+    }
+  }
+  float* pr = partial + (size_t)blockIdx.x * h;
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = threadIdx.x + k * kThreads;
+    if (i < nv) {
+      float4* p4 = reinterpret_cast<float4*>(pr + (size_t)i * 8);
+      p4[0] = make_float4(DW[k][0], DW[k][1], DW[k][2], DW[k][3]);
+      p4[1] = make_float4(DW[k][4], DW[k][5], DW[k][6], DW[k][7]);
+    }
+  }
+}
+
+// dw[j] = sum over CTA partials, in CTA order
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    rms_dw_reduce(const float* __restrict__ partial, T* __restrict__ dw, int nparts, int h) {
+  const int j = blockIdx.x * kThreads + threadIdx.x;
+  if (j >= h) return;
+  float s = 0.f;
+  for (int c = 0; c < nparts; ++c) s += partial[(size_t)c * h + j];
+  dw[j] = fromf<T>(s);
+}
+
+// ---------------------------------------------------------------- rotary
+// one thread per (tensor, row, head, 8-element group of the first half)
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    rope(const T* __restrict__ q, const T* __restrict__ k, T* __restrict__ qo,
+         T* __restrict__ ko, const T* __restrict__ cs, const T* __restrict__ sn, int64_t rows,
+         int seq, int heads, int dh, int bwd) {
+  const int half = dh / 2, gph = half / 8;
+  const int64_t per_tensor = rows * heads * gph;
+  const int64_t total = 2 * per_tensor;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const bool is_k = t >= per_tensor;
+    const int64_t u = is_k ? t - per_tensor : t;
+    const int gi = (int)(u % gph);
+    const int64_t rh = u / gph;              // row * heads + head
+    const int pos = (int)((rh / heads) % seq);
+    const T* src = (is_k ? k : q) + rh * dh;
+    T* dst = (is_k ? ko : qo) + rh * dh;
+    Vec8<T> X1, X2, C1, C2, S1, S2, O1, O2;
+    X1.u = ld_nc(src + gi * 8);
+    X2.u = ld_nc(src + half + gi * 8);
+    const T* cr = cs + (size_t)pos * dh;
+    const T* sr = sn + (size_t)pos * dh;
+    C1.u = *reinterpret_cast<const uint4*>(cr + gi * 8);
+    C2.u = *reinterpret_cast<const uint4*>(cr + half + gi * 8);
+    S1.u = *reinterpret_cast<const uint4*>(sr + gi * 8);
+    S2.u = *reinterpret_cast<const uint4*>(sr + half + gi * 8);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float x1 = tof(X1.e[e]), x2 = tof(X2.e[e]);
+      const float c1 = tof(C1.e[e]), c2 = tof(C2.e[e]);
+      const float s1 = tof(S1.e[e]), s2 = tof(S2.e[e]);
+      if (!bwd) {  // out = x*cos + cat(-x2, x1)*sin
+        O1.e[e] = fromf<T>(x1 * c1 - x2 * s1);
+        O2.e[e] = fromf<T>(x2 * c2 + x1 * s2);
+      } else {     // its transpose
+        O1.e[e] = fromf<T>(x1 * c1 + x2 * s2);
+        O2.e[e] = fromf<T>(x2 * c2 - x1 * s1);
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + gi * 8) = O1.u;
+    *reinterpret_cast<uint4*>(dst + half + gi * 8) = O2.u;
+  }
+}
+
+// ---------------------------------------------------------------- SwiGLU
+__device__ __forceinline__ float sigmoidf_(float g) { return 1.f / (1.f + __expf(-g)); }
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    swiglu_fwd(const T* __restrict__ g, const T* __restrict__ u, T* __restrict__ out,
+               int64_t nvec) {
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const uint4* uv = reinterpret_cast<const uint4*>(u);
+  uint4* ov = reinterpret_cast<uint4*>(out);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    Vec8<T> G, U, O;
+    G.u = ld_nc(gv + i);
+    U.u = ld_nc(uv + i);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float x = tof(G.e[e]);
+      O.e[e] = fromf<T>(x * sigmoidf_(x) * tof(U.e[e]));
+    }
+    ov[i] = O.u;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    swiglu_bwd(const T* __restrict__ dout, const T* __restrict__ g, const T* __restrict__ u,
+               T* __restrict__ dg, T* __restrict__ du, int64_t nvec) {
+  const uint4* dv = reinterpret_cast<const uint4*>(dout);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const uint4* uv = reinterpret_cast<const uint4*>(u);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    Vec8<T> D, G, U, DG, DU;
+    D.u = ld_nc(dv + i);
+    G.u = ld_nc(gv + i);
+    U.u = ld_nc(uv + i);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float x = tof(G.e[e]), d = tof(D.e[e]), y = tof(U.e[e]);
+      const float s = sigmoidf_(x);
+      DU.e[e] = fromf<T>(d * x * s);
+      DG.e[e] = fromf<T>(d * y * s * (1.f + x * (1.f - s)));
+    }
+    reinterpret_cast<uint4*>(dg)[i] = DG.u;
+    reinterpret_cast<uint4*>(du)[i] = DU.u;
+  }
+}
+
+inline int grid_for(int64_t work) {
+  // enough CTAs to fill 148 SMs x 8 resident CTAs, no more than the work
+  const int64_t cap = 148 * 8;
+  const int64_t need = (work + kThreads - 1) / kThreads;
+  return (int)(need < cap ? (need > 0 ? need : 1) : cap);
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <template <typename> class F, typename... A>
+int dispatch(int dtype, A... a) {
+  if (dtype == LOMO_F16) return F<__half>::run(a...);
+  if (dtype == LOMO_BF16) return F<__nv_bfloat16>::run(a...);
+  return LOMO_E_ARG;
+}
+
+inline int status() { return (int)cudaGetLastError(); }
+
+template <typename T>
+struct RmsFwd {
+  static int run(const void* x, const void* w, void* y, float* rstd, int64_t rows, int h,
+                 float eps, cudaStream_t s) {
+    // vectors per thread as a template constant: registers hold the row
+    switch ((h / 8 + kThreads - 1) / kThreads) {
+      case 1: rms_fwd<T, 1><<<(unsigned)rows, kThreads, 0, s>>>((const T*)x, (const T*)w, (T*)y, rstd, h, eps); break;
+      case 2: rms_fwd<T, 2><<<(unsigned)rows, kThreads, 0, s>>>((const T*)x, (const T*)w, (T*)y, rstd, h, eps); break;
+      case 3: rms_fwd<T, 3><<<(unsigned)rows, kThreads, 0, s>>>((const T*)x, (const T*)w, (T*)y, rstd, h, eps); break;
+      default: rms_fwd<T, 4><<<(unsigned)rows, kThreads, 0, s>>>((const T*)x, (const T*)w, (T*)y, rstd, h, eps); break;
+    }
+    return status();
+  }
+};
+
+inline int rms_rows_per_cta(int64_t rows) { return (int)((rows + kTargetCtas - 1) / kTargetCtas); }
+
+template <typename T>
+struct RmsBwd {
+  static int run(const void* dy, const void* x, const void* w, const float* rstd, void* dx,
+                 void* dw, float* partial, int64_t rows, int h, cudaStream_t s) {
+    const int rpc = rms_rows_per_cta(rows);
+    const int nparts = (int)((rows + rpc - 1) / rpc);
+#define WL_RMS_BWD(NV)                                                                   \
+  rms_bwd<T, NV><<<nparts, kThreads, 0, s>>>((const T*)dy, (const T*)x, (const T*)w, rstd, \
+                                             (T*)dx, partial, rows, h, rpc)
+    switch ((h / 8 + kThreads - 1) / kThreads) {
+      case 1: WL_RMS_BWD(1); break;
+      case 2: WL_RMS_BWD(2); break;
+      case 3: WL_RMS_BWD(3); break;
+      default: WL_RMS_BWD(4); break;
+    }
+#undef WL_RMS_BWD
+    rms_dw_reduce<T><<<(h + kThreads - 1) / kThreads, kThreads, 0, s>>>(partial, (T*)dw, nparts,
+                                                                         h);
+    return status();
+  }
+};
+
+template <typename T>
+struct Rope {
+  static int run(const void* q, const void* k, void* qo, void* ko, const void* c,
+                 const void* sn, int64_t rows, int seq, int heads, int dh, int bwd,
+                 cudaStream_t s) {
+    const int64_t work = 2 * rows * heads * (dh / 16);
+    rope<T><<<grid_for(work), kThreads, 0, s>>>((const T*)q, (const T*)k, (T*)qo, (T*)ko,
+                                                (const T*)c, (const T*)sn, rows, seq, heads, dh,
+                                                bwd);
+    return status();
+  }
+};
+
+template <typename T>
+struct SwigluFwd {
+  static int run(const void* g, const void* u, void* o, int64_t n, cudaStream_t s) {
+    swiglu_fwd<T><<<grid_for(n / 8), kThreads, 0, s>>>((const T*)g, (const T*)u, (T*)o, n / 8);
+    return status();
+  }
+};
+
+template <typename T>
+struct SwigluBwd {
+  static int run(const void* d, const void* g, const void* u, void* dg, void* du, int64_t n,
+                 cudaStream_t s) {
+    swiglu_bwd<T><<<grid_for(n / 8), kThreads, 0, s>>>((const T*)d, (const T*)g, (const T*)u,
+                                                       (T*)dg, (T*)du, n / 8);
+    return status();
+  }
+};
+
+}  // namespace wl
+
+extern "C" {
+
+int lomo_wl_rmsnorm_partial_rows(int64_t rows) {
+  if (rows <= 0) return 0;
+  const int rpc = wl::rms_rows_per_cta(rows);
+  return (int)((rows + rpc - 1) / rpc);
+}
+
+int lomo_wl_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows, int h,
+                        int dtype, float eps, void* stream) {
+  if (rows < 0 || h <= 0 || h % 8 || h > wl::kThreads * wl::kRmsMaxVec * 8) return LOMO_E_ARG;
+  if (rows == 0) return 0;
+  if (!x || !w || !y || !rstd || !wl::aligned16(x) || !wl::aligned16(w) || !wl::aligned16(y))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::RmsFwd>(dtype, x, w, y, rstd, rows, h, eps, (cudaStream_t)stream);
+}
+
+int lomo_wl_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
+                        void* dx, void* dw, float* partial, int64_t rows, int h, int dtype,
+                        void* stream) {
+  if (rows <= 0 || h <= 0 || h % 8 || h > wl::kThreads * wl::kRmsMaxVec * 8) return LOMO_E_ARG;
+  if (!dy || !x || !w || !rstd || !dx || !dw || !partial) return LOMO_E_ARG;
+  if (!wl::aligned16(dy) || !wl::aligned16(x) || !wl::aligned16(w) || !wl::aligned16(dx) ||
+      !wl::aligned16(partial))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::RmsBwd>(dtype, dy, x, w, rstd, dx, dw, partial, rows, h,
+                                  (cudaStream_t)stream);
+}
+
+int lomo_wl_rope(const void* q, const void* k, void* qo, void* ko, const void* cos,
+                 const void* sin, int64_t rows, int seq, int heads, int dh, int dtype,
+                 int direction, void* stream) {
+  if (rows < 0 || seq <= 0 || heads <= 0 || dh <= 0 || dh % 16 || (direction & ~1))
+    return LOMO_E_ARG;
+  if (rows == 0) return 0;
+  if (!q || !k || !qo || !ko || !cos || !sin || q == qo || k == ko) return LOMO_E_ARG;
+  if (!wl::aligned16(q) || !wl::aligned16(k) || !wl::aligned16(qo) || !wl::aligned16(ko) ||
+      !wl::aligned16(cos) || !wl::aligned16(sin))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::Rope>(dtype, q, k, qo, ko, cos, sin, rows, seq, heads, dh, direction,
+                                (cudaStream_t)stream);
+}
+
+int lomo_wl_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, int dtype,
+                       void* stream) {
+  if (n < 0 || n % 8) return LOMO_E_ARG;
+  if (n == 0) return 0;
+  if (!g || !u || !out || !wl::aligned16(g) || !wl::aligned16(u) || !wl::aligned16(out))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::SwigluFwd>(dtype, g, u, out, n, (cudaStream_t)stream);
+}
+
+int lomo_wl_swiglu_bwd(const void* dout, const void* g, const void* u, void* dg, void* du,
+                       int64_t n, int dtype, void* stream) {
+  if (n < 0 || n % 8) return LOMO_E_ARG;
+  if (n == 0) return 0;
+  if (!dout || !g || !u || !dg || !du || !wl::aligned16(dout) || !wl::aligned16(g) ||
+      !wl::aligned16(u) || !wl::aligned16(dg) || !wl::aligned16(du))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::SwigluBwd>(dtype, dout, g, u, dg, du, n, (cudaStream_t)stream);
+}
+
+}  // extern "C"

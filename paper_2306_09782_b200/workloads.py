@@ -204,15 +204,137 @@ def llama_param_count(size: str = "7b") -> int:
     return sum(math.prod(s) for _, s in llama_param_shapes(size))
 
 
+# ---------------------------------------------------------------------------
+# Fused layers (csrc/workload_kernels.cu, include/lomo_workload.h): one kernel
+# per layer per direction for fp16/bf16 CUDA tensors; other dtypes/devices use
+# the eager formulas below (same math, several kernels).  Not the LOMO path.
+# ---------------------------------------------------------------------------
+_WL_DTYPES = {torch.float16: 1, torch.bfloat16: 2}
+
+
+def _wl():
+    from . import _lib
+    return _lib.load()
+
+
+def _wl_ok(*ts) -> bool:
+    return all(t.is_cuda and t.dtype in _WL_DTYPES and t.is_contiguous() for t in ts)
+
+
+def _wl_call(rc, what):
+    if rc != 0:
+        from .errors import NativeError
+        raise NativeError(f"{what} failed with status {rc}")
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class _RMSNormFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, eps):
+        h = x.shape[-1]
+        rows = x.numel() // h
+        y = torch.empty_like(x)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        _wl_call(_wl().lomo_wl_rmsnorm_fwd(x.data_ptr(), w.data_ptr(), y.data_ptr(),
+                                           rstd.data_ptr(), rows, h, _WL_DTYPES[x.dtype], eps,
+                                           _stream()), "lomo_wl_rmsnorm_fwd")
+        ctx.save_for_backward(x, w, rstd)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, w, rstd = ctx.saved_tensors
+        dy = dy.contiguous()
+        h = x.shape[-1]
+        rows = x.numel() // h
+        lib = _wl()
+        dx, dw = torch.empty_like(x), torch.empty_like(w)
+        part = torch.empty(lib.lomo_wl_rmsnorm_partial_rows(rows) * h, dtype=torch.float32,
+                           device=x.device)
+        _wl_call(lib.lomo_wl_rmsnorm_bwd(dy.data_ptr(), x.data_ptr(), w.data_ptr(),
+                                         rstd.data_ptr(), dx.data_ptr(), dw.data_ptr(),
+                                         part.data_ptr(), rows, h, _WL_DTYPES[x.dtype],
+                                         _stream()), "lomo_wl_rmsnorm_bwd")
+        return dx, dw, None
+
+
+class _RopeFn(torch.autograd.Function):
+    """q, k: [b, s, heads, dh] contiguous -> rotated copies (same layout)."""
+
+    @staticmethod
+    def _run(q, k, cos, sin, direction):
+        b, s, nh, dh = q.shape
+        qo, ko = torch.empty_like(q), torch.empty_like(k)
+        _wl_call(_wl().lomo_wl_rope(q.data_ptr(), k.data_ptr(), qo.data_ptr(), ko.data_ptr(),
+                                    cos.data_ptr(), sin.data_ptr(), b * s, s, nh, dh,
+                                    _WL_DTYPES[q.dtype], direction, _stream()), "lomo_wl_rope")
+        return qo, ko
+
+    @staticmethod
+    def forward(ctx, q, k, cos, sin):
+        ctx.save_for_backward(cos, sin)
+        return _RopeFn._run(q, k, cos, sin, 0)
+
+    @staticmethod
+    def backward(ctx, dq, dk):
+        cos, sin = ctx.saved_tensors
+        dq, dk = _RopeFn._run(dq.contiguous(), dk.contiguous(), cos, sin, 1)
+        return dq, dk, None, None
+
+
+class _SwiGLUFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, g, u):
+        out = torch.empty_like(g)
+        _wl_call(_wl().lomo_wl_swiglu_fwd(g.data_ptr(), u.data_ptr(), out.data_ptr(), g.numel(),
+                                          _WL_DTYPES[g.dtype], _stream()), "lomo_wl_swiglu_fwd")
+        ctx.save_for_backward(g, u)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        g, u = ctx.saved_tensors
+        dout = dout.contiguous()
+        dg, du = torch.empty_like(g), torch.empty_like(u)
+        _wl_call(_wl().lomo_wl_swiglu_bwd(dout.data_ptr(), g.data_ptr(), u.data_ptr(),
+                                          dg.data_ptr(), du.data_ptr(), g.numel(),
+                                          _WL_DTYPES[g.dtype], _stream()), "lomo_wl_swiglu_bwd")
+        return dg, du
+
+
+def rms_norm(x, w, eps=RMSNORM_EPS, fused=True):
+    if fused and _wl_ok(x, w) and x.shape[-1] % 8 == 0 and x.shape[-1] <= 8192:
+        return _RMSNormFn.apply(x, w, eps)
+    xf = x.float()
+    y = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)
+    return y.to(x.dtype) * w
+
+
+def rope_qk(q, k, cos, sin, fused=True):
+    """Rotary embedding of q, k in [b, s, heads, dh] layout."""
+    if fused and _wl_ok(q, k, cos, sin) and q.shape[-1] % 16 == 0:
+        return _RopeFn.apply(q, k, cos, sin)
+    c, s_ = cos[:, None, :], sin[:, None, :]       # [s, 1, dh] against [b, s, heads, dh]
+    return _rope(q, c, s_), _rope(k, c, s_)
+
+
+def swiglu(g, u, fused=True):
+    if fused and _wl_ok(g, u) and g.numel() % 8 == 0:
+        return _SwiGLUFn.apply(g, u)
+    return F.silu(g) * u
+
+
 class RMSNorm(nn.Module):
     def __init__(self, h: int, dtype, device):
         super().__init__()
         self.weight = nn.Parameter(torch.ones(h, dtype=dtype, device=device))
+        self.fused = True
 
     def forward(self, x):
-        xf = x.float()
-        y = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + RMSNORM_EPS)
-        return y.to(x.dtype) * self.weight
+        return rms_norm(x, self.weight, RMSNORM_EPS, self.fused)
 
 
 def _linear(h_in: int, h_out: int, dtype, device, std: float) -> nn.Parameter:
@@ -238,15 +360,17 @@ class LlamaLayer(nn.Module):
     def forward(self, x, cos, sin):
         b, s, h = x.shape
         nh, dh = self.nh, h // self.nh
+        fused = self.input_layernorm.fused
         a = self.input_layernorm(x)
-        q = rlinear(a, self.q).view(b, s, nh, dh).transpose(1, 2)
-        k = rlinear(a, self.k).view(b, s, nh, dh).transpose(1, 2)
+        q = rlinear(a, self.q).view(b, s, nh, dh)
+        k = rlinear(a, self.k).view(b, s, nh, dh)
         v = rlinear(a, self.v).view(b, s, nh, dh).transpose(1, 2)
-        q, k = _rope(q, cos, sin), _rope(k, cos, sin)
-        o = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        q, k = rope_qk(q, k, cos, sin, fused)          # rotated in [b, s, heads, dh]
+        o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v,
+                                           is_causal=True)
         x = x + rlinear(o.transpose(1, 2).reshape(b, s, h), self.o)
         y = self.post_attention_layernorm(x)
-        return x + rlinear(F.silu(rlinear(y, self.gate)) * rlinear(y, self.up), self.down)
+        return x + rlinear(swiglu(rlinear(y, self.gate), rlinear(y, self.up), fused), self.down)
 
 
 def _rope(x, cos, sin):
@@ -258,7 +382,8 @@ class Llama(nn.Module):
     """LLaMA-1 decoder, random init N(0, 0.02), parameters in ``dtype``."""
 
     def __init__(self, size="7b", dtype=torch.float16, device="cuda",
-                 checkpointing: bool = False, layers: int | None = None, seed: int = 0):
+                 checkpointing: bool = False, layers: int | None = None, seed: int = 0,
+                 fused_layers: bool = True):
         super().__init__()
         c = dict(LLAMA[size]) if isinstance(size, str) else dict(size)
         if layers is not None:
@@ -277,6 +402,9 @@ class Llama(nn.Module):
         self.norm = RMSNorm(h, dtype, device)
         self.lm_head = nn.Parameter(torch.empty(v, h, dtype=dtype, device=device).normal_(0, std))
         self._rope_cache = {}
+        for m in self.modules():
+            if isinstance(m, RMSNorm):
+                m.fused = fused_layers
 
     def _cos_sin(self, s, device, dtype):
         key = (s, device, dtype)

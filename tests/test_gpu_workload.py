@@ -1,0 +1,124 @@
+"""The benchmark decoder's fused layers (csrc/workload_kernels.cu) against a
+plain PyTorch fp32 reference of the same op, forward and backward.
+
+These kernels are not on the LOMO path; they make the config-3 training step
+(workloads.Llama) GEMM-bound.  Tolerance: the fused kernels compute in fp32
+and round once per output, so they are compared with the fp32 reference
+rounded to the storage dtype at 2 ulp of the storage type (relative), plus an
+absolute floor for values that cancel."""
+import pytest
+import torch
+
+from paper_2306_09782_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+DT = [torch.float16, torch.bfloat16]
+ULP = {torch.float16: 2.0 ** -10, torch.bfloat16: 2.0 ** -7}
+
+
+def close(got, want, dtype, k=2.0, floor=None):
+    want = want.float()
+    tol = k * ULP[dtype] * want.abs() + (floor if floor is not None else k * ULP[dtype] * want.abs().mean())
+    err = (got.float() - want).abs()
+    bad = (err > tol).sum().item()
+    assert bad == 0, f"{bad} elements out of tolerance; max err {err.max().item():.3e}"
+
+
+@pytest.fixture(autouse=True)
+def _dev():
+    torch.cuda.set_device(0)
+    torch.manual_seed(0)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("rows,h", [(1, 8), (7, 4096), (1024, 4096), (33, 5120), (5, 8192), (3, 2056)])
+def test_rmsnorm_fwd_bwd(dtype, rows, h):
+    x = torch.randn(rows, h, device="cuda").to(dtype)
+    w = (1 + 0.1 * torch.randn(h, device="cuda")).to(dtype)
+    dy = torch.randn(rows, h, device="cuda").to(dtype)
+    xa, wa = x.clone().requires_grad_(), w.clone().requires_grad_()
+    y = W.rms_norm(xa, wa)
+    y.backward(dy)
+    # fp32 reference (the eager formula, all in fp32)
+    xr, wr = x.float().requires_grad_(), w.float().requires_grad_()
+    yr = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + W.RMSNORM_EPS) * wr
+    yr.backward(dy.float())
+    close(y, yr.detach(), dtype)
+    close(xa.grad, xr.grad, dtype, k=4.0)
+    close(wa.grad, wr.grad, dtype, k=4.0, floor=4 * ULP[dtype] * wr.grad.abs().max().item())
+
+
+def test_rmsnorm_deterministic():
+    x = torch.randn(1024, 4096, device="cuda").half().requires_grad_()
+    w = torch.ones(4096, device="cuda").half().requires_grad_()
+    dy = torch.randn(1024, 4096, device="cuda").half()
+    out = []
+    for _ in range(2):
+        x.grad = w.grad = None
+        W.rms_norm(x, w).backward(dy)
+        out.append((x.grad.clone(), w.grad.clone()))
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+
+
+def _cos_sin(s, dh, dtype):
+    inv = 1.0 / (10000 ** (torch.arange(0, dh, 2, device="cuda", dtype=torch.float32) / dh))
+    fr = torch.outer(torch.arange(s, device="cuda", dtype=torch.float32), inv)
+    emb = torch.cat((fr, fr), -1)
+    return emb.cos().to(dtype), emb.sin().to(dtype)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("b,s,nh,dh", [(1, 1024, 32, 128), (2, 17, 3, 64), (1, 5, 1, 16)])
+def test_rope_fwd_bwd(dtype, b, s, nh, dh):
+    cos, sin = _cos_sin(s, dh, dtype)
+    q = torch.randn(b, s, nh, dh, device="cuda").to(dtype)
+    k = torch.randn(b, s, nh, dh, device="cuda").to(dtype)
+    dq = torch.randn_like(q)
+    dk = torch.randn_like(k)
+    qa, ka = q.clone().requires_grad_(), k.clone().requires_grad_()
+    qo, ko = W.rope_qk(qa, ka, cos, sin)
+    torch.autograd.backward((qo, ko), (dq, dk))
+    qr, kr = q.float().requires_grad_(), k.float().requires_grad_()
+    qro, kro = W.rope_qk(qr, kr, cos.float(), sin.float())      # eager formula in fp32
+    torch.autograd.backward((qro, kro), (dq.float(), dk.float()))
+    close(qo, qro.detach(), dtype)
+    close(ko, kro.detach(), dtype)
+    close(qa.grad, qr.grad, dtype)
+    close(ka.grad, kr.grad, dtype)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("n", [8, 1024 * 11008, 40])
+def test_swiglu_fwd_bwd(dtype, n):
+    g = (2 * torch.randn(n, device="cuda")).to(dtype)
+    u = torch.randn(n, device="cuda").to(dtype)
+    d = torch.randn(n, device="cuda").to(dtype)
+    ga, ua = g.clone().requires_grad_(), u.clone().requires_grad_()
+    out = W.swiglu(ga, ua)
+    out.backward(d)
+    gr, ur = g.float().requires_grad_(), u.float().requires_grad_()
+    ref = torch.nn.functional.silu(gr) * ur
+    ref.backward(d.float())
+    close(out, ref.detach(), dtype, k=3.0)
+    close(ga.grad, gr.grad, dtype, k=4.0)
+    close(ua.grad, ur.grad, dtype, k=3.0)
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_llama_fused_layers_match_eager(dtype):
+    """A 2-layer decoder with fused layers vs the same weights through the
+    eager formulas: same loss to storage precision, gradients close."""
+    cfg = dict(hidden=256, ffn=688, heads=4, vocab=512, layers=2)
+    a = W.Llama(cfg, dtype=dtype, device="cuda", seed=0, fused_layers=True)
+    b = W.Llama(cfg, dtype=dtype, device="cuda", seed=0, fused_layers=False)
+    d = torch.randint(0, 512, (2, 65), device="cuda")
+    la = a.loss(d[:, :-1], d[:, 1:])
+    lb = b.loss(d[:, :-1], d[:, 1:])
+    la.backward()
+    lb.backward()
+    assert abs(la.item() - lb.item()) <= 1e-2 * abs(lb.item())
+    for (n, pa), pb in zip(a.named_parameters(), b.parameters()):
+        ga, gb = pa.grad.float(), pb.grad.float()
+        rel = (ga - gb).norm() / gb.norm().clamp_min(1e-30)
+        assert rel < (2e-2 if dtype == torch.float16 else 6e-2), (n, rel.item())

@@ -10,15 +10,18 @@ from conftest import ROOT
 from paper_2306_09782_b200 import _lib
 
 HEADER = ROOT / "include" / "lomo_b200.h"
+WL_HEADER = ROOT / "include" / "lomo_workload.h"
 
 
-def _declared():
-    text = HEADER.read_text()
+def _declared(header=None):
+    text = "".join(h.read_text() for h in ([header] if header else sorted((ROOT / "include").glob("*.h"))))
     return sorted(set(re.findall(r"^\s*(?:int|size_t)\s+(lomo_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declarations_match_binding():
-    assert _declared() == sorted(_lib.EXPORTS)
+    assert _declared(HEADER) == sorted(_lib.EXPORTS)
+    assert _declared(WL_HEADER) == sorted(_lib.WL_EXPORTS)
+    assert _declared() == sorted(_lib.EXPORTS + _lib.WL_EXPORTS)
 
 
 def test_library_exports_every_declared_symbol():
@@ -50,6 +53,17 @@ def test_argument_errors_need_no_gpu():
     assert lib.lomo_finalize_norm(None, None) == -1
     assert lib.lomo_state_init(None, 1, 1.0, 1, 1.0, 1.0, 0.0, 1.0, None) == -1
     assert lib.lomo_finalize_norm_ranks(1, None, 2, None) == -1
+    # workload layers: shape / dtype / alignment checks happen before any launch
+    assert lib.lomo_wl_rmsnorm_fwd(16, 16, 16, 16, 4, 12, 1, 1e-6, None) == -1      # h % 8
+    assert lib.lomo_wl_rmsnorm_fwd(16, 16, 16, 16, 4, 16384, 1, 1e-6, None) == -1   # h > 8192
+    assert lib.lomo_wl_rmsnorm_fwd(None, None, None, None, 0, 4096, 1, 1e-6, None) == 0
+    assert lib.lomo_wl_rope(16, 16, 16, 16, 16, 16, 2, 2, 1, 24, 1, 0, None) == -1  # dh % 16
+    assert lib.lomo_wl_rope(16, 16, 16, 32, 16, 16, 2, 2, 1, 32, 1, 0, None) == -1  # q aliases qo
+    assert lib.lomo_wl_swiglu_fwd(16, 16, 16, 12, 1, None) == -1
+    assert lib.lomo_wl_swiglu_fwd(16, 16, 16, 16, 0, None) == -1                    # f32 storage
+    assert lib.lomo_wl_swiglu_bwd(8, 16, 16, 16, 16, 16, 1, None) == -1             # misaligned
+    assert lib.lomo_wl_rmsnorm_partial_rows(1024) == 256
+    assert lib.lomo_wl_rmsnorm_partial_rows(0) == 0
 
 
 def test_status_struct_layout_matches_c(tmp_path):

@@ -21,11 +21,16 @@ ap.add_argument("--layers", type=int, default=None)
 ap.add_argument("--ckpt", action="store_true")
 ap.add_argument("--replay", action="store_true")
 ap.add_argument("--fuse", action="store_true")
+ap.add_argument("--grouped", action="store_true")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 model = Llama("7b", dtype=torch.float16, device="cuda", layers=a.layers, checkpointing=a.ckpt)
-opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 10),
-           replay=a.replay, fuse_gemm=a.fuse)
+if a.grouped:
+    from paper_2306_09782_b200 import GroupedLOMO  # noqa: E402
+    opt = GroupedLOMO(model, lr=1e-3, max_norm=1.0, window=1)
+else:
+    opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 10),
+               replay=a.replay, fuse_gemm=a.fuse)
 d = torch.randint(0, 32000, (a.batch, a.seq + 1), device="cuda")
 step = lambda: opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
 for _ in range(3):
@@ -36,6 +41,13 @@ with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     for _ in range(2):
         step()
     torch.cuda.synchronize()
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ev[0].record()
+for _ in range(3):
+    step()
+ev[1].record()
+torch.cuda.synchronize()
+print(f"wall (events, unprofiled) per step: {ev[0].elapsed_time(ev[1]) / 3:.2f} ms")
 fam = defaultdict(float)
 total = 0.0
 for e in prof.events():          # device kernels only (no CPU-op double counting)
