@@ -95,63 +95,102 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// one CTA per `rpc` consecutive rows: dx per row, dw partial per CTA
-template <typename T, int kMaxVec>
+// One CTA per `rpc` consecutive rows, taken R rows at a time: all R rows'
+// x and dy loads are issued before any arithmetic, their R dot products share
+// one block reduction, and the CTA's dw partial stays in registers until the
+// end (written once).
+template <int R>
+__device__ __forceinline__ void block_sum_r(float (&v)[R], float* sm) {  // sm: R * 8 floats
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0)
+#pragma unroll
+    for (int r = 0; r < R; ++r) sm[r * (kThreads / 32) + w] = v[r];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < kThreads / 32; ++i) t += sm[r * (kThreads / 32) + i];
+    v[r] = t;
+  }
+}
+
+template <typename T, int kMaxVec, int R>
 __global__ void __launch_bounds__(kThreads)
     rms_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ w,
             const float* __restrict__ rstd, T* __restrict__ dx, float* __restrict__ partial,
             int64_t rows, int h, int rpc) {
-  __shared__ float sm[kThreads / 32];
+  __shared__ float sm[R * (kThreads / 32)];
   const int nv = h / 8;
   const uint4* wv = reinterpret_cast<const uint4*>(w);
-  float W[kMaxVec][8], DW[kMaxVec][8];
+  float DW[kMaxVec][8];
+  Vec8<T> Wt[kMaxVec];
 #pragma unroll
   for (int k = 0; k < kMaxVec; ++k) {
     const int i = threadIdx.x + k * kThreads;
-    Vec8<T> t;
-    t.u = i < nv ? wv[i] : make_uint4(0, 0, 0, 0);
+    Wt[k].u = i < nv ? wv[i] : make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      W[k][e] = tof(t.e[e]);
-      DW[k][e] = 0.f;
-    }
+    for (int e = 0; e < 8; ++e) DW[k][e] = 0.f;
   }
   const int64_t r0 = (int64_t)blockIdx.x * rpc;
   const int64_t r1 = min(r0 + rpc, rows);
-  for (int64_t row = r0; row < r1; ++row) {
-    const float r = rstd[row];
-    const uint4* xv = reinterpret_cast<const uint4*>(x + row * h);
-    const uint4* dv = reinterpret_cast<const uint4*>(dy + row * h);
-    float N[kMaxVec][8], DT[kMaxVec][8];
-    float dot = 0.f;
+  for (int64_t rb = r0; rb < r1; rb += R) {
+    Vec8<T> X[R][kMaxVec], D[R][kMaxVec];
+    float rs[R];
 #pragma unroll
-    for (int k = 0; k < kMaxVec; ++k) {
-      const int i = threadIdx.x + k * kThreads;
-      if (i < nv) {
-        Vec8<T> X, D;
-        X.u = ld_nc(xv + i);
-        D.u = ld_nc(dv + i);
+    for (int r = 0; r < R; ++r) {
+      const int64_t row = rb + r;
+      rs[r] = row < r1 ? rstd[row] : 0.f;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float n = tof(X.e[e]) * r;
-          const float d = tof(D.e[e]);
-          N[k][e] = n;
-          DT[k][e] = rnd<T>(d * W[k][e]);            // grad of round(n) * w w.r.t. round(n)
-          DW[k][e] = fmaf(d, rnd<T>(n), DW[k][e]);   // grad w.r.t. w
-          dot = fmaf(DT[k][e], n, dot);
+      for (int k = 0; k < kMaxVec; ++k) {
+        const int i = threadIdx.x + k * kThreads;
+        if (row < r1 && i < nv) {
+          X[r][k].u = ld_nc(reinterpret_cast<const uint4*>(x + row * h) + i);
+          D[r][k].u = ld_nc(reinterpret_cast<const uint4*>(dy + row * h) + i);
+        } else {
+          X[r][k].u = make_uint4(0, 0, 0, 0);
+          D[r][k].u = make_uint4(0, 0, 0, 0);
         }
       }
     }
-    const float m = block_sum(dot, sm) / (float)h;
-    uint4* ov = reinterpret_cast<uint4*>(dx + row * h);
+    float dot[R];
 #pragma unroll
-    for (int k = 0; k < kMaxVec; ++k) {
-      const int i = threadIdx.x + k * kThreads;
-      if (i < nv) {
-        Vec8<T> O;
+    for (int r = 0; r < R; ++r) {
+      dot[r] = 0.f;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) O.e[e] = fromf<T>(r * (DT[k][e] - N[k][e] * m));
-        ov[i] = O.u;
+      for (int k = 0; k < kMaxVec; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float n = tof(X[r][k].e[e]) * rs[r];
+          const float d = tof(D[r][k].e[e]);
+          const float dt = rnd<T>(d * tof(Wt[k].e[e]));  // grad of round(n) * w w.r.t. round(n)
+          DW[k][e] = fmaf(d, rnd<T>(n), DW[k][e]);        // grad w.r.t. w
+          dot[r] = fmaf(dt, n, dot[r]);
+        }
+    }
+    block_sum_r<R>(dot, sm);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t row = rb + r;
+      const float m = dot[r] / (float)h;
+#pragma unroll
+      for (int k = 0; k < kMaxVec; ++k) {
+        const int i = threadIdx.x + k * kThreads;
+        if (row < r1 && i < nv) {
+          Vec8<T> O;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float n = tof(X[r][k].e[e]) * rs[r];
+            const float dt = rnd<T>(tof(D[r][k].e[e]) * tof(Wt[k].e[e]));
+            O.e[e] = fromf<T>(rs[r] * (dt - n * m));
+          }
+          reinterpret_cast<uint4*>(dx + row * h)[i] = O.u;
+        }
       }
     }
   }
@@ -167,15 +206,28 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// dw[j] = sum over CTA partials, in CTA order
+// dw[j] = sum over the CTA partials.  32 columns x 8 row-slices per CTA: each
+// warp sums every 8th partial row of its 32 columns (independent loads in
+// flight), then warp 0 adds the 8 slice sums in slice order (deterministic).
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
     rms_dw_reduce(const float* __restrict__ partial, T* __restrict__ dw, int nparts, int h) {
-  const int j = blockIdx.x * kThreads + threadIdx.x;
-  if (j >= h) return;
+  __shared__ float sm[kThreads / 32][33];
+  const int lane = threadIdx.x & 31, slice = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int c = 0; c < nparts; ++c) s += partial[(size_t)c * h + j];
-  dw[j] = fromf<T>(s);
+  if (j < h) {
+#pragma unroll 4
+    for (int c = slice; c < nparts; c += kThreads / 32) s += partial[(size_t)c * h + j];
+  }
+  sm[slice][lane] = s;
+  __syncthreads();
+  if (slice == 0 && j < h) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < kThreads / 32; ++i) t += sm[i][lane];
+    dw[j] = fromf<T>(t);
+  }
 }
 
 // ---------------------------------------------------------------- rotary
@@ -314,18 +366,17 @@ struct RmsBwd {
                  void* dw, float* partial, int64_t rows, int h, cudaStream_t s) {
     const int rpc = rms_rows_per_cta(rows);
     const int nparts = (int)((rows + rpc - 1) / rpc);
-#define WL_RMS_BWD(NV)                                                                   \
-  rms_bwd<T, NV><<<nparts, kThreads, 0, s>>>((const T*)dy, (const T*)x, (const T*)w, rstd, \
-                                             (T*)dx, partial, rows, h, rpc)
-    switch ((h / 8 + kThreads - 1) / kThreads) {
-      case 1: WL_RMS_BWD(1); break;
-      case 2: WL_RMS_BWD(2); break;
-      case 3: WL_RMS_BWD(3); break;
-      default: WL_RMS_BWD(4); break;
+#define WL_RMS_BWD(NV, R)                                                                   \
+  rms_bwd<T, NV, R><<<nparts, kThreads, 0, s>>>((const T*)dy, (const T*)x, (const T*)w, rstd, \
+                                                (T*)dx, partial, rows, h, rpc)
+    switch ((h / 8 + kThreads - 1) / kThreads) {  // rows in flight x vectors <= 8
+      case 1: WL_RMS_BWD(1, 4); break;
+      case 2: WL_RMS_BWD(2, 2); break;
+      case 3: WL_RMS_BWD(3, 2); break;
+      default: WL_RMS_BWD(4, 2); break;
     }
 #undef WL_RMS_BWD
-    rms_dw_reduce<T><<<(h + kThreads - 1) / kThreads, kThreads, 0, s>>>(partial, (T*)dw, nparts,
-                                                                         h);
+    rms_dw_reduce<T><<<(h + 31) / 32, kThreads, 0, s>>>(partial, (T*)dw, nparts, h);
     return status();
   }
 };

@@ -22,9 +22,12 @@ ap.add_argument("--ckpt", action="store_true")
 ap.add_argument("--replay", action="store_true")
 ap.add_argument("--fuse", action="store_true")
 ap.add_argument("--grouped", action="store_true")
+ap.add_argument("--graph", action="store_true", help="GraphedLOMOStep (implies --replay --fuse)")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 model = Llama("7b", dtype=torch.float16, device="cuda", layers=a.layers, checkpointing=a.ckpt)
+if a.graph:
+    a.replay = a.fuse = True
 if a.grouped:
     from paper_2306_09782_b200 import GroupedLOMO  # noqa: E402
     opt = GroupedLOMO(model, lr=1e-3, max_norm=1.0, window=1)
@@ -33,6 +36,10 @@ else:
                replay=a.replay, fuse_gemm=a.fuse)
 d = torch.randint(0, 32000, (a.batch, a.seq + 1), device="cuda")
 step = lambda: opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
+if a.graph:
+    from paper_2306_09782_b200.graphs import GraphedLOMOStep  # noqa: E402
+    gs = GraphedLOMOStep(opt, lambda t: model.loss(t[:, :-1], t[:, 1:]), (d,), warmup=2)
+    step = lambda: gs.step(1e-3)
 for _ in range(3):
     step()
 torch.cuda.synchronize()
