@@ -69,6 +69,8 @@ typedef enum {
 #define LOMO_LR_FROM_STATE 0x10u /* K1: lr = state->lr (set by lomo_set_lr), so a  */
                                  /* CUDA graph of the step needs no re-capture when */
                                  /* the schedule changes lr                         */
+#define LOMO_DEFER_ROWS 0x20u /* K6: leave the partial sums in the workspace; */
+                              /* lomo_gemm_probe_finish reduces a batch of them  */
 #define LOMO_ACCUM_F64 0x8u /* K2: accumulate every square in f64 (the reference's */
                             /* float64 dot, stabilize.py:199); default for 16-bit   */
                             /* storage: exact fp32 squares summed per 16-byte      */
@@ -222,6 +224,42 @@ int lomo_gemm_update_dev(void* p, const void* dy, const void* x, int64_t out_fea
                          void* stream);
 int lomo_update_coefs(const void* state, double weight_decay, unsigned flags,
                       float* coefs_dev, void* stream);
+
+/* ---- K6: weight-gradient GEMM with the pass-1 probe as its epilogue ---- */
+/* Replaces, for a linear layer, the weight-gradient GEMM dW = dy^T x followed
+ * by a K2 launch over dW (stabilize.py:190-200 probe_hook): the tensor cores
+ * compute dW tile by tile (the same mainloop as K5, so pass 2 sees
+ * bit-identical accumulators) and the epilogue rounds each element to the
+ * storage dtype, raises state->overflow if it is non-finite and accumulates
+ * (g * inv_scale)^2 into norm slot `slot`, so the gradient is never read back.
+ * grad_out ([out, in], dtype) receives dW as a by-product of the epilogue's
+ * store (a scratch buffer the caller may reuse at once, stream-ordered).
+ * flags: LOMO_USE_SCALE (LOMO_ACCUM_F64 is refused with LOMO_E_ARG: the
+ * exactness mode keeps GEMM + K2).  workspace: >= lomo_gemm_probe_workspace
+ * bytes of device memory, reused by every call on one stream.  Shapes as
+ * lomo_gemm_update. */
+int lomo_gemm_probe(const void* dy, const void* x, void* grad_out, int64_t out_features,
+                    int64_t in_features, int64_t tokens, int dtype, int slot, unsigned flags,
+                    void* state, void* workspace, size_t workspace_bytes, void* stream);
+size_t lomo_gemm_probe_workspace(int64_t out_features, int64_t in_features, int64_t tokens,
+                                 int dtype);
+/* K6's second stage (also usable on its own): sum a [rows, ld] fp32 matrix of
+ * partial sums of squares (first `cols` entries of each row valid; K6 passes
+ * one row per 256-column tile of dW) in fixed order into norm slot `slot`
+ * (one K2-style partial per row, finished by K3a); a NaN partial raises
+ * state->overflow.  rows <= LOMO_PROBE_BLOCKS_PER_SLOT. */
+int lomo_probe_rows(const float* partials_dev, int64_t rows, int64_t ld, int64_t cols, int slot,
+                    void* state, void* stream);
+/* lomo_probe_rows for `count` matrices in ceil(count/64) launches (host arrays). */
+int lomo_probe_rows_multi(const float* const* partials_dev, const int64_t* rows,
+                          const int64_t* ld, const int64_t* cols, const int* slots, int count,
+                          void* state, void* stream);
+/* Deferred K6 (flags & LOMO_DEFER_ROWS): each such call must get its own
+ * workspace; after the batch, this reduces every call's partial sums into its
+ * slot (one launch per 64 calls instead of one per call).  Host arrays. */
+int lomo_gemm_probe_finish(void* const* workspaces, const int64_t* out_features,
+                           const int64_t* in_features, const int* slots, int count, int dtype,
+                           void* state, void* stream);
 
 /* Number of SMs the library sized its grids for (device of the current
  * context); 0 if no device. */

@@ -19,6 +19,7 @@ LIB_PATH = _HERE / "_native" / "liblomo_b200.so"
 F32, F16, BF16, F64 = 0, 1, 2, 3
 MATH_F32, MATH_F64 = 0, 1
 USE_SCALE, USE_COEF, USE_SKIP, ACCUM_F64, LR_FROM_STATE = 0x1, 0x2, 0x4, 0x8, 0x10
+DEFER_ROWS = 0x20
 PROBE_BLOCKS_PER_SLOT = 4096
 ABI_VERSION = 1
 
@@ -45,6 +46,11 @@ EXPORTS = (
     "lomo_set_lr",
     "lomo_update_coefs",
     "lomo_gemm_update_dev",
+    "lomo_gemm_probe",
+    "lomo_gemm_probe_workspace",
+    "lomo_probe_rows",
+    "lomo_probe_rows_multi",
+    "lomo_gemm_probe_finish",
 )
 
 # include/lomo_workload.h: the benchmark decoder's fused layers (not the LOMO path)
@@ -123,6 +129,12 @@ _SIGS = {
     "lomo_update_coefs": (_i32, [_vp, _dbl, _u32, _vp, _vp]),
     "lomo_gemm_update_dev": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp,
                                     ctypes.c_size_t, _vp]),
+    "lomo_gemm_probe": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _u32, _vp, _vp,
+                               ctypes.c_size_t, _vp]),
+    "lomo_gemm_probe_workspace": (ctypes.c_size_t, [_i64, _i64, _i64, _i32]),
+    "lomo_probe_rows": (_i32, [_vp, _i64, _i64, _i64, _i32, _vp, _vp]),
+    "lomo_probe_rows_multi": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
+    "lomo_gemm_probe_finish": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
     "lomo_wl_rmsnorm_fwd": (_i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, ctypes.c_float, _vp]),
     "lomo_wl_rmsnorm_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp]),
     "lomo_wl_rmsnorm_partial_rows": (_i32, [_i64]),

@@ -31,7 +31,7 @@ namespace lomo_gemm {
 
 using namespace cute;
 
-template <typename Element>
+template <typename Element, int ClusterN = 1>
 struct FusedUpdateGemm {
   using ElementA = Element;                      // dy  [T, out] row-major == A (M=out, K=T), M-major
   using LayoutA = cutlass::layout::ColumnMajor;
@@ -44,7 +44,10 @@ struct FusedUpdateGemm {
   static constexpr int kAlign = 128 / cutlass::sizeof_bits<Element>::value;
 
   using MmaTileShape = Shape<_256, _256, _64>;
-  using ClusterShape = Shape<_2, _1, _1>;
+  // one CTA pair per 256x256 tile; a 2x2 cluster (TMA multicast of the
+  // A/B panels, cuBLAS's choice for 4096x4096) measured 1-5% slower here
+  // (profiles/r01_gemm_shapes.md)
+  using ClusterShape = Shape<_2, Int<ClusterN>, _1>;
 
   using Fusion = cutlass::epilogue::fusion::LinearCombination<ElementC, ElementCompute, ElementC,
                                                               ElementCompute>;
@@ -163,6 +166,7 @@ int lomo_gemm_update_dev(void* p, const void* dy, const void* x, int64_t out_fea
 
 size_t lomo_gemm_update_workspace(int64_t out_features, int64_t in_features, int64_t tokens,
                                   int dtype) {
+  if (out_features <= 0 || in_features <= 0 || tokens <= 0) return 0;
   if (dtype == LOMO_BF16)
     return lomo_gemm::FusedUpdateGemm<cutlass::bfloat16_t>::workspace(
         (int)out_features, (int)in_features, (int)tokens);

@@ -511,6 +511,66 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// K6 second stage: row r of the [rows, ld] fp32 partial matrix (K6's per
+// tile-row column sums) -> partial r of the slot, in fixed order; a NaN
+// partial marks a non-finite gradient element (lomo_gemm_probe.cu).
+__global__ void __launch_bounds__(kThreads)
+    k6_rows(const float* __restrict__ part, int64_t ld, int64_t cols, int slot, void* state) {
+  __shared__ double sm[kThreads / 32];
+  pdl_wait();
+  pdl_launch_dependents();
+  lomo_state* st = hdr(state);
+  const float* row = part + (int64_t)blockIdx.x * ld;
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t c = threadIdx.x; c < cols; c += kThreads) {
+    const float v = row[c];
+    bad |= isnan(v);
+    acc += (double)v;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
+  const double bsum = block_sum(acc, sm);
+  if (threadIdx.x == 0) {
+    partials_of(st, slot)[blockIdx.x] = bsum;
+    if (blockIdx.x == 0) nblocks_of(st)[slot] = (int32_t)gridDim.x;
+  }
+}
+
+// Many K6 partial matrices in one launch (deferred mode): blockIdx.y picks
+// the entry, blockIdx.x its row; the table travels by value.
+struct RowsTable {
+  const float* part[kMulti];
+  int64_t rows[kMulti];
+  int64_t ld[kMulti];
+  int64_t cols[kMulti];
+  int32_t slot[kMulti];
+};
+
+__global__ void __launch_bounds__(kThreads) k6_rows_multi(const __grid_constant__ RowsTable tab,
+                                                          void* state) {
+  __shared__ double sm[kThreads / 32];
+  pdl_wait();
+  pdl_launch_dependents();
+  const int e = blockIdx.y;
+  if ((int64_t)blockIdx.x >= tab.rows[e]) return;  // CTA-uniform
+  lomo_state* st = hdr(state);
+  const float* row = tab.part[e] + (int64_t)blockIdx.x * tab.ld[e];
+  const int64_t cols = tab.cols[e];
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t c = threadIdx.x; c < cols; c += kThreads) {
+    const float v = row[c];
+    bad |= isnan(v);
+    acc += (double)v;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
+  const double bsum = block_sum(acc, sm);
+  if (threadIdx.x == 0) {
+    partials_of(st, tab.slot[e])[blockIdx.x] = bsum;
+    if (blockIdx.x == 0) nblocks_of(st)[tab.slot[e]] = (int32_t)tab.rows[e];
+  }
+}
+
 // --------------------------------------------------------------------------
 // K4: reduce-scatter fused with the update / probe over peer memory
 // --------------------------------------------------------------------------
@@ -1216,6 +1276,48 @@ int lomo_fused_rs_probe(const void* const* peer_bufs_dev, int world, int64_t off
     case LOMO_F64: return launch_rs_probe<double, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
   }
   return LOMO_E_ARG;
+}
+
+int lomo_probe_rows(const float* partials_dev, int64_t rows, int64_t ld, int64_t cols, int slot,
+                    void* state, void* stream) {
+  if (state == nullptr || partials_dev == nullptr) return LOMO_E_ARG;
+  if (rows < 1 || rows > LOMO_PROBE_BLOCKS_PER_SLOT || cols < 1 || ld < cols) return LOMO_E_ARG;
+  if (slot < 0) return LOMO_E_SLOT;
+  return launch(k6_rows, dim3((unsigned)rows), dim3(kThreads), (cudaStream_t)stream, partials_dev,
+                ld, cols, slot, state);
+}
+
+int lomo_probe_rows_multi(const float* const* partials_dev, const int64_t* rows,
+                          const int64_t* ld, const int64_t* cols, const int* slots, int count,
+                          void* state, void* stream) {
+  if (state == nullptr || count < 0) return LOMO_E_ARG;
+  if (count == 0) return 0;
+  if (partials_dev == nullptr || rows == nullptr || ld == nullptr || cols == nullptr ||
+      slots == nullptr)
+    return LOMO_E_ARG;
+  for (int i = 0; i < count; ++i) {
+    if (partials_dev[i] == nullptr || rows[i] < 1 || rows[i] > LOMO_PROBE_BLOCKS_PER_SLOT ||
+        cols[i] < 1 || ld[i] < cols[i])
+      return LOMO_E_ARG;
+    if (slots[i] < 0) return LOMO_E_SLOT;
+  }
+  for (int base = 0; base < count; base += kMulti) {
+    RowsTable tab;
+    const int k = count - base < kMulti ? count - base : kMulti;
+    int64_t max_rows = 1;
+    for (int i = 0; i < k; ++i) {
+      tab.part[i] = partials_dev[base + i];
+      tab.rows[i] = rows[base + i];
+      tab.ld[i] = ld[base + i];
+      tab.cols[i] = cols[base + i];
+      tab.slot[i] = slots[base + i];
+      if (rows[base + i] > max_rows) max_rows = rows[base + i];
+    }
+    const int rc = launch(k6_rows_multi, dim3((unsigned)max_rows, (unsigned)k), dim3(kThreads),
+                          (cudaStream_t)stream, tab, state);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 int lomo_finalize_norm(void* state, void* stream) {

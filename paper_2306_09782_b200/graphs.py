@@ -24,7 +24,6 @@ from typing import Callable, Sequence
 import torch
 
 from . import _lib
-from . import replay as _replay
 from .errors import ConfigError, ScaleUnderflowError
 from .lomo import LOMO, _PROBE
 from .stabilize import StepOutcome
@@ -83,22 +82,7 @@ class GraphedLOMOStep:
                                              self.coefs.data_ptr(), eng.stream()),
                    "lomo_update_coefs")
         eng.configure(0.0, opt.clip_value, opt.weight_decay, flags)
-        st = opt._stash
-        for p in reversed(opt.params):
-            pid = id(p)
-            if pid in st.linear:
-                x, dy = st.linear.pop(pid)
-                if opt.fuse_gemm and opt._gemm_update(p, x, dy, 0.0, coefs=self.coefs):
-                    continue
-                g = _replay.weight_grad(x, dy)
-            elif pid in st.grads:
-                g = st.grads.pop(pid)
-            else:
-                continue
-            eng.update(p, g)
-            del g
-        eng.flush()
-        st.clear()
+        opt._replay_pass(0.0, coefs=self.coefs if opt.fuse_gemm else None)
         eng.on_clean()
 
     def step(self, lr: float) -> torch.Tensor:

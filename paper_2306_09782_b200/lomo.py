@@ -28,6 +28,8 @@ How the reference maps onto this file:
 """
 from __future__ import annotations
 
+import ctypes
+import os
 from typing import Callable
 
 import torch
@@ -260,13 +262,21 @@ class LOMO(_Protocol):
             csrc/lomo_gemm_update.cu): ``p <- p - lr*coef/scale * (dy^T x)`` from
             the fp32 accumulator, the gradient never materialised.  16-bit
             parameters, no value clip; other parameters keep K1.
+        fuse_probe: with ``replay`` (default: on when ``fuse_gemm`` is), run
+            each linear's pass-1 probe as the epilogue of its weight-gradient
+            GEMM (K6, csrc/lomo_gemm_probe.cu): the overflow flag and the sum of
+            squares come out of the tensor-core accumulator, so no K2 launch
+            re-reads the gradient and autograd never holds it.
+        gemm_streams / probe_stream: run pass 2's K5 GEMMs over that many
+            streams / pass 1's K6 GEMMs on a side stream (off by default).
     """
 
     def __init__(self, model, lr: float = 1e-3, clip_grad_norm: float | None = None,
                  loss_scale=None, *, clip_grad_value: float | None = None,
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
                  math: str = "f32", overlap: bool = False, replay: bool = False,
-                 fuse_gemm: bool = False):
+                 fuse_gemm: bool = False, fuse_probe: bool | None = None,
+                 gemm_streams: int = 1, probe_stream: bool = False):
         if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
             raise ConfigError("pass either a Stabilizer or the clip/loss_scale arguments")
         st = stabilizer if stabilizer is not None else stabilizer_from_args(
@@ -302,7 +312,29 @@ class LOMO(_Protocol):
             raise ConfigError("fuse_gemm fuses the update into the replayed weight-gradient GEMM: "
                               "it needs replay=True")
         self.fuse_gemm = bool(fuse_gemm) and self.clip_value == 0.0
-        self._ws = None
+        if fuse_probe and not replay:
+            raise ConfigError("fuse_probe fuses the pass-1 probe into the weight-gradient GEMM: "
+                              "it needs replay=True")
+        self.fuse_probe = bool(fuse_gemm if fuse_probe is None else fuse_probe) and replay \
+            and math == "f32"
+        if self.fuse_probe:
+            self._stash.probe = self._gemm_probe
+        self._pws = {}         # K6 workspace per weight (its partial sums stay until
+                               # the end of pass 1: one deferred reduction launch)
+        self._pending_probe = []  # (workspace ptr, out, in, slot) awaiting that launch
+        self._gscratch = None  # K6 by-product dW, reused by every linear
+        self._ws = {}          # K5 workspace per stream
+        # Optional stream concurrency of the tensor-core GEMMs: pass 2's K5
+        # launches are independent of each other and may rotate over
+        # `gemm_streams` streams; pass 1's K6 may run on a side stream beside
+        # the rest of the backward (it only reads the stashed x/dy).  Joined
+        # before K3a / at the end of pass 2.  Off by default: on LLaMA-7B the
+        # overlap cost more than the filled wave tails (profiles/r01_summary.md).
+        # LOMO_GEMM_STREAMS / LOMO_PROBE_STREAM override.
+        self.gemm_streams = max(1, int(os.environ.get("LOMO_GEMM_STREAMS", gemm_streams)))
+        self.probe_stream = os.environ.get("LOMO_PROBE_STREAM", "1" if probe_stream else "0") == "1"
+        self._streams = None
+        self._pstream = None
         self._largest = max(p.numel() * p.element_size() for p in uniq)
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in uniq]
 
@@ -322,14 +354,21 @@ class LOMO(_Protocol):
             self.engine.probe(g, self._slot[id(p)])
             st = self._stash
             if st is not None:
-                if id(p) not in st.linear:
+                if id(p) in st.probed:
+                    # K6 already probed this weight's linear: a hook means another
+                    # op contributed gradient too (tied weight), which replay drops
+                    self._replay_mismatch.append(tuple(p.shape))
+                elif id(p) not in st.linear:
                     st.grads[id(p)] = g  # not a replayable linear: keep its gradient
                 elif not self._replay_checked:
                     # first step: the replayed dW must BE the whole gradient
                     # (a weight tied to another op would also collect that op's
                     # contribution, which replay would silently drop)
                     x, dy = st.linear[id(p)]
-                    if not torch.equal(_replay.weight_grad(x, dy), g):
+                    r = _replay.weight_grad(x, dy)
+                    # NaN-aware: an overflowing first step must not read as a mismatch
+                    if not torch.equal(r, g) and not bool(((r == g) | (r.isnan() & g.isnan()))
+                                                          .all()):
                         self._replay_mismatch.append(tuple(p.shape))
         else:
             self.engine.update(p, g)
@@ -353,6 +392,7 @@ class LOMO(_Protocol):
             self._mode = 0
             if stash is not None:
                 _replay._ACTIVE = None
+            self._finish_probes()  # deferred K6 partial sums -> their slots
             self.engine.flush()  # the parked tiny tensors, same stream as the hooks
         if stash is not None:
             kept = sum(g.numel() * g.element_size() for g in stash.grads.values())
@@ -386,9 +426,13 @@ class LOMO(_Protocol):
             return False
         lib, dt = self.engine.lib, dtype_code(p.dtype)
         need = lib.lomo_gemm_update_workspace(out_f, in_f, dy2.shape[0], dt)
-        if need and (self._ws is None or self._ws.numel() < need):
-            self._ws = torch.empty(need, dtype=torch.uint8, device=p.device)
-        ws = self._ws.data_ptr() if need else None
+        ws = None
+        if need:
+            key = self.engine.stream()
+            buf = self._ws.get(key)
+            if buf is None or buf.numel() < need:
+                buf = self._ws[key] = torch.empty(need, dtype=torch.uint8, device=p.device)
+            ws = buf.data_ptr()
         if coefs is not None:
             rc = lib.lomo_gemm_update_dev(p.data_ptr(), dy2.data_ptr(), x2.data_ptr(), out_f,
                                           in_f, dy2.shape[0], dt, coefs.data_ptr(), ws, need,
@@ -405,19 +449,105 @@ class LOMO(_Protocol):
         _lib.check(rc, "lomo_gemm_update")
         return True
 
-    def _replay_pass(self, lr: float) -> None:
+    def _gemm_probe(self, w, x, dy) -> bool:
+        """K6 (from the linear's backward in pass 1): probe dW = dy^T x on the
+        tensor cores into w's norm slot.  False when the shape/dtype is not
+        supported -- the caller then returns dW to autograd and K2 probes it."""
+        if w.dtype not in (torch.bfloat16, torch.float16) or w.dim() != 2:
+            return False
+        out_f, in_f = w.shape
+        if out_f % 8 or in_f % 8:
+            return False
+        dy2 = dy.reshape(-1, out_f)
+        x2 = x.reshape(-1, in_f)
+        if not (dy2.is_contiguous() and x2.is_contiguous()) or dy2.dtype != w.dtype \
+                or x2.dtype != w.dtype:
+            return False
+        lib, dt = self.engine.lib, dtype_code(w.dtype)
+        need = lib.lomo_gemm_probe_workspace(out_f, in_f, dy2.shape[0], dt)
+        if need == 0:
+            return False
+        ws = self._pws.get(id(w))
+        if ws is None or ws.numel() < need:
+            ws = self._pws[id(w)] = torch.empty(need, dtype=torch.uint8, device=w.device)
+        n = w.numel()
+        if self._gscratch is None or self._gscratch.numel() < n or self._gscratch.dtype != w.dtype:
+            self._gscratch = torch.empty(n, dtype=w.dtype, device=w.device)
+        slot = self._slot[id(w)]
+        stream = self.engine.stream()
+        if self.probe_stream:
+            # beside the rest of the backward: x/dy stay alive in the stash and
+            # the partial sums go to this weight's own workspace; joined in
+            # _finish_probes, before K3a
+            if self._pstream is None:
+                self._pstream = torch.cuda.Stream(w.device)
+            self._pstream.wait_stream(torch.cuda.current_stream(w.device))
+            stream = self._pstream.cuda_stream
+        rc = lib.lomo_gemm_probe(dy2.data_ptr(), x2.data_ptr(), self._gscratch.data_ptr(), out_f,
+                                 in_f, dy2.shape[0], dt, slot,
+                                 self.engine.dispatch.flags | _lib.DEFER_ROWS, self.engine.ptr,
+                                 ws.data_ptr(), need, stream)
+        if rc == _E_ARG:
+            return False
+        _lib.check(rc, "lomo_gemm_probe")
+        self._pending_probe.append((ws.data_ptr(), out_f, in_f, slot, dt))
+        self.hook_calls += 1
+        return True
+
+    def _finish_probes(self) -> None:
+        """One launch (per 64 linears) folds every deferred K6 partial-sum matrix
+        of this pass into its norm slot, in stream order before K3a."""
+        pend, self._pending_probe = self._pending_probe, []
+        if not pend:
+            return
+        if self._pstream is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self._pstream)
+        for dt in {e[4] for e in pend}:
+            sel = [e for e in pend if e[4] == dt]
+            k = len(sel)
+            _lib.check(self.engine.lib.lomo_gemm_probe_finish(
+                (ctypes.c_void_p * k)(*[e[0] for e in sel]),
+                (ctypes.c_int64 * k)(*[e[1] for e in sel]),
+                (ctypes.c_int64 * k)(*[e[2] for e in sel]),
+                (ctypes.c_int * k)(*[e[3] for e in sel]), k, dt, self.engine.ptr,
+                self.engine.stream()), "lomo_gemm_probe_finish")
+
+    def _gemm_stream_list(self) -> list:
+        """[current stream] + the side streams K5 rotates over."""
+        main = torch.cuda.current_stream(self.device)
+        if self.gemm_streams <= 1:
+            return [main]
+        if self._streams is None or len(self._streams) != self.gemm_streams - 1:
+            self._streams = [torch.cuda.Stream(self.device) for _ in range(self.gemm_streams - 1)]
+        return [main] + self._streams
+
+    def _replay_pass(self, lr: float, coefs: torch.Tensor | None = None) -> None:
         """Pass 2 from the stash, in delivery order: for a replayable linear
         either K5 (GEMM with the update as epilogue) or dW = dy^T x (the
         pass-1 GEMM) -> K1; other parameters K1 on their kept gradient.  Every
-        gradient is dropped right after its launch."""
+        gradient is dropped right after its launch.  ``coefs``: device
+        [alpha, beta] for K5 (graph capture, graphs.py)."""
         st = self._stash
+        streams = self._gemm_stream_list() if self.fuse_gemm else []
+        main = torch.cuda.current_stream(self.device)
+        for s in streams[1:]:
+            s.wait_stream(main)
+        j = 0
         for p in reversed(self.params):
             pid = id(p)
             if pid in st.linear:
                 x, dy = st.linear.pop(pid)
-                if self.fuse_gemm and self._gemm_update(p, x, dy, lr):
-                    self.hook_calls += 1
-                    continue
+                if self.fuse_gemm:
+                    s = streams[j % len(streams)]
+                    with torch.cuda.stream(s):
+                        ok = self._gemm_update(p, x, dy, lr, coefs=coefs)
+                    if ok:
+                        j += 1
+                        if s is not main:   # freed on main: keep them until s used them
+                            x.record_stream(s)
+                            dy.record_stream(s)
+                        self.hook_calls += 1
+                        continue
                 g = _replay.weight_grad(x, dy)
                 del x, dy
             elif pid in st.grads:
@@ -427,6 +557,8 @@ class LOMO(_Protocol):
             self.engine.update(p, g)
             self.hook_calls += 1
             del g
+        for s in streams[1:]:
+            main.wait_stream(s)
         self.engine.flush()
         st.clear()
 

@@ -29,11 +29,17 @@ class ReplayStash:
         self.linear: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
         self.grads: dict[int, torch.Tensor] = {}
         self.shared: set[int] = set()   # weights that fed more than one linear
+        # pass-1 probe fused into the weight-gradient GEMM (K6): called as
+        # probe(w, x, dy) -> bool from the linear's backward; True means the
+        # gradient was probed on the tensor cores and is not returned to autograd
+        self.probe = None
+        self.probed: set[int] = set()
 
     def clear(self):
         self.linear.clear()
         self.grads.clear()
         self.shared.clear()
+        self.probed.clear()
 
     def nbytes(self) -> int:
         n = sum(x.numel() * x.element_size() + d.numel() * d.element_size()
@@ -57,12 +63,18 @@ class _StashLinear(torch.autograd.Function):
     def backward(ctx, dy):
         x, w = ctx.saved_tensors
         dx = dy.matmul(w) if ctx.needs_input_grad[0] else None
-        dw = weight_grad(x, dy) if ctx.needs_input_grad[1] else None
         st = _ACTIVE
+        dw = None
         if st is not None:
             if ctx.wid in st.linear:
                 st.shared.add(ctx.wid)
             st.linear[ctx.wid] = (x, dy)
+        if ctx.needs_input_grad[1]:
+            if st is not None and st.probe is not None and ctx.wid not in st.shared \
+                    and st.probe(w, x, dy):
+                st.probed.add(ctx.wid)   # K6 probed dW: nothing for autograd to deliver
+            else:
+                dw = weight_grad(x, dy)
         return dx, dw
 
 

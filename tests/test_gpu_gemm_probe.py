@@ -1,0 +1,236 @@
+"""K6: the weight-gradient GEMM with the pass-1 probe (stabilize.py:190-200) as
+its epilogue (csrc/lomo_gemm_probe.cu), through the C-ABI.
+
+Checks, per shape and dtype:
+  * the by-product dW (the epilogue's store) is the storage rounding of the
+    fp32-accumulated product: |dW - exact| <= ulp(exact) + K * 2^-24 * (|dy|^T |x|)
+    (one storage rounding plus the worst-case fp32 accumulation error, which
+    dominates only where the product cancels);
+  * the slot's sum of squares equals K2's over that same dW to fp32 summation
+    rounding (stated tolerance: relative 1e-5), with and without the loss
+    scale applied on device;
+  * overflow: a product that leaves the fp16 range (finite inputs) or a NaN
+    input raises the state's overflow flag, as probe_hook does for a
+    non-finite gradient; a clean product does not.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import gpu_util as U
+    from paper_2306_09782_b200 import _lib
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    torch.cuda.set_device(0)
+
+
+def _probe(st, dy, x, slot, flags, grad=None):
+    lib = U.lib()
+    dt = U.CODE[dy.dtype]
+    out_f, in_f = dy.shape[1], x.shape[1]
+    need = lib.lomo_gemm_probe_workspace(out_f, in_f, dy.shape[0], dt)
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+    if grad is None:
+        grad = torch.empty(out_f, in_f, dtype=dy.dtype, device="cuda")
+    rc = lib.lomo_gemm_probe(dy.data_ptr(), x.data_ptr(), grad.data_ptr(), out_f, in_f,
+                             dy.shape[0], dt, slot, flags, st.ptr, ws.data_ptr(), need, U.stream())
+    return rc, grad
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("out_f,in_f,tokens", [(256, 128, 64), (4096, 4096, 1024),
+                                               (1000, 2816, 1000), (11008, 4096, 512),
+                                               (8, 8, 8)])
+def test_gemm_probe_matches_k2_on_the_same_gradient(dtype, out_f, in_f, tokens):
+    g = torch.Generator(device="cuda").manual_seed(out_f + tokens)
+    dy = (torch.randn(tokens, out_f, device="cuda", generator=g) * 1e-2).to(dtype)
+    x = torch.randn(tokens, in_f, device="cuda", generator=g).to(dtype)
+    st = U.State(4, scale=1024.0)
+    st.begin()
+    for flags in (0, _lib.USE_SCALE):
+        slot = 0 if flags == 0 else 2
+        rc, grad = _probe(st, dy, x, slot, flags)
+        assert rc == 0
+        st.probe(grad, slot + 1, flags)             # K2 over the by-product
+    sums = st.slots(4)
+    assert st.status().overflow == 0
+    exact = (dy.double().t() @ x.double())
+    mag = dy.double().abs().t() @ x.double().abs()
+    mant = 7 if dtype == torch.bfloat16 else 10
+    ulp = torch.exp2(torch.floor(torch.log2(exact.abs().clamp_min(1e-30))) - mant)
+    bound = ulp + tokens * 2.0 ** -24 * mag
+    err = (grad.double() - exact).abs()
+    d = U.ulp_diff(grad, exact.to(dtype))
+    print(f"{dtype} {out_f}x{in_f}x{tokens}: dW max ulp {d.max().item()} "
+          f"(frac>1: {(d > 1).float().mean().item():.1e}), max err/bound "
+          f"{(err / bound).max().item():.3f}, sums {sums}, "
+          f"rel {abs(sums[0] - sums[1]) / sums[1]:.2e}")
+    assert (err <= bound).all()
+    np.testing.assert_allclose(sums[0], sums[1], rtol=1e-5)
+    np.testing.assert_allclose(sums[2], sums[3], rtol=1e-5)
+    np.testing.assert_allclose(sums[2], sums[0] / 1024.0 ** 2, rtol=1e-5)
+
+
+def test_gemm_probe_overflow_and_nan():
+    dt = torch.float16
+    g = torch.Generator(device="cuda").manual_seed(3)
+    dy = torch.randn(256, 512, device="cuda", generator=g).to(dt)
+    x = torch.randn(256, 256, device="cuda", generator=g).to(dt)
+    st = U.State(2, scale=1024.0)
+    st.begin()
+    assert _probe(st, dy, x, 0, _lib.USE_SCALE)[0] == 0
+    assert st.status().overflow == 0
+    # every input finite, the product leaves fp16 (|dW| ~ 16 * 300 * 300 > 65504)
+    big_dy = torch.full((16, 512), 300.0, device="cuda", dtype=dt)
+    big_x = torch.full((16, 256), 300.0, device="cuda", dtype=dt)
+    st.begin()
+    rc, grad = _probe(st, big_dy, big_x, 1, _lib.USE_SCALE)
+    assert rc == 0 and torch.isinf(grad).all()
+    assert st.status().overflow == 1
+    # a NaN in the input
+    st.begin()
+    x2 = x.clone()
+    x2[17, 33] = float("nan")
+    assert _probe(st, dy, x2, 0, 0)[0] == 0
+    assert st.status().overflow == 1
+    # begin_step clears it again
+    st.begin()
+    assert _probe(st, dy, x, 0, 0)[0] == 0
+    assert st.status().overflow == 0
+
+
+def test_gemm_probe_rejects():
+    lib = U.lib()
+    st = U.State(1)
+    t = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    args = (t.data_ptr(), t.data_ptr(), t.data_ptr(), 64, 64, 64)
+    assert lib.lomo_gemm_probe(*args, _lib.F32, 0, 0, st.ptr, ws.data_ptr(), 1 << 20,
+                               U.stream()) == -1
+    assert lib.lomo_gemm_probe(*args, _lib.BF16, 0, _lib.ACCUM_F64, st.ptr, ws.data_ptr(),
+                               1 << 20, U.stream()) == -1
+    assert lib.lomo_gemm_probe(*args, _lib.BF16, -1, 0, st.ptr, ws.data_ptr(), 1 << 20,
+                               U.stream()) == -2
+    assert lib.lomo_gemm_probe(*args, _lib.BF16, 0, 0, st.ptr, ws.data_ptr(), 16,
+                               U.stream()) == -1  # workspace too small
+
+
+# --- K6 inside the LOMO two-pass replay step ---------------------------------------
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_lomo_fused_probe_matches_k2_probe(dtype):
+    """Pass 1 with K6 (fuse_probe) against pass 1 with GEMM -> K2: same
+    decisions, norms equal to fp32 summation rounding, and -- since pass 2
+    is the same K5 in both -- parameters equal up to that norm difference."""
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.workloads import Llama
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+    torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+    cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
+    a = Llama(cfg, dtype=dtype, device="cuda", seed=0)
+    b = Llama(cfg, dtype=dtype, device="cuda", seed=0)
+    scale = 2.0 ** 16 if dtype == torch.float16 else 2.0 ** 8
+    kw = dict(lr=0.05, clip_grad_norm=0.3, loss_scale=scale, replay=True, fuse_gemm=True)
+    oa = LOMO(a, fuse_probe=False, **kw)
+    ob = LOMO(b, fuse_probe=True, **kw)
+    assert ob.fuse_probe and not oa.fuse_probe
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    for step in range(3):
+        d = torch.randint(0, 256, (2, 65), device="cuda", generator=gen)
+        la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+        lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+        assert oa.last_outcome == ob.last_outcome
+        print(step, la, lb, oa.last_norm, ob.last_norm)
+        assert abs(oa.last_norm - ob.last_norm) <= 1e-5 * oa.last_norm
+        assert ob.hook_calls > 0
+    for x, y in zip(a.parameters(), b.parameters()):
+        torch.testing.assert_close(x.float(), y.float(), rtol=2 ** -7, atol=1e-6)
+
+
+def test_lomo_fused_probe_overflow_skips_like_k2():
+    """An fp16 overflow inside a weight gradient (finite activations) is caught
+    by K6 and the step is skipped with the scale halved, exactly as with K2."""
+    from paper_2306_09782_b200 import LOMO, LossScaler
+    from paper_2306_09782_b200.stabilize import StepOutcome
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
+    outs = []
+    for fuse_probe in (False, True):
+        m = Llama(cfg, dtype=torch.float16, device="cuda", seed=0)
+        opt = LOMO(m, lr=0.05, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 24),
+                   replay=True, fuse_gemm=True, fuse_probe=fuse_probe)
+        d = torch.randint(0, 256, (2, 65), device="cuda",
+                          generator=torch.Generator(device="cuda").manual_seed(1))
+        before = [p.detach().clone() for p in m.parameters()]
+        opt.step(lambda: m.loss(d[:, :-1], d[:, 1:]), 0.05)
+        outs.append((opt.last_outcome, opt.loss_scale))
+        if opt.last_outcome == StepOutcome.SKIPPED_OVERFLOW:
+            assert all(torch.equal(x, y) for x, y in zip(before, m.parameters()))
+    assert outs[0] == outs[1]
+    assert outs[0][0] == StepOutcome.SKIPPED_OVERFLOW and outs[0][1] == 2.0 ** 23
+
+
+def test_lomo_fused_probe_refuses_tied_weight():
+    """A weight that gets gradient from a linear AND another op cannot be
+    replayed (pass 2 would drop the other contribution): K6 mode detects the
+    extra hook and raises, like the unfused first-step check."""
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.errors import ConfigError
+    from paper_2306_09782_b200.replay import linear
+
+    class Tied(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.w = torch.nn.Parameter(torch.randn(64, 64, device="cuda",
+                                                    dtype=torch.bfloat16) * 0.02)
+
+        def forward(self, x):
+            return (linear(x, self.w).float().square().mean()
+                    + self.w.float().sum() * 1e-3)  # second use: not a linear
+
+    m = Tied()
+    opt = LOMO(m, lr=0.01, clip_grad_norm=1.0, replay=True, fuse_gemm=True)
+    x = torch.randn(32, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(ConfigError):
+        opt.step(lambda: m(x), 0.01)
+
+
+def test_gemm_probe_deferred_rows_match_immediate():
+    """LOMO_DEFER_ROWS + lomo_gemm_probe_finish (one launch for a batch of
+    linears) leaves exactly the slot partials of the immediate mode."""
+    import ctypes
+    lib = U.lib()
+    dt = torch.bfloat16
+    shapes = [(512, 256, 128), (1000, 2816, 64), (256, 4096, 96)]
+    g = torch.Generator(device="cuda").manual_seed(9)
+    ins = [((torch.randn(t, o, device="cuda", generator=g) * 1e-2).to(dt),
+            torch.randn(t, i, device="cuda", generator=g).to(dt)) for o, i, t in shapes]
+    a, b = U.State(len(shapes), scale=256.0), U.State(len(shapes), scale=256.0)
+    a.begin()
+    b.begin()
+    for k, (dy, x) in enumerate(ins):
+        assert _probe(a, dy, x, k, _lib.USE_SCALE)[0] == 0
+    wss = []
+    for k, (dy, x) in enumerate(ins):
+        need = lib.lomo_gemm_probe_workspace(dy.shape[1], x.shape[1], dy.shape[0], U.CODE[dt])
+        ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        wss.append(ws)
+        grad = torch.empty(dy.shape[1], x.shape[1], dtype=dt, device="cuda")
+        assert lib.lomo_gemm_probe(dy.data_ptr(), x.data_ptr(), grad.data_ptr(), dy.shape[1],
+                                   x.shape[1], dy.shape[0], U.CODE[dt], k,
+                                   _lib.USE_SCALE | _lib.DEFER_ROWS, b.ptr, ws.data_ptr(), need,
+                                   U.stream()) == 0
+    n = len(shapes)
+    assert lib.lomo_gemm_probe_finish(
+        (ctypes.c_void_p * n)(*[w.data_ptr() for w in wss]),
+        (ctypes.c_int64 * n)(*[s[0] for s in shapes]),
+        (ctypes.c_int64 * n)(*[s[1] for s in shapes]),
+        (ctypes.c_int * n)(*range(n)), n, U.CODE[dt], b.ptr, U.stream()) == 0
+    assert np.array_equal(a.slots(n), b.slots(n))
