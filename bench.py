@@ -443,7 +443,8 @@ def bench_train(args, rank, world):
     torch.cuda.reset_peak_memory_stats()
     size = args.train_model
     ckpt = args.ckpt or size == "65b"
-    model = Llama(size, dtype=torch.float16, device="cuda", checkpointing=ckpt)
+    model = Llama(size, dtype=torch.float16, device="cuda", checkpointing=ckpt,
+                  fused_proj=not args.separate_proj)
     model.train()
     params_bytes = sum(p.numel() * p.element_size() for p in model.parameters())
     largest = max(p.numel() * p.element_size() for p in model.parameters())
@@ -452,6 +453,8 @@ def bench_train(args, rank, world):
     data = [torch.randint(0, 32000, (batch, seq + 1), device="cuda", generator=gen)
             for _ in range(4)]
     out = {"model": f"llama-{size} (random init N(0,0.02)), fp16 params, no master copy",
+           "projections": "separate q/k/v, gate/up" if args.separate_proj else
+           "stacked qkv [3h,h] and gate_up [2f,h] weights (same parameters and math)",
            "seq_len": seq, "batch": batch, "steps": args.train_steps, "passes_per_step": 2,
            "clip_grad_norm": 1.0, "activation_checkpointing": bool(ckpt),
            "paper_tgs_rtx3090": 769.92}
@@ -673,6 +676,8 @@ def main():
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--ckpt", action="store_true", help="per-layer activation checkpointing")
+    ap.add_argument("--separate-proj", action="store_true",
+                    help="train leg: q/k/v and gate/up as separate weights (default: stacked)")
     ap.add_argument("--memory-table", action="store_true",
                     help="also measure the Table-1 setting (seq 512 x batch 8, AC off/on)")
     ap.add_argument("--train-model", default="7b", choices=["7b", "13b", "30b", "65b"],

@@ -42,6 +42,21 @@ int lomo_wl_rope(const void* q, const void* k, void* qo, void* ko, const void* c
                  const void* sin, int64_t rows, int seq, int heads, int dh, int dtype,
                  int direction, void* stream);
 
+/* lomo_wl_rope with input rows `ld_in` and output rows `ld_out` elements
+ * apart: the forward reads q/k as views of a fused [rows, 3*heads*dh] QKV
+ * projection, the backward writes dq/dk straight into d(qkv). */
+int lomo_wl_rope_ld(const void* q, const void* k, int64_t ld_in, void* qo, void* ko,
+                    int64_t ld_out, const void* cos, const void* sin, int64_t rows, int seq,
+                    int heads, int dh, int dtype, int direction, void* stream);
+
+/* SwiGLU over a fused gate/up projection gu [rows, 2f] (gate = gu[:, :f],
+ * up = gu[:, f:]): out [rows, f] = silu(gate) * up; the backward writes
+ * dgu [rows, 2f] in the same layout. */
+int lomo_wl_swiglu_gu_fwd(const void* gu, void* out, int64_t rows, int64_t f, int dtype,
+                          void* stream);
+int lomo_wl_swiglu_gu_bwd(const void* dout, const void* gu, void* dgu, int64_t rows, int64_t f,
+                          int dtype, void* stream);
+
 /* out = silu(g) * u;  backward: dg = dout*u*silu'(g), du = dout*silu(g). */
 int lomo_wl_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, int dtype,
                        void* stream);

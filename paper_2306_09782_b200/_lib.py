@@ -61,6 +61,9 @@ WL_EXPORTS = (
     "lomo_wl_rope",
     "lomo_wl_swiglu_fwd",
     "lomo_wl_swiglu_bwd",
+    "lomo_wl_rope_ld",
+    "lomo_wl_swiglu_gu_fwd",
+    "lomo_wl_swiglu_gu_bwd",
 )
 
 
@@ -142,6 +145,10 @@ _SIGS = {
                             _vp]),
     "lomo_wl_swiglu_fwd": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp]),
     "lomo_wl_swiglu_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
+    "lomo_wl_rope_ld": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32,
+                               _i32, _i32, _vp]),
+    "lomo_wl_swiglu_gu_fwd": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp]),
+    "lomo_wl_swiglu_gu_bwd": (_i32, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
 }
 
 _LIB = None

@@ -236,7 +236,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads)
     rope(const T* __restrict__ q, const T* __restrict__ k, T* __restrict__ qo,
          T* __restrict__ ko, const T* __restrict__ cs, const T* __restrict__ sn, int64_t rows,
-         int seq, int heads, int dh, int bwd) {
+         int seq, int heads, int dh, int bwd, int64_t ld_in, int64_t ld_out) {
   const int half = dh / 2, gph = half / 8;
   const int64_t per_tensor = rows * heads * gph;
   const int64_t total = 2 * per_tensor;
@@ -247,8 +247,8 @@ __global__ void __launch_bounds__(kThreads)
     const int gi = (int)(u % gph);
     const int64_t rh = u / gph;              // row * heads + head
     const int pos = (int)((rh / heads) % seq);
-    const T* src = (is_k ? k : q) + rh * dh;
-    T* dst = (is_k ? ko : qo) + rh * dh;
+    const T* src = (is_k ? k : q) + (rh / heads) * ld_in + (rh % heads) * dh;
+    T* dst = (is_k ? ko : qo) + (rh / heads) * ld_out + (rh % heads) * dh;
     Vec8<T> X1, X2, C1, C2, S1, S2, O1, O2;
     X1.u = ld_nc(src + gi * 8);
     X2.u = ld_nc(src + half + gi * 8);
@@ -325,6 +325,55 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Fused gate/up layout: gu[r, 0:f] = gate, gu[r, f:2f] = up (one GEMM output);
+// out[r, :] = silu(gate) * up, and the backward writes d(gu) in the same
+// layout, so neither direction needs a split or a concatenation copy.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    swiglu_gu_fwd(const T* __restrict__ gu, T* __restrict__ out, int64_t rows, int64_t fv) {
+  const int64_t total = rows * fv;  // fv = f / 8 vectors per row half
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / fv, c = i - r * fv;
+    const uint4* row = reinterpret_cast<const uint4*>(gu) + r * 2 * fv;
+    Vec8<T> G, U, O;
+    G.u = ld_nc(row + c);
+    U.u = ld_nc(row + fv + c);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float x = tof(G.e[e]);
+      O.e[e] = fromf<T>(x * sigmoidf_(x) * tof(U.e[e]));
+    }
+    reinterpret_cast<uint4*>(out)[i] = O.u;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    swiglu_gu_bwd(const T* __restrict__ dout, const T* __restrict__ gu, T* __restrict__ dgu,
+                  int64_t rows, int64_t fv) {
+  const int64_t total = rows * fv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / fv, c = i - r * fv;
+    const uint4* row = reinterpret_cast<const uint4*>(gu) + r * 2 * fv;
+    uint4* drow = reinterpret_cast<uint4*>(dgu) + r * 2 * fv;
+    Vec8<T> D, G, U, DG, DU;
+    D.u = ld_nc(reinterpret_cast<const uint4*>(dout) + i);
+    G.u = ld_nc(row + c);
+    U.u = ld_nc(row + fv + c);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float x = tof(G.e[e]), d = tof(D.e[e]), y = tof(U.e[e]);
+      const float s = sigmoidf_(x);
+      DU.e[e] = fromf<T>(d * x * s);
+      DG.e[e] = fromf<T>(d * y * s * (1.f + x * (1.f - s)));
+    }
+    drow[c] = DG.u;
+    drow[fv + c] = DU.u;
+  }
+}
+
 inline int grid_for(int64_t work) {
   // enough CTAs to fill 148 SMs x 8 resident CTAs, no more than the work
   const int64_t cap = 148 * 8;
@@ -385,11 +434,11 @@ template <typename T>
 struct Rope {
   static int run(const void* q, const void* k, void* qo, void* ko, const void* c,
                  const void* sn, int64_t rows, int seq, int heads, int dh, int bwd,
-                 cudaStream_t s) {
+                 int64_t ld_in, int64_t ld_out, cudaStream_t s) {
     const int64_t work = 2 * rows * heads * (dh / 16);
     rope<T><<<grid_for(work), kThreads, 0, s>>>((const T*)q, (const T*)k, (T*)qo, (T*)ko,
                                                 (const T*)c, (const T*)sn, rows, seq, heads, dh,
-                                                bwd);
+                                                bwd, ld_in, ld_out);
     return status();
   }
 };
@@ -408,6 +457,20 @@ struct SwigluBwd {
                  cudaStream_t s) {
     swiglu_bwd<T><<<grid_for(n / 8), kThreads, 0, s>>>((const T*)d, (const T*)g, (const T*)u,
                                                        (T*)dg, (T*)du, n / 8);
+    return status();
+  }
+};
+
+template <typename T>
+struct SwigluGu {
+  static int run(const void* a, const void* b, void* c, int64_t rows, int64_t f, int bwd,
+                 cudaStream_t s) {
+    const int64_t fv = f / 8;
+    if (!bwd)
+      swiglu_gu_fwd<T><<<grid_for(rows * fv), kThreads, 0, s>>>((const T*)a, (T*)c, rows, fv);
+    else
+      swiglu_gu_bwd<T><<<grid_for(rows * fv), kThreads, 0, s>>>((const T*)a, (const T*)b, (T*)c,
+                                                               rows, fv);
     return status();
   }
 };
@@ -454,7 +517,41 @@ int lomo_wl_rope(const void* q, const void* k, void* qo, void* ko, const void* c
       !wl::aligned16(cos) || !wl::aligned16(sin))
     return LOMO_E_ARG;
   return wl::dispatch<wl::Rope>(dtype, q, k, qo, ko, cos, sin, rows, seq, heads, dh, direction,
-                                (cudaStream_t)stream);
+                                (int64_t)heads * dh, (int64_t)heads * dh, (cudaStream_t)stream);
+}
+
+int lomo_wl_rope_ld(const void* q, const void* k, int64_t ld_in, void* qo, void* ko,
+                    int64_t ld_out, const void* cos, const void* sin, int64_t rows, int seq,
+                    int heads, int dh, int dtype, int direction, void* stream) {
+  if (rows < 0 || seq <= 0 || heads <= 0 || dh <= 0 || dh % 16 || (direction & ~1))
+    return LOMO_E_ARG;
+  if (ld_in < (int64_t)heads * dh || ld_in % 8 || ld_out < (int64_t)heads * dh || ld_out % 8)
+    return LOMO_E_ARG;
+  if (rows == 0) return 0;
+  if (!q || !k || !qo || !ko || !cos || !sin || q == qo || k == ko) return LOMO_E_ARG;
+  if (!wl::aligned16(q) || !wl::aligned16(k) || !wl::aligned16(qo) || !wl::aligned16(ko) ||
+      !wl::aligned16(cos) || !wl::aligned16(sin))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::Rope>(dtype, q, k, qo, ko, cos, sin, rows, seq, heads, dh, direction,
+                                ld_in, ld_out, (cudaStream_t)stream);
+}
+
+int lomo_wl_swiglu_gu_fwd(const void* gu, void* out, int64_t rows, int64_t f, int dtype,
+                          void* stream) {
+  if (rows < 0 || f <= 0 || f % 8) return LOMO_E_ARG;
+  if (rows == 0) return 0;
+  if (!gu || !out || !wl::aligned16(gu) || !wl::aligned16(out)) return LOMO_E_ARG;
+  return wl::dispatch<wl::SwigluGu>(dtype, gu, (const void*)nullptr, out, rows, f, 0,
+                                    (cudaStream_t)stream);
+}
+
+int lomo_wl_swiglu_gu_bwd(const void* dout, const void* gu, void* dgu, int64_t rows, int64_t f,
+                          int dtype, void* stream) {
+  if (rows < 0 || f <= 0 || f % 8) return LOMO_E_ARG;
+  if (rows == 0) return 0;
+  if (!dout || !gu || !dgu || !wl::aligned16(dout) || !wl::aligned16(gu) || !wl::aligned16(dgu))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::SwigluGu>(dtype, dout, gu, dgu, rows, f, 1, (cudaStream_t)stream);
 }
 
 int lomo_wl_swiglu_fwd(const void* g, const void* u, void* out, int64_t n, int dtype,

@@ -305,6 +305,69 @@ class _SwiGLUFn(torch.autograd.Function):
         return dg, du
 
 
+class _QKVRopeFn(torch.autograd.Function):
+    """Fused QKV projection [b, s, 3h] -> rotated q, k ([b, s, heads, dh],
+    contiguous) and v (a [b, heads, s, dh] view of qkv, as SDPA takes it).  The
+    backward assembles d(qkv) in place -- the rotary transpose writes dq/dk
+    into their column blocks, dv is copied into its block -- instead of
+    autograd's zero-filled slice gradients."""
+
+    @staticmethod
+    def forward(ctx, qkv, cos, sin, nh):
+        b, s, h3 = qkv.shape
+        h = h3 // 3
+        dh = h // nh
+        qo = torch.empty(b, s, nh, dh, dtype=qkv.dtype, device=qkv.device)
+        ko = torch.empty_like(qo)
+        _wl_call(_wl().lomo_wl_rope_ld(qkv.data_ptr(), qkv[..., h:].data_ptr(), h3,
+                                       qo.data_ptr(), ko.data_ptr(), h, cos.data_ptr(),
+                                       sin.data_ptr(), b * s, s, nh, dh, _WL_DTYPES[qkv.dtype],
+                                       0, _stream()), "lomo_wl_rope_ld")
+        v = qkv[..., 2 * h:].view(b, s, nh, dh).transpose(1, 2)  # strided view: SDPA takes it
+        ctx.save_for_backward(cos, sin)
+        ctx.dims = (b, s, h, nh, dh)
+        return qo, ko, v
+
+    @staticmethod
+    def backward(ctx, dq, dk, dv):
+        cos, sin = ctx.saved_tensors
+        b, s, h, nh, dh = ctx.dims
+        dqkv = torch.empty(b, s, 3 * h, dtype=dq.dtype, device=dq.device)
+        dq, dk = dq.contiguous(), dk.contiguous()
+        _wl_call(_wl().lomo_wl_rope_ld(dq.data_ptr(), dk.data_ptr(), h, dqkv.data_ptr(),
+                                       dqkv[..., h:].data_ptr(), 3 * h, cos.data_ptr(),
+                                       sin.data_ptr(), b * s, s, nh, dh, _WL_DTYPES[dq.dtype],
+                                       1, _stream()), "lomo_wl_rope_ld")
+        dqkv[..., 2 * h:].view(b, s, nh, dh).copy_(dv.transpose(1, 2))
+        return dqkv, None, None, None
+
+
+class _SwiGLUGuFn(torch.autograd.Function):
+    """silu(gu[..., :f]) * gu[..., f:] for a fused gate/up projection."""
+
+    @staticmethod
+    def forward(ctx, gu):
+        f = gu.shape[-1] // 2
+        rows = gu.numel() // (2 * f)
+        out = torch.empty(*gu.shape[:-1], f, dtype=gu.dtype, device=gu.device)
+        _wl_call(_wl().lomo_wl_swiglu_gu_fwd(gu.data_ptr(), out.data_ptr(), rows, f,
+                                             _WL_DTYPES[gu.dtype], _stream()),
+                 "lomo_wl_swiglu_gu_fwd")
+        ctx.save_for_backward(gu)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        (gu,) = ctx.saved_tensors
+        dout = dout.contiguous()
+        f = gu.shape[-1] // 2
+        dgu = torch.empty_like(gu)
+        _wl_call(_wl().lomo_wl_swiglu_gu_bwd(dout.data_ptr(), gu.data_ptr(), dgu.data_ptr(),
+                                             gu.numel() // (2 * f), f, _WL_DTYPES[gu.dtype],
+                                             _stream()), "lomo_wl_swiglu_gu_bwd")
+        return dgu
+
+
 def rms_norm(x, w, eps=RMSNORM_EPS, fused=True):
     if fused and _wl_ok(x, w) and x.shape[-1] % 8 == 0 and x.shape[-1] <= 8192:
         return _RMSNormFn.apply(x, w, eps)
@@ -344,20 +407,55 @@ def _linear(h_in: int, h_out: int, dtype, device, std: float) -> nn.Parameter:
 
 
 class LlamaLayer(nn.Module):
-    def __init__(self, h, nh, f, dtype, device, std):
+    def __init__(self, h, nh, f, dtype, device, std, fused_proj: bool = False):
         super().__init__()
         self.nh = nh
+        self.fused_proj = fused_proj
         self.input_layernorm = RMSNorm(h, dtype, device)
-        self.q = _linear(h, h, dtype, device, std)
-        self.k = _linear(h, h, dtype, device, std)
-        self.v = _linear(h, h, dtype, device, std)
+        if fused_proj:
+            # q, k, v stacked in one [3h, h] weight and gate, up in one [2f, h]:
+            # the same parameters and arithmetic, 2 GEMMs instead of 5 per
+            # direction (bigger tiles grids, fewer launches; tools/proj_fusion.py)
+            self.qkv = _linear(h, 3 * h, dtype, device, std)
+        else:
+            self.q = _linear(h, h, dtype, device, std)
+            self.k = _linear(h, h, dtype, device, std)
+            self.v = _linear(h, h, dtype, device, std)
         self.o = _linear(h, h, dtype, device, std)
         self.post_attention_layernorm = RMSNorm(h, dtype, device)
-        self.gate = _linear(h, f, dtype, device, std)
-        self.up = _linear(h, f, dtype, device, std)
+        if fused_proj:
+            self.gate_up = _linear(h, 2 * f, dtype, device, std)
+        else:
+            self.gate = _linear(h, f, dtype, device, std)
+            self.up = _linear(h, f, dtype, device, std)
         self.down = _linear(f, h, dtype, device, std)
 
+    def _forward_fused(self, x, cos, sin):
+        b, s, h = x.shape
+        nh, dh = self.nh, h // self.nh
+        a = self.input_layernorm(x)
+        qkv = rlinear(a, self.qkv)                                  # [b, s, 3h]
+        if _wl_ok(qkv, cos, sin) and dh % 16 == 0:
+            q, k, v = _QKVRopeFn.apply(qkv, cos, sin, nh)
+        else:
+            q, k, v = qkv.split(h, dim=-1)
+            q, k = rope_qk(q.reshape(b, s, nh, dh), k.reshape(b, s, nh, dh), cos, sin, False)
+            v = v.reshape(b, s, nh, dh).transpose(1, 2)
+        o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v,
+                                           is_causal=True)
+        x = x + rlinear(o.transpose(1, 2).reshape(b, s, h), self.o)
+        y = self.post_attention_layernorm(x)
+        gu = rlinear(y, self.gate_up)                                # [b, s, 2f]
+        if _wl_ok(gu) and gu.shape[-1] % 16 == 0:
+            m = _SwiGLUGuFn.apply(gu)
+        else:
+            f = gu.shape[-1] // 2
+            m = F.silu(gu[..., :f]) * gu[..., f:]
+        return x + rlinear(m, self.down)
+
     def forward(self, x, cos, sin):
+        if self.fused_proj:
+            return self._forward_fused(x, cos, sin)
         b, s, h = x.shape
         nh, dh = self.nh, h // self.nh
         fused = self.input_layernorm.fused
@@ -383,7 +481,7 @@ class Llama(nn.Module):
 
     def __init__(self, size="7b", dtype=torch.float16, device="cuda",
                  checkpointing: bool = False, layers: int | None = None, seed: int = 0,
-                 fused_layers: bool = True):
+                 fused_layers: bool = True, fused_proj: bool = False):
         super().__init__()
         c = dict(LLAMA[size]) if isinstance(size, str) else dict(size)
         if layers is not None:
@@ -397,7 +495,7 @@ class Llama(nn.Module):
             torch.manual_seed(seed)
         std = 0.02
         self.embed_tokens = nn.Parameter(torch.empty(v, h, dtype=dtype, device=device).normal_(0, std))
-        self.layers = nn.ModuleList(LlamaLayer(h, nh, f, dtype, device, std)
+        self.layers = nn.ModuleList(LlamaLayer(h, nh, f, dtype, device, std, fused_proj)
                                     for _ in range(c["layers"]))
         self.norm = RMSNorm(h, dtype, device)
         self.lm_head = nn.Parameter(torch.empty(v, h, dtype=dtype, device=device).normal_(0, std))

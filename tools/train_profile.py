@@ -23,9 +23,11 @@ ap.add_argument("--replay", action="store_true")
 ap.add_argument("--fuse", action="store_true")
 ap.add_argument("--grouped", action="store_true")
 ap.add_argument("--graph", action="store_true", help="GraphedLOMOStep (implies --replay --fuse)")
+ap.add_argument("--fused-proj", action="store_true", help="stacked qkv / gate_up weights")
 a = ap.parse_args()
 torch.cuda.set_device(0)
-model = Llama("7b", dtype=torch.float16, device="cuda", layers=a.layers, checkpointing=a.ckpt)
+model = Llama("7b", dtype=torch.float16, device="cuda", layers=a.layers, checkpointing=a.ckpt,
+              fused_proj=a.fused_proj)
 if a.graph:
     a.replay = a.fuse = True
 if a.grouped:
