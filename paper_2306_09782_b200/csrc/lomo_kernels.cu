@@ -29,6 +29,8 @@
 #include <stddef.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "lomo_b200.h"
 
 namespace lomo_k {
@@ -423,8 +425,50 @@ __device__ __forceinline__ double vec_sumsq(const uint4& gv, M inv_scale, bool u
   return (double)acc;
 }
 
+// Hot-loop form (M = float): no per-element finiteness test.  A non-finite
+// element makes its square inf/NaN, so the thread's running sum is
+// non-finite; only then does the thread re-scan its elements to tell a
+// non-finite gradient (probe_hook's overflow) from squares that merely
+// overflowed fp32 (which stay an inf partial, as before).  Same arithmetic as
+// vec_sumsq -- (g*inv_scale)^2 by FMA in fp32 per 16-byte vector -- at about
+// half the instructions per element: at 5+ TB/s K2 is issue-bound otherwise.
+template <typename T>
+__device__ __forceinline__ double vec_sumsq_nocheck(const uint4& gv, float inv_scale,
+                                                    bool use_scale) {
+  Vec16<T> G;
+  G.u = gv;
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < (int)(16 / sizeof(T)); ++k) {
+    float x = to_m<float>(G.e[k]);
+    if (use_scale) x = x * inv_scale;
+    acc = fmaf(x, x, acc);
+  }
+  return (double)acc;
+}
+
+template <typename T>
+__device__ __forceinline__ bool vec_has_nonfinite(const uint4& gv) {
+  Vec16<T> G;
+  G.u = gv;
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < (int)(16 / sizeof(T)); ++k) bad |= !is_fin(to_m<float>(G.e[k]));
+  return bad;
+}
+
 template <typename T, typename M>
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ double tile_sumsq(const uint4& gv, M inv_scale, bool use_scale,
+                                             bool& bad) {
+  if constexpr (std::is_same<M, float>::value) {
+    return vec_sumsq_nocheck<T>(gv, inv_scale, use_scale);
+  } else {
+    return vec_sumsq<T, M>(gv, inv_scale, use_scale, bad);
+  }
+}
+
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads, 5)  // 48 registers: 5 CTAs per SM, no spills
     k2_probe(const T* __restrict__ g, int64_t n, int head, int64_t nvec, int64_t per_cta,
              int slot, unsigned flags, void* state) {
   constexpr int V = 16 / sizeof(T);
@@ -433,11 +477,23 @@ __global__ void __launch_bounds__(kThreads)
   pdl_launch_dependents();
   lomo_state* st = hdr(state);
   const bool use_scale = (flags & LOMO_USE_SCALE) != 0;
-  const M inv_scale = use_scale ? (M)st->inv_scale : (M)1;
 
   double acc = 0.0;
   bool bad = false;
-  if (blockIdx.x == 0) {
+  // small fixed tiles (>= 2048 vectors = 32 KB, <= LOMO_PROBE_BLOCKS_PER_SLOT
+  // CTAs): the block scheduler balances them across SMs like K1's tiles.
+  // The first tile's loads are issued before the (dependent, L2-latency)
+  // read of inv_scale, as in K1: most CTAs run exactly one tile.
+  const int64_t beg = (int64_t)blockIdx.x * per_cta;
+  const int64_t end = min(beg + per_cta, nvec);
+  const uint4* gv = reinterpret_cast<const uint4*>(g + head);
+  M inv_scale = (M)1;
+  bool have_scale = !use_scale;
+  if (blockIdx.x == 0) {  // scalar head (before the first aligned vector) and tail, first:
+    if (!have_scale) {    // CTA 0 keeps the summation order of the partial it always had
+      inv_scale = (M)st->inv_scale;
+      have_scale = true;
+    }
     const int64_t tail0 = head + nvec * V;
     const int64_t ntail = n - tail0;
     for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
@@ -448,11 +504,6 @@ __global__ void __launch_bounds__(kThreads)
       acc += (double)x * (double)x;
     }
   }
-  // small fixed tiles (>= 2048 vectors = 32 KB, <= LOMO_PROBE_BLOCKS_PER_SLOT
-  // CTAs): the block scheduler balances them across SMs like K1's tiles
-  const int64_t beg = (int64_t)blockIdx.x * per_cta;
-  const int64_t end = min(beg + per_cta, nvec);
-  const uint4* gv = reinterpret_cast<const uint4*>(g + head);
   for (int64_t base = beg + threadIdx.x; base < end; base += (int64_t)kThreads * kUnroll) {
     uint4 G[kUnroll];
 #pragma unroll
@@ -460,10 +511,22 @@ __global__ void __launch_bounds__(kThreads)
       const int64_t i = base + (int64_t)u * kThreads;
       if (i < end) G[u] = ld_stream_ro(gv + i);
     }
+    if (!have_scale) {
+      double sc;
+      asm volatile("ld.global.f64 %0, [%1];" : "=d"(sc) : "l"(&st->inv_scale));
+      inv_scale = (M)sc;
+      have_scale = true;
+    }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
-      if (i < end) acc += vec_sumsq<T, M>(G[u], inv_scale, use_scale, bad);
+      if (i < end) acc += tile_sumsq<T, M>(G[u], inv_scale, use_scale, bad);
+    }
+  }
+  if constexpr (std::is_same<M, float>::value) {
+    if (!is_fin(acc)) {  // rare: was it a non-finite element or fp32 overflow?
+      for (int64_t i = beg + threadIdx.x; i < end && !bad; i += kThreads)
+        bad = vec_has_nonfinite<T>(ld_stream_ro(gv + i));
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;

@@ -134,6 +134,46 @@ __global__ void __launch_bounds__(256) v_probe(const bf* __restrict__ g, int64_t
   if (threadIdx.x == 0) part[blockIdx.x] = r + (bad ? 1.0 : 0.0);
 }
 
+// ---- K2 variant: the product's structure minus one feature at a time -------
+// MODE 0: product-like (state partial row, nblocks, __syncthreads_or flag)
+// MODE 1: flag folded into the partial as NaN (no extra barrier)
+// MODE 2: MODE 1 + no nblocks write
+template <int MODE>
+__global__ void __launch_bounds__(256, 5) v_probe2(const bf* __restrict__ g, int64_t nvec,
+                                                   int64_t per, void* state, int slot) {
+  __shared__ double sm[8];
+  pdl_wait();
+  pdl_launch_dependents();
+  lomo_state* st = hdr(state);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const int64_t beg = (int64_t)blockIdx.x * per, end = min(beg + per, nvec);
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t base = beg + threadIdx.x; base < end; base += 256 * 8) {
+    uint4 G[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = base + u * 256;
+      if (i < end) G[u] = ld_stream_ro(gv + i);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = base + u * 256;
+      if (i < end) acc += vec_sumsq<bf, float>(G[u], 1.0f, false, bad);
+    }
+  }
+  if (MODE == 0) {
+    if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
+  } else if (bad) {
+    acc = __longlong_as_double(0x7ff8000000000000ll);
+  }
+  const double r = block_sum(acc, sm);
+  if (threadIdx.x == 0) {
+    partials_of(st, slot)[blockIdx.x] = r;
+    if (MODE < 2 && blockIdx.x == 0) nblocks_of(st)[slot] = (int32_t)gridDim.x;
+  }
+}
+
 // ---- variant: TMA bulk copies through a 4-stage shared-memory ring ---------
 constexpr int kTileElems = 8192;  // 16 KB per operand per stage
 constexpr int kStages = 4;
@@ -422,6 +462,43 @@ int main() {
       }, 10);
       printf("%-44s %8.3f ms  %7.1f GB/s\n", name, ms, gbp / (ms * 1e-3));
     };
+    {  // the product K2 through the C-ABI, with and without the scale read
+      void* st;
+      const int ns = (int)ts.size();
+      CK(cudaMalloc(&st, lomo_state_bytes(ns)));
+      CK((cudaError_t)lomo_state_init(st, ns, 1024.0, 16, 1.0, 16777216.0, 1.0, 1.0, nullptr));
+      for (unsigned fl : {0u, (unsigned)LOMO_USE_SCALE}) {
+        float ms = time_passes([&] {
+          for (int i = ns - 1; i >= 0; --i)
+            lomo_probe(ts[i].g, ts[i].n, LOMO_BF16, ns - 1 - i, fl, st, nullptr);
+        }, 10);
+        printf("%-44s %8.3f ms  %7.1f GB/s\n",
+               fl ? "product lomo_probe (per tensor, USE_SCALE)" : "product lomo_probe (per tensor)",
+               ms, gbp / (ms * 1e-3));
+      }
+      auto p2 = [&](auto kern, const char* name) {
+        float ms = time_passes([&] {
+          for (int i = ns - 1; i >= 0; --i) {
+            const int64_t nvec = ts[i].n / 8;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)((nvec + 2047) / 2048));
+            cfg.blockDim = dim3(256);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&cfg, kern, (const bf*)ts[i].g, nvec, (int64_t)2048, st,
+                                  ns - 1 - i));
+          }
+        }, 10);
+        printf("%-44s %8.3f ms  %7.1f GB/s\n", name, ms, gbp / (ms * 1e-3));
+      };
+      p2(v_probe2<0>, "k2-like: state row + syncthreads_or");
+      p2(v_probe2<1>, "k2-like: NaN-folded flag");
+      p2(v_probe2<2>, "k2-like: NaN flag, no nblocks");
+      CK(cudaFree(st));
+    }
     probe_pass(v_probe<1>, 256, 1 << 20, "probe 256 vec/CTA u1");
     probe_pass(v_probe<2>, 512, 1 << 20, "probe 512 vec/CTA u2");
     probe_pass(v_probe<4>, 1024, 1 << 20, "probe 1024 vec/CTA u4");
