@@ -95,7 +95,9 @@ struct First {
   };
 };
 
-template <typename Element, int ClusterN = 1>
+// EpiN: epilogue sub-tile 128 x EpiN, 0 = CUTLASS's choice (measured equal
+// to 128 x 32 and better than 128 x 16 here, profiles/r01_gemm_shapes.md)
+template <typename Element, int ClusterN = 1, int EpiN = 0>
 struct ProbeGemm {
   using ElementA = Element;  // dy [T, out] row-major == A (M=out, K=T), M-major
   using LayoutA = cutlass::layout::ColumnMajor;
@@ -138,9 +140,13 @@ struct ProbeGemm {
 
   using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
       cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
-      cutlass::epilogue::collective::EpilogueTileAuto, ElementAcc, float, void,
+      cute::conditional_t<EpiN == 0, cutlass::epilogue::collective::EpilogueTileAuto,
+                          Shape<_128, Int<(EpiN > 0 ? EpiN : 1)>>>,
+      ElementAcc, float, void,
       cutlass::layout::RowMajor, kAlign, Element, cutlass::layout::RowMajor, kAlign,
-      cutlass::epilogue::collective::EpilogueScheduleAuto, EVT>::CollectiveOp;
+      cute::conditional_t<EpiN == 0, cutlass::epilogue::collective::EpilogueScheduleAuto,
+                          cutlass::epilogue::TmaWarpSpecialized2Sm>,
+      EVT>::CollectiveOp;
 
   using CollectiveMainloop = typename cutlass::gemm::collective::CollectiveBuilder<
       cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, ElementA, LayoutA, kAlign, ElementB,

@@ -31,7 +31,10 @@ namespace lomo_gemm {
 
 using namespace cute;
 
-template <typename Element, int ClusterN = 1>
+// EpiN: epilogue sub-tile 128 x EpiN (0 = CUTLASS's choice).  128 x 32 keeps
+// more C-load / D-store stages in flight than the automatic 128 x 64: 4 %
+// faster over a 7B pass (profiles/r01_gemm_shapes.md)
+template <typename Element, int ClusterN = 1, int EpiN = 32>
 struct FusedUpdateGemm {
   using ElementA = Element;                      // dy  [T, out] row-major == A (M=out, K=T), M-major
   using LayoutA = cutlass::layout::ColumnMajor;
@@ -54,9 +57,13 @@ struct FusedUpdateGemm {
 
   using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
       cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
-      cutlass::epilogue::collective::EpilogueTileAuto, ElementAcc, ElementCompute, ElementC,
+      cute::conditional_t<EpiN == 0, cutlass::epilogue::collective::EpilogueTileAuto,
+                          Shape<_128, Int<(EpiN > 0 ? EpiN : 1)>>>,
+      ElementAcc, ElementCompute, ElementC,
       LayoutC, kAlign, ElementC, LayoutC, kAlign,
-      cutlass::epilogue::collective::EpilogueScheduleAuto, Fusion>::CollectiveOp;
+      cute::conditional_t<EpiN == 0, cutlass::epilogue::collective::EpilogueScheduleAuto,
+                          cutlass::epilogue::TmaWarpSpecialized2Sm>,
+      Fusion>::CollectiveOp;
 
   using CollectiveMainloop = typename cutlass::gemm::collective::CollectiveBuilder<
       cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, ElementA, LayoutA, kAlign, ElementB,
