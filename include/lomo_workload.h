@@ -34,6 +34,17 @@ int lomo_wl_rmsnorm_bwd(const void* dy, const void* x, const void* w, const floa
                         void* stream);
 int lomo_wl_rmsnorm_partial_rows(int64_t rows);
 
+/* The decoder's residual add fused into the norm that follows it:
+ * hout = round(x + r) (the residual stream), then y = rmsnorm(hout) as above.
+ * The backward's counterpart adds the residual stream's other gradient:
+ * dx = round(round(rmsnorm_bwd) + dres), the sum autograd would form. */
+int lomo_wl_add_rmsnorm_fwd(const void* x, const void* r, const void* w, void* hout, void* y,
+                            float* rstd, int64_t rows, int h, int dtype, float eps,
+                            void* stream);
+int lomo_wl_rmsnorm_bwd_add(const void* dy, const void* x, const void* w, const float* rstd,
+                            const void* dres, void* dx, void* dw, float* partial, int64_t rows,
+                            int h, int dtype, void* stream);
+
 /* Rotary embedding of q and k in [rows = b*s, heads, dh] layout, position
  * = row % seq; cos/sin are [seq, dh] tables in the storage dtype.
  * direction 0: out = x*cos + rotate_half(x)*sin (forward);
@@ -48,6 +59,15 @@ int lomo_wl_rope(const void* q, const void* k, void* qo, void* ko, const void* c
 int lomo_wl_rope_ld(const void* q, const void* k, int64_t ld_in, void* qo, void* ko,
                     int64_t ld_out, const void* cos, const void* sin, int64_t rows, int seq,
                     int heads, int dh, int dtype, int direction, void* stream);
+
+/* The fused-QKV backward in one launch: dq/dk ([batch*seq, heads, dh],
+ * contiguous) through the rotary transpose into dqkv[:, 0:2h], and dv (a
+ * [batch, heads, seq, dh] tensor with element strides dv_stride_b/h/s, dh
+ * contiguous) copied into dqkv[:, 2h:3h]; dqkv is [batch*seq, 3h]. */
+int lomo_wl_qkv_rope_bwd(const void* dq, const void* dk, const void* dv, int64_t dv_stride_b,
+                         int64_t dv_stride_h, int64_t dv_stride_s, void* dqkv, const void* cos,
+                         const void* sin, int64_t batch, int seq, int heads, int dh, int dtype,
+                         void* stream);
 
 /* SwiGLU over a fused gate/up projection gu [rows, 2f] (gate = gu[:, :f],
  * up = gu[:, f:]): out [rows, f] = silu(gate) * up; the backward writes

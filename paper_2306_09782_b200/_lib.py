@@ -64,6 +64,9 @@ WL_EXPORTS = (
     "lomo_wl_rope_ld",
     "lomo_wl_swiglu_gu_fwd",
     "lomo_wl_swiglu_gu_bwd",
+    "lomo_wl_qkv_rope_bwd",
+    "lomo_wl_add_rmsnorm_fwd",
+    "lomo_wl_rmsnorm_bwd_add",
 )
 
 
@@ -148,6 +151,12 @@ _SIGS = {
     "lomo_wl_rope_ld": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32,
                                _i32, _i32, _vp]),
     "lomo_wl_swiglu_gu_fwd": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp]),
+    "lomo_wl_add_rmsnorm_fwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32,
+                                       ctypes.c_float, _vp]),
+    "lomo_wl_rmsnorm_bwd_add": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32,
+                                       _vp]),
+    "lomo_wl_qkv_rope_bwd": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _i32,
+                                    _i32, _i32, _i32, _vp]),
     "lomo_wl_swiglu_gu_bwd": (_i32, [_vp, _vp, _vp, _i64, _i64, _i32, _vp]),
 }
 

@@ -58,10 +58,13 @@ __device__ __forceinline__ float block_sum(float v, float* sm) {
 }
 
 // ---------------------------------------------------------------- RMSNorm
-template <typename T, int kMaxVec>
+// ADD: the residual add of the decoder fused in front, hout = round(x + r)
+// (the same rounding as the separate add), normalised from registers.
+template <typename T, int kMaxVec, bool ADD = false>
 __global__ void __launch_bounds__(kThreads)
     rms_fwd(const T* __restrict__ x, const T* __restrict__ w, T* __restrict__ y,
-            float* __restrict__ rstd, int h, float eps) {
+            float* __restrict__ rstd, int h, float eps, const T* __restrict__ res = nullptr,
+            T* __restrict__ hout = nullptr) {
   __shared__ float sm[kThreads / 32];
   const int nv = h / 8;
   const size_t row = blockIdx.x;
@@ -73,6 +76,13 @@ __global__ void __launch_bounds__(kThreads)
     const int i = threadIdx.x + k * kThreads;
     if (i < nv) {
       X[k].u = ld_nc(xv + i);
+      if (ADD) {
+        Vec8<T> Rv;
+        Rv.u = ld_nc(reinterpret_cast<const uint4*>(res + row * h) + i);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) X[k].e[e] = fromf<T>(tof(X[k].e[e]) + tof(Rv.e[e]));
+        reinterpret_cast<uint4*>(hout + row * h)[i] = X[k].u;
+      }
 #pragma unroll
       for (int e = 0; e < 8; ++e) ss = fmaf(tof(X[k].e[e]), tof(X[k].e[e]), ss);
     }
@@ -120,11 +130,13 @@ __device__ __forceinline__ void block_sum_r(float (&v)[R], float* sm) {  // sm: 
   }
 }
 
-template <typename T, int kMaxVec, int R>
+// ADD: dx = round(round(rms_bwd) + dres) -- the residual stream's two
+// gradient contributions summed as autograd would, without a separate add.
+template <typename T, int kMaxVec, int R, bool ADD = false>
 __global__ void __launch_bounds__(kThreads)
     rms_bwd(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ w,
             const float* __restrict__ rstd, T* __restrict__ dx, float* __restrict__ partial,
-            int64_t rows, int h, int rpc) {
+            int64_t rows, int h, int rpc, const T* __restrict__ dres = nullptr) {
   __shared__ float sm[R * (kThreads / 32)];
   const int nv = h / 8;
   const uint4* wv = reinterpret_cast<const uint4*>(w);
@@ -182,12 +194,14 @@ __global__ void __launch_bounds__(kThreads)
       for (int k = 0; k < kMaxVec; ++k) {
         const int i = threadIdx.x + k * kThreads;
         if (row < r1 && i < nv) {
-          Vec8<T> O;
+          Vec8<T> O, Rg;
+          if (ADD) Rg.u = ld_nc(reinterpret_cast<const uint4*>(dres + row * h) + i);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const float n = tof(X[r][k].e[e]) * rs[r];
             const float dt = rnd<T>(tof(D[r][k].e[e]) * tof(Wt[k].e[e]));
             O.e[e] = fromf<T>(rs[r] * (dt - n * m));
+            if (ADD) O.e[e] = fromf<T>(tof(O.e[e]) + tof(Rg.e[e]));
           }
           reinterpret_cast<uint4*>(dx + row * h)[i] = O.u;
         }
@@ -270,6 +284,59 @@ __global__ void __launch_bounds__(kThreads)
         O1.e[e] = fromf<T>(x1 * c1 + x2 * s2);
         O2.e[e] = fromf<T>(x2 * c2 - x1 * s1);
       }
+    }
+    *reinterpret_cast<uint4*>(dst + gi * 8) = O1.u;
+    *reinterpret_cast<uint4*>(dst + half + gi * 8) = O2.u;
+  }
+}
+
+// The fused-QKV backward in one launch: the rotary transpose of dq/dk
+// (contiguous [rows, heads, dh]) into d(qkv)[:, 0:2h] and the copy of dv
+// (any [b, heads, s, dh] strides with dh contiguous, as SDPA returns it) into
+// d(qkv)[:, 2h:3h].  One thread per 8-element group, as in `rope`.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    qkv_bwd(const T* __restrict__ dq, const T* __restrict__ dk, const T* __restrict__ dv,
+            int64_t vsb, int64_t vsh, int64_t vss, T* __restrict__ dqkv,
+            const T* __restrict__ cs, const T* __restrict__ sn, int64_t rows, int seq, int heads,
+            int dh) {
+  const int half = dh / 2, gph = half / 8, gv = dh / 8;
+  const int64_t per_rot = rows * heads * gph;      // per rotated tensor
+  const int64_t total = 2 * per_rot + rows * heads * gv;
+  const int64_t h = (int64_t)heads * dh, ld = 3 * h;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t >= 2 * per_rot) {  // dv copy
+      const int64_t u = t - 2 * per_rot;
+      const int gi = (int)(u % gv);
+      const int64_t rh = u / gv;
+      const int64_t row = rh / heads, hd = rh % heads;
+      const int64_t b = row / seq, sp = row % seq;
+      const uint4 x = ld_nc(dv + b * vsb + hd * vsh + sp * vss + gi * 8);
+      *reinterpret_cast<uint4*>(dqkv + row * ld + 2 * h + hd * dh + gi * 8) = x;
+      continue;
+    }
+    const bool is_k = t >= per_rot;
+    const int64_t u = is_k ? t - per_rot : t;
+    const int gi = (int)(u % gph);
+    const int64_t rh = u / gph;
+    const int pos = (int)((rh / heads) % seq);
+    const T* src = (is_k ? dk : dq) + rh * dh;
+    T* dst = dqkv + (rh / heads) * ld + (is_k ? h : 0) + (rh % heads) * dh;
+    Vec8<T> X1, X2, C1, C2, S1, S2, O1, O2;
+    X1.u = ld_nc(src + gi * 8);
+    X2.u = ld_nc(src + half + gi * 8);
+    const T* cr = cs + (size_t)pos * dh;
+    const T* sr = sn + (size_t)pos * dh;
+    C1.u = *reinterpret_cast<const uint4*>(cr + gi * 8);
+    C2.u = *reinterpret_cast<const uint4*>(cr + half + gi * 8);
+    S1.u = *reinterpret_cast<const uint4*>(sr + gi * 8);
+    S2.u = *reinterpret_cast<const uint4*>(sr + half + gi * 8);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {  // the transpose of the forward rotation
+      const float x1 = tof(X1.e[e]), x2 = tof(X2.e[e]);
+      O1.e[e] = fromf<T>(x1 * tof(C1.e[e]) + x2 * tof(S2.e[e]));
+      O2.e[e] = fromf<T>(x2 * tof(C2.e[e]) - x1 * tof(S1.e[e]));
     }
     *reinterpret_cast<uint4*>(dst + gi * 8) = O1.u;
     *reinterpret_cast<uint4*>(dst + half + gi * 8) = O2.u;
@@ -395,14 +462,20 @@ inline int status() { return (int)cudaGetLastError(); }
 template <typename T>
 struct RmsFwd {
   static int run(const void* x, const void* w, void* y, float* rstd, int64_t rows, int h,
-                 float eps, cudaStream_t s) {
+                 float eps, const void* res, void* hout, cudaStream_t s) {
     // vectors per thread as a template constant: registers hold the row
+#define WL_RMS_FWD(NV)                                                                       \
+  if (res) rms_fwd<T, NV, true><<<(unsigned)rows, kThreads, 0, s>>>(                         \
+      (const T*)x, (const T*)w, (T*)y, rstd, h, eps, (const T*)res, (T*)hout);               \
+  else rms_fwd<T, NV><<<(unsigned)rows, kThreads, 0, s>>>((const T*)x, (const T*)w, (T*)y, \
+                                                          rstd, h, eps)
     switch ((h / 8 + kThreads - 1) / kThreads) {
-      case 1: rms_fwd<T, 1><<<(unsigned)rows, kThreads, 0, s>>>((const T*)x, (const T*)w, (T*)y, rstd, h, eps); break;
-      case 2: rms_fwd<T, 2><<<(unsigned)rows, kThreads, 0, s>>>((const T*)x, (const T*)w, (T*)y, rstd, h, eps); break;
-      case 3: rms_fwd<T, 3><<<(unsigned)rows, kThreads, 0, s>>>((const T*)x, (const T*)w, (T*)y, rstd, h, eps); break;
-      default: rms_fwd<T, 4><<<(unsigned)rows, kThreads, 0, s>>>((const T*)x, (const T*)w, (T*)y, rstd, h, eps); break;
+      case 1: WL_RMS_FWD(1); break;
+      case 2: WL_RMS_FWD(2); break;
+      case 3: WL_RMS_FWD(3); break;
+      default: WL_RMS_FWD(4); break;
     }
+#undef WL_RMS_FWD
     return status();
   }
 };
@@ -412,12 +485,16 @@ inline int rms_rows_per_cta(int64_t rows) { return (int)((rows + kTargetCtas - 1
 template <typename T>
 struct RmsBwd {
   static int run(const void* dy, const void* x, const void* w, const float* rstd, void* dx,
-                 void* dw, float* partial, int64_t rows, int h, cudaStream_t s) {
+                 void* dw, float* partial, int64_t rows, int h, const void* dres,
+                 cudaStream_t s) {
     const int rpc = rms_rows_per_cta(rows);
     const int nparts = (int)((rows + rpc - 1) / rpc);
 #define WL_RMS_BWD(NV, R)                                                                   \
-  rms_bwd<T, NV, R><<<nparts, kThreads, 0, s>>>((const T*)dy, (const T*)x, (const T*)w, rstd, \
-                                                (T*)dx, partial, rows, h, rpc)
+  if (dres) rms_bwd<T, NV, R, true><<<nparts, kThreads, 0, s>>>(                            \
+      (const T*)dy, (const T*)x, (const T*)w, rstd, (T*)dx, partial, rows, h, rpc,          \
+      (const T*)dres);                                                                      \
+  else rms_bwd<T, NV, R><<<nparts, kThreads, 0, s>>>((const T*)dy, (const T*)x, (const T*)w, \
+                                                     rstd, (T*)dx, partial, rows, h, rpc)
     switch ((h / 8 + kThreads - 1) / kThreads) {  // rows in flight x vectors <= 8
       case 1: WL_RMS_BWD(1, 4); break;
       case 2: WL_RMS_BWD(2, 2); break;
@@ -462,6 +539,19 @@ struct SwigluBwd {
 };
 
 template <typename T>
+struct QkvBwd {
+  static int run(const void* dq, const void* dk, const void* dv, int64_t vsb, int64_t vsh,
+                 int64_t vss, void* dqkv, const void* c, const void* sn, int64_t rows, int seq,
+                 int heads, int dh, cudaStream_t s) {
+    const int64_t work = rows * heads * (2 * (dh / 16) + dh / 8);  // threads of qkv_bwd
+    qkv_bwd<T><<<grid_for(work), kThreads, 0, s>>>((const T*)dq, (const T*)dk, (const T*)dv, vsb,
+                                                   vsh, vss, (T*)dqkv, (const T*)c,
+                                                   (const T*)sn, rows, seq, heads, dh);
+    return status();
+  }
+};
+
+template <typename T>
 struct SwigluGu {
   static int run(const void* a, const void* b, void* c, int64_t rows, int64_t f, int bwd,
                  cudaStream_t s) {
@@ -491,7 +581,21 @@ int lomo_wl_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int6
   if (rows == 0) return 0;
   if (!x || !w || !y || !rstd || !wl::aligned16(x) || !wl::aligned16(w) || !wl::aligned16(y))
     return LOMO_E_ARG;
-  return wl::dispatch<wl::RmsFwd>(dtype, x, w, y, rstd, rows, h, eps, (cudaStream_t)stream);
+  return wl::dispatch<wl::RmsFwd>(dtype, x, w, y, rstd, rows, h, eps, (const void*)nullptr,
+                                  (void*)nullptr, (cudaStream_t)stream);
+}
+
+int lomo_wl_add_rmsnorm_fwd(const void* x, const void* r, const void* w, void* hout, void* y,
+                            float* rstd, int64_t rows, int h, int dtype, float eps,
+                            void* stream) {
+  if (rows < 0 || h <= 0 || h % 8 || h > wl::kThreads * wl::kRmsMaxVec * 8) return LOMO_E_ARG;
+  if (rows == 0) return 0;
+  if (!x || !r || !w || !hout || !y || !rstd) return LOMO_E_ARG;
+  if (!wl::aligned16(x) || !wl::aligned16(r) || !wl::aligned16(w) || !wl::aligned16(hout) ||
+      !wl::aligned16(y))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::RmsFwd>(dtype, x, w, y, rstd, rows, h, eps, r, hout,
+                                  (cudaStream_t)stream);
 }
 
 int lomo_wl_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
@@ -503,6 +607,18 @@ int lomo_wl_rmsnorm_bwd(const void* dy, const void* x, const void* w, const floa
       !wl::aligned16(partial))
     return LOMO_E_ARG;
   return wl::dispatch<wl::RmsBwd>(dtype, dy, x, w, rstd, dx, dw, partial, rows, h,
+                                  (const void*)nullptr, (cudaStream_t)stream);
+}
+
+int lomo_wl_rmsnorm_bwd_add(const void* dy, const void* x, const void* w, const float* rstd,
+                            const void* dres, void* dx, void* dw, float* partial, int64_t rows,
+                            int h, int dtype, void* stream) {
+  if (rows <= 0 || h <= 0 || h % 8 || h > wl::kThreads * wl::kRmsMaxVec * 8) return LOMO_E_ARG;
+  if (!dy || !x || !w || !rstd || !dres || !dx || !dw || !partial) return LOMO_E_ARG;
+  if (!wl::aligned16(dy) || !wl::aligned16(x) || !wl::aligned16(w) || !wl::aligned16(dx) ||
+      !wl::aligned16(dres) || !wl::aligned16(partial))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::RmsBwd>(dtype, dy, x, w, rstd, dx, dw, partial, rows, h, dres,
                                   (cudaStream_t)stream);
 }
 
@@ -534,6 +650,22 @@ int lomo_wl_rope_ld(const void* q, const void* k, int64_t ld_in, void* qo, void*
     return LOMO_E_ARG;
   return wl::dispatch<wl::Rope>(dtype, q, k, qo, ko, cos, sin, rows, seq, heads, dh, direction,
                                 ld_in, ld_out, (cudaStream_t)stream);
+}
+
+int lomo_wl_qkv_rope_bwd(const void* dq, const void* dk, const void* dv, int64_t dv_stride_b,
+                         int64_t dv_stride_h, int64_t dv_stride_s, void* dqkv, const void* cos,
+                         const void* sin, int64_t batch, int seq, int heads, int dh, int dtype,
+                         void* stream) {
+  if (batch < 0 || seq <= 0 || heads <= 0 || dh <= 0 || dh % 16) return LOMO_E_ARG;
+  if (batch == 0) return 0;
+  if (!dq || !dk || !dv || !dqkv || !cos || !sin) return LOMO_E_ARG;
+  if (!wl::aligned16(dq) || !wl::aligned16(dk) || !wl::aligned16(dv) || !wl::aligned16(dqkv) ||
+      !wl::aligned16(cos) || !wl::aligned16(sin))
+    return LOMO_E_ARG;
+  if (dv_stride_b % 8 || dv_stride_h % 8 || dv_stride_s % 8) return LOMO_E_ARG;
+  return wl::dispatch<wl::QkvBwd>(dtype, dq, dk, dv, dv_stride_b, dv_stride_h, dv_stride_s, dqkv,
+                                  cos, sin, batch * (int64_t)seq, seq, heads, dh,
+                                  (cudaStream_t)stream);
 }
 
 int lomo_wl_swiglu_gu_fwd(const void* gu, void* out, int64_t rows, int64_t f, int dtype,

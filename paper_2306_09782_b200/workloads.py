@@ -334,11 +334,14 @@ class _QKVRopeFn(torch.autograd.Function):
         b, s, h, nh, dh = ctx.dims
         dqkv = torch.empty(b, s, 3 * h, dtype=dq.dtype, device=dq.device)
         dq, dk = dq.contiguous(), dk.contiguous()
-        _wl_call(_wl().lomo_wl_rope_ld(dq.data_ptr(), dk.data_ptr(), h, dqkv.data_ptr(),
-                                       dqkv[..., h:].data_ptr(), 3 * h, cos.data_ptr(),
-                                       sin.data_ptr(), b * s, s, nh, dh, _WL_DTYPES[dq.dtype],
-                                       1, _stream()), "lomo_wl_rope_ld")
-        dqkv[..., 2 * h:].view(b, s, nh, dh).copy_(dv.transpose(1, 2))
+        if dv.stride(3) != 1:
+            dv = dv.contiguous()
+        # rotary transpose of dq/dk and the dv copy, all into d(qkv), one launch
+        _wl_call(_wl().lomo_wl_qkv_rope_bwd(dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                                            dv.stride(0), dv.stride(1), dv.stride(2),
+                                            dqkv.data_ptr(), cos.data_ptr(), sin.data_ptr(), b,
+                                            s, nh, dh, _WL_DTYPES[dq.dtype], _stream()),
+                 "lomo_wl_qkv_rope_bwd")
         return dqkv, None, None, None
 
 
@@ -366,6 +369,63 @@ class _SwiGLUGuFn(torch.autograd.Function):
                                              gu.numel() // (2 * f), f, _WL_DTYPES[gu.dtype],
                                              _stream()), "lomo_wl_swiglu_gu_bwd")
         return dgu
+
+
+class _AddRMSNormFn(torch.autograd.Function):
+    """(x, r) -> (h = x + r, y = rmsnorm(h) * w): the decoder's residual add and
+    the norm after it in one kernel each way.  The backward receives the
+    residual stream's gradient dh and the norm output's dy and returns
+    round(round(rms_bwd(dy)) + dh) for both x and r -- what autograd would
+    sum -- from the same kernel (csrc/workload_kernels.cu)."""
+
+    @staticmethod
+    def forward(ctx, x, r, w, eps):
+        hdim = x.shape[-1]
+        rows = x.numel() // hdim
+        h, y = torch.empty_like(x), torch.empty_like(x)
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        _wl_call(_wl().lomo_wl_add_rmsnorm_fwd(x.data_ptr(), r.data_ptr(), w.data_ptr(),
+                                               h.data_ptr(), y.data_ptr(), rstd.data_ptr(), rows,
+                                               hdim, _WL_DTYPES[x.dtype], eps, _stream()),
+                 "lomo_wl_add_rmsnorm_fwd")
+        ctx.save_for_backward(h, w, rstd)
+        return h, y
+
+    @staticmethod
+    def backward(ctx, dh, dy):
+        h, w, rstd = ctx.saved_tensors
+        hdim = h.shape[-1]
+        rows = h.numel() // hdim
+        if dy is None:
+            return dh, dh, None, None
+        dy = dy.contiguous()
+        lib = _wl()
+        dx, dw = torch.empty_like(h), torch.empty_like(w)
+        part = torch.empty(lib.lomo_wl_rmsnorm_partial_rows(rows) * hdim, dtype=torch.float32,
+                           device=h.device)
+        if dh is None:
+            _wl_call(lib.lomo_wl_rmsnorm_bwd(dy.data_ptr(), h.data_ptr(), w.data_ptr(),
+                                             rstd.data_ptr(), dx.data_ptr(), dw.data_ptr(),
+                                             part.data_ptr(), rows, hdim, _WL_DTYPES[h.dtype],
+                                             _stream()), "lomo_wl_rmsnorm_bwd")
+        else:
+            dh = dh.contiguous()
+            _wl_call(lib.lomo_wl_rmsnorm_bwd_add(dy.data_ptr(), h.data_ptr(), w.data_ptr(),
+                                                 rstd.data_ptr(), dh.data_ptr(), dx.data_ptr(),
+                                                 dw.data_ptr(), part.data_ptr(), rows, hdim,
+                                                 _WL_DTYPES[h.dtype], _stream()),
+                     "lomo_wl_rmsnorm_bwd_add")
+        return dx, dx, dw, None
+
+
+def add_rms_norm(x, r, w, eps=RMSNORM_EPS):
+    """(x + r, rmsnorm(x + r) * w); r may be None (no residual pending)."""
+    if r is None:
+        return x, rms_norm(x, w, eps)
+    if _wl_ok(x, r, w) and x.shape[-1] % 8 == 0 and x.shape[-1] <= 8192:
+        return _AddRMSNormFn.apply(x, r, w, eps)
+    h = x + r
+    return h, rms_norm(h, w, eps, fused=False)
 
 
 def rms_norm(x, w, eps=RMSNORM_EPS, fused=True):
@@ -430,10 +490,14 @@ class LlamaLayer(nn.Module):
             self.up = _linear(h, f, dtype, device, std)
         self.down = _linear(f, h, dtype, device, std)
 
-    def _forward_fused(self, x, cos, sin):
+    def forward_res(self, x, pending, cos, sin):
+        """Stacked-projection layer on the residual stream: ``x`` plus the
+        previous layer's not-yet-added MLP output ``pending`` (None for the
+        first layer) -> (residual stream, this layer's MLP output).  Each
+        residual add is fused into the RMSNorm after it."""
         b, s, h = x.shape
         nh, dh = self.nh, h // self.nh
-        a = self.input_layernorm(x)
+        x, a = add_rms_norm(x, pending, self.input_layernorm.weight)
         qkv = rlinear(a, self.qkv)                                  # [b, s, 3h]
         if _wl_ok(qkv, cos, sin) and dh % 16 == 0:
             q, k, v = _QKVRopeFn.apply(qkv, cos, sin, nh)
@@ -443,19 +507,20 @@ class LlamaLayer(nn.Module):
             v = v.reshape(b, s, nh, dh).transpose(1, 2)
         o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v,
                                            is_causal=True)
-        x = x + rlinear(o.transpose(1, 2).reshape(b, s, h), self.o)
-        y = self.post_attention_layernorm(x)
+        x, y = add_rms_norm(x, rlinear(o.transpose(1, 2).reshape(b, s, h), self.o),
+                            self.post_attention_layernorm.weight)
         gu = rlinear(y, self.gate_up)                                # [b, s, 2f]
         if _wl_ok(gu) and gu.shape[-1] % 16 == 0:
             m = _SwiGLUGuFn.apply(gu)
         else:
             f = gu.shape[-1] // 2
             m = F.silu(gu[..., :f]) * gu[..., f:]
-        return x + rlinear(m, self.down)
+        return x, rlinear(m, self.down)
 
     def forward(self, x, cos, sin):
         if self.fused_proj:
-            return self._forward_fused(x, cos, sin)
+            x, mlp = self.forward_res(x, None, cos, sin)
+            return x + mlp
         b, s, h = x.shape
         nh, dh = self.nh, h // self.nh
         fused = self.input_layernorm.fused
@@ -488,6 +553,7 @@ class Llama(nn.Module):
             c["layers"] = layers
         self.cfg = c
         self.checkpointing = checkpointing
+        self.fused_proj = fused_proj
         h, f, v, nh = c["hidden"], c["ffn"], c["vocab"], c["heads"]
         if str(device).startswith("cuda"):
             torch.cuda.manual_seed(seed)
@@ -518,6 +584,16 @@ class Llama(nn.Module):
     def forward(self, ids):
         x = F.embedding(ids, self.embed_tokens)
         cos, sin = self._cos_sin(ids.shape[1], ids.device, x.dtype)
+        if self.fused_proj:  # residual adds fused into the norms (forward_res)
+            pending = None
+            for layer in self.layers:
+                if self.checkpointing and self.training:
+                    x, pending = torch.utils.checkpoint.checkpoint(
+                        layer.forward_res, x, pending, cos, sin, use_reentrant=False)
+                else:
+                    x, pending = layer.forward_res(x, pending, cos, sin)
+            _, y = add_rms_norm(x, pending, self.norm.weight)
+            return rlinear(y, self.lm_head)
         for layer in self.layers:
             if self.checkpointing and self.training:
                 x = torch.utils.checkpoint.checkpoint(layer, x, cos, sin, use_reentrant=False)

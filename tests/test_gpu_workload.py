@@ -213,3 +213,52 @@ def test_lomo_step_on_fused_projections():
     assert abs(oa.last_norm - ob.last_norm) <= 1e-5 * oa.last_norm
     for x, y in zip(a.parameters(), b.parameters()):
         torch.testing.assert_close(x.float(), y.float(), rtol=2 ** -7, atol=1e-6)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("rows,h", [(3, 8), (1024, 4096), (33, 2056)])
+def test_add_rmsnorm_equals_add_then_norm(dtype, rows, h):
+    """The fused residual add + RMSNorm (both directions) is bit-identical to
+    the separate add followed by the fused RMSNorm: same roundings."""
+    x = torch.randn(rows, h, device="cuda").to(dtype)
+    r = torch.randn(rows, h, device="cuda").to(dtype)
+    w = (1 + 0.1 * torch.randn(h, device="cuda")).to(dtype)
+    dh = torch.randn(rows, h, device="cuda").to(dtype)
+    dy = torch.randn(rows, h, device="cuda").to(dtype)
+    xa, ra, wa = (t.clone().requires_grad_() for t in (x, r, w))
+    ha, ya = W._AddRMSNormFn.apply(xa, ra, wa, W.RMSNORM_EPS)
+    torch.autograd.backward((ha, ya), (dh, dy))
+    xb, rb, wb = (t.clone().requires_grad_() for t in (x, r, w))
+    hb = xb + rb
+    yb = W.rms_norm(hb, wb)
+    torch.autograd.backward((hb, yb), (dh, dy))
+    assert torch.equal(ha, hb) and torch.equal(ya, yb)
+    assert torch.equal(xa.grad, xb.grad) and torch.equal(ra.grad, rb.grad)
+    assert torch.equal(wa.grad, wb.grad)
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_fused_decoder_residual_stream_is_exact(dtype):
+    """The stacked-projection decoder threads the residual stream through the
+    fused add+norm kernels; with every layer fused it equals the same layers
+    called one by one (x + layer(x)) bit for bit, and per-layer activation
+    checkpointing of the (x, pending) stream is transparent."""
+    cfg = dict(hidden=256, ffn=688, heads=4, vocab=512, layers=3)
+    m = W.Llama(cfg, dtype=dtype, device="cuda", seed=0, fused_proj=True)
+    mc = W.Llama(cfg, dtype=dtype, device="cuda", seed=0, fused_proj=True, checkpointing=True)
+    d = torch.randint(0, 512, (2, 65), device="cuda")
+    la = m.loss(d[:, :-1], d[:, 1:])
+    la.backward()
+    lc = mc.loss(d[:, :-1], d[:, 1:])
+    lc.backward()
+    assert la.item() == lc.item()
+    for p, q in zip(m.parameters(), mc.parameters()):
+        assert torch.equal(p.grad, q.grad)
+    # the unfused residual decomposition of the same model
+    with torch.no_grad():
+        x = torch.nn.functional.embedding(d[:, :-1], m.embed_tokens)
+        cos, sin = m._cos_sin(64, x.device, x.dtype)
+        for layer in m.layers:
+            x = layer(x, cos, sin)
+        ref = W.rlinear(W.rms_norm(x, m.norm.weight), m.lm_head)
+        assert torch.equal(m(d[:, :-1]), ref)
