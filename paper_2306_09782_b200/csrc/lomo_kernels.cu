@@ -233,6 +233,17 @@ __device__ __forceinline__ void pdl_enter() {
   pdl_launch_dependents();
 }
 
+// Bulk L2 prefetch (TMA unit; 16-byte aligned, multiple of 16 bytes).  Issued
+// BEFORE griddepcontrol.wait: a PDL-launched CTA becomes resident while the
+// previous grid drains, and its tile's DRAM fetch then overlaps that drain.
+// Memory-model safe: it only fills L2, the point of coherence -- a line the
+// previous grid is still writing is updated in L2 by that write, and the
+// real loads come after the wait (and bypass L1).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes)
+                          : "memory");
+}
+
 // Step-state scalars (skip, 1/scale, clip coefficient, lr).  Kernels issue
 // their data loads BEFORE calling this: the loads do not depend on the
 // state, so the state read's L2 latency overlaps them.  Reading the state
@@ -289,9 +300,10 @@ __global__ void __launch_bounds__(kThreads)
     k1_update(T* __restrict__ p, const T* __restrict__ g, int64_t n, int head,
               int64_t nvec, UpdArgs<M> a, unsigned flags, const lomo_state* st) {
   constexpr int V = 16 / sizeof(T);
-  pdl_enter();
   uint4* pv = reinterpret_cast<uint4*>(p + head);
   const uint4* gv = reinterpret_cast<const uint4*>(g + head);
+  // (no L2 prefetch here, unlike K2: with 4 KB tiles it measured 5 % slower)
+  pdl_enter();
   const int64_t base = (int64_t)blockIdx.x * (kThreads * kK1Vec) + threadIdx.x;
   uint4 P[kK1Vec], G[kK1Vec];
 #pragma unroll
@@ -473,6 +485,11 @@ __global__ void __launch_bounds__(kThreads, 5)  // 48 registers: 5 CTAs per SM, 
              int slot, unsigned flags, void* state) {
   constexpr int V = 16 / sizeof(T);
   __shared__ double sm[kThreads / 32];
+  if (threadIdx.x == 0) {  // this CTA's tile into L2 while the previous grid drains
+    const int64_t b0 = (int64_t)blockIdx.x * per_cta;
+    const int64_t nt = min(per_cta, nvec - b0);
+    if (nt > 0) prefetch_l2(reinterpret_cast<const uint4*>(g + head) + b0, (uint32_t)(nt * 16));
+  }
   pdl_wait();
   pdl_launch_dependents();
   lomo_state* st = hdr(state);
