@@ -449,7 +449,7 @@ class LOMO(_Protocol):
         _lib.check(rc, "lomo_gemm_update")
         return True
 
-    def _gemm_probe(self, w, x, dy) -> bool:
+    def _gemm_probe(self, wid: int, w, x, dy) -> bool:
         """K6 (from the linear's backward in pass 1): probe dW = dy^T x on the
         tensor cores into w's norm slot.  False when the shape/dtype is not
         supported -- the caller then returns dW to autograd and K2 probes it."""
@@ -467,13 +467,13 @@ class LOMO(_Protocol):
         need = lib.lomo_gemm_probe_workspace(out_f, in_f, dy2.shape[0], dt)
         if need == 0:
             return False
-        ws = self._pws.get(id(w))
+        ws = self._pws.get(wid)
         if ws is None or ws.numel() < need:
-            ws = self._pws[id(w)] = torch.empty(need, dtype=torch.uint8, device=w.device)
+            ws = self._pws[wid] = torch.empty(need, dtype=torch.uint8, device=w.device)
         n = w.numel()
         if self._gscratch is None or self._gscratch.numel() < n or self._gscratch.dtype != w.dtype:
             self._gscratch = torch.empty(n, dtype=w.dtype, device=w.device)
-        slot = self._slot[id(w)]
+        slot = self._slot[wid]
         stream = self.engine.stream()
         if self.probe_stream:
             # beside the rest of the backward: x/dy stay alive in the stash and

@@ -30,7 +30,9 @@ class ReplayStash:
         self.grads: dict[int, torch.Tensor] = {}
         self.shared: set[int] = set()   # weights that fed more than one linear
         # pass-1 probe fused into the weight-gradient GEMM (K6): called as
-        # probe(w, x, dy) -> bool from the linear's backward; True means the
+        # probe(weight id, w, x, dy) -> bool from the linear's backward (under
+        # activation checkpointing the saved `w` is not the Parameter object
+        # itself, so the id recorded at forward time names it); True means the
         # gradient was probed on the tensor cores and is not returned to autograd
         self.probe = None
         self.probed: set[int] = set()
@@ -71,7 +73,7 @@ class _StashLinear(torch.autograd.Function):
             st.linear[ctx.wid] = (x, dy)
         if ctx.needs_input_grad[1]:
             if st is not None and st.probe is not None and ctx.wid not in st.shared \
-                    and st.probe(w, x, dy):
+                    and st.probe(ctx.wid, w, x, dy):
                 st.probed.add(ctx.wid)   # K6 probed dW: nothing for autograd to deliver
             else:
                 dw = weight_grad(x, dy)

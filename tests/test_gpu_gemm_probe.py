@@ -234,3 +234,27 @@ def test_gemm_probe_deferred_rows_match_immediate():
         (ctypes.c_int64 * n)(*[s[1] for s in shapes]),
         (ctypes.c_int * n)(*range(n)), n, U.CODE[dt], b.ptr, U.stream()) == 0
     assert np.array_equal(a.slots(n), b.slots(n))
+
+
+@pytest.mark.parametrize("fused_proj", [False, True])
+def test_k6_k5_step_with_activation_checkpointing(fused_proj):
+    """Config 5's setting: per-layer activation checkpointing under the
+    replay + K6/K5 step (the recomputed forward re-saves the weights, so the
+    probe must name them by their forward-time id) -- bit-identical to the
+    same step without checkpointing."""
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=128, layers=3, heads=4, ffn=256, vocab=256)
+    a = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=fused_proj)
+    b = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=fused_proj,
+              checkpointing=True)
+    kw = dict(lr=0.05, clip_grad_norm=0.3, loss_scale=2.0 ** 8, replay=True, fuse_gemm=True)
+    oa, ob = LOMO(a, **kw), LOMO(b, **kw)
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    for _ in range(2):
+        d = torch.randint(0, 256, (2, 65), device="cuda", generator=gen)
+        la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+        lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+        assert la == lb and oa.last_norm == ob.last_norm
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)
