@@ -459,7 +459,8 @@ def bench_train(args, rank, world):
            "clip_grad_norm": 1.0, "activation_checkpointing": bool(ckpt),
            "paper_tgs_rtx3090": 769.92}
     gstep = None
-    variants = ("strict", "replay", "replay_fused_gemm", "replay_fused_gemm_graph", "grouped") \
+    variants = ("strict", "strict_fused_gemm", "replay", "replay_fused_gemm",
+                "replay_fused_gemm_graph", "grouped") \
         if not args.train_variants else \
         tuple(args.train_variants.split(","))
     for key in variants:
@@ -482,7 +483,8 @@ def bench_train(args, rank, world):
         else:
             opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
                        loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
-                       replay=key.startswith("replay"), fuse_gemm=key == "replay_fused_gemm")
+                       replay=key.startswith("replay"),
+                       fuse_gemm=key in ("replay_fused_gemm", "strict_fused_gemm"))
 
         if key != "replay_fused_gemm_graph":
             def step(k, opt=opt):

@@ -179,6 +179,12 @@ class _Protocol:
             self._after_update()
             self.last_outcome = StepOutcome.APPLIED
             return
+        if getattr(self, "_fused_update", False) and not bool(torch.isfinite(loss.detach()).all()):
+            # K5 applies p <- alpha*acc + beta*p: a skip (alpha = 0) would still
+            # turn a non-finite accumulator into NaN, so the non-finite-loss
+            # check runs on the host here, as the reference's does (optim.py:63-65)
+            self.last_outcome = None
+            raise NonFiniteLossError(f"loss is non-finite ({float(loss.detach())}); step aborted")
         self.engine.begin(self._check_loss(loss))
         self.engine.configure(lr, self.clip_value, self.weight_decay, flags)
         self._run_backward(loss, _UPDATE, False)
@@ -308,17 +314,20 @@ class LOMO(_Protocol):
         self._stash = ReplayStash() if replay else None
         self._replay_checked = False
         self._replay_mismatch: list = []
-        if fuse_gemm and not replay:
-            raise ConfigError("fuse_gemm fuses the update into the replayed weight-gradient GEMM: "
-                              "it needs replay=True")
         self.fuse_gemm = bool(fuse_gemm) and self.clip_value == 0.0
-        if fuse_probe and not replay:
-            raise ConfigError("fuse_probe fuses the pass-1 probe into the weight-gradient GEMM: "
-                              "it needs replay=True")
-        self.fuse_probe = bool(fuse_gemm if fuse_probe is None else fuse_probe) and replay \
-            and math == "f32"
-        if self.fuse_probe:
-            self._stash.probe = self._gemm_probe
+        if fuse_probe and self.passes != 2:
+            raise ConfigError("fuse_probe fuses pass 1's probe into the weight-gradient GEMM: "
+                              "it needs the two-pass protocol (clip_grad_norm / loss_scale)")
+        self.fuse_probe = bool(fuse_gemm if fuse_probe is None else fuse_probe) \
+            and self.passes == 2 and math == "f32"
+        # the linears' backward context: the replay stash, or (no replay) just
+        # the fused-GEMM callbacks -- K6 in pass 1, and K5 inside the update
+        # backward (the single fused pass, or the strict second backward)
+        self._fused_update = self.fuse_gemm and not replay
+        self._lin = self._stash if replay else (
+            ReplayStash(keep=False) if (self.fuse_probe or self._fused_update) else None)
+        self._by_id = {id(p): p for p in uniq}
+        self._coefs = None
         self._pws = {}         # K6 workspace per weight (its partial sums stay until
                                # the end of pass 1: one deferred reduction launch)
         self._pending_probe = []  # (workspace ptr, out, in, slot) awaiting that launch
@@ -352,13 +361,14 @@ class LOMO(_Protocol):
             g = g.contiguous()
         if mode == _PROBE:
             self.engine.probe(g, self._slot[id(p)])
-            st = self._stash
-            if st is not None:
-                if id(p) in st.probed:
-                    # K6 already probed this weight's linear: a hook means another
-                    # op contributed gradient too (tied weight), which replay drops
-                    self._replay_mismatch.append(tuple(p.shape))
-                elif id(p) not in st.linear:
+            lin, st = self._lin, self._stash
+            if lin is not None and id(p) in lin.probed:
+                # K6 already probed this weight's linear: a hook means another
+                # op contributed gradient too (tied weight), which the fused
+                # paths cannot fold into the norm or the update
+                self._replay_mismatch.append(tuple(p.shape))
+            elif st is not None:
+                if id(p) not in st.linear:
                     st.grads[id(p)] = g  # not a replayable linear: keep its gradient
                 elif not self._replay_checked:
                     # first step: the replayed dW must BE the whole gradient
@@ -371,6 +381,11 @@ class LOMO(_Protocol):
                                                           .all()):
                         self._replay_mismatch.append(tuple(p.shape))
         else:
+            lin = self._lin
+            if lin is not None and id(p) in lin.updated:
+                # K5 already applied this weight's linear gradient in place; a
+                # hook means another op fed it too (tied weight)
+                self._replay_mismatch.append(tuple(p.shape))
             self.engine.update(p, g)
         self.hook_calls += 1
         p.grad = None  # CONSUME: the caching allocator reuses the block stream-ordered
@@ -381,19 +396,39 @@ class LOMO(_Protocol):
                 raise TapeStateError("a parameter already holds a gradient; LOMO consumes "
                                      "gradients inside backward (call zero_grad(set_to_none=True))")
         self._mode = mode
-        stash = self._stash if (mode == _PROBE and self._stash is not None) else None
-        if stash is not None:
-            stash.clear()
-            _replay._ACTIVE = stash
-            retain_graph = False  # pass 2 replays from the stash, not from the graph
+        lin = self._lin
+        if lin is not None and not (
+                (mode == _PROBE and (lin.keep or self.fuse_probe)) or
+                (mode == _UPDATE and self._fused_update)):
+            lin = None
+        stash = lin if (lin is not None and lin.keep) else None
+        if lin is not None:
+            lin.clear()
+            lin.probe = self._gemm_probe if (mode == _PROBE and self.fuse_probe) else None
+            lin.update = self._gemm_update_bw if mode == _UPDATE else None
+            if mode == _UPDATE:
+                self._load_coefs()
+            _replay._ACTIVE = lin
+            if stash is not None:
+                retain_graph = False  # pass 2 replays from the stash, not from the graph
         try:
             target.backward(retain_graph=retain_graph)
         finally:
             self._mode = 0
-            if stash is not None:
+            if lin is not None:
                 _replay._ACTIVE = None
             self._finish_probes()  # deferred K6 partial sums -> their slots
             self.engine.flush()  # the parked tiny tensors, same stream as the hooks
+        if lin is not None and stash is None:
+            bad = None
+            if lin.shared:
+                bad = f"fuse_gemm: {len(lin.shared)} weight(s) feed more than one linear"
+            elif self._replay_mismatch:
+                bad = (f"fuse_gemm: weights {self._replay_mismatch[:3]} receive gradient from "
+                       "ops other than their linear (tied weights?)")
+            if bad is not None:
+                self._replay_mismatch = []
+                raise ConfigError(bad)
         if stash is not None:
             kept = sum(g.numel() * g.element_size() for g in stash.grads.values())
             bad = None
@@ -491,6 +526,26 @@ class LOMO(_Protocol):
             return False
         _lib.check(rc, "lomo_gemm_probe")
         self._pending_probe.append((ws.data_ptr(), out_f, in_f, slot, dt))
+        self.hook_calls += 1
+        return True
+
+    def _load_coefs(self) -> None:
+        """K5-in-backward constants on device: alpha = -lr*coef/scale (0 on a
+        skipped step), beta = 1 - lr*wd, from the step state (lomo_update_coefs)."""
+        eng = self.engine
+        if self._coefs is None:
+            self._coefs = torch.zeros(2, dtype=torch.float32, device=self.device)
+        d = eng.dispatch
+        _lib.check(eng.lib.lomo_set_lr(eng.ptr, d.lr, eng.stream()), "lomo_set_lr")
+        _lib.check(eng.lib.lomo_update_coefs(eng.ptr, self.weight_decay, d.flags,
+                                             self._coefs.data_ptr(), eng.stream()),
+                   "lomo_update_coefs")
+
+    def _gemm_update_bw(self, wid: int, w, x, dy) -> bool:
+        """K5 from inside the update backward: the weight's update applied as
+        the epilogue of its weight-gradient GEMM (alpha/beta from device)."""
+        if not self._gemm_update(self._by_id[wid], x, dy, 0.0, coefs=self._coefs):
+            return False
         self.hook_calls += 1
         return True
 

@@ -25,9 +25,16 @@ _ACTIVE: "ReplayStash | None" = None
 
 
 class ReplayStash:
-    def __init__(self):
+    """What the linears' backward consults while a LOMO pass is active.
+
+    ``keep``: stash each linear's (x, dy) for pass-2 replay (``replay=True``);
+    without it the object only carries the fused-GEMM callbacks."""
+
+    def __init__(self, keep: bool = True):
+        self.keep = keep
         self.linear: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
         self.grads: dict[int, torch.Tensor] = {}
+        self.seen: set[int] = set()     # weights whose linear backward ran this pass
         self.shared: set[int] = set()   # weights that fed more than one linear
         # pass-1 probe fused into the weight-gradient GEMM (K6): called as
         # probe(weight id, w, x, dy) -> bool from the linear's backward (under
@@ -36,12 +43,19 @@ class ReplayStash:
         # gradient was probed on the tensor cores and is not returned to autograd
         self.probe = None
         self.probed: set[int] = set()
+        # the update fused into the weight-gradient GEMM inside the backward
+        # (K5, single pass or the strict second backward): update(weight id,
+        # w, x, dy) -> bool, True when the weight was updated in place
+        self.update = None
+        self.updated: set[int] = set()
 
     def clear(self):
         self.linear.clear()
         self.grads.clear()
+        self.seen.clear()
         self.shared.clear()
         self.probed.clear()
+        self.updated.clear()
 
     def nbytes(self) -> int:
         n = sum(x.numel() * x.element_size() + d.numel() * d.element_size()
@@ -68,13 +82,19 @@ class _StashLinear(torch.autograd.Function):
         st = _ACTIVE
         dw = None
         if st is not None:
-            if ctx.wid in st.linear:
+            if ctx.wid in st.seen:
                 st.shared.add(ctx.wid)
-            st.linear[ctx.wid] = (x, dy)
+            st.seen.add(ctx.wid)
+            if st.keep:
+                st.linear[ctx.wid] = (x, dy)
         if ctx.needs_input_grad[1]:
-            if st is not None and st.probe is not None and ctx.wid not in st.shared \
+            # dx above was enqueued first: it reads w before an in-place update
+            if st is not None and ctx.wid not in st.shared and st.probe is not None \
                     and st.probe(ctx.wid, w, x, dy):
                 st.probed.add(ctx.wid)   # K6 probed dW: nothing for autograd to deliver
+            elif st is not None and ctx.wid not in st.shared and st.update is not None \
+                    and st.update(ctx.wid, w, x, dy):
+                st.updated.add(ctx.wid)  # K5 applied the update: dW never existed
             else:
                 dw = weight_grad(x, dy)
         return dx, dw

@@ -258,3 +258,81 @@ def test_k6_k5_step_with_activation_checkpointing(fused_proj):
         assert la == lb and oa.last_norm == ob.last_norm
     for x, y in zip(a.parameters(), b.parameters()):
         assert torch.equal(x, y)
+
+
+# --- the fused update inside the backward, no replay (single pass / strict) -----------
+
+def test_single_pass_fused_update_matches_k1():
+    """LOMO's single fused pass (no clip, no scaler) with K5 in each linear's
+    backward -- the gradient never exists -- against the hook + K1 pass:
+    same losses, parameters equal up to K1's extra rounding of dW; no weight
+    ever holds .grad."""
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
+    a = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    b = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    oa, ob = LOMO(a, lr=0.05), LOMO(b, lr=0.05, fuse_gemm=True)
+    assert ob._fused_update and not oa._fused_update
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    for step in range(3):
+        p0 = [p.detach().float().clone() for p in a.parameters()]
+        d = torch.randint(0, 256, (2, 65), device="cuda", generator=gen)
+        la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+        lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+        assert abs(la - lb) <= 1e-2 * abs(la)
+        assert all(p.grad is None for p in b.parameters())
+        # one step from identical parameters: K1 rounds dW to bf16 before the
+        # update, K5 applies the fp32 accumulator, so they differ by up to
+        # 2^-7 of the update plus one bf16 ulp of the result (stated tolerance)
+        for x, y, q in zip(a.parameters(), b.parameters(), p0):
+            xf, yf = x.detach().float(), y.detach().float()
+            tol = 2 ** -7 * torch.maximum(xf.abs(), yf.abs()) + 2 ** -7 * (xf - q).abs() + 1e-9
+            assert ((xf - yf).abs() <= tol).all(), (step, ((xf - yf).abs() / tol).max().item())
+        with torch.no_grad():            # realign: the next step starts from equal weights
+            for x, y in zip(a.parameters(), b.parameters()):
+                y.copy_(x)
+
+
+def test_single_pass_fused_update_nonfinite_loss_untouched():
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.errors import NonFiniteLossError
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=128, layers=1, heads=4, ffn=256, vocab=256)
+    m = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    opt = LOMO(m, lr=0.05, fuse_gemm=True)
+    before = [p.detach().clone() for p in m.parameters()]
+    d = torch.randint(0, 256, (2, 33), device="cuda")
+    with pytest.raises(NonFiniteLossError):
+        opt.step(lambda: m.loss(d[:, :-1], d[:, 1:]) * float("nan"), 0.05)
+    assert all(torch.equal(x, y) for x, y in zip(before, m.parameters()))
+
+
+@pytest.mark.parametrize("scaler_overflow", [False, True])
+def test_strict_two_pass_fused_matches_replay(scaler_overflow):
+    """The reference's two-pass protocol as is (pass 2 = a second backward, no
+    stash) with K6 in pass 1 and K5 in pass 2: decisions equal to the replay
+    step's, parameters equal to its within the nondeterminism of the second
+    backward's attention kernels; a skipped step leaves them untouched."""
+    from paper_2306_09782_b200 import LOMO, LossScaler
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
+    dt = torch.float16
+    a = Llama(cfg, dtype=dt, device="cuda", seed=0, fused_proj=True)
+    b = Llama(cfg, dtype=dt, device="cuda", seed=0, fused_proj=True)
+    sc = (lambda: LossScaler(2.0 ** 24)) if scaler_overflow else (lambda: LossScaler(2.0 ** 12))
+    oa = LOMO(a, lr=0.05, clip_grad_norm=0.5, loss_scale=sc(), replay=True, fuse_gemm=True)
+    ob = LOMO(b, lr=0.05, clip_grad_norm=0.5, loss_scale=sc(), fuse_gemm=True)
+    assert ob._fused_update and ob.fuse_probe and ob._stash is None
+    gen = torch.Generator(device="cuda").manual_seed(6)
+    for _ in range(3):
+        d = torch.randint(0, 256, (2, 65), device="cuda", generator=gen)
+        before = [p.detach().clone() for p in b.parameters()]
+        oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+        ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+        assert oa.last_outcome == ob.last_outcome
+        if ob.last_outcome.value != "applied":
+            assert all(torch.equal(x, y) for x, y in zip(before, b.parameters()))
+    assert oa.loss_scale == ob.loss_scale
+    for x, y in zip(a.parameters(), b.parameters()):
+        torch.testing.assert_close(x.float(), y.float(), rtol=2 ** -8, atol=1e-4)
