@@ -423,14 +423,16 @@ def bench_e2e(args, rank, world):
 def bench_train(args, rank, world):
     """Config 3: LLaMA-7B fp16 LOMO, dynamic loss scale + two-pass clip.
 
-    Timed three ways on the same model (successive runs continue training it):
+    Timed several ways on the same model (successive runs continue training it):
     ``strict`` -- the reference protocol, pass 2 is a second backward over the
     retained graph, each hook launches on the autograd stream, one gradient
-    alive; ``replay`` -- pass 2 recomputes each weight gradient from the
+    alive; ``strict_fused_gemm`` -- the same protocol with each linear's probe
+    (K6, pass 1) and update (K5, pass 2) fused into its weight-gradient GEMM
+    inside the backward: no gradient materialised and no stash;
+    ``replay`` -- pass 2 recomputes each weight gradient from the
     (input, output-gradient) pairs stashed in pass 1 (replay.py) and feeds K1
-    without a second backward; ``replay_fused_gemm`` -- replay with each
-    linear's update fused into its weight-gradient GEMM on the tensor cores
-    (K5), so pass 2 never materialises a gradient; ``replay_fused_gemm_graph``
+    without a second backward; ``replay_fused_gemm`` -- replay with K6 in
+    pass 1 and K5 in pass 2; ``replay_fused_gemm_graph``
     -- the same step captured into two CUDA graphs around the host decision
     (graphs.py); ``grouped`` -- the paper's
     single-pass alternative (per-layer norm clip, GroupedLOMO), reported beside
