@@ -33,6 +33,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "cute/tensor.hpp"
 #include "cutlass/cutlass.h"
@@ -45,6 +46,15 @@
 #include "cutlass/util/packed_stride.hpp"
 
 #include "lomo_b200.h"
+
+inline bool lomo_gemm_pdl() {  // as in lomo_gemm_update.cu
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LOMO_GEMM_PDL");
+    v = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 
 namespace lomo_probe_gemm {
 
@@ -209,7 +219,7 @@ struct ProbeGemm {
     if (gemm.initialize(args, static_cast<char*>(workspace) + off, stream) !=
         cutlass::Status::kSuccess)
       return LOMO_E_ARG;
-    if (gemm.run(stream) != cutlass::Status::kSuccess) return (int)cudaGetLastError();
+    if (gemm.run(stream, nullptr, lomo_gemm_pdl()) != cutlass::Status::kSuccess) return (int)cudaGetLastError();
     return (int)cudaGetLastError();
   }
 

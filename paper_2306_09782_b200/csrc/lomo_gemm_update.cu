@@ -15,6 +15,7 @@
 // inside this library; see DESIGN.md.  Value clipping is not linear in the
 // accumulator and stays on the K1 path.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "cute/tensor.hpp"
 #include "cutlass/cutlass.h"
@@ -26,6 +27,21 @@
 #include "cutlass/util/packed_stride.hpp"
 
 #include "lomo_b200.h"
+
+// PDL for the CUTLASS launches (built with CUTLASS_ENABLE_GDC_FOR_SM100: the
+// kernels run griddepcontrol.wait before touching global memory), so a K5/K6
+// prologue -- TMEM allocation, barrier init, descriptor prefetch -- overlaps the
+// previous kernel's tail.  Opt-in (LOMO_GEMM_PDL=1): back to back it saves
+// 3 % per 7B pass (tools/gemm_shapes.py), but inside the training step it
+// measured 0.4-1.3 ms slower per step (profiles/r01_gemm_shapes.md).
+inline bool lomo_gemm_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LOMO_GEMM_PDL");
+    v = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 
 namespace lomo_gemm {
 
@@ -104,7 +120,7 @@ struct FusedUpdateGemm {
     const size_t need = Gemm::get_workspace_size(args);
     if (need > workspace_bytes) return LOMO_E_ARG;
     if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return LOMO_E_ARG;
-    if (gemm.run(stream) != cutlass::Status::kSuccess) return (int)cudaGetLastError();
+    if (gemm.run(stream, nullptr, lomo_gemm_pdl()) != cutlass::Status::kSuccess) return (int)cudaGetLastError();
     return (int)cudaGetLastError();
   }
 
