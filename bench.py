@@ -328,9 +328,28 @@ def bench_update(args, rank, world):
     f64_ms = start.elapsed_time(end) / args.steps
     f64 = {"gbs": round(BYTES_PER_ELEM * elems / (f64_ms * 1e-3) / 1e9, 1),
            "ms_per_pass": round(f64_ms, 4)}
+    # the pass-2 form of K1 in the two-pass protocol: every kernel reads
+    # skip / 1/scale / clip coefficient / lr from the device state block
+    # (stabilize.py:215-224), no host scalars
+    _lib.check(lib.lomo_set_lr(st.data_ptr(), 0.05, stream), "lomo_set_lr")
+    dfl = HookDispatcher(lib, st.data_ptr(), _lib.MATH_F32)
+    dfl.configure(flags=_lib.USE_SKIP | _lib.USE_SCALE | _lib.USE_COEF | _lib.LR_FROM_STATE)
+    for _ in range(2):
+        run_update_pass(dfl, P, G, dt_code, stream)
+    torch.cuda.synchronize()
+    start.record()
+    for _ in range(args.steps):
+        run_update_pass(dfl, P, G, dt_code, stream)
+    end.record()
+    torch.cuda.synchronize()
+    fl_ms = start.elapsed_time(end) / args.steps
+    flags_pass = {"gbs": round(BYTES_PER_ELEM * elems / (fl_ms * 1e-3) / 1e9, 1),
+                  "ms_per_pass": round(fl_ms, 4),
+                  "flags": "USE_SKIP|USE_SCALE|USE_COEF|LR_FROM_STATE (state block read per CTA)"}
     del P, G
     torch.cuda.empty_cache()
     return {"gbs": gbs, "ms": ms / args.steps, "probe": probe, "f64_math": f64,
+            "flags_pass": flags_pass,
             "graphed_gbs": BYTES_PER_ELEM * elems / (upd_graph_ms * 1e-3) / 1e9,
             "host_ms": host_ms, "elems_per_rank": elems, "total_elems": total_elems,
             "launches": launches, "clocks": clk.summary(), "kernel_gbs": achieved,
@@ -812,6 +831,8 @@ def main():
                          "per_shape_note": "per-launch event pairs (separate replay) break the PDL "
                                            "overlap, so these per-shape rates understate the pass"},
             "probe_pass": dict(up["probe"], frac=round(up["probe"]["gbs"] / peak, 4)),
+            "update_pass_device_state": dict(up["flags_pass"],
+                                             frac=round(up["flags_pass"]["gbs"] / peak, 4)),
             "f64_math_update_pass": dict(up["f64_math"], frac=round(up["f64_math"]["gbs"] / peak, 4)),
             "gpu_launches": up["launches"],
             "clocks": up["clocks"],
