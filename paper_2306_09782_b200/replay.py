@@ -100,6 +100,51 @@ class _StashLinear(torch.autograd.Function):
         return dx, dw
 
 
+class _StashLinearIO(torch.autograd.Function):
+    """y = x @ W for a weight stored [in, out] (the reference zoo's layout,
+    ops.py:58-75).  dW = x^T dy is the same GEMM as the [out, in] case with
+    the operands' roles swapped, so stash and callbacks receive (dy, x) in
+    place of (x, dy): ``weight_grad(dy, x)`` = x^T dy, and the fused kernels'
+    out x in problem is W's own [in, out] shape."""
+
+    @staticmethod
+    def forward(ctx, x, w):
+        ctx.save_for_backward(x, w)
+        ctx.wid = id(w)
+        return x.matmul(w)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, w = ctx.saved_tensors
+        dx = dy.matmul(w.t()) if ctx.needs_input_grad[0] else None
+        st = _ACTIVE
+        dw = None
+        if st is not None:
+            if ctx.wid in st.seen:
+                st.shared.add(ctx.wid)
+            st.seen.add(ctx.wid)
+            if st.keep:
+                st.linear[ctx.wid] = (dy, x)
+        if ctx.needs_input_grad[1]:
+            if st is not None and ctx.wid not in st.shared and st.probe is not None \
+                    and st.probe(ctx.wid, w, dy, x):
+                st.probed.add(ctx.wid)
+            elif st is not None and ctx.wid not in st.shared and st.update is not None \
+                    and st.update(ctx.wid, w, dy, x):
+                st.updated.add(ctx.wid)
+            else:
+                dw = weight_grad(dy, x)
+        return dx, dw
+
+
+def matmul_in_out(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """``x @ w`` for a weight stored [in, out], with the same stash/fused-GEMM
+    backward as :func:`linear`."""
+    if torch.is_grad_enabled() and w.requires_grad:
+        return _StashLinearIO.apply(x, w)
+    return x.matmul(w)
+
+
 def linear(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     """``F.linear(x, w)`` whose backward can stash (x, dy) for pass-2 replay."""
     if torch.is_grad_enabled() and w.requires_grad:

@@ -30,6 +30,7 @@ import torch.nn as nn
 import torch.nn.functional as F
 
 from .replay import linear as rlinear
+from .replay import matmul_in_out as _mm_in_out
 
 INIT_RANGE = 0.08   # zoo.py:26
 RMSNORM_EPS = 1e-5  # zoo.py:27
@@ -104,10 +105,14 @@ class MiniTransformer(nn.Module):
 
     def __init__(self, cfg: MiniConfig, dtype: torch.dtype = torch.float32,
                  device: str | torch.device = "cuda",
-                 init: list[tuple[str, np.ndarray]] | None = None):
+                 init: list[tuple[str, np.ndarray]] | None = None,
+                 fused_linear: bool = False):
         super().__init__()
         self.cfg = cfg
         self.dtype = dtype
+        # route every x @ W through replay.matmul_in_out, so LOMO's replay /
+        # fused-GEMM paths (K6, K5) apply to the reference's own model
+        self._mm = _mm_in_out if fused_linear else torch.matmul
         init = init if init is not None else mini_transformer_init(cfg)
         self._names = []
         for name, arr in init:
@@ -148,19 +153,19 @@ class MiniTransformer(nn.Module):
             a = self._rmsnorm(x, self.param(f"{pre}.attn_norm.scale"))
             heads = []
             for nm in ("q", "k", "v"):
-                y = a @ self.param(f"{pre}.attn.{nm}_proj")
+                y = self._mm(a, self.param(f"{pre}.attn.{nm}_proj"))
                 heads.append(y.view(b, s, nh, dh).transpose(1, 2))
             q, k, v = heads
             scores = _op((q @ k.transpose(-1, -2)).to(self.inner) * (1.0 / math.sqrt(dh)), dt)
             probs = _op(torch.softmax(scores.to(self.inner), dim=-1), dt)
             ctx = (probs @ v).transpose(1, 2).reshape(b, s, h)
-            x = x + ctx @ self.param(f"{pre}.attn.out_proj")
+            x = x + self._mm(ctx, self.param(f"{pre}.attn.out_proj"))
             y = self._rmsnorm(x, self.param(f"{pre}.ffn_norm.scale"))
-            gated = self._gelu(y @ self.param(f"{pre}.ffn.gate_proj")) * \
-                (y @ self.param(f"{pre}.ffn.up_proj"))
-            x = x + gated @ self.param(f"{pre}.ffn.down_proj")
+            gated = self._gelu(self._mm(y, self.param(f"{pre}.ffn.gate_proj"))) * \
+                self._mm(y, self.param(f"{pre}.ffn.up_proj"))
+            x = x + self._mm(gated, self.param(f"{pre}.ffn.down_proj"))
         xf = self._rmsnorm(x, self.param("final_norm.scale"))
-        return xf @ self.param("head.weight")
+        return self._mm(xf, self.param("head.weight"))
 
 
 def mean_cross_entropy(logits: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:

@@ -40,8 +40,8 @@ def _tokens(step):
     return torch.from_numpy(sequence_copy_batch(0, step, 4, 128, 1024)).cuda()
 
 
-def _run_c1(dtype, opt_kwargs, steps=10, math_mode="f32"):
-    model = MiniTransformer(C1, dtype=dtype, device="cuda")
+def _run_c1(dtype, opt_kwargs, steps=10, math_mode="f32", fused_linear=False):
+    model = MiniTransformer(C1, dtype=dtype, device="cuda", fused_linear=fused_linear)
     opt = LOMO(model, lr=0.05, math=math_mode, **opt_kwargs)
     losses, outcomes, scales = [], [], []
     for step in range(steps):
@@ -111,6 +111,36 @@ def test_c1_fixture_fp16_two_pass(c1_meta, c1_arrays, key, scaler, math_mode):
           f">2ulp fraction {(u > 2).mean():.2e}, max loss rel {rel:.2e}")
     assert rel < 5e-3
     assert u.mean() < 0.25 and u.max() <= 64
+
+
+@pytest.mark.parametrize("replay", [True, False])
+@pytest.mark.parametrize("key,scaler", [("B", LossScaler(2.0 ** 16, growth_interval=2)),
+                                        ("C", LossScaler(2.0 ** 24, growth_interval=2,
+                                                         max_scale=2.0 ** 24))])
+def test_c1_fixture_fp16_two_pass_fused_gemm(c1_meta, c1_arrays, key, scaler, replay):
+    """The reference's own model (weights [in, out]) through the fused
+    training path: K6 probes every weight gradient inside its GEMM in pass 1,
+    K5 applies every update inside its GEMM in pass 2 (replayed, or in the
+    strict second backward).  Fixtures B (norm clip + growing scale) and C
+    (forced fp16 overflows): skip decisions and the scale trajectory equal the
+    reference run's exactly; parameters differ only by K5 applying the fp32
+    accumulator instead of the fp16-rounded gradient (max / mean ulp printed)."""
+    stab = Stabilizer(ClipMode.by_global_norm(1.0), LossScaler(
+        scaler.scale, growth_interval=scaler.growth_interval, max_scale=scaler.max_scale))
+    model, opt, losses, outcomes, scales = _run_c1(
+        torch.float16, {"stabilizer": stab, "replay": replay, "fuse_gemm": True},
+        fused_linear=True)
+    assert opt.fuse_probe and opt.fuse_gemm
+    ref = c1_meta[key]
+    assert outcomes == ref["outcomes"]
+    assert [math.log2(s) for s in scales] == ref["log2_scale"]
+    u = np.concatenate([_ulps16(g, r) for g, r in _sampled(model, c1_arrays, key).values()])
+    rel = max(abs(a - b) / abs(b) for a, b in zip(losses, ref["losses"]) if math.isfinite(b))
+    print(f"fixture {key} fp16 fused GEMM path ({'replay' if replay else 'strict'}): "
+          f"max ulp {u.max()}, mean ulp {u.mean():.4f}, >2ulp fraction {(u > 2).mean():.2e}, "
+          f"max loss rel {rel:.2e}")
+    assert rel < 5e-3
+    assert u.mean() < 0.5 and u.max() <= 64
 
 
 def test_lomo_equals_sgd_bit_exact_fp64():
