@@ -69,6 +69,17 @@ int lomo_wl_qkv_rope_bwd(const void* dq, const void* dk, const void* dv, int64_t
                          const void* sin, int64_t batch, int seq, int heads, int dh, int dtype,
                          void* stream);
 
+/* Mean token cross entropy over logits [rows, V] (V % 8 == 0), int64
+ * targets: the forward writes the per-row log-sum-exp (fp32, for the
+ * backward) and the per-row loss (the caller averages it); the backward
+ * writes dlogits = grad * (softmax - onehot) * inv_rows in the logits' dtype,
+ * grad read from device memory (fp32 scalar). */
+int lomo_wl_ce_fwd(const void* logits, const int64_t* targets, float* lse, float* loss_rows,
+                   int64_t rows, int V, int dtype, void* stream);
+int lomo_wl_ce_bwd(const void* logits, const int64_t* targets, const float* lse,
+                   const float* grad_dev, float inv_rows, void* dlogits, int64_t rows, int V,
+                   int dtype, void* stream);
+
 /* SwiGLU over a fused gate/up projection gu [rows, 2f] (gate = gu[:, :f],
  * up = gu[:, f:]): out [rows, f] = silu(gate) * up; the backward writes
  * dgu [rows, 2f] in the same layout. */

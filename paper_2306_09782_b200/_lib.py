@@ -67,6 +67,8 @@ WL_EXPORTS = (
     "lomo_wl_qkv_rope_bwd",
     "lomo_wl_add_rmsnorm_fwd",
     "lomo_wl_rmsnorm_bwd_add",
+    "lomo_wl_ce_fwd",
+    "lomo_wl_ce_bwd",
 )
 
 
@@ -151,6 +153,8 @@ _SIGS = {
     "lomo_wl_rope_ld": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32,
                                _i32, _i32, _vp]),
     "lomo_wl_swiglu_gu_fwd": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp]),
+    "lomo_wl_ce_fwd": (_i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp]),
+    "lomo_wl_ce_bwd": (_i32, [_vp, _vp, _vp, _vp, ctypes.c_float, _vp, _i64, _i32, _i32, _vp]),
     "lomo_wl_add_rmsnorm_fwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32,
                                        ctypes.c_float, _vp]),
     "lomo_wl_rmsnorm_bwd_add": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32,

@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include "lomo_b200.h"
@@ -343,6 +344,95 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---------------------------------------------------------------- cross entropy
+// Mean token cross entropy over fp16/bf16 logits [rows, V] (the decoder's
+// loss, ops.py:332-352 semantics: mean over positions), one CTA per row.
+// Forward: lse[r] = max + log(sum exp(x - max)), loss_rows[r] = lse - x[t_r].
+// Backward: dlogits = g * (exp(x - lse) - onehot) * inv_rows, g the upstream
+// gradient read from device memory (it carries the loss scale), one rounding.
+__device__ __forceinline__ void row_max_sum(float& m, float& sexp, float* sm_m, float* sm_s) {
+  // combine (max, sum exp) pairs: warp shuffle, then across warps in order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, sexp, o);
+    const float mm = fmaxf(m, m2);
+    sexp = (m == -INFINITY ? 0.f : sexp * __expf(m - mm)) +
+           (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+    m = mm;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+    sm_m[w] = m;
+    sm_s[w] = sexp;
+  }
+  __syncthreads();
+  float M = -INFINITY, S = 0.f;
+#pragma unroll
+  for (int i = 0; i < kThreads / 32; ++i) {
+    const float mm = fmaxf(M, sm_m[i]);
+    S = (M == -INFINITY ? 0.f : S * __expf(M - mm)) +
+        (sm_m[i] == -INFINITY ? 0.f : sm_s[i] * __expf(sm_m[i] - mm));
+    M = mm;
+  }
+  m = M;
+  sexp = S;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    ce_fwd(const T* __restrict__ logits, const int64_t* __restrict__ tgt, int V,
+           float* __restrict__ lse, float* __restrict__ loss_rows) {
+  __shared__ float sm_m[kThreads / 32], sm_s[kThreads / 32];
+  const int64_t r = blockIdx.x;
+  const uint4* xv = reinterpret_cast<const uint4*>(logits + r * V);
+  const int nv = V / 8;
+  float m = -INFINITY, se = 0.f;
+  for (int i = threadIdx.x; i < nv; i += kThreads) {
+    Vec8<T> X;
+    X.u = ld_nc(xv + i);
+    float vm = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) vm = fmaxf(vm, tof(X.e[e]));
+    const float mm = fmaxf(m, vm);
+    float acc = (m == -INFINITY) ? 0.f : se * __expf(m - mm);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc += __expf(tof(X.e[e]) - mm);
+    se = acc;
+    m = mm;
+  }
+  row_max_sum(m, se, sm_m, sm_s);
+  if (threadIdx.x == 0) {
+    const float l = m + __logf(se);
+    lse[r] = l;
+    loss_rows[r] = l - tof(logits[r * V + tgt[r]]);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    ce_bwd(const T* __restrict__ logits, const int64_t* __restrict__ tgt,
+           const float* __restrict__ lse, const float* __restrict__ gptr, float inv_rows,
+           T* __restrict__ dlogits, int V) {
+  const int64_t r = blockIdx.x;
+  const float g = *gptr * inv_rows, l = lse[r];
+  const int64_t t = tgt[r];
+  const uint4* xv = reinterpret_cast<const uint4*>(logits + r * V);
+  uint4* dv = reinterpret_cast<uint4*>(dlogits + r * V);
+  const int nv = V / 8;
+  for (int i = threadIdx.x; i < nv; i += kThreads) {
+    Vec8<T> X, D;
+    X.u = ld_nc(xv + i);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float p = __expf(tof(X.e[e]) - l);
+      D.e[e] = fromf<T>(g * (p - ((int64_t)(i * 8 + e) == t ? 1.f : 0.f)));
+    }
+    dv[i] = D.u;
+  }
+}
+
 // ---------------------------------------------------------------- SwiGLU
 __device__ __forceinline__ float sigmoidf_(float g) { return 1.f / (1.f + __expf(-g)); }
 
@@ -552,6 +642,20 @@ struct QkvBwd {
 };
 
 template <typename T>
+struct Ce {
+  static int run(const void* logits, const int64_t* tgt, float* lse, float* loss_rows,
+                 const float* g, float inv_rows, void* dlogits, int64_t rows, int V, int bwd,
+                 cudaStream_t s) {
+    if (!bwd)
+      ce_fwd<T><<<(unsigned)rows, kThreads, 0, s>>>((const T*)logits, tgt, V, lse, loss_rows);
+    else
+      ce_bwd<T><<<(unsigned)rows, kThreads, 0, s>>>((const T*)logits, tgt, lse, g, inv_rows,
+                                                    (T*)dlogits, V);
+    return status();
+  }
+};
+
+template <typename T>
 struct SwigluGu {
   static int run(const void* a, const void* b, void* c, int64_t rows, int64_t f, int bwd,
                  cudaStream_t s) {
@@ -666,6 +770,27 @@ int lomo_wl_qkv_rope_bwd(const void* dq, const void* dk, const void* dv, int64_t
   return wl::dispatch<wl::QkvBwd>(dtype, dq, dk, dv, dv_stride_b, dv_stride_h, dv_stride_s, dqkv,
                                   cos, sin, batch * (int64_t)seq, seq, heads, dh,
                                   (cudaStream_t)stream);
+}
+
+int lomo_wl_ce_fwd(const void* logits, const int64_t* targets, float* lse, float* loss_rows,
+                   int64_t rows, int V, int dtype, void* stream) {
+  if (rows < 0 || V <= 0 || V % 8 || rows > INT32_MAX) return LOMO_E_ARG;
+  if (rows == 0) return 0;
+  if (!logits || !targets || !lse || !loss_rows || !wl::aligned16(logits)) return LOMO_E_ARG;
+  return wl::dispatch<wl::Ce>(dtype, logits, targets, lse, loss_rows, (const float*)nullptr, 0.f,
+                              (void*)nullptr, rows, V, 0, (cudaStream_t)stream);
+}
+
+int lomo_wl_ce_bwd(const void* logits, const int64_t* targets, const float* lse,
+                   const float* grad_dev, float inv_rows, void* dlogits, int64_t rows, int V,
+                   int dtype, void* stream) {
+  if (rows < 0 || V <= 0 || V % 8 || rows > INT32_MAX) return LOMO_E_ARG;
+  if (rows == 0) return 0;
+  if (!logits || !targets || !lse || !grad_dev || !dlogits || !wl::aligned16(logits) ||
+      !wl::aligned16(dlogits))
+    return LOMO_E_ARG;
+  return wl::dispatch<wl::Ce>(dtype, logits, targets, (float*)lse, (float*)nullptr, grad_dev,
+                              inv_rows, dlogits, rows, V, 1, (cudaStream_t)stream);
 }
 
 int lomo_wl_swiglu_gu_fwd(const void* gu, void* out, int64_t rows, int64_t f, int dtype,

@@ -433,6 +433,45 @@ def add_rms_norm(x, r, w, eps=RMSNORM_EPS):
     return h, rms_norm(h, w, eps, fused=False)
 
 
+class _CrossEntropyFn(torch.autograd.Function):
+    """Mean token cross entropy of fp16/bf16 logits in one kernel per
+    direction (csrc/workload_kernels.cu): the forward keeps only the per-row
+    log-sum-exp; the backward writes dlogits in the logits' dtype, scaled by
+    the upstream gradient read on device (it carries the loss scale)."""
+
+    @staticmethod
+    def forward(ctx, logits, targets):
+        rows, V = logits.shape
+        lse = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        loss_rows = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        _wl_call(_wl().lomo_wl_ce_fwd(logits.data_ptr(), targets.data_ptr(), lse.data_ptr(),
+                                      loss_rows.data_ptr(), rows, V, _WL_DTYPES[logits.dtype],
+                                      _stream()), "lomo_wl_ce_fwd")
+        ctx.save_for_backward(logits, targets, lse)
+        return loss_rows.mean()
+
+    @staticmethod
+    def backward(ctx, g):
+        logits, targets, lse = ctx.saved_tensors
+        rows, V = logits.shape
+        g = g.detach().to(torch.float32).contiguous()
+        dlogits = torch.empty_like(logits)
+        _wl_call(_wl().lomo_wl_ce_bwd(logits.data_ptr(), targets.data_ptr(), lse.data_ptr(),
+                                      g.data_ptr(), 1.0 / rows, dlogits.data_ptr(), rows, V,
+                                      _WL_DTYPES[logits.dtype], _stream()), "lomo_wl_ce_bwd")
+        return dlogits, None
+
+
+def token_cross_entropy(logits, targets):
+    """Mean cross entropy over [rows, V] logits (fp32 math)."""
+    if _wl_ok(logits, targets.new_empty(0, dtype=logits.dtype)) and logits.dim() == 2 \
+            and logits.shape[1] % 8 == 0 and targets.dtype == torch.int64 \
+            and targets.is_contiguous():
+        return _CrossEntropyFn.apply(logits, targets)
+    inner = torch.float64 if logits.dtype == torch.float64 else torch.float32
+    return F.cross_entropy(logits.to(inner), targets)
+
+
 def rms_norm(x, w, eps=RMSNORM_EPS, fused=True):
     if fused and _wl_ok(x, w) and x.shape[-1] % 8 == 0 and x.shape[-1] <= 8192:
         return _RMSNormFn.apply(x, w, eps)
@@ -608,5 +647,5 @@ class Llama(nn.Module):
 
     def loss(self, ids, targets):
         logits = self(ids)
-        inner = torch.float64 if logits.dtype == torch.float64 else torch.float32
-        return F.cross_entropy(logits.reshape(-1, logits.shape[-1]).to(inner), targets.reshape(-1))
+        return token_cross_entropy(logits.reshape(-1, logits.shape[-1]),
+                                   targets.reshape(-1).contiguous())

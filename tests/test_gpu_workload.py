@@ -262,3 +262,21 @@ def test_fused_decoder_residual_stream_is_exact(dtype):
             x = layer(x, cos, sin)
         ref = W.rlinear(W.rms_norm(x, m.norm.weight), m.lm_head)
         assert torch.equal(m(d[:, :-1]), ref)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("rows,V", [(1, 8), (1024, 32000), (37, 520)])
+def test_cross_entropy_fused(dtype, rows, V):
+    """The fused token cross entropy against torch's fp32 cross entropy of the
+    same logits: loss to fp32 rounding, dlogits to 2 ulp of the storage type
+    (with a loss-scale-like upstream gradient)."""
+    x = (3 * torch.randn(rows, V, device="cuda")).to(dtype)
+    t = torch.randint(0, V, (rows,), device="cuda")
+    xa = x.clone().requires_grad_()
+    la = W._CrossEntropyFn.apply(xa, t)
+    (la * 1024.0).backward()
+    xr = x.float().requires_grad_()
+    lr_ = torch.nn.functional.cross_entropy(xr, t)
+    (lr_ * 1024.0).backward()
+    assert abs(la.item() - lr_.item()) <= 1e-5 * abs(lr_.item()) + 1e-6
+    close(xa.grad, xr.grad, dtype, k=2.0, floor=1e-3 * xr.grad.abs().max().item())
