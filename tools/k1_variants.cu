@@ -174,6 +174,44 @@ __global__ void __launch_bounds__(256, 5) v_probe2(const bf* __restrict__ g, int
   }
 }
 
+// ---- K2 variant with the L2 prefetch: PF tiles ahead (0 = own tile only) ----
+template <int U, int AHEAD>
+__global__ void __launch_bounds__(256, 5) v_probe_pf(const bf* __restrict__ g, int64_t nvec,
+                                                     int64_t per, double* __restrict__ part) {
+  __shared__ double sm[8];
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const int64_t beg = (int64_t)blockIdx.x * per, end = min(beg + per, nvec);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int a = 0; a <= AHEAD; ++a) {
+      const int64_t b0 = beg + a * per * gridDim.x / gridDim.x * 0 + a * per;
+      const int64_t nt = min(per, nvec - b0);
+      if (nt > 0 && (a == 0 || blockIdx.x < 148 * 5))
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gv + b0),
+                     "r"((uint32_t)(nt * 16)) : "memory");
+    }
+  }
+  pdl_wait();
+  pdl_launch_dependents();
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t base = beg + threadIdx.x; base < end; base += 256 * U) {
+    uint4 G[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 256;
+      if (i < end) G[u] = ld_stream_ro(gv + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + u * 256;
+      if (i < end) acc += vec_sumsq<bf, float>(G[u], 1.0f, false, bad);
+    }
+  }
+  const double r = block_sum(acc, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = r + (bad ? 1.0 : 0.0);
+}
+
 // ---- variant: TMA bulk copies through a 4-stage shared-memory ring ---------
 constexpr int kTileElems = 8192;  // 16 KB per operand per stage
 constexpr int kStages = 4;
@@ -505,6 +543,11 @@ int main() {
     probe_pass(v_probe<4>, 1024, 4096, "probe >=1024 vec/CTA u4, <=4096 CTAs");
     probe_pass(v_probe<4>, 2048, 1 << 20, "probe 2048 vec/CTA u4");
     probe_pass(v_probe<8>, 2048, 1 << 20, "probe 2048 vec/CTA u8");
+    probe_pass(v_probe_pf<8, 0>, 2048, 1 << 20, "probe 2048 u8 + L2 prefetch own tile");
+    probe_pass(v_probe_pf<4, 0>, 1024, 1 << 20, "probe 1024 u4 + L2 prefetch own tile");
+    probe_pass(v_probe_pf<8, 0>, 4096, 1 << 20, "probe 4096 u8 + L2 prefetch own tile");
+    probe_pass(v_probe_pf<8, 1>, 2048, 1 << 20, "probe 2048 u8 + prefetch own + next");
+    probe_pass(v_probe_pf<16, 0>, 4096, 1 << 20, "probe 4096 u16 + L2 prefetch own tile");
     probe_pass(v_probe<8>, 4096, 1 << 20, "probe 4096 vec/CTA u8");
     probe_pass(v_probe<8>, 8192, 1 << 20, "probe 8192 vec/CTA u8");
     probe_pass(v_probe<16>, 8192, 1 << 20, "probe 8192 vec/CTA u16");
