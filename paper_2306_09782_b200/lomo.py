@@ -267,7 +267,9 @@ class LOMO(_Protocol):
             epilogue of its weight-gradient GEMM on the tensor cores (K5,
             csrc/lomo_gemm_update.cu): ``p <- p - lr*coef/scale * (dy^T x)`` from
             the fp32 accumulator, the gradient never materialised.  16-bit
-            parameters, no value clip; other parameters keep K1.
+            parameters, fp32 math, no value clip; other parameters keep K1.
+            Without ``replay`` the update runs inside each linear's backward
+            (the single fused pass, or the strict protocol's second backward).
         fuse_probe: with ``replay`` (default: on when ``fuse_gemm`` is), run
             each linear's pass-1 probe as the epilogue of its weight-gradient
             GEMM (K6, csrc/lomo_gemm_probe.cu): the overflow flag and the sum of
@@ -314,7 +316,9 @@ class LOMO(_Protocol):
         self._stash = ReplayStash() if replay else None
         self._replay_checked = False
         self._replay_mismatch: list = []
-        self.fuse_gemm = bool(fuse_gemm) and self.clip_value == 0.0
+        # the fused GEMMs apply/probe the fp32 accumulator: not the f64
+        # exactness mode, and value clipping is not linear in dW
+        self.fuse_gemm = bool(fuse_gemm) and self.clip_value == 0.0 and math == "f32"
         if fuse_probe and self.passes != 2:
             raise ConfigError("fuse_probe fuses pass 1's probe into the weight-gradient GEMM: "
                               "it needs the two-pass protocol (clip_grad_norm / loss_scale)")
@@ -338,7 +342,7 @@ class LOMO(_Protocol):
         # `gemm_streams` streams; pass 1's K6 may run on a side stream beside
         # the rest of the backward (it only reads the stashed x/dy).  Joined
         # before K3a / at the end of pass 2.  Off by default: on LLaMA-7B the
-        # overlap cost more than the filled wave tails (profiles/r01_summary.md).
+        # overlap cost more than the filled wave tails (profiles/r01_gemm_shapes.md).
         # LOMO_GEMM_STREAMS / LOMO_PROBE_STREAM override.
         self.gemm_streams = max(1, int(os.environ.get("LOMO_GEMM_STREAMS", gemm_streams)))
         self.probe_stream = os.environ.get("LOMO_PROBE_STREAM", "1" if probe_stream else "0") == "1"
