@@ -111,7 +111,7 @@ typedef struct lomo_state {
    * order, then the slots in slot order: deterministic. */
 } lomo_state;
 
-#define LOMO_PROBE_BLOCKS_PER_SLOT 4096
+#define LOMO_PROBE_BLOCKS_PER_SLOT 8192
 
 /* 128-byte host snapshot of the state header (lomo_read_status). */
 typedef lomo_state lomo_status;
