@@ -502,7 +502,8 @@ def bench_train(args, rank, world):
            "paper_tgs_rtx3090": 769.92}
     gstep = None
     variants = ("strict", "strict_fused_gemm", "replay", "replay_fused_gemm",
-                "replay_fused_gemm_graph", "grouped", "single_pass_fused_gemm") \
+                "replay_fused_gemm_graph", "grouped", "grouped_fused_gemm",
+                "single_pass_fused_gemm") \
         if not args.train_variants else \
         tuple(args.train_variants.split(","))
     for key in variants:
@@ -523,10 +524,12 @@ def bench_train(args, rank, world):
             # with every linear's update inside its weight-gradient GEMM (K5 in
             # the backward); reported beside the headline, not config 3's protocol
             opt = LOMO(model, lr=1e-3, fuse_gemm=True)
-        elif key == "grouped":
+        elif key in ("grouped", "grouped_fused_gemm"):
             # the paper's single-pass alternative (stabilize.py:234-274): clip
             # each decoder layer by its own norm, no loss scaler, one backward
-            opt = GroupedLOMO(model, lr=1e-3, max_norm=1.0, window=1)
+            # (_fused_gemm: each linear's group probe inside its GEMM, K6)
+            opt = GroupedLOMO(model, lr=1e-3, max_norm=1.0, window=1,
+                              fuse_gemm=key == "grouped_fused_gemm")
         else:
             opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
                        loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
@@ -560,7 +563,8 @@ def bench_train(args, rank, world):
         del opt
         step = gstep = None  # noqa: F841  (release the graphs' memory pool)
         torch.cuda.empty_cache()
-    two_pass = [k for k in variants if k not in ("grouped", "single_pass_fused_gemm")]
+    two_pass = [k for k in variants
+                if k not in ("grouped", "grouped_fused_gemm", "single_pass_fused_gemm")]
     # the headline: config 3's two-pass protocol
     best = max(two_pass or variants, key=lambda k: out[k]["tokens_per_s"])
     out["tokens_per_s"] = out[best]["tokens_per_s"]

@@ -12,15 +12,23 @@ is non-finite is dropped alone (earlier groups were already applied); the
 step outcome is SKIPPED_OVERFLOW if any group was dropped.  One backward pass,
 no second forward; biased relative to global clipping (PAPER.md:154-159);
 gradient peak = the largest group (pkg/README.md:103-107).
+
+With ``fuse_gemm=True`` every linear routed through ``replay.linear`` /
+``replay.matmul_in_out`` is probed inside its weight-gradient GEMM (K6): the
+GEMM's epilogue writes the retained gradient *and* its group slot's sum of
+squares / overflow, so the group flush runs K2 only over the other
+parameters (norm scales, embedding) before K3a and K1.
 """
 from __future__ import annotations
 
+import ctypes
 import re
 from typing import Callable
 
 import torch
 
 from . import _lib
+from . import replay as _replay
 from .engine import CudaEngine, dtype_code
 from .errors import ConfigError, NonFiniteLossError, TapeStateError
 from .lomo import trainable_params
@@ -60,7 +68,8 @@ class GroupedLOMO:
     """
 
     def __init__(self, model, lr: float = 1e-3, max_norm: float = 1.0, window: int = 1, *,
-                 layer_of: dict | None = None, math: str = "f32", weight_decay: float = 0.0):
+                 layer_of: dict | None = None, math: str = "f32", weight_decay: float = 0.0,
+                 fuse_gemm: bool = False):
         self.clip = ClipMode.by_group_norm(max_norm, window)  # validation (stabilize.py:65-74)
         params = trainable_params(model)
         dev = params[0].device
@@ -84,37 +93,103 @@ class GroupedLOMO:
         self._skipped_before = 0
         self.last_outcome: StepOutcome | None = None
         self.peak_group_grads = 0
+        self.fuse_gemm = bool(fuse_gemm) and math == "f32"
+        self._lin = _replay.ReplayStash(keep=False) if self.fuse_gemm else None
+        self._by_id = {id(p): p for p in params}
+        self._probed: set[int] = set()       # this group's K6-probed weights
+        self._pending = []                   # deferred K6 partial sums of this group
+        self._pws = {}                       # K6 workspace per weight
+        self._mismatch: list = []
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
 
-    def _hook(self, p: torch.Tensor) -> None:
-        if not self._active or p.grad is None:
-            return
-        g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
-        p.grad = None  # RETAIN in our buffer (stabilize.py:260-266), not in .grad
-        group = self.layer[id(p)] // self.clip.window
+    def _enter_group(self, pid: int) -> None:
+        group = self.layer[pid] // self.clip.window
         if self._group is not None and group != self._group:
             self._flush()
+        if self._group != group:
+            self.engine.begin(None)           # fresh slots / overflow for this group
         self._group = group
+
+    def _retain(self, p, g) -> None:
         self._buf.append((p, g))
         self.peak_group_grads = max(self.peak_group_grads,
                                     sum(x.numel() * x.element_size() for _, x in self._buf))
 
+    def _hook(self, p: torch.Tensor) -> None:
+        if not self._active or p.grad is None:
+            return
+        if id(p) in self._probed:             # K6 took this weight: another op fed it too
+            self._mismatch.append(tuple(p.shape))
+        g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+        p.grad = None  # RETAIN in our buffer (stabilize.py:260-266), not in .grad
+        self._enter_group(id(p))
+        self._retain(p, g)
+
+    def _gemm_probe(self, wid: int, w, x, dy) -> bool:
+        """K6 from the linear's backward: the retained gradient and the group
+        slot's sum of squares / overflow from one tensor-core GEMM."""
+        p = self._by_id[wid]
+        if p.dtype not in (torch.bfloat16, torch.float16) or p.dim() != 2:
+            return False
+        out_f, in_f = p.shape
+        if out_f % 8 or in_f % 8:
+            return False
+        dy2, x2 = dy.reshape(-1, out_f), x.reshape(-1, in_f)
+        if not (dy2.is_contiguous() and x2.is_contiguous()) or dy2.dtype != p.dtype \
+                or x2.dtype != p.dtype:
+            return False
+        eng, dt = self.engine, dtype_code(p.dtype)
+        need = eng.lib.lomo_gemm_probe_workspace(out_f, in_f, dy2.shape[0], dt)
+        if need == 0:
+            return False
+        self._enter_group(wid)
+        ws = self._pws.get(wid)
+        if ws is None or ws.numel() < need:
+            ws = self._pws[wid] = torch.empty(need, dtype=torch.uint8, device=p.device)
+        g = torch.empty_like(p)               # the retained gradient: K6's store
+        slot = self._slot[wid]
+        rc = eng.lib.lomo_gemm_probe(dy2.data_ptr(), x2.data_ptr(), g.data_ptr(), out_f, in_f,
+                                     dy2.shape[0], dt, slot, _lib.DEFER_ROWS, eng.ptr,
+                                     ws.data_ptr(), need, eng.stream())
+        if rc == -1:
+            return False
+        _lib.check(rc, "lomo_gemm_probe")
+        self._pending.append((ws.data_ptr(), out_f, in_f, slot, dt))
+        self._probed.add(wid)
+        self._retain(p, g)
+        return True
+
+    def _finish_probes(self) -> None:
+        pend, self._pending = self._pending, []
+        for dt in {e[4] for e in pend}:
+            sel = [e for e in pend if e[4] == dt]
+            k = len(sel)
+            _lib.check(self.engine.lib.lomo_gemm_probe_finish(
+                (ctypes.c_void_p * k)(*[e[0] for e in sel]),
+                (ctypes.c_int64 * k)(*[e[1] for e in sel]),
+                (ctypes.c_int64 * k)(*[e[2] for e in sel]),
+                (ctypes.c_int * k)(*[e[3] for e in sel]), k, dt, self.engine.ptr,
+                self.engine.stream()), "lomo_gemm_probe_finish")
+
     def _flush(self) -> None:
-        """stabilize.py:239-258 on the device: K2 -> K3a -> K1 for one group."""
+        """stabilize.py:239-258 on the device: K2 (or K6's partials) -> K3a ->
+        K1 for one group."""
         if not self._buf:
             return
         eng = self.engine
-        eng.begin(None)                       # fresh slots / overflow for this group
         eng.configure(flags=self._probe_flags)
         for p, g in self._buf:
-            eng.probe(g, self._slot[id(p)])
+            if id(p) not in self._probed:
+                eng.probe(g, self._slot[id(p)])
         eng.flush()
+        self._finish_probes()
         eng.finalize()                        # N, coef = min(1, max_norm/N), skip if !finite
         eng.configure(self._lr, 0.0, self.weight_decay, _lib.USE_SKIP | _lib.USE_COEF)
         for p, g in self._buf:
             eng.update(p, g)
         eng.flush()
         self._buf = []                        # gradients released (stream-ordered)
+        self._probed = set()
 
     def fused_backward(self, loss: torch.Tensor, lr: float | None = None) -> None:
         """One grouped fused pass (stabilize.py:234-274)."""
@@ -125,11 +200,22 @@ class GroupedLOMO:
                 raise TapeStateError("a parameter already holds a gradient")
         self._lr = self.lr if lr is None else float(lr)
         self._active, self._group = True, None
+        self._mismatch = []
+        if self._lin is not None:
+            self._lin.clear()
+            self._lin.probe = self._gemm_probe
+            _replay._ACTIVE = self._lin
         try:
             loss.backward()
             self._flush()
         finally:
+            if self._lin is not None:
+                _replay._ACTIVE = None
             self._active, self._buf, self._group = False, [], None
+            self._pending, self._probed = [], set()
+        if self._lin is not None and (self._lin.shared or self._mismatch):
+            raise ConfigError("fuse_gemm: a weight feeds more than one op (shared or tied); "
+                              "use GroupedLOMO(fuse_gemm=False)")
         st = self.engine.read_status()
         skipped = st.steps_skipped > self._skipped_before
         self._skipped_before = st.steps_skipped

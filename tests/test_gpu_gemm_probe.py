@@ -380,3 +380,33 @@ def test_fused_paths_fall_back_per_linear(replay):
         assert abs(opts[0].last_norm - opts[1].last_norm) <= tol * opts[0].last_norm
     for p, q in zip(nets[0].parameters(), nets[1].parameters()):
         torch.testing.assert_close(p.float(), q.float(), rtol=2 ** -6, atol=1e-4)
+
+
+@pytest.mark.parametrize("window", [1, 2])
+def test_grouped_lomo_with_k6_matches_k2(window):
+    """GroupedLOMO (single-pass per-layer-window clipping) with each linear's
+    group probe taken by K6 inside its weight-gradient GEMM -- whose store is
+    the retained gradient -- against the hook + K2 flush: same outcomes,
+    parameters within one ulp (the group norms differ only by summation
+    order)."""
+    from paper_2306_09782_b200 import GroupedLOMO
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=128, layers=3, heads=4, ffn=256, vocab=256)
+    a = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    b = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    oa = GroupedLOMO(a, lr=0.05, max_norm=0.05, window=window)
+    ob = GroupedLOMO(b, lr=0.05, max_norm=0.05, window=window, fuse_gemm=True)
+    gen = torch.Generator(device="cuda").manual_seed(8)
+    for step in range(3):
+        d = torch.randint(0, 256, (2, 65), device="cuda", generator=gen)
+        la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+        lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
+        assert oa.last_outcome == ob.last_outcome
+        assert abs(la - lb) <= 1e-2 * abs(la)
+        for x, y in zip(a.parameters(), b.parameters()):
+            d_ = U.ulp_diff(x.detach(), y.detach())
+            assert d_.max().item() <= 1, (step, d_.max().item())
+        with torch.no_grad():            # realign for the next step
+            for x, y in zip(a.parameters(), b.parameters()):
+                y.copy_(x)
+    assert ob.peak_group_grads > 0
