@@ -259,12 +259,21 @@ __device__ __forceinline__ bool resolve_args(UpdArgs<M>& a, unsigned flags,
     // together (the state was written by an earlier kernel: after the PDL
     // wait, no volatile/strong access is needed -- a volatile read of `skip`
     // compiled to LDG.STRONG.SYS and serialised a second round trip)
-    int32_t skip;
-    double inv_scale, coef, lr;
-    asm volatile("ld.global.s32 %0, [%1];" : "=r"(skip) : "l"(&st->skip));
-    asm volatile("ld.global.f64 %0, [%1];" : "=d"(inv_scale) : "l"(&st->inv_scale));
-    asm volatile("ld.global.f64 %0, [%1];" : "=d"(coef) : "l"(&st->clip_coef));
-    asm volatile("ld.global.f64 %0, [%1];" : "=d"(lr) : "l"(&st->lr));
+    // One lane per warp loads, the warp shares by shuffle: four loads per
+    // thread would triple K1's load instructions (one 16-byte vector of p
+    // and of g per thread) and cost ~7 % of its bandwidth.
+    int32_t skip = 0;
+    double inv_scale = 0.0, coef = 0.0, lr = 0.0;
+    if ((threadIdx.x & 31) == 0) {
+      asm volatile("ld.global.s32 %0, [%1];" : "=r"(skip) : "l"(&st->skip));
+      asm volatile("ld.global.f64 %0, [%1];" : "=d"(inv_scale) : "l"(&st->inv_scale));
+      asm volatile("ld.global.f64 %0, [%1];" : "=d"(coef) : "l"(&st->clip_coef));
+      asm volatile("ld.global.f64 %0, [%1];" : "=d"(lr) : "l"(&st->lr));
+    }
+    skip = __shfl_sync(0xffffffffu, skip, 0);
+    inv_scale = __shfl_sync(0xffffffffu, inv_scale, 0);
+    coef = __shfl_sync(0xffffffffu, coef, 0);
+    lr = __shfl_sync(0xffffffffu, lr, 0);
     if ((flags & LOMO_USE_SKIP) && skip) return false;
     if (flags & LOMO_USE_SCALE) a.inv_scale = (M)inv_scale;
     if (flags & LOMO_USE_COEF) a.coef = (M)coef;
