@@ -16,6 +16,7 @@ from paper_2306_09782_b200 import _lib  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--tokens", type=int, default=1024)
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--fused", action="store_true", help="the stacked-projection shapes (qkv, gate_up)")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 lib = _lib.load()
@@ -25,6 +26,9 @@ code = _lib.F16
 T = a.tokens
 # (out, in, count per 7B model)
 shapes = [(4096, 4096, 128), (11008, 4096, 64), (4096, 11008, 32), (32000, 4096, 1)]
+if a.fused:
+    shapes = [(12288, 4096, 32), (4096, 4096, 32), (22016, 4096, 32), (4096, 11008, 32),
+              (32000, 4096, 1)]
 state = torch.zeros(_lib.state_bytes(4), dtype=torch.uint8, device="cuda")
 _lib.check(lib.lomo_state_init(state.data_ptr(), 4, 1024.0, 16, 1.0, 2.0 ** 24, 1.0, 1.0, s),
            "init")
