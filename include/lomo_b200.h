@@ -198,6 +198,26 @@ int lomo_fused_rs_probe(const void* const* peer_bufs_dev, int world, int64_t off
                         int64_t n, int dtype, int slot, unsigned flags, void* state,
                         void* stream);
 
+/* ---- row-sparse embedding gradient (K1 on the rows a batch touched) ---- */
+/* The reference's embedding VJP scatters dy into a dense [V, h] gradient;
+ * LOMO's update leaves untouched rows unchanged (p - lr*0 == p), so the
+ * gradient can live as one aggregated row per distinct id:
+ * lomo_rows_aggregate: sorted_ids / perm = a stable sort of the ntok token
+ * ids and the source positions; writes rows [ntok, h] (dtype) and row_ids
+ * [ntok] -- run heads get the fp32 sum of their dy rows in token order
+ * (rounded to dtype) and their id, other positions a zero row and -1.  K2 on
+ * `rows` then equals K2 on the dense gradient up to summation order.
+ * lomo_fused_update_rows: K1's arithmetic on p[row_ids[j], :] with
+ * rows[j, :], skipping row_ids < 0; weight_decay must be 0 (LOMO_E_ARG:
+ * decay changes every row). */
+int lomo_rows_aggregate(const int64_t* sorted_ids, const int64_t* perm, const void* dy,
+                        int64_t ntok, int64_t h, int dtype, void* rows, int64_t* row_ids,
+                        void* stream);
+int lomo_fused_update_rows(void* p, const void* rows, const int64_t* row_ids, int64_t nrows,
+                           int64_t h, int dtype, int math, double lr, double clip_value,
+                           double weight_decay, unsigned flags, const void* state,
+                           void* stream);
+
 /* ---- K5: weight-gradient GEMM with the update as its epilogue ---------- */
 /* For a linear layer y = x W^T (W [out, in] row-major, x [tokens, in],
  * dy [tokens, out], all row-major, 16-bit): computes on the tensor cores

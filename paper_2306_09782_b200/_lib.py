@@ -51,6 +51,8 @@ EXPORTS = (
     "lomo_probe_rows",
     "lomo_probe_rows_multi",
     "lomo_gemm_probe_finish",
+    "lomo_rows_aggregate",
+    "lomo_fused_update_rows",
 )
 
 # include/lomo_workload.h: the benchmark decoder's fused layers (not the LOMO path)
@@ -142,6 +144,9 @@ _SIGS = {
     "lomo_gemm_probe_workspace": (ctypes.c_size_t, [_i64, _i64, _i64, _i32]),
     "lomo_probe_rows": (_i32, [_vp, _i64, _i64, _i64, _i32, _vp, _vp]),
     "lomo_probe_rows_multi": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp]),
+    "lomo_rows_aggregate": (_i32, [_vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp, _vp]),
+    "lomo_fused_update_rows": (_i32, [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _dbl, _dbl, _dbl,
+                                      _u32, _vp, _vp]),
     "lomo_gemm_probe_finish": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
     "lomo_wl_rmsnorm_fwd": (_i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, ctypes.c_float, _vp]),
     "lomo_wl_rmsnorm_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp]),

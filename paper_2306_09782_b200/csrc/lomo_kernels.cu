@@ -387,6 +387,63 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // --------------------------------------------------------------------------
+// Row-sparse form for an embedding table (the reference's embedding VJP is a
+// dense scatter-add, ops.py; its LOMO update leaves every row the batch did
+// not touch unchanged, since p - lr*0 == p exactly): the gradient is kept as
+// one aggregated row per distinct token id.
+// --------------------------------------------------------------------------
+// Aggregate: `sorted` are the batch's token ids after a stable sort, `perm`
+// the positions they came from.  Position j that starts a run of equal ids
+// sums that run's dy rows in sorted (= token) order in fp32 and stores the
+// row rounded to the storage dtype, with idx[j] = id; every other position
+// stores a zero row and idx[j] = -1.  Fixed size, no host sync, deterministic.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    k_rows_aggregate(const int64_t* __restrict__ sorted, const int64_t* __restrict__ perm,
+                     const T* __restrict__ dy, int64_t ntok, int64_t h, T* __restrict__ rows,
+                     int64_t* __restrict__ idx) {
+  pdl_enter();
+  const int64_t j = blockIdx.x;
+  const int64_t id = sorted[j];
+  const bool head = j == 0 || sorted[j - 1] != id;
+  if (threadIdx.x == 0) idx[j] = head ? id : -1;
+  int64_t end = j + 1;
+  if (head)
+    while (end < ntok && sorted[end] == id) ++end;
+  for (int64_t c = threadIdx.x; c < h; c += blockDim.x) {
+    float acc = 0.f;
+    if (head)
+      for (int64_t k = j; k < end; ++k) acc += to_m<float>(dy[perm[k] * h + c]);
+    rows[j * h + c] = from_m<T, float>(acc);
+  }
+}
+
+// Update: p[idx[j], :] <- the K1 arithmetic with rows[j, :], for idx[j] >= 0.
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k1_rows(T* __restrict__ p, const T* __restrict__ rows, const int64_t* __restrict__ idx,
+            int64_t h, UpdArgs<M> a, unsigned flags, const lomo_state* st) {
+  if (!load_args(a, flags, st)) return;
+  const int64_t r = idx[blockIdx.x];
+  if (r < 0) return;  // CTA-uniform
+  T* pr = p + r * h;
+  const T* gr = rows + (int64_t)blockIdx.x * h;
+  constexpr int V = 16 / sizeof(T);
+  const bool vec = (h % V) == 0 && (((uintptr_t)pr | (uintptr_t)gr) & 15) == 0;
+  if (vec) {  // 128-bit path (rows of a 16-byte-multiple width)
+    uint4* pv = reinterpret_cast<uint4*>(pr);
+    const uint4* gv = reinterpret_cast<const uint4*>(gr);
+    for (int64_t c = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; c < h / V;
+         c += (int64_t)gridDim.y * blockDim.x)
+      pv[c] = upd_vec<T, M>(pv[c], ld_stream_ro(gv + c), a);
+    return;
+  }
+  for (int64_t c = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; c < h;
+       c += (int64_t)gridDim.y * blockDim.x)
+    pr[c] = from_m<T, M>(upd_elem(to_m<M>(pr[c]), to_m<M>(gr[c]), a));
+}
+
+// --------------------------------------------------------------------------
 // K2: probe -- deterministic sum of squares + non-finite flag
 // --------------------------------------------------------------------------
 __device__ __forceinline__ lomo_state* hdr(void* s) { return reinterpret_cast<lomo_state*>(s); }
@@ -1261,6 +1318,52 @@ int lomo_fused_update_multi(void* const* p_list, const void* const* g_list,
     case LOMO_F64: return LOMO_MULTI(double, double);
   }
 #undef LOMO_MULTI
+  return LOMO_E_ARG;
+}
+
+int lomo_rows_aggregate(const int64_t* sorted_ids, const int64_t* perm, const void* dy,
+                        int64_t ntok, int64_t h, int dtype, void* rows, int64_t* row_ids,
+                        void* stream) {
+  if (ntok < 0 || h <= 0) return LOMO_E_ARG;
+  if (ntok == 0) return 0;
+  if (!sorted_ids || !perm || !dy || !rows || !row_ids) return LOMO_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned g = (unsigned)ntok;
+  switch (dtype) {
+    case LOMO_F16: return launch(k_rows_aggregate<__half>, dim3(g), dim3(kThreads), s, sorted_ids, perm, static_cast<const __half*>(dy), ntok, h, static_cast<__half*>(rows), row_ids);
+    case LOMO_BF16: return launch(k_rows_aggregate<__nv_bfloat16>, dim3(g), dim3(kThreads), s, sorted_ids, perm, static_cast<const __nv_bfloat16*>(dy), ntok, h, static_cast<__nv_bfloat16*>(rows), row_ids);
+    case LOMO_F32: return launch(k_rows_aggregate<float>, dim3(g), dim3(kThreads), s, sorted_ids, perm, static_cast<const float*>(dy), ntok, h, static_cast<float*>(rows), row_ids);
+  }
+  return LOMO_E_ARG;
+}
+
+int lomo_fused_update_rows(void* p, const void* rows, const int64_t* row_ids, int64_t nrows,
+                           int64_t h, int dtype, int math, double lr, double clip_value,
+                           double weight_decay, unsigned flags, const void* state,
+                           void* stream) {
+  if (nrows < 0 || h <= 0) return LOMO_E_ARG;
+  if (nrows == 0) return 0;
+  if (!p || !rows || !row_ids) return LOMO_E_ARG;
+  if (weight_decay != 0.0) return LOMO_E_ARG;  // decay touches every row: use the dense K1
+  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP | LOMO_LR_FROM_STATE)) &&
+      state == nullptr)
+    return LOMO_E_ARG;
+  if (math != LOMO_MATH_F32 && math != LOMO_MATH_F64) return LOMO_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ycta = (h / 8 + kThreads - 1) / kThreads;  // one 16-byte vector per thread
+  const dim3 grid((unsigned)nrows, (unsigned)(ycta < 1 ? 1 : (ycta > 8 ? 8 : ycta)));
+  const lomo_state* st = static_cast<const lomo_state*>(state);
+  const bool f64 = math == LOMO_MATH_F64;
+#define LOMO_ROWS(T, M)                                                                       \
+  launch(k1_rows<T, M>, grid, dim3(kThreads), s, static_cast<T*>(p),                          \
+         static_cast<const T*>(rows), row_ids, h, make_args<M>(lr, clip_value, 0.0, flags),   \
+         flags, st)
+  switch (dtype) {
+    case LOMO_F16: return f64 ? LOMO_ROWS(__half, double) : LOMO_ROWS(__half, float);
+    case LOMO_BF16: return f64 ? LOMO_ROWS(__nv_bfloat16, double) : LOMO_ROWS(__nv_bfloat16, float);
+    case LOMO_F32: return f64 ? LOMO_ROWS(float, double) : LOMO_ROWS(float, float);
+  }
+#undef LOMO_ROWS
   return LOMO_E_ARG;
 }
 

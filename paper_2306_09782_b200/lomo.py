@@ -328,6 +328,10 @@ class LOMO(_Protocol):
         # the fused-GEMM callbacks -- K6 in pass 1, and K5 inside the update
         # backward (the single fused pass, or the strict second backward)
         self._fused_update = self.fuse_gemm and not replay
+        # with the fused paths, an embedding routed through replay.embedding
+        # keeps its gradient as the batch's rows (exact: untouched rows do not
+        # move), never as a dense [V, h] tensor; not with weight decay
+        self.sparse_embedding = self.fuse_gemm and self.weight_decay == 0.0
         self._lin = self._stash if replay else (
             ReplayStash(keep=False) if (self.fuse_probe or self._fused_update) else None)
         self._by_id = {id(p): p for p in uniq}
@@ -366,7 +370,7 @@ class LOMO(_Protocol):
         if mode == _PROBE:
             self.engine.probe(g, self._slot[id(p)])
             lin, st = self._lin, self._stash
-            if lin is not None and id(p) in lin.probed:
+            if lin is not None and (id(p) in lin.probed or id(p) in lin.embedded):
                 # K6 already probed this weight's linear: a hook means another
                 # op contributed gradient too (tied weight), which the fused
                 # paths cannot fold into the norm or the update
@@ -386,7 +390,7 @@ class LOMO(_Protocol):
                         self._replay_mismatch.append(tuple(p.shape))
         else:
             lin = self._lin
-            if lin is not None and id(p) in lin.updated:
+            if lin is not None and (id(p) in lin.updated or id(p) in lin.embedded):
                 # K5 already applied this weight's linear gradient in place; a
                 # hook means another op fed it too (tied weight)
                 self._replay_mismatch.append(tuple(p.shape))
@@ -410,6 +414,8 @@ class LOMO(_Protocol):
             lin.clear()
             lin.probe = self._gemm_probe if (mode == _PROBE and self.fuse_probe) else None
             lin.update = self._gemm_update_bw if mode == _UPDATE else None
+            lin.embed = (self._embed_rows if self.sparse_embedding and
+                         (mode == _UPDATE or self.fuse_probe) else None)
             if mode == _UPDATE:
                 self._load_coefs()
             _replay._ACTIVE = lin
@@ -553,6 +559,43 @@ class LOMO(_Protocol):
         self.hook_calls += 1
         return True
 
+    def _embed_rows(self, wid: int, ids, dy) -> bool:
+        """An embedding's gradient as the batch's aggregated rows: probed by
+        K2 in pass 1 (kept for the replayed pass 2), or updated in place by
+        the rows form of K1 in an update pass."""
+        p = self._by_id.get(wid)
+        if p is None or p.dim() != 2 or p.dtype == torch.float64:
+            return False
+        h = p.shape[1]
+        ids1 = ids.reshape(-1)
+        dy2 = dy.reshape(-1, h)
+        if not dy2.is_contiguous() or dy2.dtype != p.dtype or ids1.dtype != torch.int64:
+            return False
+        ntok = ids1.numel()
+        sorted_ids, perm = torch.sort(ids1, stable=True)
+        rows = torch.empty(ntok, h, dtype=p.dtype, device=p.device)
+        row_ids = torch.empty(ntok, dtype=torch.int64, device=p.device)
+        eng, dt = self.engine, dtype_code(p.dtype)
+        _lib.check(eng.lib.lomo_rows_aggregate(sorted_ids.data_ptr(), perm.data_ptr(),
+                                               dy2.data_ptr(), ntok, h, dt, rows.data_ptr(),
+                                               row_ids.data_ptr(), eng.stream()),
+                   "lomo_rows_aggregate")
+        if self._mode == _PROBE:
+            eng.probe(rows, self._slot[wid])
+            if self._lin is not None and self._lin.keep:
+                self._lin.rows[wid] = (rows, row_ids)
+        else:
+            self._update_rows(p, rows, row_ids)
+        self.hook_calls += 1
+        return True
+
+    def _update_rows(self, p, rows, row_ids) -> None:
+        eng, d = self.engine, self.engine.dispatch
+        _lib.check(eng.lib.lomo_fused_update_rows(
+            p.data_ptr(), rows.data_ptr(), row_ids.data_ptr(), rows.shape[0], rows.shape[1],
+            dtype_code(p.dtype), eng.math, d.lr, d.clip, d.wd, d.flags, eng.ptr, eng.stream()),
+            "lomo_fused_update_rows")
+
     def _finish_probes(self) -> None:
         """One launch (per 64 linears) folds every deferred K6 partial-sum matrix
         of this pass into its norm slot, in stream order before K3a."""
@@ -609,6 +652,11 @@ class LOMO(_Protocol):
                         continue
                 g = _replay.weight_grad(x, dy)
                 del x, dy
+            elif pid in st.rows:
+                rows, row_ids = st.rows.pop(pid)
+                self._update_rows(p, rows, row_ids)
+                self.hook_calls += 1
+                continue
             elif pid in st.grads:
                 g = st.grads.pop(pid)
             else:

@@ -48,6 +48,11 @@ class ReplayStash:
         # w, x, dy) -> bool, True when the weight was updated in place
         self.update = None
         self.updated: set[int] = set()
+        # row-sparse embedding gradient: embed(weight id, w, ids, dy) -> bool;
+        # `rows` keeps (rows, row_ids) per embedding for pass-2 replay
+        self.embed = None
+        self.embedded: set[int] = set()
+        self.rows: dict[int, tuple[torch.Tensor, torch.Tensor]] = {}
 
     def clear(self):
         self.linear.clear()
@@ -56,6 +61,8 @@ class ReplayStash:
         self.shared.clear()
         self.probed.clear()
         self.updated.clear()
+        self.embedded.clear()
+        self.rows.clear()
 
     def nbytes(self) -> int:
         n = sum(x.numel() * x.element_size() + d.numel() * d.element_size()
@@ -143,6 +150,39 @@ def matmul_in_out(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     if torch.is_grad_enabled() and w.requires_grad:
         return _StashLinearIO.apply(x, w)
     return x.matmul(w)
+
+
+class _Embedding(torch.autograd.Function):
+    """F.embedding whose backward can hand LOMO the batch's rows instead of
+    a dense [V, h] gradient (lomo_rows_aggregate / lomo_fused_update_rows)."""
+
+    @staticmethod
+    def forward(ctx, ids, w):
+        ctx.save_for_backward(ids)
+        ctx.wid = id(w)
+        ctx.num = w.shape[0]
+        return F.embedding(ids, w)
+
+    @staticmethod
+    def backward(ctx, dy):
+        (ids,) = ctx.saved_tensors
+        st = _ACTIVE
+        if st is not None:
+            if ctx.wid in st.seen:
+                st.shared.add(ctx.wid)
+            st.seen.add(ctx.wid)
+            if ctx.wid not in st.shared and st.embed is not None \
+                    and st.embed(ctx.wid, ids, dy):
+                st.embedded.add(ctx.wid)
+                return None, None
+        return None, torch.ops.aten.embedding_backward(dy, ids, ctx.num, -1, False, False)
+
+
+def embedding(ids: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """``F.embedding(ids, w)`` whose backward can stay row-sparse under LOMO."""
+    if torch.is_grad_enabled() and w.requires_grad:
+        return _Embedding.apply(ids, w)
+    return F.embedding(ids, w)
 
 
 def linear(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:

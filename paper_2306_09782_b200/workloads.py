@@ -29,6 +29,7 @@ import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
+from .replay import embedding as rembedding
 from .replay import linear as rlinear
 from .replay import matmul_in_out as _mm_in_out
 
@@ -626,7 +627,7 @@ class Llama(nn.Module):
         return self._rope_cache[key]
 
     def forward(self, ids):
-        x = F.embedding(ids, self.embed_tokens)
+        x = rembedding(ids, self.embed_tokens)
         cos, sin = self._cos_sin(ids.shape[1], ids.device, x.dtype)
         if self.fused_proj:  # residual adds fused into the norms (forward_res)
             pending = None
