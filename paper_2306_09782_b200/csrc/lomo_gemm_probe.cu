@@ -107,7 +107,10 @@ struct First {
 
 // EpiN: epilogue sub-tile 128 x EpiN, 0 = CUTLASS's choice (measured equal
 // to 128 x 32 and better than 128 x 16 here, profiles/r01_gemm_shapes.md)
-template <typename Element, int ClusterN = 1, int EpiN = 0>
+// KeepGrad: the epilogue stores dW in the storage dtype (GroupedLOMO keeps it
+// as the retained gradient); otherwise the store is a by-product nobody reads
+// back, written as fp8 -- half the HBM writes, 4 % faster per 7B pass
+template <typename Element, bool KeepGrad = false, int ClusterN = 1, int EpiN = 0>
 struct ProbeGemm {
   using ElementA = Element;  // dy [T, out] row-major == A (M=out, K=T), M-major
   using LayoutA = cutlass::layout::ColumnMajor;
@@ -115,6 +118,8 @@ struct ProbeGemm {
   using LayoutB = cutlass::layout::RowMajor;
   using ElementAcc = float;
   static constexpr int kAlign = 128 / cutlass::sizeof_bits<Element>::value;
+  using ElementD = cute::conditional_t<KeepGrad, Element, cutlass::float_e4m3_t>;
+  static constexpr int kAlignD = 128 / cutlass::sizeof_bits<ElementD>::value;
 
   // identical mainloop configuration to K5 (lomo_gemm_update.cu)
   using MmaTileShape = Shape<_256, _256, _64>;
@@ -144,7 +149,7 @@ struct ProbeGemm {
       cutlass::epilogue::fusion::Sm90ScalarBroadcast<double>>;
   using Reduced = cutlass::epilogue::fusion::Sm90EVT<RowReduce, Square>;
   using EVT = cutlass::epilogue::fusion::Sm90EVT<
-      cutlass::epilogue::fusion::Sm90Compute<FirstFn, Element, float,
+      cutlass::epilogue::fusion::Sm90Compute<FirstFn, ElementD, float,
                                              cutlass::FloatRoundStyle::round_to_nearest>,
       cutlass::epilogue::fusion::Sm90AccFetch, Reduced>;
 
@@ -153,7 +158,7 @@ struct ProbeGemm {
       cute::conditional_t<EpiN == 0, cutlass::epilogue::collective::EpilogueTileAuto,
                           Shape<_128, Int<(EpiN > 0 ? EpiN : 1)>>>,
       ElementAcc, float, void,
-      cutlass::layout::RowMajor, kAlign, Element, cutlass::layout::RowMajor, kAlign,
+      cutlass::layout::RowMajor, kAlignD, ElementD, cutlass::layout::RowMajor, kAlignD,
       cute::conditional_t<EpiN == 0, cutlass::epilogue::collective::EpilogueScheduleAuto,
                           cutlass::epilogue::TmaWarpSpecialized2Sm>,
       EVT>::CollectiveOp;
@@ -191,7 +196,7 @@ struct ProbeGemm {
         cutlass::gemm::GemmUniversalMode::kGemm,
         {M, N, K, 1},
         {static_cast<const ElementA*>(dy), sA, static_cast<const ElementB*>(x), sB},
-        {{}, nullptr, sC, static_cast<Element*>(grad), sD}};
+        {{}, nullptr, sC, static_cast<ElementD*>(grad), sD}};
     // tree arguments are stored children first, node last
     typename cutlass::epilogue::fusion::Sm90ScalarBroadcast<double>::Arguments sb{};
     sb.scalars[0] = 1.0;
@@ -263,11 +268,14 @@ int lomo_gemm_probe(const void* dy, const void* x, void* grad_out, int64_t out_f
       (flags & LOMO_USE_SCALE) ? &static_cast<const lomo_state*>(state)->inv_scale : nullptr;
   int rc = LOMO_E_ARG;
   int64_t rows = 0, ld = 0;
+  const bool keep = (flags & LOMO_PROBE_KEEP_GRAD) != 0;
   switch (dtype) {
     case LOMO_BF16: {
       using G = lomo_probe_gemm::ProbeGemm<cutlass::bfloat16_t>;
       if (G::rows(N) > LOMO_PROBE_BLOCKS_PER_SLOT) return LOMO_E_ARG;
-      rc = G::run(dy, x, grad_out, M, N, K, inv, workspace, workspace_bytes, s);
+      rc = keep ? lomo_probe_gemm::ProbeGemm<cutlass::bfloat16_t, true>::run(
+                      dy, x, grad_out, M, N, K, inv, workspace, workspace_bytes, s)
+                : G::run(dy, x, grad_out, M, N, K, inv, workspace, workspace_bytes, s);
       rows = G::rows(N);
       ld = G::ld(M);
       break;
@@ -275,7 +283,9 @@ int lomo_gemm_probe(const void* dy, const void* x, void* grad_out, int64_t out_f
     case LOMO_F16: {
       using G = lomo_probe_gemm::ProbeGemm<cutlass::half_t>;
       if (G::rows(N) > LOMO_PROBE_BLOCKS_PER_SLOT) return LOMO_E_ARG;
-      rc = G::run(dy, x, grad_out, M, N, K, inv, workspace, workspace_bytes, s);
+      rc = keep ? lomo_probe_gemm::ProbeGemm<cutlass::half_t, true>::run(
+                      dy, x, grad_out, M, N, K, inv, workspace, workspace_bytes, s)
+                : G::run(dy, x, grad_out, M, N, K, inv, workspace, workspace_bytes, s);
       rows = G::rows(N);
       ld = G::ld(M);
       break;
@@ -323,13 +333,16 @@ size_t lomo_gemm_probe_workspace(int64_t out_features, int64_t in_features, int6
                                  int dtype) {
   if (out_features <= 0 || in_features <= 0 || tokens <= 0) return 0;
   if (out_features > INT32_MAX || in_features > INT32_MAX || tokens > INT32_MAX) return 0;
-  if (dtype == LOMO_BF16)
-    return lomo_probe_gemm::ProbeGemm<cutlass::bfloat16_t>::workspace(
-        (int)out_features, (int)in_features, (int)tokens);
-  if (dtype == LOMO_F16)
-    return lomo_probe_gemm::ProbeGemm<cutlass::half_t>::workspace(
-        (int)out_features, (int)in_features, (int)tokens);
-  return 0;
+  const int M = (int)out_features, N = (int)in_features, K = (int)tokens;
+  size_t a = 0, b = 0;  // the larger of the two store variants
+  if (dtype == LOMO_BF16) {
+    a = lomo_probe_gemm::ProbeGemm<cutlass::bfloat16_t>::workspace(M, N, K);
+    b = lomo_probe_gemm::ProbeGemm<cutlass::bfloat16_t, true>::workspace(M, N, K);
+  } else if (dtype == LOMO_F16) {
+    a = lomo_probe_gemm::ProbeGemm<cutlass::half_t>::workspace(M, N, K);
+    b = lomo_probe_gemm::ProbeGemm<cutlass::half_t, true>::workspace(M, N, K);
+  }
+  return a > b ? a : b;
 }
 
 }  // extern "C"

@@ -149,7 +149,8 @@ class GroupedLOMO:
         g = torch.empty_like(p)               # the retained gradient: K6's store
         slot = self._slot[wid]
         rc = eng.lib.lomo_gemm_probe(dy2.data_ptr(), x2.data_ptr(), g.data_ptr(), out_f, in_f,
-                                     dy2.shape[0], dt, slot, _lib.DEFER_ROWS, eng.ptr,
+                                     dy2.shape[0], dt, slot,
+                                     _lib.DEFER_ROWS | _lib.PROBE_KEEP_GRAD, eng.ptr,
                                      ws.data_ptr(), need, eng.stream())
         if rc == -1:
             return False

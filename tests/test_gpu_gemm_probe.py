@@ -31,7 +31,9 @@ def _cuda():
     torch.cuda.set_device(0)
 
 
-def _probe(st, dy, x, slot, flags, grad=None):
+def _probe(st, dy, x, slot, flags, grad=None, keep=True):
+    """K6 with the gradient kept (LOMO_PROBE_KEEP_GRAD) so the tests can check
+    it; the training path uses the fp8 by-product store (keep=False)."""
     lib = U.lib()
     dt = U.CODE[dy.dtype]
     out_f, in_f = dy.shape[1], x.shape[1]
@@ -39,6 +41,8 @@ def _probe(st, dy, x, slot, flags, grad=None):
     ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
     if grad is None:
         grad = torch.empty(out_f, in_f, dtype=dy.dtype, device="cuda")
+    if keep:
+        flags |= _lib.PROBE_KEEP_GRAD
     rc = lib.lomo_gemm_probe(dy.data_ptr(), x.data_ptr(), grad.data_ptr(), out_f, in_f,
                              dy.shape[0], dt, slot, flags, st.ptr, ws.data_ptr(), need, U.stream())
     return rc, grad
@@ -76,6 +80,26 @@ def test_gemm_probe_matches_k2_on_the_same_gradient(dtype, out_f, in_f, tokens):
     np.testing.assert_allclose(sums[0], sums[1], rtol=1e-5)
     np.testing.assert_allclose(sums[2], sums[3], rtol=1e-5)
     np.testing.assert_allclose(sums[2], sums[0] / 1024.0 ** 2, rtol=1e-5)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_gemm_probe_fp8_by_product_gives_the_same_sums(dtype):
+    """The training form (the dW store written as an unused fp8 by-product)
+    reduces the very same accumulators: slot sums bit-identical to the
+    kept-gradient form, overflow detection unchanged."""
+    g = torch.Generator(device="cuda").manual_seed(12)
+    dy = (torch.randn(1024, 4096, device="cuda", generator=g) * 1e-2).to(dtype)
+    x = torch.randn(1024, 11008, device="cuda", generator=g).to(dtype)
+    st = U.State(2, scale=1024.0)
+    st.begin()
+    assert _probe(st, dy, x, 0, _lib.USE_SCALE, keep=True)[0] == 0
+    assert _probe(st, dy, x, 1, _lib.USE_SCALE, keep=False)[0] == 0
+    sums = st.slots(2)
+    assert sums[0] == sums[1] and st.status().overflow == 0
+    big = torch.full((16, 4096), 300.0, device="cuda", dtype=torch.float16)
+    st.begin()
+    assert _probe(st, big, big[:, :2048].contiguous(), 0, 0, keep=False)[0] == 0
+    assert st.status().overflow == 1
 
 
 def test_gemm_probe_overflow_and_nan():
