@@ -649,6 +649,12 @@ def bench_memory_table(args):
     from paper_2306_09782_b200 import LOMO, LossScaler
     from paper_2306_09782_b200.workloads import Llama
     rows = {}
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    # whatever earlier legs of this process still hold (graph pools) is not
+    # this table's memory: every figure below is relative to it
+    pre = torch.cuda.memory_allocated()
     for ac in (False, True):
         torch.cuda.empty_cache()
         model = Llama("7b", dtype=torch.float16, device="cuda", checkpointing=ac)
@@ -667,7 +673,7 @@ def bench_memory_table(args):
         gib = 2 ** 30
         rows["ac" if ac else "no_ac"] = {
             "params_gib": round(params / gib, 2),
-            "step_peak_gib": round(peak / gib, 2),
+            "step_peak_gib": round((peak - pre) / gib, 2),
             "peak_above_resident_gib": round((peak - base) / gib, 2),
             "largest_gradient_gib": round(max(p.numel() * p.element_size()
                                               for p in model.parameters()) / gib, 3),
