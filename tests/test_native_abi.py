@@ -64,6 +64,26 @@ def test_argument_errors_need_no_gpu():
     assert lib.lomo_wl_swiglu_bwd(8, 16, 16, 16, 16, 16, 1, None) == -1             # misaligned
     assert lib.lomo_wl_rmsnorm_partial_rows(1024) == 256
     assert lib.lomo_wl_rmsnorm_partial_rows(0) == 0
+    # K6 and its reductions, the row-sparse embedding forms
+    assert lib.lomo_gemm_probe(None, None, None, 64, 64, 64, _lib.BF16, 0, 0, None, None, 0,
+                               None) == -1
+    assert lib.lomo_gemm_probe(16, 16, 16, 64, 64, 64, _lib.BF16, -1, 0, 16, 16, 1 << 20,
+                               None) == -2                                          # slot
+    assert lib.lomo_gemm_probe(16, 16, 16, 64, 64, 64, _lib.BF16, 0, _lib.ACCUM_F64, 16, 16,
+                               1 << 20, None) == -1                                 # f64 mode
+    assert lib.lomo_gemm_probe_workspace(0, 64, 64, _lib.BF16) == 0
+    assert lib.lomo_gemm_probe_finish(None, None, None, None, 0, _lib.BF16, 16, None) == 0
+    assert lib.lomo_gemm_probe_finish(None, None, None, None, 1, _lib.BF16, 16, None) == -1
+    assert lib.lomo_probe_rows(16, 0, 8, 8, 0, 16, None) == -1                      # rows < 1
+    assert lib.lomo_probe_rows(16, 2, 4, 8, 0, 16, None) == -1                      # ld < cols
+    assert lib.lomo_probe_rows(16, 2, 8, 8, -1, 16, None) == -2
+    assert lib.lomo_probe_rows_multi(None, None, None, None, None, 0, 16, None) == 0
+    assert lib.lomo_rows_aggregate(None, None, None, 0, 8, _lib.BF16, None, None, None) == 0
+    assert lib.lomo_rows_aggregate(None, None, None, 4, 8, _lib.BF16, None, None, None) == -1
+    assert lib.lomo_fused_update_rows(16, 16, 16, 4, 8, _lib.BF16, 0, 0.1, 0.0, 0.01, 0,
+                                      None, None) == -1                             # wd != 0
+    assert lib.lomo_fused_update_rows(16, 16, 16, 4, 8, _lib.BF16, 0, 0.1, 0.0, 0.0,
+                                      _lib.USE_SKIP, None, None) == -1              # no state
 
 
 def test_status_struct_layout_matches_c(tmp_path):
