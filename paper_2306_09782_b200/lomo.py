@@ -263,14 +263,16 @@ class LOMO(_Protocol):
             from the (input, output-gradient) pair stashed in pass 1 instead of
             running a second backward (see replay.py); the model's linears
             must go through ``paper_2306_09782_b200.replay.linear``.
-        fuse_gemm: with ``replay``, run each linear's pass-2 update as the
-            epilogue of its weight-gradient GEMM on the tensor cores (K5,
+        fuse_gemm: run each linear's update as the epilogue of its
+            weight-gradient GEMM on the tensor cores (K5,
             csrc/lomo_gemm_update.cu): ``p <- p - lr*coef/scale * (dy^T x)`` from
-            the fp32 accumulator, the gradient never materialised.  16-bit
-            parameters, fp32 math, no value clip; other parameters keep K1.
-            Without ``replay`` the update runs inside each linear's backward
+            the fp32 accumulator, the gradient never materialised -- over the
+            pass-1 stash with ``replay``, else inside each linear's backward
             (the single fused pass, or the strict protocol's second backward).
-        fuse_probe: with ``replay`` (default: on when ``fuse_gemm`` is), run
+            16-bit parameters, fp32 math, no value clip; other parameters keep
+            K1, and an embedding routed through ``replay.embedding`` keeps its
+            gradient as the batch's rows (exact; not with weight decay).
+        fuse_probe: two-pass mode (default: on when ``fuse_gemm`` is): run
             each linear's pass-1 probe as the epilogue of its weight-gradient
             GEMM (K6, csrc/lomo_gemm_probe.cu): the overflow flag and the sum of
             squares come out of the tensor-core accumulator, so no K2 launch
