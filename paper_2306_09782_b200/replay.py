@@ -14,7 +14,14 @@ no second forward, no input-gradient GEMMs, no elementwise backward.
 The update arithmetic is untouched: K1 sees bit-identical gradients to the
 ones K2 probed (same kernels, same inputs).  Enabled with
 ``LOMO(..., replay=True)``; models opt in by calling :func:`linear` instead of
-``F.linear`` (``workloads.Llama`` does).
+``F.linear`` (``workloads.Llama`` does), or :func:`matmul_in_out` for weights
+stored ``[in, out]`` (the reference zoo's layout).
+
+The same backward context also carries the fused-GEMM callbacks, with or
+without replay: ``probe`` (K6: the pass-1 probe inside the weight-gradient
+GEMM), ``update`` (K5 inside the backward) and ``embed`` (an embedding's
+gradient kept as the batch's aggregated rows, :func:`embedding`).  A weight
+taken by a callback returns ``None`` to autograd: its gradient never exists.
 """
 from __future__ import annotations
 
