@@ -410,6 +410,26 @@ __global__ void __launch_bounds__(kThreads)
   int64_t end = j + 1;
   if (head)
     while (end < ntok && sorted[end] == id) ++end;
+  constexpr int V = 16 / sizeof(T);
+  if ((h % V) == 0 && (((uintptr_t)dy | (uintptr_t)rows) & 15) == 0) {  // 16-byte vectors
+    for (int64_t c = threadIdx.x; c < h / V; c += blockDim.x) {
+      float acc[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[e] = 0.f;
+      if (head)
+        for (int64_t k = j; k < end; ++k) {
+          Vec16<T> D;
+          D.u = ld_stream_ro(reinterpret_cast<const uint4*>(dy + perm[k] * h) + c);
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[e] += to_m<float>(D.e[e]);
+        }
+      Vec16<T> O;
+#pragma unroll
+      for (int e = 0; e < V; ++e) O.e[e] = from_m<T, float>(acc[e]);
+      reinterpret_cast<uint4*>(rows + j * h)[c] = O.u;
+    }
+    return;
+  }
   for (int64_t c = threadIdx.x; c < h; c += blockDim.x) {
     float acc = 0.f;
     if (head)
@@ -705,7 +725,18 @@ __global__ void __launch_bounds__(kThreads) k6_rows_multi(const __grid_constant_
   const int64_t cols = tab.cols[e];
   double acc = 0.0;
   bool bad = false;
-  for (int64_t c = threadIdx.x; c < cols; c += kThreads) {
+  int64_t c = threadIdx.x;
+  for (; c + 3 * kThreads < cols; c += 4 * kThreads) {  // four loads in flight
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = row[c + u * kThreads];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bad |= isnan(v[u]);
+      acc += (double)v[u];
+    }
+  }
+  for (; c < cols; c += kThreads) {
     const float v = row[c];
     bad |= isnan(v);
     acc += (double)v;
