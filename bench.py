@@ -501,17 +501,18 @@ def bench_train(args, rank, world):
            "clip_grad_norm": 1.0, "activation_checkpointing": bool(ckpt),
            "paper_tgs_rtx3090": 769.92}
     gstep = None
-    variants = ("strict", "strict_fused_gemm", "replay", "replay_fused_gemm",
+    variants = ("strict", "strict_fused_gemm", "strict_fused_gemm_graph", "replay",
+                "replay_fused_gemm",
                 "replay_fused_gemm_graph", "grouped", "grouped_fused_gemm",
                 "single_pass_fused_gemm") \
         if not args.train_variants else \
         tuple(args.train_variants.split(","))
     for key in variants:
-        if key == "replay_fused_gemm_graph":
+        if key in ("replay_fused_gemm_graph", "strict_fused_gemm_graph"):
             from paper_2306_09782_b200.graphs import GraphedLOMOStep
             opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
                        loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
-                       replay=True, fuse_gemm=True)
+                       replay=key.startswith("replay"), fuse_gemm=True)
             static = data[0].clone()
             gstep = GraphedLOMOStep(opt, lambda d: model.loss(d[:, :-1], d[:, 1:]), (static,),
                                     warmup=max(2, args.train_warmup), lr=1e-3)
@@ -536,7 +537,7 @@ def bench_train(args, rank, world):
                        replay=key.startswith("replay"),
                        fuse_gemm=key in ("replay_fused_gemm", "strict_fused_gemm"))
 
-        if key != "replay_fused_gemm_graph":
+        if key not in ("replay_fused_gemm_graph", "strict_fused_gemm_graph"):
             def step(k, opt=opt):
                 d = data[k % len(data)]
                 return opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)

@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from .errors import ConfigError, ScaleUnderflowError
-from .lomo import LOMO, _PROBE
+from .lomo import LOMO, _PROBE, _UPDATE
 from .stabilize import StepOutcome
 
 
@@ -33,8 +33,11 @@ class GraphedLOMOStep:
     """Capture ``loss_fn(*static_inputs)`` + the LOMO two-pass replay step.
 
     Args:
-        opt: a :class:`LOMO` built with ``replay=True`` (``fuse_gemm`` optional)
-            and a two-pass stabiliser (clip_grad_norm and/or loss_scale).
+        opt: a :class:`LOMO` with a two-pass stabiliser (clip_grad_norm and/or
+            loss_scale), built with ``replay=True`` (``fuse_gemm`` optional), or
+            with ``fuse_gemm=True`` alone: the reference's protocol as is -- pass
+            2 a second backward over the retained graph, K6 in pass 1 and K5
+            inside pass 2 -- captured the same way (no replay stash).
         loss_fn: the forward, returning the scalar loss.
         static_inputs: tensors ``loss_fn`` reads; copy each batch into them.
         warmup: eager steps run before capture (they also perform replay's
@@ -44,9 +47,11 @@ class GraphedLOMOStep:
 
     def __init__(self, opt: LOMO, loss_fn: Callable[..., torch.Tensor],
                  static_inputs: Sequence[torch.Tensor], warmup: int = 2, lr: float = 1e-3):
-        if not isinstance(opt, LOMO) or opt._stash is None or opt.passes != 2:
-            raise ConfigError("GraphedLOMOStep needs LOMO(..., replay=True) with clip_grad_norm "
-                              "and/or loss_scale")
+        if not isinstance(opt, LOMO) or opt.passes != 2 or \
+                (opt._stash is None and not opt._fused_update):
+            raise ConfigError("GraphedLOMOStep needs a two-pass LOMO (clip_grad_norm and/or "
+                              "loss_scale) with replay=True or fuse_gemm=True")
+        self.strict = opt._stash is None
         if opt.clip_value:
             raise ConfigError("value clipping is a single-pass mode; graph it with LOMO directly")
         self.opt, self.loss_fn, self.inputs = opt, loss_fn, tuple(static_inputs)
@@ -59,7 +64,7 @@ class GraphedLOMOStep:
                 opt.step(lambda: loss_fn(*self.inputs), lr)
         torch.cuda.current_stream(opt.device).wait_stream(side)
         torch.cuda.synchronize(opt.device)
-        if not opt._replay_checked:
+        if not self.strict and not opt._replay_checked:
             raise ConfigError("replay's first-step check did not run during warm-up")
 
         pool = torch.cuda.graph_pool_handle()
@@ -68,7 +73,9 @@ class GraphedLOMOStep:
             self.loss = loss_fn(*self.inputs)
             eng.begin(self.loss)
             eng.configure(flags=opt._flags(_PROBE))
-            opt._run_backward(opt._scaled(self.loss), _PROBE, False)
+            # strict: the autograd graph is kept for pass 2's backward (and
+            # across replays -- its saved tensors live in the graph pool)
+            opt._run_backward(opt._scaled(self.loss), _PROBE, self.strict)
             opt._decide()
         self.g2 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.g2, pool=pool):
@@ -78,6 +85,17 @@ class GraphedLOMOStep:
     def _capture_pass2(self) -> None:
         opt, eng = self.opt, self.opt.engine
         flags = opt._flags(2) | _lib.LR_FROM_STATE
+        if self.strict:
+            # the second backward with K5 in every linear (alpha/beta computed on
+            # device from the state, whose lr step() sets before each replay)
+            eng.configure(0.0, opt.clip_value, opt.weight_decay, flags)
+            opt._lr_from_state = True
+            try:
+                opt._run_backward(opt._scaled(self.loss), _UPDATE, True)
+            finally:
+                opt._lr_from_state = False
+            eng.on_clean()
+            return
         _lib.check(eng.lib.lomo_update_coefs(eng.ptr, opt.weight_decay, flags,
                                              self.coefs.data_ptr(), eng.stream()),
                    "lomo_update_coefs")

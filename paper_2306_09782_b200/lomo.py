@@ -338,6 +338,7 @@ class LOMO(_Protocol):
             ReplayStash(keep=False) if (self.fuse_probe or self._fused_update) else None)
         self._by_id = {id(p): p for p in uniq}
         self._coefs = None
+        self._lr_from_state = False  # graph capture: the state's lr, set per replay
         self._pws = {}         # K6 workspace per weight (its partial sums stay until
                                # the end of pass 1: one deferred reduction launch)
         self._pending_probe = []  # (workspace ptr, out, in, slot) awaiting that launch
@@ -548,7 +549,8 @@ class LOMO(_Protocol):
         if self._coefs is None:
             self._coefs = torch.zeros(2, dtype=torch.float32, device=self.device)
         d = eng.dispatch
-        _lib.check(eng.lib.lomo_set_lr(eng.ptr, d.lr, eng.stream()), "lomo_set_lr")
+        if not self._lr_from_state:
+            _lib.check(eng.lib.lomo_set_lr(eng.ptr, d.lr, eng.stream()), "lomo_set_lr")
         _lib.check(eng.lib.lomo_update_coefs(eng.ptr, self.weight_decay, d.flags,
                                              self._coefs.data_ptr(), eng.stream()),
                    "lomo_update_coefs")

@@ -160,3 +160,37 @@ def test_graphed_step_equals_eager_step(fuse):
         assert la == lb, (k, la, lb)
     for x, y in zip(a.parameters(), b.parameters()):
         assert torch.equal(x, y)
+
+
+def test_graphed_strict_fused_step_equals_eager():
+    """The reference's two-pass protocol (pass 2 a second backward, no stash)
+    with K6/K5 inside the backward, captured in two CUDA graphs: decisions
+    and loss-scale trajectory equal to the eager step, parameters equal up to
+    the second backward's attention nondeterminism."""
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.graphs import GraphedLOMOStep
+    from paper_2306_09782_b200.workloads import Llama
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+    torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
+    cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
+    a = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    b = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    kw = dict(lr=0.05, clip_grad_norm=0.3, loss_scale=2.0 ** 8, fuse_gemm=True)
+    oa, ob = LOMO(a, **kw), LOMO(b, **kw)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    data = [torch.randint(0, 256, (2, 65), device="cuda", generator=gen) for _ in range(6)]
+    static = data[0].clone()
+    for _ in range(2):
+        oa.step(lambda: a.loss(data[0][:, :-1], data[0][:, 1:]), 0.05)
+    gs = GraphedLOMOStep(ob, lambda d: b.loss(d[:, :-1], d[:, 1:]), (static,), warmup=2, lr=0.05)
+    assert gs.strict
+    for k in range(1, 6):
+        lr = 0.05 / k
+        la = oa.step(lambda: a.loss(data[k][:, :-1], data[k][:, 1:]), lr)
+        static.copy_(data[k])
+        lb = gs.step(lr).item()
+        assert oa.last_outcome == ob.last_outcome
+        assert abs(la - lb) <= 1e-3 * abs(la)
+    assert oa.loss_scale == ob.loss_scale
+    for x, y in zip(a.parameters(), b.parameters()):
+        torch.testing.assert_close(x.float(), y.float(), rtol=2 ** -6, atol=1e-4)
