@@ -431,11 +431,27 @@ def bench_e2e(args, rank, world):
     end.record()
     _barrier(world)
     ms = _max_over_ranks(start.elapsed_time(end), world) / steps
+    # the link bound: the same step's H2D copies alone (p and g of every
+    # tensor into the slots), one copy stream, nothing else running
+    with torch.cuda.stream(h2d):
+        h2d.wait_stream(comp)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(h2d)
+        for k, i in enumerate(order):
+            s = k % NS
+            DP[s][:shapes[i]].copy_(HP[i], non_blocking=True)
+            DG[s][:shapes[i]].copy_(HG[i], non_blocking=True)
+        s1.record(h2d)
+    s1.synchronize()
+    h2d_ms = s0.elapsed_time(s1)
     elems = _sum_over_ranks(sum(shapes), world)
     esz = 2
     return {"value": round(BYTES_PER_ELEM * elems / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": 2 * esz * sum(shapes), "d2h_bytes_per_step": esz * sum(shapes),
             "ms_per_step": round(ms, 2), "steps": steps,
+            "h2d_only_ms_per_step": round(h2d_ms, 2),
+            "h2d_link_gbs": round(2 * esz * sum(shapes) / (h2d_ms * 1e-3) / 1e9, 2),
+            "link_bound_frac": round(h2d_ms / ms, 3),
             "path": "C-ABI lomo_fused_update, pinned host p/g -> HBM -> K1 -> host p"}
 
 
