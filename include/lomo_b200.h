@@ -72,7 +72,7 @@ typedef enum {
 #define LOMO_DEFER_ROWS 0x20u /* K6: leave the partial sums in the workspace; */
                               /* lomo_gemm_probe_finish reduces a batch of them  */
 #define LOMO_PROBE_KEEP_GRAD 0x40u /* K6: grad_out receives dW in the storage  */
-                                   /* dtype (else an fp4 scratch, out*in/2 B)  */
+                                   /* dtype (else a 16-byte scratch)           */
 #define LOMO_ACCUM_F64 0x8u /* K2: accumulate every square in f64 (the reference's */
                             /* float64 dot, stabilize.py:199); default for 16-bit   */
                             /* storage: exact fp32 squares summed per 16-byte      */
@@ -255,10 +255,10 @@ int lomo_update_coefs(const void* state, double weight_decay, unsigned flags,
  * storage dtype, raises state->overflow if it is non-finite and accumulates
  * (g * inv_scale)^2 into norm slot `slot`, so the gradient is never read back.
  * grad_out receives the epilogue's store of dW: with LOMO_PROBE_KEEP_GRAD
- * the gradient itself ([out, in], dtype -- a retained gradient); otherwise an
- * fp4 (e2m1) by-product nobody reads (a scratch of out*in/2 bytes the caller
- * may reuse at once, stream-ordered; a quarter of the fp16 store's HBM
- * writes).  Without KEEP_GRAD in_features must be a multiple of 32.
+ * the gradient itself ([out, in], dtype -- a retained gradient); otherwise no
+ * gradient leaves the SM: grad_out is a 16-byte scratch (32 fp4 elements)
+ * the epilogue's clipped store may touch, reusable at once (stream-ordered).
+ * Without KEEP_GRAD in_features must be a multiple of 32.
  * flags: LOMO_USE_SCALE (LOMO_ACCUM_F64 is refused with LOMO_E_ARG: the
  * exactness mode keeps GEMM + K2).  workspace: >= lomo_gemm_probe_workspace
  * bytes of device memory, reused by every call on one stream.  Shapes as

@@ -19,8 +19,7 @@
 // [ceil(N/256), M] fp32 scratch matrix; k6_rows (lomo_kernels.cu,
 // lomo_probe_rows) sums it in fixed order into the parameter's norm slot and
 // raises the overflow flag if a sum is NaN.  No K2 launch re-reads the
-// gradient; the epilogue's store of dW to a reusable scratch (grad_out)
-// overlaps the next tile's mainloop.
+// gradient, and none is written to HBM (ClippedStore below).
 //
 // Semantics vs the materialised path (cuBLAS dW -> K2):
 //  * overflow: an element whose storage rounding is +-inf or NaN makes its
@@ -105,6 +104,28 @@ struct First {
   };
 };
 
+// The by-product store without its HBM traffic.  CUTLASS 4.5's sm100 TMA
+// epilogue has no void-D form, so the non-KeepGrad kernel keeps the store
+// but its TMA descriptor describes only the first kClipN elements of row 0
+// of D: every TMA store box outside that corner is clipped by the TMA unit
+// and writes nothing (the smem staging still runs).  The caller's grad_out
+// then needs only kClipN elements.  Everything else (tiles, EVT, schedule)
+// is the builder's epilogue unchanged.
+constexpr int kClipN = 32;
+template <class Base>
+struct ClippedStore : Base {
+  using Base::Base;
+  template <class ProblemShape>
+  static typename Base::Params to_underlying_arguments(ProblemShape const& problem_shape,
+                                                       typename Base::Arguments const& args,
+                                                       void* workspace) {
+    typename Base::Params p = Base::to_underlying_arguments(problem_shape, args, workspace);
+    ProblemShape corner{1, kClipN, cute::get<2>(problem_shape), cute::get<3>(problem_shape)};
+    p.tma_store_d = Base::to_underlying_arguments(corner, args, workspace).tma_store_d;
+    return p;
+  }
+};
+
 // EpiN: epilogue sub-tile 128 x EpiN, 0 = CUTLASS's choice (measured equal
 // to 128 x 32 and better than 128 x 16 here, profiles/r01_gemm_shapes.md)
 // KeepGrad: the epilogue stores dW in the storage dtype (GroupedLOMO keeps it
@@ -154,7 +175,7 @@ struct ProbeGemm {
                                              cutlass::FloatRoundStyle::round_to_nearest>,
       cutlass::epilogue::fusion::Sm90AccFetch, Reduced>;
 
-  using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+  using BuiltEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
       cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
       cute::conditional_t<EpiN == 0, cutlass::epilogue::collective::EpilogueTileAuto,
                           Shape<_128, Int<(EpiN > 0 ? EpiN : 1)>>>,
@@ -163,6 +184,8 @@ struct ProbeGemm {
       cute::conditional_t<EpiN == 0, cutlass::epilogue::collective::EpilogueScheduleAuto,
                           cutlass::epilogue::TmaWarpSpecialized2Sm>,
       EVT>::CollectiveOp;
+  using CollectiveEpilogue =
+      cute::conditional_t<KeepGrad, BuiltEpilogue, ClippedStore<BuiltEpilogue>>;
 
   using CollectiveMainloop = typename cutlass::gemm::collective::CollectiveBuilder<
       cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, ElementA, LayoutA, kAlign, ElementB,

@@ -342,7 +342,7 @@ class LOMO(_Protocol):
         self._pws = {}         # K6 workspace per weight (its partial sums stay until
                                # the end of pass 1: one deferred reduction launch)
         self._pending_probe = []  # (workspace ptr, out, in, slot) awaiting that launch
-        self._gscratch = None  # K6's by-product store (fp4 dW), reused by every linear
+        self._gscratch = None  # K6's clipped by-product store, shared by every linear
         self._ws = {}          # K5 workspace per stream
         # Optional stream concurrency of the tensor-core GEMMs: pass 2's K5
         # launches are independent of each other and may rotate over
@@ -518,9 +518,8 @@ class LOMO(_Protocol):
         ws = self._pws.get(wid)
         if ws is None or ws.numel() < need:
             ws = self._pws[wid] = torch.empty(need, dtype=torch.uint8, device=w.device)
-        n = (w.numel() + 1) // 2  # bytes: K6's by-product store is fp4
-        if self._gscratch is None or self._gscratch.numel() < n:
-            self._gscratch = torch.empty(n, dtype=torch.uint8, device=w.device)
+        if self._gscratch is None:  # K6's clipped by-product store: 16 bytes
+            self._gscratch = torch.empty(256, dtype=torch.uint8, device=w.device)
         slot = self._slot[wid]
         stream = self.engine.stream()
         if self.probe_stream:

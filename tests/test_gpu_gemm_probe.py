@@ -33,7 +33,7 @@ def _cuda():
 
 def _probe(st, dy, x, slot, flags, grad=None, keep=True):
     """K6 with the gradient kept (LOMO_PROBE_KEEP_GRAD) so the tests can check
-    it; the training path uses the fp8 by-product store (keep=False)."""
+    it; the training path clips the store to a 16-byte scratch (keep=False)."""
     lib = U.lib()
     dt = U.CODE[dy.dtype]
     out_f, in_f = dy.shape[1], x.shape[1]
@@ -83,23 +83,27 @@ def test_gemm_probe_matches_k2_on_the_same_gradient(dtype, out_f, in_f, tokens):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
-def test_gemm_probe_fp8_by_product_gives_the_same_sums(dtype):
-    """The training form (the dW store written as an unused fp8 by-product)
-    reduces the very same accumulators: slot sums bit-identical to the
-    kept-gradient form, overflow detection unchanged."""
+def test_gemm_probe_clipped_store_gives_the_same_sums(dtype):
+    """The training form (no LOMO_PROBE_KEEP_GRAD: the epilogue's dW store is
+    clipped to a 16-byte corner by its TMA descriptor) reduces the very same
+    accumulators: slot sums bit-identical to the kept-gradient form, overflow
+    detection unchanged, and nothing past the 16-byte scratch is written."""
     g = torch.Generator(device="cuda").manual_seed(12)
     dy = (torch.randn(1024, 4096, device="cuda", generator=g) * 1e-2).to(dtype)
     x = torch.randn(1024, 11008, device="cuda", generator=g).to(dtype)
     st = U.State(2, scale=1024.0)
     st.begin()
     assert _probe(st, dy, x, 0, _lib.USE_SCALE, keep=True)[0] == 0
-    assert _probe(st, dy, x, 1, _lib.USE_SCALE, keep=False)[0] == 0
+    canary = torch.full((1 << 20,), 0xAB, dtype=torch.uint8, device="cuda")
+    assert _probe(st, dy, x, 1, _lib.USE_SCALE, grad=canary, keep=False)[0] == 0
     sums = st.slots(2)
     assert sums[0] == sums[1] and st.status().overflow == 0
+    assert (canary[16:] == 0xAB).all()
     big = torch.full((16, 4096), 300.0, device="cuda", dtype=torch.float16)
     st.begin()
-    assert _probe(st, big, big[:, :2048].contiguous(), 0, 0, keep=False)[0] == 0
+    assert _probe(st, big, big[:, :2048].contiguous(), 0, 0, grad=canary, keep=False)[0] == 0
     assert st.status().overflow == 1
+    assert (canary[16:] == 0xAB).all()
 
 
 def test_gemm_probe_overflow_and_nan():
