@@ -31,6 +31,7 @@ with NCCL reduce-scatter feeding the per-shard update.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import math
 import os
@@ -138,10 +139,13 @@ def _dist_init(gpus: int):
         dev = 0 if shared else local
         torch.cuda.set_device(dev)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # a collective that never completes aborts the job after 5 minutes
+        # (NCCL watchdog) instead of holding the box until the driver's limit
+        tmo = datetime.timedelta(minutes=5)
         if shared:
-            dist.init_process_group("gloo")
+            dist.init_process_group("gloo", timeout=tmo)
         else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev), timeout=tmo)
     else:
         torch.cuda.set_device(0)
     return rank, world, local
