@@ -130,8 +130,8 @@ struct ClippedStore : Base {
 // to 128 x 32 and better than 128 x 16 here, profiles/r01_gemm_shapes.md)
 // KeepGrad: the epilogue stores dW in the storage dtype (GroupedLOMO keeps it
 // as the retained gradient); otherwise the store is a by-product nobody reads
-// back, written as fp4 (e2m1) -- a quarter of the HBM writes of fp16; per 7B
-// pass 10.8 ms with an fp16 store, 10.3 with fp8, 9.75 with fp4
+// back, staged as fp4 (e2m1, the fewest smem bytes) and clipped (ClippedStore);
+// per 7B pass 10.8 ms with an fp16 store, 10.3 fp8, 9.80 fp4, 9.5 clipped
 template <typename Element, bool KeepGrad = false, int ClusterN = 1, int EpiN = 0>
 struct ProbeGemm {
   using ElementA = Element;  // dy [T, out] row-major == A (M=out, K=T), M-major
