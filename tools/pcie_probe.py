@@ -1,44 +1,27 @@
-"""Pinned host<->device copy bandwidth on this box (the e2e leg's ceiling)."""
-import torch
-
+import torch, time
 torch.cuda.set_device(0)
-n = 512 * 2 ** 20
-h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-d = torch.empty(n, dtype=torch.uint8, device="cuda")
-d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
-s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-
-
-def t(fn, reps=10):
-    fn()
+n = 256 << 20  # 512 MB of bf16 per buffer
+H = [torch.empty(n, dtype=torch.bfloat16, pin_memory=True) for _ in range(4)]
+D = [torch.empty(n, dtype=torch.bfloat16, device="cuda") for _ in range(4)]
+S = [torch.cuda.Stream() for _ in range(4)]
+def run(kind, ns):
     torch.cuda.synchronize()
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    e[0].record()
-    for _ in range(reps):
-        fn()
-    torch.cuda.current_stream().wait_stream(s1)
-    torch.cuda.current_stream().wait_stream(s2)
-    e[1].record()
-    torch.cuda.synchronize()
-    return e[0].elapsed_time(e[1]) / reps
-
-
-def h2d():
-    with torch.cuda.stream(s1):
-        d.copy_(h, non_blocking=True)
-
-
-def d2h():
-    with torch.cuda.stream(s2):
-        h2.copy_(d2, non_blocking=True)
-
-
-def both():
-    h2d()
-    d2h()
-
-
-for name, fn, b in (("H2D", h2d, n), ("D2H", d2h, n), ("H2D+D2H concurrent", both, 2 * n)):
-    ms = t(fn)
-    print(f"{name:20s} {b / ms / 1e6:7.1f} GB/s")
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(4):
+        s = S[i % ns]
+        s.wait_event(e0)
+        with torch.cuda.stream(s):
+            if kind == "h2d": D[i].copy_(H[i], non_blocking=True)
+            elif kind == "d2h": H[i].copy_(D[i], non_blocking=True)
+            else:
+                if i % 2 == 0: D[i].copy_(H[i], non_blocking=True)
+                else: H[i].copy_(D[i], non_blocking=True)
+    for s in S[:ns]: torch.cuda.current_stream().wait_stream(s)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return 4 * n * 2 / ms / 1e6
+for kind in ("h2d", "d2h", "both"):
+    for ns in (1, 2, 4):
+        r = [run(kind, ns) for _ in range(3)]
+        print(kind, ns, "GB/s", round(max(r), 1))
