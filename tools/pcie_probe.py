@@ -1,3 +1,5 @@
+"""Pinned host<->device copy bandwidth on this box (the e2e leg's ceiling):
+H2D alone, D2H alone, and both directions at once, over 1/2/4 copy streams."""
 import torch, time
 torch.cuda.set_device(0)
 n = 256 << 20  # 512 MB of bf16 per buffer
