@@ -738,8 +738,15 @@ def bench_train_sharded(args, rank, world):
     spec = dict(hidden=512, layers=4, heads=8, ffn=1408, vocab=32000) if size == "tiny" else size
     model = Llama(spec, dtype=torch.float16, device="cuda", checkpointing=ckpt)
     model.train()
+    # 180 GB per GPU: when the gathered model takes under 40 % of HBM, the layer
+    # buckets stay gathered between forward and backward (parameters are still
+    # owned and updated per shard, and re-gathered once per applied step);
+    # otherwise (65B) ZeRO-3 frees each layer after its forward and re-gathers it
+    pbytes = sum(p.numel() * p.element_size() for p in model.parameters())
+    reshard = pbytes > 0.4 * torch.cuda.get_device_properties(0).total_memory
     opt = ShardedLOMO(model, lr=1e-3, clip_grad_norm=1.0,
-                      loss_scale=LossScaler(2.0 ** 10, growth_interval=16))
+                      loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
+                      reshard_after_forward=reshard)
     torch.cuda.empty_cache()
     seq, batch = args.seq, args.batch
     gen = torch.Generator(device="cuda").manual_seed(rank)
@@ -768,6 +775,7 @@ def bench_train_sharded(args, rank, world):
            "tokens_per_gpu_per_s": round(batch * seq / (ms * 1e-3), 1),
            "ms_per_step": round(ms, 2), "seq_len": seq, "batch_per_rank": batch,
            "activation_checkpointing": ckpt, "passes_per_step": 2, "outcomes": outcomes,
+           "reshard_after_forward": reshard,
            "peak_mem_gib_rank0": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
            "paper_tgs_rtx3090": {"13b": 66.19, "30b": 11.61, "65b": 4.93}.get(size)}
     opt.remove_hooks()
@@ -839,6 +847,8 @@ def main():
     ap.add_argument("--train-variants", default="",
                     help="comma list of strict,replay,replay_fused_gemm,replay_fused_gemm_graph,grouped "
              "(default: all)")
+    ap.add_argument("--sharded-train", action="store_true",
+                    help="run the ZeRO-3 sharded train leg even at N=1 (world-1 NCCL group)")
     ap.add_argument("--sharded-model", default="13b", choices=["tiny", "7b", "13b", "30b", "65b"],
                     help="model of the N>1 sharded train leg (config 4: 13b, config 5: 65b)")
     args = ap.parse_args()
@@ -866,6 +876,12 @@ def main():
 
     import torch
     rank, world, local = _dist_init(args.gpus)
+    if args.sharded_train and world == 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
     import __graft_entry__
     __graft_entry__.build()
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -887,7 +903,8 @@ def main():
     e2e = None if args.no_e2e else optional(bench_e2e, args, rank, world)
     train = None
     if not args.no_train:
-        train = optional(bench_train, args, rank, world) if world == 1 else \
+        train = optional(bench_train, args, rank, world) if (world == 1 and not
+                                                              args.sharded_train) else \
             optional(bench_train_sharded, args, rank, world)
     mem_table = optional(bench_memory_table, args) if (args.memory_table and world == 1) else None
     cb = None

@@ -40,6 +40,7 @@ import math
 import torch
 import torch.distributed as dist
 
+from . import replay as _replay
 from .engine import CudaEngine, dtype_code
 from .errors import ConfigError
 from .lomo import _PROBE, _Protocol, stabilizer_from_args, trainable_params
@@ -104,6 +105,8 @@ class _Bucket:
         self.dirty = False
         self.gflat = None
         self.remaining = len(params)
+        self.filled = [False] * len(params)  # which ranges of gflat hold a gradient
+        self.reduced = False  # this pass's reduce-scatter + kernel already ran
         if not persistent:
             self.release()
 
@@ -175,6 +178,13 @@ class ShardedLOMO(_Protocol):
         process_group: the data-parallel group (default: WORLD).
         fused_rs: K4 -- reduce over peer memory fused with the update instead
             of NCCL reduce_scatter + K1/K2 (CUDA + NVLink peers only).
+        direct_grads: weight gradients of the model's linears
+            (``replay.linear`` / ``replay.matmul_in_out``) are computed by the
+            linear's backward straight into the bucket's flat buffer
+            (``mm(..., out=)``): no per-parameter copy, autograd never holds
+            them.  A weight that feeds several linears gets the later
+            contributions added through its hook; one whose bucket was already
+            reduced raises ``ConfigError`` (pass ``direct_grads=False``).
     """
 
     _always_scale = True  # inv_scale carries the 1/world of the data-parallel mean
@@ -183,7 +193,8 @@ class ShardedLOMO(_Protocol):
                  loss_scale=None, *, clip_grad_value: float | None = None,
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
                  math: str = "f32", buckets=None, reshard_after_forward: bool = True,
-                 process_group=None, fused_rs: bool = False, _engine=None):
+                 process_group=None, fused_rs: bool = False, direct_grads: bool = True,
+                 _engine=None):
         if not dist.is_initialized():
             raise ConfigError("ShardedLOMO needs torch.distributed to be initialised")
         if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
@@ -216,8 +227,8 @@ class ShardedLOMO(_Protocol):
                                         self.rank, process_group))
         self._loc = {}
         for b in self.buckets:
-            for p, off, n in zip(b.params, b.offsets, b.numels):
-                self._loc[id(p)] = (b, off, n)
+            for j, (p, off, n) in enumerate(zip(b.params, b.offsets, b.numels)):
+                self._loc[id(p)] = (b, off, n, j)
         self.params = params
         self.device = params[0].device
         self.engine = _engine if _engine is not None else CudaEngine(
@@ -232,6 +243,10 @@ class ShardedLOMO(_Protocol):
             for dt in {b.dtype for b in self.buckets}:
                 n = max(b.padded for b in self.buckets if b.dtype == dt)
                 self._rings[dt] = _SymmRing(n, dt, self.device, process_group)
+        self._lin = None
+        if direct_grads:
+            self._lin = _replay.ReplayStash(keep=False)
+            self._lin.probe = self._lin.update = self._dw_into_bucket
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
         for b in self.buckets:
             if b.module is None or b.persistent:
@@ -261,28 +276,75 @@ class ShardedLOMO(_Protocol):
     def _hook(self, p: torch.Tensor) -> None:
         if self._mode == 0 or p.grad is None:
             return
-        b, off, n = self._loc[id(p)]
+        b, off, n, j = self._loc[id(p)]
+        if b.reduced:
+            raise ConfigError("direct_grads: a weight shared by several linears completed "
+                              "its bucket before its last gradient; use direct_grads=False")
+        if b.filled[j]:
+            # a weight shared by several linears: direct_grads wrote the first
+            # contributions, autograd delivers the rest here
+            b.gflat[off:off + n].add_(p.grad.reshape(-1))
+            p.grad = None
+            return
         if b.gflat is None:
             self._new_gflat(b)
         b.gflat[off:off + n].copy_(p.grad.reshape(-1))
+        b.filled[j] = True
         p.grad = None
         b.remaining -= 1
         if b.remaining == 0:
             self._reduce(b)
 
+    def _dw_into_bucket(self, wid: int, w, a: torch.Tensor, d: torch.Tensor) -> bool:
+        """The linear's weight gradient dW = d^T a, written by the GEMM into
+        the bucket's flat buffer (replay.weight_grad's GEMM with out=)."""
+        loc = self._loc.get(wid)
+        if loc is None or self._mode == 0:
+            return False
+        b, off, n, j = loc
+        if b.reduced:
+            return False  # -> autograd -> _hook raises ConfigError
+        if b.gflat is None:
+            self._new_gflat(b)
+        view = b.gflat[off:off + n].view(d.shape[-1], a.shape[-1])
+        d2, a2 = d.reshape(-1, d.shape[-1]), a.reshape(-1, a.shape[-1])
+        if b.filled[j]:
+            view.addmm_(d2.t(), a2)
+            return True
+        torch.mm(d2.t(), a2, out=view)
+        b.filled[j] = True
+        b.remaining -= 1
+        if b.remaining == 0:
+            self._reduce(b)
+        return True
+
     def _new_gflat(self, b: _Bucket) -> None:
+        """The bucket's flat gradient buffer, uninitialised: every range is
+        either written by its parameter's hook or zeroed in _zero_unfilled."""
         if self.fused_rs:
             ring = self._rings[b.dtype]
             b.ring_k = ring.acquire(b.idx)
             b.gflat = ring.bufs[b.ring_k][:b.padded]
-            b.gflat.zero_()
         else:
-            b.gflat = torch.zeros(b.padded, dtype=b.dtype, device=b.device)
+            b.gflat = torch.empty(b.padded, dtype=b.dtype, device=b.device)
+        b.filled = [False] * len(b.params)
+
+    @staticmethod
+    def _zero_unfilled(b: _Bucket) -> None:
+        """Zero the padding and the ranges of parameters that received no
+        gradient this pass (the summed gradient there is exactly 0)."""
+        end = b.offsets[-1] + b.numels[-1]
+        if end < b.padded:
+            b.gflat[end:].zero_()
+        for j, done in enumerate(b.filled):
+            if not done:
+                b.gflat[b.offsets[j]:b.offsets[j] + b.numels[j]].zero_()
 
     def _reduce(self, b: _Bucket) -> None:
         """One reduce-scatter feeding the fused kernel on this rank's shard."""
         if b.gflat is None:
             self._new_gflat(b)
+        self._zero_unfilled(b)
         if self.fused_rs:
             # K4: every rank has written the bucket -> reduce over peer memory
             # fused with the update / probe; nothing is written back
@@ -298,6 +360,7 @@ class ShardedLOMO(_Protocol):
             ring.release(b.ring_k)
             b.gflat = None
             b.remaining = len(b.params)
+            b.reduced = True
             b.release()
             return
         gshard = torch.empty(b.S, dtype=b.dtype, device=b.device)
@@ -309,10 +372,17 @@ class ShardedLOMO(_Protocol):
             self.engine.update(b.shard, gshard)
             b.dirty = True
         b.remaining = len(b.params)
+        b.reduced = True
         b.release()
 
     def _run_backward(self, target: torch.Tensor, mode: int, retain_graph: bool) -> None:
         self._mode = mode
+        for b in self.buckets:
+            b.reduced = False
+            b.filled = [False] * len(b.params)
+        if self._lin is not None:
+            self._lin.clear()
+            _replay._ACTIVE = self._lin
         try:
             target.backward(retain_graph=retain_graph)
             # parameters that received no gradient: reduce their (zero) buckets
@@ -322,6 +392,8 @@ class ShardedLOMO(_Protocol):
                     self._reduce(b)
         finally:
             self._mode = 0
+            if self._lin is not None:
+                _replay._ACTIVE = None
             self.engine.flush()
 
     def _decide(self) -> None:

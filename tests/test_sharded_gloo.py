@@ -71,6 +71,8 @@ def _worker(rank, world, port, mode, q):
 
 
 def _run(rank, world, port, mode, q):
+    direct = not mode.endswith("_copy")  # weight gradients GEMM'd into the buckets
+    mode = mode.removesuffix("_copy")
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -90,7 +92,8 @@ def _run(rank, world, port, mode, q):
             stab = Stabilizer(ClipMode.by_global_norm(max_norm), LossScaler(2.0 ** 8, 2))
         nb = len(model.layers) + 1
         eng = CpuEngine(nb, stab.scaler if stab else None, max_norm, grad_div=world)
-        opt = ShardedLOMO(model, lr=lr, stabilizer=stab, math="f64", _engine=eng)
+        opt = ShardedLOMO(model, lr=lr, stabilizer=stab, math="f64", _engine=eng,
+                          direct_grads=direct)
         # ZeRO-3: layer buckets are released between uses
         released = [not b.gathered for b in opt.buckets if b.module is not None]
         outcomes = []
@@ -115,7 +118,7 @@ def _run(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["plain", "norm", "norm_scaler", "skip"])
+@pytest.mark.parametrize("mode", ["plain", "norm", "norm_scaler", "skip", "norm_scaler_copy"])
 def test_sharded_lomo_matches_full_batch_reference(mode):
     world = 2
     ctx = mp.get_context("spawn")
