@@ -746,7 +746,7 @@ def bench_train_sharded(args, rank, world):
     reshard = pbytes > 0.4 * torch.cuda.get_device_properties(0).total_memory
     opt = ShardedLOMO(model, lr=1e-3, clip_grad_norm=1.0,
                       loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
-                      reshard_after_forward=reshard)
+                      reshard_after_forward=reshard, replay=not args.sharded_strict)
     torch.cuda.empty_cache()
     seq, batch = args.seq, args.batch
     gen = torch.Generator(device="cuda").manual_seed(rank)
@@ -776,6 +776,8 @@ def bench_train_sharded(args, rank, world):
            "ms_per_step": round(ms, 2), "seq_len": seq, "batch_per_rank": batch,
            "activation_checkpointing": ckpt, "passes_per_step": 2, "outcomes": outcomes,
            "reshard_after_forward": reshard,
+           "pass2": "second forward + backward" if args.sharded_strict else
+                    "replay of the stashed (x, dy) into the buckets",
            "peak_mem_gib_rank0": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
            "paper_tgs_rtx3090": {"13b": 66.19, "30b": 11.61, "65b": 4.93}.get(size)}
     opt.remove_hooks()
@@ -849,6 +851,8 @@ def main():
              "(default: all)")
     ap.add_argument("--sharded-train", action="store_true",
                     help="run the ZeRO-3 sharded train leg even at N=1 (world-1 NCCL group)")
+    ap.add_argument("--sharded-strict", action="store_true",
+                    help="sharded train leg: pass 2 as a second forward+backward (default: replay)")
     ap.add_argument("--sharded-model", default="13b", choices=["tiny", "7b", "13b", "30b", "65b"],
                     help="model of the N>1 sharded train leg (config 4: 13b, config 5: 65b)")
     args = ap.parse_args()

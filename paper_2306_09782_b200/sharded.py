@@ -43,7 +43,7 @@ import torch.distributed as dist
 from . import replay as _replay
 from .engine import CudaEngine, dtype_code
 from .errors import ConfigError
-from .lomo import _PROBE, _Protocol, stabilizer_from_args, trainable_params
+from .lomo import _PROBE, _UPDATE, _Protocol, stabilizer_from_args, trainable_params
 from .stabilize import Stabilizer
 
 
@@ -185,6 +185,12 @@ class ShardedLOMO(_Protocol):
             them.  A weight that feeds several linears gets the later
             contributions added through its hook; one whose bucket was already
             reduced raises ``ConfigError`` (pass ``direct_grads=False``).
+        replay: two-pass mode without the second forward/backward, as
+            :class:`~paper_2306_09782_b200.LOMO` ``replay=True``: pass 1 keeps
+            each linear's (x, dy) and the other parameters' gradients; pass 2
+            re-derives every local gradient from them (the same GEMM) into the
+            buckets and runs the same reduce-scatter + K1 per bucket.  Pass 2
+            needs no parameter gather.  Needs ``direct_grads``.
     """
 
     _always_scale = True  # inv_scale carries the 1/world of the data-parallel mean
@@ -194,7 +200,7 @@ class ShardedLOMO(_Protocol):
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
                  math: str = "f32", buckets=None, reshard_after_forward: bool = True,
                  process_group=None, fused_rs: bool = False, direct_grads: bool = True,
-                 _engine=None):
+                 replay: bool = False, _engine=None):
         if not dist.is_initialized():
             raise ConfigError("ShardedLOMO needs torch.distributed to be initialised")
         if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
@@ -243,10 +249,17 @@ class ShardedLOMO(_Protocol):
             for dt in {b.dtype for b in self.buckets}:
                 n = max(b.padded for b in self.buckets if b.dtype == dt)
                 self._rings[dt] = _SymmRing(n, dt, self.device, process_group)
+        if replay and not direct_grads:
+            raise ConfigError("ShardedLOMO(replay=True) needs direct_grads=True")
+        if replay and self.passes != 2:
+            raise ConfigError("replay replaces the second pass: it needs clip_grad_norm or "
+                              "loss_scale")
         self._lin = None
         if direct_grads:
-            self._lin = _replay.ReplayStash(keep=False)
+            self._lin = _replay.ReplayStash(keep=replay)
             self._lin.probe = self._lin.update = self._dw_into_bucket
+        self._stash = self._lin if replay else None
+        self._replay_mismatch = False
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
         for b in self.buckets:
             if b.module is None or b.persistent:
@@ -285,7 +298,10 @@ class ShardedLOMO(_Protocol):
             # contributions, autograd delivers the rest here
             b.gflat[off:off + n].add_(p.grad.reshape(-1))
             p.grad = None
+            self._replay_mismatch = True  # replay would drop this contribution
             return
+        if self._stash is not None and self._mode == _PROBE:
+            self._stash.grads[id(p)] = p.grad  # not a linear: kept for pass 2
         if b.gflat is None:
             self._new_gflat(b)
         b.gflat[off:off + n].copy_(p.grad.reshape(-1))
@@ -395,6 +411,52 @@ class ShardedLOMO(_Protocol):
             if self._lin is not None:
                 _replay._ACTIVE = None
             self.engine.flush()
+        st = self._stash
+        if st is not None and mode == _PROBE and (st.shared or self._replay_mismatch):
+            st.clear()
+            self._replay_mismatch = False
+            raise ConfigError("replay: a weight receives gradient from more than one op "
+                              "(shared or tied); use replay=False")
+
+    def _replay_pass(self, lr: float, coefs=None) -> None:
+        """Pass 2 from the stash: per bucket (a fixed order, identical on
+        every rank), every local gradient re-derived into the flat buffer --
+        dW = dy^T x for the linears, the kept tensor for the rest -- then the
+        bucket's reduce-scatter + K1 on this rank's shard."""
+        st = self._stash
+        self._mode = _UPDATE
+        try:
+            with torch.no_grad():
+                self._replay_buckets(st)
+        finally:
+            self._mode = 0
+            st.clear()
+            self.engine.flush()
+
+    def _replay_buckets(self, st) -> None:
+        for b in reversed(self.buckets):
+            b.reduced = False
+            got = False
+            for j, p in enumerate(b.params):
+                pid, off, n = id(p), b.offsets[j], b.numels[j]
+                if pid in st.linear:
+                    a, d = st.linear.pop(pid)
+                    if b.gflat is None:
+                        self._new_gflat(b)
+                    view = b.gflat[off:off + n].view(d.shape[-1], a.shape[-1])
+                    torch.mm(d.reshape(-1, d.shape[-1]).t(), a.reshape(-1, a.shape[-1]),
+                             out=view)
+                    del a, d
+                elif pid in st.grads:
+                    if b.gflat is None:
+                        self._new_gflat(b)
+                    b.gflat[off:off + n].copy_(st.grads.pop(pid).reshape(-1))
+                else:
+                    continue
+                b.filled[j] = True
+                got = True
+            if got:
+                self._reduce(b)
 
     def _decide(self) -> None:
         """K3 local partial -> all_gather of {sumsq, overflow} -> K3a on the
