@@ -59,15 +59,19 @@ def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group) -> None:
         dist.all_gather(list(out.chunk(dist.get_world_size(group))), inp, group=group)
 
 
-def reduce_scatter(out: torch.Tensor, inp: torch.Tensor, group) -> None:
-    """out = (sum over ranks of inp)[rank*S:(rank+1)*S] (NCCL reduce_scatter_tensor)."""
+def reduce_scatter(out: torch.Tensor, inp: torch.Tensor, group, async_op: bool = False):
+    """out = (sum over ranks of inp)[rank*S:(rank+1)*S] (NCCL reduce_scatter_tensor).
+    ``async_op``: returns the NCCL work handle (``wait()`` makes the current
+    stream wait for it); gloo always completes before returning (None)."""
     if _backend(group) == "nccl":
-        dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=group)
-    else:  # gloo has no reduce_scatter_tensor: all_reduce + slice (CPU tests only)
-        tmp = inp.clone()
-        dist.all_reduce(tmp, group=group)
-        r, w = dist.get_rank(group), dist.get_world_size(group)
-        out.copy_(tmp.chunk(w)[r])
+        return dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=group,
+                                          async_op=async_op)
+    # gloo has no reduce_scatter_tensor: all_reduce + slice (CPU tests only)
+    tmp = inp.clone()
+    dist.all_reduce(tmp, group=group)
+    r, w = dist.get_rank(group), dist.get_world_size(group)
+    out.copy_(tmp.chunk(w)[r])
+    return None
 
 
 class _Bucket:
@@ -260,6 +264,7 @@ class ShardedLOMO(_Protocol):
             self._lin.probe = self._lin.update = self._dw_into_bucket
         self._stash = self._lin if replay else None
         self._replay_mismatch = False
+        self._inflight: list = []
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
         for b in self.buckets:
             if b.module is None or b.persistent:
@@ -379,17 +384,31 @@ class ShardedLOMO(_Protocol):
             b.reduced = True
             b.release()
             return
+        # the reduce-scatter runs on NCCL's stream while the backward goes on;
+        # this bucket's K2/K1 is enqueued once the NEXT bucket has been handed
+        # to NCCL (or at the end of the pass), so the compute stream never
+        # waits on the collective it could overlap
+        self._drain(keep=0)
         gshard = torch.empty(b.S, dtype=b.dtype, device=b.device)
-        reduce_scatter(gshard, b.gflat, self.group)
+        work = reduce_scatter(gshard, b.gflat, self.group, async_op=True)
+        self._inflight.append((work, gshard, b, self._mode))
         b.gflat = None
-        if self._mode == _PROBE:
-            self.engine.probe(gshard, b.idx)
-        else:
-            self.engine.update(b.shard, gshard)
-            b.dirty = True
         b.remaining = len(b.params)
         b.reduced = True
         b.release()
+
+    def _drain(self, keep: int = 0) -> None:
+        """Run the fused kernel of every in-flight bucket but the newest
+        ``keep`` (after its reduce-scatter, stream-ordered)."""
+        while len(self._inflight) > keep:
+            work, gshard, b, mode = self._inflight.pop(0)
+            if work is not None:
+                work.wait()
+            if mode == _PROBE:
+                self.engine.probe(gshard, b.idx)
+            else:
+                self.engine.update(b.shard, gshard)
+                b.dirty = True
 
     def _run_backward(self, target: torch.Tensor, mode: int, retain_graph: bool) -> None:
         self._mode = mode
@@ -406,6 +425,7 @@ class ShardedLOMO(_Protocol):
             for b in self.buckets:
                 if b.remaining != len(b.params) or b.gflat is not None:
                     self._reduce(b)
+            self._drain()
         finally:
             self._mode = 0
             if self._lin is not None:
@@ -457,6 +477,7 @@ class ShardedLOMO(_Protocol):
                 got = True
             if got:
                 self._reduce(b)
+        self._drain()
 
     def _decide(self) -> None:
         """K3 local partial -> all_gather of {sumsq, overflow} -> K3a on the
