@@ -51,12 +51,14 @@ def _backend(group) -> str:
     return dist.get_backend(group)
 
 
-def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group) -> None:
-    """out[r*S:(r+1)*S] = inp of rank r (NCCL all_gather_into_tensor)."""
+def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group, async_op: bool = False):
+    """out[r*S:(r+1)*S] = inp of rank r (NCCL all_gather_into_tensor);
+    ``async_op``: returns the NCCL work handle (gloo completes, None)."""
     if _backend(group) == "nccl":
-        dist.all_gather_into_tensor(out, inp, group=group)
-    else:  # gloo (CPU tests): list form
-        dist.all_gather(list(out.chunk(dist.get_world_size(group))), inp, group=group)
+        return dist.all_gather_into_tensor(out, inp, group=group, async_op=async_op)
+    # gloo (CPU tests): list form
+    dist.all_gather(list(out.chunk(dist.get_world_size(group))), inp, group=group)
+    return None
 
 
 def reduce_scatter(out: torch.Tensor, inp: torch.Tensor, group, async_op: bool = False):
@@ -111,8 +113,15 @@ class _Bucket:
         self.remaining = len(params)
         self.filled = [False] * len(params)  # which ranges of gflat hold a gradient
         self.reduced = False  # this pass's reduce-scatter + kernel already ran
+        self.pending = None   # in-flight refresh all-gather (persistent buckets)
         if not persistent:
             self.release()
+
+    def wait(self) -> None:
+        """Make the current stream wait for this bucket's refresh gather."""
+        if self.pending is not None:
+            self.pending.wait()
+            self.pending = None
 
     def gather(self) -> None:
         if self.gathered:
@@ -267,6 +276,11 @@ class ShardedLOMO(_Protocol):
         self._inflight: list = []
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
         for b in self.buckets:
+            if b.module is not None and b.persistent:
+                # the refresh gather was issued at the model's forward start;
+                # this layer waits for its own bucket only
+                self._handles.append(b.module.register_forward_pre_hook(
+                    lambda mod, args, b=b: b.wait()))
             if b.module is None or b.persistent:
                 continue
             self._handles.append(b.module.register_forward_pre_hook(
@@ -284,11 +298,20 @@ class ShardedLOMO(_Protocol):
             b.release()
 
     def _refresh(self) -> None:
-        """Re-gather persistent buckets whose shards were updated."""
-        for b in self.buckets:
+        """Re-gather persistent buckets whose shards were updated: every
+        gather is issued at once (NCCL runs them in order: the module-less
+        buckets -- embedding, final norm, head -- first, then the layers in
+        forward order) and each layer's forward pre-hook waits for its own,
+        so the later gathers overlap the earlier layers' forward."""
+        order = [b for b in self.buckets if b.module is None] + \
+                [b for b in self.buckets if b.module is not None]
+        for b in order:
             if b.persistent and b.dirty:
-                all_gather_into(b.full, b.shard, self.group)
+                b.pending = all_gather_into(b.full, b.shard, self.group, async_op=True)
                 b.dirty = False
+        for b in order:
+            if b.module is None:
+                b.wait()
 
     # ----------------------------------------------------------------- hooks
     def _hook(self, p: torch.Tensor) -> None:
@@ -499,6 +522,8 @@ class ShardedLOMO(_Protocol):
         self._refresh()
 
     def remove_hooks(self) -> None:
+        for b in self.buckets:
+            b.wait()  # no refresh gather may outlive the hooks that wait for it
         for h in self._handles:
             h.remove()
         self._handles = []
@@ -507,4 +532,5 @@ class ShardedLOMO(_Protocol):
         """Materialise every bucket's full parameters (e.g. for evaluation)."""
         self._refresh()
         for b in self.buckets:
+            b.wait()
             b.gather()
