@@ -123,17 +123,21 @@ class _Bucket:
             self.pending.wait()
             self.pending = None
 
-    def gather(self) -> None:
-        if self.gathered:
-            return
-        self.full.untyped_storage().resize_(self.nbytes)
-        all_gather_into(self.full, self.shard, self.group)
-        self.gathered = True
-        self.dirty = False
+    def gather(self, async_op: bool = False) -> None:
+        """All-gather the full parameters; ``async_op`` only issues it (a
+        prefetch: the next ``gather()`` or ``wait()`` orders the stream)."""
+        if not self.gathered:
+            self.full.untyped_storage().resize_(self.nbytes)
+            self.pending = all_gather_into(self.full, self.shard, self.group, async_op=True)
+            self.gathered = True
+            self.dirty = False
+        if not async_op:
+            self.wait()
 
     def release(self) -> None:
         if self.persistent or not self.gathered:
             return
+        self.wait()  # never free a buffer a gather is still writing
         self.full.untyped_storage().resize_(0)
         self.gathered = False
 
@@ -275,23 +279,40 @@ class ShardedLOMO(_Protocol):
         self._replay_mismatch = False
         self._inflight: list = []
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
+        layers = [b for b in self.buckets if b.module is not None and not b.persistent]
+        for k, b in enumerate(layers):
+            # ZeRO-3: gather this layer, prefetch the next one in execution
+            # order (forward: k+1; backward: k-1) so its all-gather overlaps
+            # this layer's compute
+            nxt = layers[k + 1] if k + 1 < len(layers) else None
+            prv = layers[k - 1] if k > 0 else None
+            self._handles.append(b.module.register_forward_pre_hook(
+                lambda mod, args, b=b, n=nxt: self._gather_fwd(b, n)))
+            self._handles.append(b.module.register_forward_hook(
+                lambda mod, args, out, b=b: self._after_forward(b)))
+            self._handles.append(b.module.register_full_backward_pre_hook(
+                lambda mod, gout, b=b, n=prv: self._gather_bwd(b, n)))
         for b in self.buckets:
             if b.module is not None and b.persistent:
                 # the refresh gather was issued at the model's forward start;
                 # this layer waits for its own bucket only
                 self._handles.append(b.module.register_forward_pre_hook(
                     lambda mod, args, b=b: b.wait()))
-            if b.module is None or b.persistent:
-                continue
-            self._handles.append(b.module.register_forward_pre_hook(
-                lambda mod, args, b=b: b.gather()))
-            self._handles.append(b.module.register_forward_hook(
-                lambda mod, args, out, b=b: self._after_forward(b)))
-            self._handles.append(b.module.register_full_backward_pre_hook(
-                lambda mod, gout, b=b: b.gather()))
         self._handles.append(model.register_forward_pre_hook(lambda mod, args: self._refresh()))
 
     # ---------------------------------------------------------------- ZeRO-3
+    @staticmethod
+    def _gather_fwd(b: _Bucket, nxt) -> None:
+        b.gather()
+        if nxt is not None and torch._C._current_graph_task_id() == -1:
+            nxt.gather(async_op=True)  # not during a checkpoint recompute
+
+    @staticmethod
+    def _gather_bwd(b: _Bucket, prv) -> None:
+        b.gather()
+        if prv is not None:
+            prv.gather(async_op=True)
+
     def _after_forward(self, b: _Bucket) -> None:
         # keep the parameters while autograd recomputes a checkpointed layer
         if torch._C._current_graph_task_id() == -1:
