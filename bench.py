@@ -770,7 +770,8 @@ def bench_train_sharded(args, rank, world):
     end.record()
     _barrier(world)
     ms = _max_over_ranks(start.elapsed_time(end), world) / args.train_steps
-    out = {"model": f"llama-{size} (random init), fp16, ZeRO-3 shards over {world} GPUs",
+    out = {"model": f"llama-{size} (random init), fp16, parameters sharded over {world} GPUs "
+                    f"({'ZeRO-3: layers freed after use' if reshard else 'layers kept gathered'})",
            "tokens_per_s": round(world * batch * seq / (ms * 1e-3), 1),
            "tokens_per_gpu_per_s": round(batch * seq / (ms * 1e-3), 1),
            "ms_per_step": round(ms, 2), "seq_len": seq, "batch_per_rank": batch,
