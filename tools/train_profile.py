@@ -76,3 +76,21 @@ print(f"GPU time per step: {total / 2 / 1e3:.2f} ms")
 for k, v in sorted(fam.items(), key=lambda x: -x[1]):
     print(f"  {k:20s} {v / 2 / 1e3:8.2f} ms  {100 * v / total:5.1f}%")
 print(prof.key_averages().table(sort_by="self_cuda_time_total", row_limit=25))
+
+# idle time between consecutive kernels on the device (the profiled steps):
+# where the wall-minus-kernel time goes
+ks = sorted((e.time_range.start, e.time_range.end, e.name) for e in prof.events()
+            if e.device_type.name == "CUDA" and e.device_time_total > 0)
+gaps = [(ks[i + 1][0] - ks[i][1], ks[i][2], ks[i + 1][2]) for i in range(len(ks) - 1)]
+pos = [g for g in gaps if g[0] > 0]
+print(f"kernels: {len(ks)}; device span {(ks[-1][1] - ks[0][0]) / 2 / 1e3:.2f} ms per step; "
+      f"idle between kernels {sum(g[0] for g in pos) / 2 / 1e3:.2f} ms per step")
+hist = defaultdict(float)
+for g, _, _ in pos:
+    b = "<1us" if g < 1 else "1-2us" if g < 2 else "2-5us" if g < 5 else "5-20us" if g < 20 \
+        else "20-100us" if g < 100 else ">100us"
+    hist[b] += g
+print("  idle by gap size (ms per step): " +
+      ", ".join(f"{k} {v / 2 / 1e3:.2f}" for k, v in sorted(hist.items())))
+for g, a_, b_ in sorted(pos, reverse=True)[:12]:
+    print(f"  {g:9.1f} us  after {a_[:50]!r}  before {b_[:50]!r}")
