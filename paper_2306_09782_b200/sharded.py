@@ -10,16 +10,22 @@ GPUs of one box (north star (3)).
 * ZeRO-3 life cycle of a layer bucket: ``all_gather_into_tensor`` into the full
   buffer before the module's forward, released (storage freed) after it;
   gathered again before the module's backward, released once its gradients
-  have been reduced.  The rest bucket stays gathered and is refreshed from
-  the updated shards after every applied step.
-* Gradients: each parameter hook copies its gradient into the bucket's flat
-  gradient buffer and drops ``p.grad``; when the last gradient of a bucket
-  arrives, ONE ``reduce_scatter_tensor`` (SUM, NCCL over NVLink) produces this
-  rank's shard of the summed gradient and the fused kernel runs on it:
-  K2 (pass 1: overflow + sum of squares) or K1 (pass 2 / single pass:
-  ``p_shard -= lr * ...``).  The 1/world of the data-parallel mean is folded
-  into the state's ``inv_scale`` (``grad_div``), so clipping sees the mean
-  gradient exactly like the single-GPU reference.
+  have been reduced; each gather prefetches the next layer's.  With
+  ``reshard_after_forward=False`` (or for the rest bucket) the full buffer
+  stays and is refreshed from the updated shards after every applied step:
+  all refresh gathers are issued at once, each layer waits for its own.
+* Gradients: a linear's backward GEMMs its weight gradient straight into the
+  bucket's flat buffer (``direct_grads``); other parameters' hooks copy theirs
+  and drop ``p.grad``.  When the last gradient of a bucket arrives, ONE
+  asynchronous ``reduce_scatter_tensor`` (SUM, NCCL over NVLink) produces this
+  rank's shard of the summed gradient and the fused kernel runs on it --
+  enqueued once the next bucket's collective is issued, so the collective
+  overlaps the backward: K2 (pass 1: overflow + sum of squares) or K1 (pass 2 /
+  single pass: ``p_shard -= lr * ...``).  The 1/world of the data-parallel
+  mean is folded into the state's ``inv_scale`` (``grad_div``), so clipping
+  sees the mean gradient exactly like the single-GPU reference.
+* ``replay=True``: pass 2 re-derives the local gradients from the stashed
+  (x, dy) of pass 1 instead of a second forward/backward.
 * Global norm (two-pass mode): each rank reduces its slots (K3, local mode),
   one ``all_gather`` exchanges ``{sumsq, overflow}`` per rank, and K3a decides
   on the rank-ordered sum -- the same bits on every rank, no float atomics.
@@ -392,7 +398,6 @@ class ShardedLOMO(_Protocol):
             b.gflat = ring.bufs[b.ring_k][:b.padded]
         else:
             b.gflat = torch.empty(b.padded, dtype=b.dtype, device=b.device)
-        b.filled = [False] * len(b.params)
 
     @staticmethod
     def _zero_unfilled(b: _Bucket) -> None:
