@@ -505,6 +505,7 @@ class ShardedLOMO(_Protocol):
     def _replay_buckets(self, st) -> None:
         for b in reversed(self.buckets):
             b.reduced = False
+            b.filled = [False] * len(b.params)
             got = False
             for j, p in enumerate(b.params):
                 pid, off, n = id(p), b.offsets[j], b.numels[j]
