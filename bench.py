@@ -20,6 +20,9 @@ Also on the line:
                 fp16 emulation = the reference's 16-bit path) on all host cores
   train         config 3: LLaMA-7B fp16 LOMO, dynamic loss scale + two-pass
                 global-norm clip (1.0), seq 1024 x batch 1, tokens/s
+  train_sharded_world1
+                config 4's sharded train leg (LLaMA-13B, ShardedLOMO) in a world-1
+                NCCL group: the sharded machinery's cost next to plain LOMO
   clocks        NVML SM clock / throttle reasons sampled during the timed region
 
 N > 1 (torchrun): weak scaling -- every rank runs the same 7B-shaped update
@@ -762,13 +765,14 @@ def bench_train_sharded(args, rank, world):
     _barrier(world)
     torch.cuda.reset_peak_memory_stats()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
     outcomes = []
-    for k in range(args.train_steps):
-        step(k)
-        outcomes.append(opt.last_outcome.value)
-    end.record()
-    _barrier(world)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        start.record()
+        for k in range(args.train_steps):
+            step(k)
+            outcomes.append(opt.last_outcome.value)
+        end.record()
+        _barrier(world)
     ms = _max_over_ranks(start.elapsed_time(end), world) / args.train_steps
     out = {"model": f"llama-{size} (random init), fp16, parameters sharded over {world} GPUs "
                     f"({'ZeRO-3: layers freed after use' if reshard else 'layers kept gathered'})",
@@ -776,7 +780,7 @@ def bench_train_sharded(args, rank, world):
            "tokens_per_gpu_per_s": round(batch * seq / (ms * 1e-3), 1),
            "ms_per_step": round(ms, 2), "seq_len": seq, "batch_per_rank": batch,
            "activation_checkpointing": ckpt, "passes_per_step": 2, "outcomes": outcomes,
-           "reshard_after_forward": reshard,
+           "reshard_after_forward": reshard, "clocks": clk.summary(),
            "pass2": "second forward + backward" if args.sharded_strict else
                     "replay of the stashed (x, dy) into the buckets",
            "peak_mem_gib_rank0": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
@@ -785,6 +789,19 @@ def bench_train_sharded(args, rank, world):
     del opt, model
     torch.cuda.empty_cache()
     return out
+
+
+def _sharded_world1(args):
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29561")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0),
+                            timeout=datetime.timedelta(minutes=5))
+    try:
+        return bench_train_sharded(args, 0, 1)
+    finally:
+        dist.destroy_process_group()
 
 
 def cpu_baseline(max_seconds=20.0, steps=None):
@@ -852,6 +869,8 @@ def main():
              "(default: all)")
     ap.add_argument("--sharded-train", action="store_true",
                     help="run the ZeRO-3 sharded train leg even at N=1 (world-1 NCCL group)")
+    ap.add_argument("--no-sharded-world1", dest="sharded_world1", action="store_false",
+                    help="skip the N=1 run of the sharded train leg (world-1 NCCL group)")
     ap.add_argument("--sharded-strict", action="store_true",
                     help="sharded train leg: pass 2 as a second forward+backward (default: replay)")
     ap.add_argument("--sharded-model", default="13b", choices=["tiny", "7b", "13b", "30b", "65b"],
@@ -911,6 +930,12 @@ def main():
         train = optional(bench_train, args, rank, world) if (world == 1 and not
                                                               args.sharded_train) else \
             optional(bench_train_sharded, args, rank, world)
+    sharded1 = None
+    if world == 1 and not args.no_train and not args.sharded_train and args.sharded_world1:
+        # config 4's data path (ZeRO-3 buckets, NCCL reduce-scatter -> K2/K1 per
+        # shard) on this one GPU: a world-1 NCCL group, where the collectives are
+        # local copies -- the sharded machinery's own cost, next to plain LOMO
+        sharded1 = optional(_sharded_world1, args)
     mem_table = optional(bench_memory_table, args) if (args.memory_table and world == 1) else None
     cb = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -958,6 +983,8 @@ def main():
         }
         if mem_table is not None:
             line["memory_table"] = mem_table
+        if sharded1 is not None:
+            line["train_sharded_world1"] = sharded1
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
