@@ -24,7 +24,7 @@ from typing import Callable, Sequence
 import torch
 
 from . import _lib
-from .errors import ConfigError, ScaleUnderflowError
+from .errors import ConfigError, NonFiniteLossError, ScaleUnderflowError
 from .lomo import LOMO, _PROBE, _UPDATE
 from .stabilize import StepOutcome
 
@@ -37,7 +37,10 @@ class GraphedLOMOStep:
             loss_scale), built with ``replay=True`` (``fuse_gemm`` optional), or
             with ``fuse_gemm=True`` alone: the reference's protocol as is -- pass
             2 a second backward over the retained graph, K6 in pass 1 and K5
-            inside pass 2 -- captured the same way (no replay stash).
+            inside pass 2 -- captured the same way (no replay stash); or a
+            single-pass LOMO with ``fuse_gemm=True`` (K5 inside the one
+            backward): graph 1 is the forward, the host checks the loss
+            (optim.py:63-65), graph 2 the backward.
         loss_fn: the forward, returning the scalar loss.
         static_inputs: tensors ``loss_fn`` reads; copy each batch into them.
         warmup: eager steps run before capture (they also perform replay's
@@ -47,10 +50,10 @@ class GraphedLOMOStep:
 
     def __init__(self, opt: LOMO, loss_fn: Callable[..., torch.Tensor],
                  static_inputs: Sequence[torch.Tensor], warmup: int = 2, lr: float = 1e-3):
-        if not isinstance(opt, LOMO) or opt.passes != 2 or \
-                (opt._stash is None and not opt._fused_update):
-            raise ConfigError("GraphedLOMOStep needs a two-pass LOMO (clip_grad_norm and/or "
-                              "loss_scale) with replay=True or fuse_gemm=True")
+        if not isinstance(opt, LOMO) or (opt._stash is None and not opt._fused_update):
+            raise ConfigError("GraphedLOMOStep needs a LOMO with replay=True (two-pass) or "
+                              "fuse_gemm=True")
+        self.single = opt.passes == 1
         self.strict = opt._stash is None
         if opt.clip_value:
             raise ConfigError("value clipping is a single-pass mode; graph it with LOMO directly")
@@ -68,6 +71,10 @@ class GraphedLOMOStep:
             raise ConfigError("replay's first-step check did not run during warm-up")
 
         pool = torch.cuda.graph_pool_handle()
+        if self.single:
+            self._capture_single(pool)
+            self.steps = 0
+            return
         self.g1 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.g1, pool=pool):
             self.loss = loss_fn(*self.inputs)
@@ -81,6 +88,27 @@ class GraphedLOMOStep:
         with torch.cuda.graph(self.g2, pool=pool):
             self._capture_pass2()
         self.steps = 0
+
+    def _capture_single(self, pool) -> None:
+        """Single pass: g1 = forward (+ the device loss flag), g2 = the
+        backward with K5 in every linear and K1 for the rest (lr, alpha and
+        beta from the device state).  The autograd graph is kept across
+        replays (its saved tensors live in the graph pool)."""
+        opt, eng = self.opt, self.opt.engine
+        self.g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g1, pool=pool):
+            self.loss = self.loss_fn(*self.inputs)
+            eng.begin(opt._check_loss(self.loss))
+        self.g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g2, pool=pool):
+            eng.configure(0.0, opt.clip_value, opt.weight_decay,
+                          opt._flags(_UPDATE) | _lib.LR_FROM_STATE)
+            opt._lr_from_state = True
+            try:
+                opt._run_backward(self.loss, _UPDATE, True)
+            finally:
+                opt._lr_from_state = False
+            eng.on_clean()
 
     def _capture_pass2(self) -> None:
         opt, eng = self.opt, self.opt.engine
@@ -108,6 +136,15 @@ class GraphedLOMOStep:
         opt, eng = self.opt, self.opt.engine
         _lib.check(eng.lib.lomo_set_lr(eng.ptr, float(lr), eng.stream()), "lomo_set_lr")
         self.g1.replay()
+        if self.single:
+            loss = float(self.loss)     # the one host sync: the loss check
+            if loss != loss or loss in (float("inf"), float("-inf")):
+                opt.last_outcome = None
+                raise NonFiniteLossError(f"loss is non-finite ({loss}); step aborted")
+            self.g2.replay()
+            opt.last_outcome = None if opt.stabilizer is None else StepOutcome.APPLIED
+            self.steps += 1
+            return self.loss
         st = eng.read_status()          # the one host sync of the step
         if st.underflow:
             raise ScaleUnderflowError(

@@ -194,3 +194,40 @@ def test_graphed_strict_fused_step_equals_eager():
     assert oa.loss_scale == ob.loss_scale
     for x, y in zip(a.parameters(), b.parameters()):
         torch.testing.assert_close(x.float(), y.float(), rtol=2 ** -6, atol=1e-4)
+
+
+def test_graphed_single_pass_fused_step_equals_eager():
+    """LOMO's single fused pass (K5 inside the backward) captured as forward
+    graph + host loss check + backward graph: losses and parameters equal
+    to the eager single pass up to the attention backward's nondeterminism;
+    a non-finite loss raises with every parameter untouched."""
+    from paper_2306_09782_b200 import LOMO
+    from paper_2306_09782_b200.errors import NonFiniteLossError
+    from paper_2306_09782_b200.graphs import GraphedLOMOStep
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
+    a = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    b = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    oa, ob = LOMO(a, lr=0.05, fuse_gemm=True), LOMO(b, lr=0.05, fuse_gemm=True)
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    data = [torch.randint(0, 256, (2, 65), device="cuda", generator=gen) for _ in range(6)]
+    static = data[0].clone()
+    poison = torch.ones((), device="cuda")
+    for _ in range(2):
+        oa.step(lambda: a.loss(data[0][:, :-1], data[0][:, 1:]), 0.05)
+    gs = GraphedLOMOStep(ob, lambda d: b.loss(d[:, :-1], d[:, 1:]) * poison, (static,),
+                         warmup=2, lr=0.05)
+    assert gs.single
+    for k in range(1, 6):
+        lr = 0.05 / k
+        la = oa.step(lambda: a.loss(data[k][:, :-1], data[k][:, 1:]), lr)
+        static.copy_(data[k])
+        lb = gs.step(lr).item()
+        assert abs(la - lb) <= 1e-3 * abs(la)
+    for x, y in zip(a.parameters(), b.parameters()):
+        torch.testing.assert_close(x.float(), y.float(), rtol=2 ** -6, atol=1e-4)
+    before = [p.detach().clone() for p in b.parameters()]
+    poison.fill_(float("inf"))
+    with pytest.raises(NonFiniteLossError):
+        gs.step(0.05)
+    assert all(torch.equal(p, q) for p, q in zip(before, b.parameters()))
