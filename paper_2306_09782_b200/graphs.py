@@ -137,7 +137,7 @@ class GraphedLOMOStep:
         _lib.check(eng.lib.lomo_set_lr(eng.ptr, float(lr), eng.stream()), "lomo_set_lr")
         self.g1.replay()
         if self.single:
-            loss = float(self.loss)     # the one host sync: the loss check
+            loss = float(self.loss.detach())  # the one host sync: the loss check
             if loss != loss or loss in (float("inf"), float("-inf")):
                 opt.last_outcome = None
                 raise NonFiniteLossError(f"loss is non-finite ({loss}); step aborted")
@@ -155,5 +155,58 @@ class GraphedLOMOStep:
         else:
             self.g2.replay()
             opt.last_outcome = StepOutcome.APPLIED
+        self.steps += 1
+        return self.loss
+
+
+class GraphedGroupedStep:
+    """``GroupedLOMO``'s single pass (per-group clipping, stabilize.py:234-274)
+    captured as two CUDA graphs: graph 1 the forward; the host checks the
+    loss (optim.py:63-65); graph 2 the backward, whose group flushes run K2
+    (or read K6's partials), K3a and K1 with the learning rate from the
+    device state.  The outcome is read after graph 2, as the eager step does.
+
+    Args as :class:`GraphedLOMOStep`.
+    """
+
+    def __init__(self, opt, loss_fn: Callable[..., torch.Tensor],
+                 static_inputs: Sequence[torch.Tensor], warmup: int = 2, lr: float = 1e-3):
+        from .grouped import GroupedLOMO
+        if not isinstance(opt, GroupedLOMO):
+            raise ConfigError("GraphedGroupedStep needs a GroupedLOMO")
+        self.opt, self.loss_fn, self.inputs = opt, loss_fn, tuple(static_inputs)
+        dev = opt.params[0].device
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(max(1, warmup)):
+                opt.step(lambda: loss_fn(*self.inputs), lr)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        pool = torch.cuda.graph_pool_handle()
+        self.g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g1, pool=pool):
+            self.loss = loss_fn(*self.inputs)
+        self.g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g2, pool=pool):
+            opt._lr_from_state = True
+            try:
+                opt._backward_core(self.loss, True)
+            finally:
+                opt._lr_from_state = False
+        self.steps = 0
+
+    def step(self, lr: float) -> torch.Tensor:
+        opt, eng = self.opt, self.opt.engine
+        _lib.check(eng.lib.lomo_set_lr(eng.ptr, float(lr), eng.stream()), "lomo_set_lr")
+        self.g1.replay()
+        loss = float(self.loss.detach())
+        if loss != loss or loss in (float("inf"), float("-inf")):
+            raise NonFiniteLossError(f"loss is non-finite ({loss}); step aborted")
+        self.g2.replay()
+        st = eng.read_status()
+        skipped = st.steps_skipped > opt._skipped_before
+        opt._skipped_before = st.steps_skipped
+        opt.last_outcome = StepOutcome.SKIPPED_OVERFLOW if skipped else StepOutcome.APPLIED
         self.steps += 1
         return self.loss

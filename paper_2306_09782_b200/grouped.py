@@ -98,6 +98,7 @@ class GroupedLOMO:
         self._by_id = {id(p): p for p in params}
         self._probed: set[int] = set()       # this group's K6-probed weights
         self._pending = []                   # deferred K6 partial sums of this group
+        self._lr_from_state = False          # graph capture: K1 reads lr from the state
         self._pws = {}                       # K6 workspace per weight
         self._mismatch: list = []
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
@@ -185,7 +186,9 @@ class GroupedLOMO:
         eng.flush()
         self._finish_probes()
         eng.finalize()                        # N, coef = min(1, max_norm/N), skip if !finite
-        eng.configure(self._lr, 0.0, self.weight_decay, _lib.USE_SKIP | _lib.USE_COEF)
+        eng.configure(0.0 if self._lr_from_state else self._lr, 0.0, self.weight_decay,
+                      _lib.USE_SKIP | _lib.USE_COEF |
+                      (_lib.LR_FROM_STATE if self._lr_from_state else 0))
         for p, g in self._buf:
             eng.update(p, g)
         eng.flush()
@@ -200,6 +203,14 @@ class GroupedLOMO:
             if p.grad is not None:
                 raise TapeStateError("a parameter already holds a gradient")
         self._lr = self.lr if lr is None else float(lr)
+        self._backward_core(loss, False)
+        st = self.engine.read_status()
+        skipped = st.steps_skipped > self._skipped_before
+        self._skipped_before = st.steps_skipped
+        self.last_outcome = StepOutcome.SKIPPED_OVERFLOW if skipped else StepOutcome.APPLIED
+
+    def _backward_core(self, loss: torch.Tensor, retain_graph: bool) -> None:
+        """The backward with the group hooks and flushes (no host sync)."""
         self._active, self._group = True, None
         self._mismatch = []
         if self._lin is not None:
@@ -207,7 +218,7 @@ class GroupedLOMO:
             self._lin.probe = self._gemm_probe
             _replay._ACTIVE = self._lin
         try:
-            loss.backward()
+            loss.backward(retain_graph=retain_graph)
             self._flush()
         finally:
             if self._lin is not None:
@@ -217,10 +228,6 @@ class GroupedLOMO:
         if self._lin is not None and (self._lin.shared or self._mismatch):
             raise ConfigError("fuse_gemm: a weight feeds more than one op (shared or tied); "
                               "use GroupedLOMO(fuse_gemm=False)")
-        st = self.engine.read_status()
-        skipped = st.steps_skipped > self._skipped_before
-        self._skipped_before = st.steps_skipped
-        self.last_outcome = StepOutcome.SKIPPED_OVERFLOW if skipped else StepOutcome.APPLIED
 
     def step(self, closure: Callable[[], torch.Tensor], lr: float | None = None) -> float:
         loss = closure()

@@ -499,3 +499,35 @@ def test_sparse_embedding_update_matches_dense(replay):
     tol = 2 ** -4 * (xa - x0).abs() + 2 ** -7 * torch.maximum(xa.abs(), xb.abs()) + 1e-9
     assert ((xa - xb).abs() <= tol).all(), ((xa - xb).abs() / tol).max().item()
     assert b.embed_tokens.grad is None
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_graphed_grouped_step_equals_eager(fused):
+    """GroupedLOMO's single pass captured as forward graph + host loss check +
+    backward graph (lr from the device state): losses, outcomes and
+    parameters equal to the eager grouped step up to the attention
+    backward's nondeterminism."""
+    from paper_2306_09782_b200 import GroupedLOMO
+    from paper_2306_09782_b200.graphs import GraphedGroupedStep
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
+    a = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    b = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
+    oa = GroupedLOMO(a, lr=0.05, max_norm=0.05, window=1, fuse_gemm=fused)
+    ob = GroupedLOMO(b, lr=0.05, max_norm=0.05, window=1, fuse_gemm=fused)
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    data = [torch.randint(0, 256, (2, 65), device="cuda", generator=gen) for _ in range(6)]
+    static = data[0].clone()
+    for _ in range(2):
+        oa.step(lambda: a.loss(data[0][:, :-1], data[0][:, 1:]), 0.05)
+    gs = GraphedGroupedStep(ob, lambda d: b.loss(d[:, :-1], d[:, 1:]), (static,), warmup=2,
+                            lr=0.05)
+    for k in range(1, 6):
+        lr = 0.05 / k
+        la = oa.step(lambda: a.loss(data[k][:, :-1], data[k][:, 1:]), lr)
+        static.copy_(data[k])
+        lb = gs.step(lr).item()
+        assert abs(la - lb) <= 1e-3 * abs(la)
+        assert oa.last_outcome == ob.last_outcome
+    for x, y in zip(a.parameters(), b.parameters()):
+        torch.testing.assert_close(x.float(), y.float(), rtol=2 ** -6, atol=1e-4)
