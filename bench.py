@@ -758,10 +758,15 @@ def bench_train_sharded(args, rank, world):
     # owned and updated per shard, and re-gathered once per applied step);
     # otherwise (65B) ZeRO-3 frees each layer after its forward and re-gathers it
     pbytes = sum(p.numel() * p.element_size() for p in model.parameters())
-    reshard = pbytes > 0.4 * torch.cuda.get_device_properties(0).total_memory
+    hbm = torch.cuda.get_device_properties(0).total_memory
+    reshard = pbytes > 0.4 * hbm
+    # pass 2: K1 over pass 1's reduced gradient shards when 1/world of the
+    # gradients fits in 15 % of HBM, else replay of the stashed (x, dy)
+    keep = not args.sharded_strict and pbytes / world < 0.15 * hbm
     opt = ShardedLOMO(model, lr=1e-3, clip_grad_norm=1.0,
                       loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
-                      reshard_after_forward=reshard, replay=not args.sharded_strict)
+                      reshard_after_forward=reshard,
+                      replay=not args.sharded_strict and not keep, keep_grads=keep)
     torch.cuda.empty_cache()
     seq, batch = args.seq, args.batch
     gen = torch.Generator(device="cuda").manual_seed(rank)
@@ -794,7 +799,8 @@ def bench_train_sharded(args, rank, world):
            "activation_checkpointing": ckpt, "passes_per_step": 2, "outcomes": outcomes,
            "reshard_after_forward": reshard, "clocks": clk.summary(),
            "pass2": "second forward + backward" if args.sharded_strict else
-                    "replay of the stashed (x, dy) into the buckets",
+                    (f"K1 over pass 1's reduced gradient shards ({pbytes / world / 2**30:.1f} GiB "
+                     "kept per rank)" if keep else "replay of the stashed (x, dy) into the buckets"),
            "peak_mem_gib_rank0": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
            "paper_tgs_rtx3090": {"13b": 66.19, "30b": 11.61, "65b": 4.93}.get(size)}
     opt.remove_hooks()

@@ -148,6 +148,17 @@ class _Bucket:
         self.gathered = False
 
 
+class _KeptShards:
+    """ShardedLOMO(keep_grads=True): pass 1's reduced gradient shard per
+    bucket, consumed by pass 2 (the protocol treats it like a replay stash)."""
+
+    def __init__(self):
+        self.shards: dict[int, torch.Tensor] = {}
+
+    def clear(self) -> None:
+        self.shards.clear()
+
+
 class _SymmRing:
     """A few symmetric-memory gradient buffers per dtype.  Autograd can
     interleave the gradients of adjacent buckets, so a buffer is owned by one
@@ -214,6 +225,12 @@ class ShardedLOMO(_Protocol):
             re-derives every local gradient from them (the same GEMM) into the
             buckets and runs the same reduce-scatter + K1 per bucket.  Pass 2
             needs no parameter gather.  Needs ``direct_grads``.
+        keep_grads: two-pass mode keeping this rank's reduced gradient shard
+            of every bucket from pass 1 (1/world of the gradients: 180 GB of
+            HBM holds them) -- pass 2 is K1 over the kept shards, with no
+            gradient recompute and no second reduce-scatter.  The update is
+            the same as the strict protocol's (pass 1's reduced gradient IS
+            pass 2's).  Not with ``fused_rs`` (K4 never materialises a shard).
     """
 
     _always_scale = True  # inv_scale carries the 1/world of the data-parallel mean
@@ -223,7 +240,7 @@ class ShardedLOMO(_Protocol):
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
                  math: str = "f32", buckets=None, reshard_after_forward: bool = True,
                  process_group=None, fused_rs: bool = False, direct_grads: bool = True,
-                 replay: bool = False, _engine=None):
+                 replay: bool = False, keep_grads: bool = False, _engine=None):
         if not dist.is_initialized():
             raise ConfigError("ShardedLOMO needs torch.distributed to be initialised")
         if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
@@ -272,6 +289,12 @@ class ShardedLOMO(_Protocol):
             for dt in {b.dtype for b in self.buckets}:
                 n = max(b.padded for b in self.buckets if b.dtype == dt)
                 self._rings[dt] = _SymmRing(n, dt, self.device, process_group)
+        if keep_grads and (fused_rs or replay):
+            raise ConfigError("keep_grads replaces replay and needs the NCCL reduce-scatter "
+                              "(not fused_rs)")
+        if keep_grads and self.passes != 2:
+            raise ConfigError("keep_grads replaces the second pass: it needs clip_grad_norm "
+                              "or loss_scale")
         if replay and not direct_grads:
             raise ConfigError("ShardedLOMO(replay=True) needs direct_grads=True")
         if replay and self.passes != 2:
@@ -281,7 +304,7 @@ class ShardedLOMO(_Protocol):
         if direct_grads:
             self._lin = _replay.ReplayStash(keep=replay)
             self._lin.probe = self._lin.update = self._dw_into_bucket
-        self._stash = self._lin if replay else None
+        self._stash = self._lin if replay else (_KeptShards() if keep_grads else None)
         self._replay_mismatch = False
         self._inflight: list = []
         self._handles = [p.register_post_accumulate_grad_hook(self._hook) for p in params]
@@ -355,8 +378,8 @@ class ShardedLOMO(_Protocol):
             p.grad = None
             self._replay_mismatch = True  # replay would drop this contribution
             return
-        if self._stash is not None and self._mode == _PROBE:
-            self._stash.grads[id(p)] = p.grad  # not a linear: kept for pass 2
+        if self._stash is self._lin and self._stash is not None and self._mode == _PROBE:
+            self._stash.grads[id(p)] = p.grad  # replay: not a linear, kept for pass 2
         if b.gflat is None:
             self._new_gflat(b)
         b.gflat[off:off + n].copy_(p.grad.reshape(-1))
@@ -455,6 +478,8 @@ class ShardedLOMO(_Protocol):
                 work.wait()
             if mode == _PROBE:
                 self.engine.probe(gshard, b.idx)
+                if isinstance(self._stash, _KeptShards):
+                    self._stash.shards[b.idx] = gshard  # pass 2 updates from it
             else:
                 self.engine.update(b.shard, gshard)
                 b.dirty = True
@@ -481,7 +506,8 @@ class ShardedLOMO(_Protocol):
                 _replay._ACTIVE = None
             self.engine.flush()
         st = self._stash
-        if st is not None and mode == _PROBE and (st.shared or self._replay_mismatch):
+        if st is not None and st is self._lin and mode == _PROBE and \
+                (st.shared or self._replay_mismatch):
             st.clear()
             self._replay_mismatch = False
             raise ConfigError("replay: a weight receives gradient from more than one op "
@@ -493,6 +519,19 @@ class ShardedLOMO(_Protocol):
         dW = dy^T x for the linears, the kept tensor for the rest -- then the
         bucket's reduce-scatter + K1 on this rank's shard."""
         st = self._stash
+        if isinstance(st, _KeptShards):
+            # pass 1 already produced this rank's reduced gradient shards
+            try:
+                for b in self.buckets:
+                    g = st.shards.pop(b.idx, None)
+                    if g is not None:
+                        self.engine.update(b.shard, g)
+                        b.dirty = True
+                        del g
+            finally:
+                st.clear()
+                self.engine.flush()
+            return
         self._mode = _UPDATE
         try:
             with torch.no_grad():

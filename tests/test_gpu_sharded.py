@@ -32,7 +32,7 @@ def nccl_world():
 
 
 @pytest.mark.parametrize("stab_kind", ["plain", "norm_scaler", "norm_scaler_replay",
-                                       "norm_scaler_replay_ckpt"])
+                                       "norm_scaler_replay_ckpt", "norm_scaler_keep"])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_sharded_world1_matches_lomo(nccl_world, stab_kind, dtype):
     from paper_2306_09782_b200 import LOMO, ClipMode, LossScaler, Stabilizer
@@ -46,11 +46,12 @@ def test_sharded_world1_matches_lomo(nccl_world, stab_kind, dtype):
         return Stabilizer(ClipMode.by_global_norm(0.5), LossScaler(2.0 ** 8, 2))
 
     replay, ckpt = "replay" in stab_kind, stab_kind.endswith("ckpt")
-    stab_kind = stab_kind.split("_replay")[0]
+    keep = stab_kind.endswith("_keep")
+    stab_kind = stab_kind.split("_replay")[0].removesuffix("_keep")
     a = Llama(CFG, dtype=dtype, device="cuda", seed=0)
     b = Llama(CFG, dtype=dtype, device="cuda", seed=0, checkpointing=ckpt)
     oa = LOMO(a, lr=0.05, stabilizer=stab())
-    ob = ShardedLOMO(b, lr=0.05, stabilizer=stab(), replay=replay)
+    ob = ShardedLOMO(b, lr=0.05, stabilizer=stab(), replay=replay, keep_grads=keep)
     assert all(not bk.gathered for bk in ob.buckets if bk.module is not None)
     g = torch.Generator(device="cuda").manual_seed(1)
     for step in range(3):

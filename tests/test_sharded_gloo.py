@@ -73,7 +73,8 @@ def _worker(rank, world, port, mode, q):
 def _run(rank, world, port, mode, q):
     direct = not mode.endswith("_copy")  # weight gradients GEMM'd into the buckets
     replay = mode.endswith("_replay")    # pass 2 from the stashed (x, dy)
-    mode = mode.removesuffix("_copy").removesuffix("_replay")
+    keep = mode.endswith("_keep")        # pass 2 from pass 1's reduced shards
+    mode = mode.removesuffix("_copy").removesuffix("_replay").removesuffix("_keep")
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -94,7 +95,7 @@ def _run(rank, world, port, mode, q):
         nb = len(model.layers) + 1
         eng = CpuEngine(nb, stab.scaler if stab else None, max_norm, grad_div=world)
         opt = ShardedLOMO(model, lr=lr, stabilizer=stab, math="f64", _engine=eng,
-                          direct_grads=direct, replay=replay)
+                          direct_grads=direct, replay=replay, keep_grads=keep)
         # ZeRO-3: layer buckets are released between uses
         released = [not b.gathered for b in opt.buckets if b.module is not None]
         outcomes = []
@@ -120,7 +121,8 @@ def _run(rank, world, port, mode, q):
 
 
 @pytest.mark.parametrize("mode", ["plain", "norm", "norm_scaler", "skip", "norm_scaler_copy",
-                                  "norm_replay", "norm_scaler_replay", "skip_replay"])
+                                  "norm_replay", "norm_scaler_replay", "skip_replay",
+                                  "norm_scaler_keep", "skip_keep"])
 def test_sharded_lomo_matches_full_batch_reference(mode):
     world = 2
     ctx = mp.get_context("spawn")
@@ -141,7 +143,7 @@ def test_sharded_lomo_matches_full_batch_reference(mode):
         p.join(timeout=60)
         assert p.exitcode == 0
     res.sort(key=lambda t: t[0])
-    mode = mode.removesuffix("_copy").removesuffix("_replay")
+    mode = mode.removesuffix("_copy").removesuffix("_replay").removesuffix("_keep")
     max_norm = 0.5 if mode != "plain" else None
     want, want_out = _reference(3, world, max_norm, 0.05, inf_step=1 if mode == "skip" else None)
     for rank, released, outcomes, got in res:
