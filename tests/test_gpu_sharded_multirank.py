@@ -33,7 +33,8 @@ def _batch(step, world):
     return d[:, :-1], d[:, 1:]
 
 
-def _worker(rank, world, port, fused_rs, q):
+def _worker(rank, world, port, mode, q):
+    fused_rs = mode == "fused_rs"
     try:
         import torch.distributed as dist
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -44,7 +45,8 @@ def _worker(rank, world, port, fused_rs, q):
         from paper_2306_09782_b200.workloads import Llama
         model = Llama(CFG, dtype=torch.float64, device="cuda", seed=rank)  # rank 0 broadcast
         opt = ShardedLOMO(model, lr=0.05, clip_grad_norm=0.5, loss_scale=2.0 ** 8, math="f64",
-                          fused_rs=fused_rs)
+                          fused_rs=fused_rs, replay=mode == "replay",
+                          keep_grads=mode == "keep_grads")
         outs = []
         for step in range(3):
             ids, tgt = _batch(step, world)
@@ -77,15 +79,16 @@ def _reference(world):
     return {n: p.detach().cpu().numpy() for n, p in model.named_parameters()}
 
 
-@pytest.mark.parametrize("fused_rs", [False, True])
-def test_sharded_two_ranks_real_kernels(fused_rs):
+@pytest.mark.parametrize("mode", ["nccl_path", "fused_rs", "replay", "keep_grads"])
+def test_sharded_two_ranks_real_kernels(mode):
+    fused_rs = mode == "fused_rs"
     if not torch.cuda.is_available():
         pytest.skip("needs CUDA")
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, fused_rs, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = []
