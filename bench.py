@@ -798,6 +798,8 @@ def bench_train_sharded(args, rank, world):
            "ms_per_step": round(ms, 2), "seq_len": seq, "batch_per_rank": batch,
            "activation_checkpointing": ckpt, "passes_per_step": 2, "outcomes": outcomes,
            "reshard_after_forward": reshard, "clocks": clk.summary(),
+           "tensor_roofline": _sharded_roofline(model, batch, seq, ms, keep,
+                                                args.sharded_strict, ckpt, clk.summary()),
            "pass2": "second forward + backward" if args.sharded_strict else
                     (f"K1 over pass 1's reduced gradient shards ({pbytes / world / 2**30:.1f} GiB "
                      "kept per rank)" if keep else "replay of the stashed (x, dy) into the buckets"),
@@ -807,6 +809,31 @@ def bench_train_sharded(args, rank, world):
     del opt, model
     torch.cuda.empty_cache()
     return out
+
+
+def _sharded_roofline(model, batch, seq, ms, keep, strict, ckpt, clk):
+    """Tensor work per rank of one sharded step (the linears' GEMMs: 2 flop
+    per weight per token for the forward, the input gradient and the weight
+    gradient; plus causal attention) against the bf16 peak."""
+    tokens = batch * seq
+    lin = sum(p.numel() for n, p in model.named_parameters() if p.dim() == 2
+              and "embed" not in n)
+    cfg = model.cfg
+    attn_fwd = 2 * 2 * tokens * seq * 0.5 * cfg["hidden"] * cfg["layers"]
+    # forward + backward (dx, dW); strict adds a second forward + backward,
+    # replay a second dW GEMM, keep_grads nothing; checkpointing one more forward
+    gemms = 3 + (3 if strict else 0 if keep else 1) + (1 if ckpt else 0)
+    attn = attn_fwd * (3.5 + (3.5 if strict else 0) + (1 if ckpt else 0))
+    tflop = (gemms * 2 * tokens * lin + attn) / 1e12
+    pflops = tflop / (ms * 1e-3) / 1e3
+    peak_tf, peak_src = _bf16_peak_tflops()
+    peak_pf = peak_tf / 1e3
+    scale = (clk.get("sm_mhz") or 0) / (clk.get("sm_max_mhz") or 1) if clk.get("sm_mhz") else None
+    return {"tflop_per_step_per_rank": round(tflop, 2), "achieved_pflops_per_rank": round(pflops, 3),
+            "peak_pflops": round(peak_pf, 3), "peak_source": peak_src,
+            "frac": round(pflops / peak_pf, 3),
+            "frac_at_run_clock": (round(pflops / (peak_pf * scale), 3)
+                                  if scale and "sustained" not in peak_src else None)}
 
 
 def _sharded_world1(args):
