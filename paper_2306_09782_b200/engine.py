@@ -7,6 +7,8 @@ Every method only enqueues work on the current CUDA stream except
 """
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import _lib
@@ -68,7 +70,11 @@ class CudaEngine:
         self.ptr = self.state.data_ptr()
         off = _lib.SCALE_F32_OFFSET
         self.scale_view = self.state[off:off + 4].view(torch.float32).view(())
-        self.status = _lib.LomoStatus()
+        # the status block lands in pinned host memory: the read is one DMA,
+        # not a staged pageable copy, on the step's one host round trip
+        self._status_buf = torch.empty(ctypes.sizeof(_lib.LomoStatus), dtype=torch.uint8,
+                                       pin_memory=True)
+        self.status = _lib.LomoStatus.from_address(self._status_buf.data_ptr())
         with torch.cuda.device(device):
             _lib.check(self.lib.lomo_state_init(
                 self.ptr, self.nslots,
