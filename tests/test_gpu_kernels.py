@@ -521,3 +521,37 @@ def test_k4_rejects_misaligned_slices():
                                         _lib.MATH_F32, 0.1, 0.0, 0.0, 0, None, U.stream()) == -1
     assert U.lib().lomo_fused_rs_update(p.data_ptr(), peers.data_ptr(), 17, 0, 8, _lib.BF16,
                                         _lib.MATH_F32, 0.1, 0.0, 0.0, 0, None, U.stream()) == -1
+
+
+def test_k1_k2_beyond_2_31_elements():
+    """One tensor of 2^31 + 27 bf16 elements (8.6 GB for p and g): 64-bit
+    indexing in K1 and K2, the grid for more than 2^31 elements, the scalar
+    tail.  K1 (f32 math) against torch's fp32 update on the slices around
+    2^31 and at the tail (<= 1 ulp); K2's sum of squares against a float64
+    sum; the overflow flag for a NaN placed beyond 2^31."""
+    n = (1 << 31) + 27
+    free, _ = torch.cuda.mem_get_info()
+    if free < 12 * 2 ** 30:
+        pytest.skip("needs 12 GiB of free device memory")
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    p = torch.empty(n, dtype=torch.bfloat16, device="cuda").uniform_(-0.08, 0.08, generator=gen)
+    g = torch.empty(n, dtype=torch.bfloat16, device="cuda").normal_(0.0, 1e-2, generator=gen)
+    lo, hi = (1 << 31) - 4096, (1 << 31) + 27
+    windows = [slice(0, 4096), slice(lo, hi)]
+    want = [(p[w].float() - 0.05 * g[w].float()) for w in windows]
+    st = U.State(1)
+    st.begin()
+    st.probe(g, 0, 0)
+    ref = sum(float((g[i:i + (1 << 28)].double() ** 2).sum()) for i in range(0, n, 1 << 28))
+    got = float(st.slots(1)[0])
+    assert abs(got - ref) <= 1e-5 * ref, (got, ref)
+    U.fused_update(p, g, lr=0.05)
+    for w, x in zip(windows, want):
+        d = U.ulp_diff(p[w], x.to(torch.bfloat16))
+        assert int(d.max()) <= 1, w
+    g[(1 << 31) + 20] = float("nan")
+    st.begin()
+    st.probe(g, 0, 0)
+    assert st.status().overflow == 1
+    del p, g
+    torch.cuda.empty_cache()
