@@ -248,6 +248,18 @@ class ShardedLOMO(_Protocol):
         st = stabilizer if stabilizer is not None else stabilizer_from_args(
             clip_grad_norm, clip_grad_value, loss_scale)
         self._init_protocol(st, lr, weight_decay)
+        # option checks before the parameters are moved into buckets
+        if keep_grads and (fused_rs or replay):
+            raise ConfigError("keep_grads replaces replay and needs the NCCL reduce-scatter "
+                              "(not fused_rs)")
+        if keep_grads and self.passes != 2:
+            raise ConfigError("keep_grads replaces the second pass: it needs clip_grad_norm "
+                              "or loss_scale")
+        if replay and not direct_grads:
+            raise ConfigError("ShardedLOMO(replay=True) needs direct_grads=True")
+        if replay and self.passes != 2:
+            raise ConfigError("replay replaces the second pass: it needs clip_grad_norm or "
+                              "loss_scale")
         self.group = process_group
         self.world = dist.get_world_size(process_group)
         self.rank = dist.get_rank(process_group)
@@ -289,17 +301,6 @@ class ShardedLOMO(_Protocol):
             for dt in {b.dtype for b in self.buckets}:
                 n = max(b.padded for b in self.buckets if b.dtype == dt)
                 self._rings[dt] = _SymmRing(n, dt, self.device, process_group)
-        if keep_grads and (fused_rs or replay):
-            raise ConfigError("keep_grads replaces replay and needs the NCCL reduce-scatter "
-                              "(not fused_rs)")
-        if keep_grads and self.passes != 2:
-            raise ConfigError("keep_grads replaces the second pass: it needs clip_grad_norm "
-                              "or loss_scale")
-        if replay and not direct_grads:
-            raise ConfigError("ShardedLOMO(replay=True) needs direct_grads=True")
-        if replay and self.passes != 2:
-            raise ConfigError("replay replaces the second pass: it needs clip_grad_norm or "
-                              "loss_scale")
         self._lin = None
         if direct_grads:
             self._lin = _replay.ReplayStash(keep=replay)
