@@ -399,6 +399,8 @@ class ShardedLOMO(_Protocol):
         b, off, n, j = loc
         if b.reduced:
             return False  # -> autograd -> _hook raises ConfigError
+        if a.dtype != b.dtype or d.dtype != b.dtype:
+            return False  # e.g. autocast activations: autograd's dW, then the hook
         if b.gflat is None:
             self._new_gflat(b)
         view = b.gflat[off:off + n].view(d.shape[-1], a.shape[-1])
