@@ -551,7 +551,12 @@ class ShardedLOMO(_Protocol):
             got = False
             for j, p in enumerate(b.params):
                 pid, off, n = id(p), b.offsets[j], b.numels[j]
-                if pid in st.linear:
+                if pid in st.grads:  # not a linear (or a linear autograd handled)
+                    st.linear.pop(pid, None)
+                    if b.gflat is None:
+                        self._new_gflat(b)
+                    b.gflat[off:off + n].copy_(st.grads.pop(pid).reshape(-1))
+                elif pid in st.linear:
                     a, d = st.linear.pop(pid)
                     if b.gflat is None:
                         self._new_gflat(b)
@@ -559,10 +564,6 @@ class ShardedLOMO(_Protocol):
                     torch.mm(d.reshape(-1, d.shape[-1]).t(), a.reshape(-1, a.shape[-1]),
                              out=view)
                     del a, d
-                elif pid in st.grads:
-                    if b.gflat is None:
-                        self._new_gflat(b)
-                    b.gflat[off:off + n].copy_(st.grads.pop(pid).reshape(-1))
                 else:
                     continue
                 b.filled[j] = True
