@@ -81,6 +81,7 @@ class ClockSampler:
 
     def __init__(self, index: int, period: float = 0.02):
         self.samples, self.reasons, self.period = [], set(), period
+        self.power = []
         self._stop = threading.Event()
         self.ok = False
         try:
@@ -89,6 +90,10 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1e3
+            except Exception:
+                self.limit_w = None
             self.ok = True
         except Exception:
             self.max_mhz = None
@@ -98,6 +103,10 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1e3)
+                except Exception:
+                    pass
                 fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
                     nv.nvmlDeviceGetCurrentClocksThrottleReasons
                 r = fn(self.h)
@@ -122,8 +131,12 @@ class ClockSampler:
     def summary(self):
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power:
+            out["power_w"] = round(statistics.median(self.power), 1)
+            out["power_limit_w"] = self.limit_w
+        return out
 
 
 # --------------------------------------------------------------------------
