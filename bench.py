@@ -509,7 +509,7 @@ def _bf16_peak_tflops() -> tuple[float, str]:
 
 
 _GRAPHED = ("replay_fused_gemm_graph", "strict_fused_gemm_graph", "single_pass_fused_gemm_graph",
-            "grouped_fused_gemm_graph")
+            "grouped_fused_gemm_graph", "strict_graph")
 
 
 def bench_train(args, rank, world):
@@ -553,7 +553,7 @@ def bench_train(args, rank, world):
            "clip_grad_norm": 1.0, "activation_checkpointing": bool(ckpt),
            "paper_tgs_rtx3090": 769.92}
     gstep = None
-    variants = ("strict", "strict_fused_gemm", "strict_fused_gemm_graph", "replay",
+    variants = ("strict", "strict_graph", "strict_fused_gemm", "strict_fused_gemm_graph", "replay",
                 "replay_fused_gemm",
                 "replay_fused_gemm_graph", "grouped", "grouped_fused_gemm",
                 "grouped_fused_gemm_graph", "single_pass_fused_gemm",
@@ -570,7 +570,7 @@ def bench_train(args, rank, world):
             else:
                 opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
                            loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
-                           replay=key.startswith("replay"), fuse_gemm=True)
+                           replay=key.startswith("replay"), fuse_gemm="fused_gemm" in key)
             static = data[0].clone()
             G = GraphedGroupedStep if key.startswith("grouped") else GraphedLOMOStep
             gstep = G(opt, lambda d: model.loss(d[:, :-1], d[:, 1:]), (static,),

@@ -37,7 +37,9 @@ class GraphedLOMOStep:
             loss_scale), built with ``replay=True`` (``fuse_gemm`` optional), or
             with ``fuse_gemm=True`` alone: the reference's protocol as is -- pass
             2 a second backward over the retained graph, K6 in pass 1 and K5
-            inside pass 2 -- captured the same way (no replay stash); or a
+            inside pass 2 -- captured the same way (no replay stash; also
+            without ``fuse_gemm``: the hook kernels K2 / K1 in the two
+            backwards); or a
             single-pass LOMO with ``fuse_gemm=True`` (K5 inside the one
             backward): graph 1 is the forward, the host checks the loss
             (optim.py:63-65), graph 2 the backward.
@@ -50,9 +52,9 @@ class GraphedLOMOStep:
 
     def __init__(self, opt: LOMO, loss_fn: Callable[..., torch.Tensor],
                  static_inputs: Sequence[torch.Tensor], warmup: int = 2, lr: float = 1e-3):
-        if not isinstance(opt, LOMO) or (opt._stash is None and not opt._fused_update):
-            raise ConfigError("GraphedLOMOStep needs a LOMO with replay=True (two-pass) or "
-                              "fuse_gemm=True")
+        if not isinstance(opt, LOMO) or (opt.passes == 1 and not opt._fused_update):
+            raise ConfigError("GraphedLOMOStep needs a two-pass LOMO (clip_grad_norm and/or "
+                              "loss_scale) or a single-pass LOMO with fuse_gemm=True")
         self.single = opt.passes == 1
         self.strict = opt._stash is None
         if opt.clip_value:

@@ -162,7 +162,8 @@ def test_graphed_step_equals_eager_step(fuse):
         assert torch.equal(x, y)
 
 
-def test_graphed_strict_fused_step_equals_eager():
+@pytest.mark.parametrize("fuse", [True, False])
+def test_graphed_strict_fused_step_equals_eager(fuse):
     """The reference's two-pass protocol (pass 2 a second backward, no stash)
     with K6/K5 inside the backward, captured in two CUDA graphs: decisions
     and loss-scale trajectory equal to the eager step, parameters equal up to
@@ -175,7 +176,7 @@ def test_graphed_strict_fused_step_equals_eager():
     cfg = dict(hidden=128, layers=2, heads=4, ffn=256, vocab=256)
     a = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
     b = Llama(cfg, dtype=torch.bfloat16, device="cuda", seed=0, fused_proj=True)
-    kw = dict(lr=0.05, clip_grad_norm=0.3, loss_scale=2.0 ** 8, fuse_gemm=True)
+    kw = dict(lr=0.05, clip_grad_norm=0.3, loss_scale=2.0 ** 8, fuse_gemm=fuse)
     oa, ob = LOMO(a, **kw), LOMO(b, **kw)
     gen = torch.Generator(device="cuda").manual_seed(7)
     data = [torch.randint(0, 256, (2, 65), device="cuda", generator=gen) for _ in range(6)]
