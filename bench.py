@@ -509,7 +509,7 @@ def _bf16_peak_tflops() -> tuple[float, str]:
 
 
 _GRAPHED = ("replay_fused_gemm_graph", "strict_fused_gemm_graph", "single_pass_fused_gemm_graph",
-            "grouped_fused_gemm_graph", "strict_graph")
+            "grouped_fused_gemm_graph", "strict_graph", "replay_graph")
 
 
 def bench_train(args, rank, world):
@@ -554,6 +554,7 @@ def bench_train(args, rank, world):
            "paper_tgs_rtx3090": 769.92}
     gstep = None
     variants = ("strict", "strict_graph", "strict_fused_gemm", "strict_fused_gemm_graph", "replay",
+                "replay_graph",
                 "replay_fused_gemm",
                 "replay_fused_gemm_graph", "grouped", "grouped_fused_gemm",
                 "grouped_fused_gemm_graph", "single_pass_fused_gemm",
