@@ -1,4 +1,7 @@
-"""CUDA-graph capture of a whole two-pass LOMO step (replay mode).
+"""CUDA-graph capture of a whole LOMO step: the two-pass replay step (below),
+the strict two-pass step (pass 2 a second backward over the retained autograd
+graph, with or without the fused GEMMs), the single fused pass, and
+GroupedLOMO's single pass (``GraphedGroupedStep``).
 
 A LLaMA-7B step issues ~3,000 kernels -- autograd's, the hook kernels, K5 --
 and at seq 1024 the host cannot launch them as fast as the B200 runs them.
