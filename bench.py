@@ -620,6 +620,9 @@ def bench_train(args, rank, world):
                     "peak_mem_gib": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
                     "loss_scale_final": getattr(opt, "loss_scale", None), "outcomes": outcomes,
                     "losses": [round(x, 4) for x in losses], "clocks": clk.summary()}
+        pw = out[key]["clocks"].get("power_w")
+        if pw:
+            out[key]["tokens_per_joule"] = round(out[key]["tokens_per_s"] / pw, 2)
         opt.remove_hooks()
         del opt
         step = gstep = None  # noqa: F841  (release the graphs' memory pool)
