@@ -579,7 +579,10 @@ def bench_train(args, rank, world):
 
             def step(k):
                 static.copy_(data[k % len(data)])
-                return gstep.step(1e-3).detach().item()
+                # the loss stays on the device until the timed loop ends: the
+                # graphed step's one host sync is its status read, and the next
+                # step's graphs are queued while this one's pass 2 runs
+                return gstep.step(1e-3).detach().clone()
         elif key == "single_pass_fused_gemm":
             # LOMO's own single fused pass (no clip, no scaler: optim.py:118-132)
             # with every linear's update inside its weight-gradient GEMM (K5 in
@@ -616,6 +619,7 @@ def bench_train(args, rank, world):
             end.record()
             torch.cuda.synchronize()
         ms = start.elapsed_time(end) / args.train_steps
+        losses = [float(x) for x in losses]
         out[key] = {"tokens_per_s": round(batch * seq / (ms * 1e-3), 1), "ms_per_step": round(ms, 2),
                     "peak_mem_gib": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
                     "loss_scale_final": getattr(opt, "loss_scale", None), "outcomes": outcomes,
@@ -687,7 +691,7 @@ def bench_train(args, rank, world):
             start.record()
             for k in range(args.train_steps):
                 static.copy_(d1[k % len(d1)])
-                gstep.step(1e-3).detach().item()
+                gstep.step(1e-3)
                 outcomes.append(opt.last_outcome.value)
             end.record()
             torch.cuda.synchronize()
