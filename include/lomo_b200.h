@@ -103,7 +103,8 @@ typedef struct lomo_state {
   uint32_t ticket;       /*  96: K2 last-block ticket (internal)                     */
   int32_t has_scaler;    /* 100                                                      */
   float scale_f32;       /* 104: scale as fp32 (exact: power of two), for loss*scale */
-  int32_t pad0;          /* 108                                                      */
+  int32_t error;         /* 108: sticky; 1: a probe kernel got slot >= nslots;   */
+                         /*      2: a peer barrier timed out (sharded K4)        */
   double grad_div;       /* 112: data-parallel gradient divisor (world size; 1)      */
   double lr;             /* 120: learning rate read under LOMO_LR_FROM_STATE          */
   /* followed by: double  sumsq[nslots];                      (per-slot totals)
@@ -199,6 +200,69 @@ int lomo_fused_rs_update(void* p_shard, const void* const* peer_bufs_dev, int wo
 int lomo_fused_rs_probe(const void* const* peer_bufs_dev, int world, int64_t offset,
                         int64_t n, int dtype, int slot, unsigned flags, void* state,
                         void* stream);
+/* NVLS form of K4: `mc` is this rank's slice [offset, offset+n) of the bucket
+ * at a MULTICAST address (lomo_mc_bind); every 16-byte vector is fetched with
+ * multimem.ld_reduce.add (the NVSwitch sums the `world` copies in flight, fp32
+ * accumulation for 16-bit storage, one rounding to the storage dtype -- what
+ * an NCCL reduce-scatter would deliver) and fed to the K1 arithmetic / the K2
+ * sum of squares.  dtype F32, F16 or BF16; n*sizeof(dtype) and the address
+ * 16-byte aligned. */
+int lomo_fused_mc_update(void* p_shard, const void* mc, int64_t n, int dtype, int math, double lr,
+                         double clip_value, double weight_decay, unsigned flags,
+                         const void* state, void* stream);
+int lomo_fused_mc_probe(const void* mc, int64_t n, int dtype, int slot, unsigned flags,
+                        void* state, void* stream);
+
+/* ---- peer memory for K4 (transport; one process per GPU) --------------- */
+/* The reduce-over-peers kernels need the ranks' bucket buffers mapped into
+ * each other's address space and a device-side barrier between ranks.  Two
+ * transports, both set up once per optimizer (host calls, synchronous):
+ *
+ * (1) CUDA IPC (any CUDA peers: NVLink P2P, or two processes sharing one GPU).
+ *     lomo_ipc_alloc: cudaMalloc(bytes) zero-filled + its IPC handle
+ *     (lomo_ipc_handle_bytes() bytes, copied to handle_out) -- the buffers
+ *     and a signal area live in this one allocation; lomo_ipc_open maps a
+ *     peer's handle (lazy peer access), lomo_ipc_close unmaps it,
+ *     lomo_ipc_free frees an own allocation.
+ * (2) NVLS multicast (NVSwitch; lomo_mc_supported() == 1).  Rank 0 creates
+ *     the multicast object (lomo_mc_create; world > 1 also exports a POSIX
+ *     file descriptor), the other ranks import it from rank 0's (pid, fd)
+ *     (lomo_mc_import, pidfd_getfd), every rank adds its device
+ *     (lomo_mc_add_device), and after ALL ranks have added theirs
+ *     (a host barrier), binds local memory and maps both views
+ *     (lomo_mc_bind: uc = this GPU's copy, mc = the multicast address).
+ *     `obj` is an opaque handle; lomo_mc_free releases everything.
+ *
+ * Device barrier: every rank calls it with the same (channel, epoch) sequence,
+ * epochs strictly increasing per channel (the caller counts).  It is one
+ * stream-ordered kernel: a system-scope release of everything this stream
+ * wrote before it, a signal to every peer, and an acquire-wait for every
+ * peer's signal.  A wait longer than timeout_ns sets *err_dev = 2 and returns
+ * (never hangs the GPU).  Pass &state->error: the step's status read then
+ * surfaces the timeout.
+ *   lomo_peer_barrier: sig_dev = DEVICE array of the world ranks' signal
+ *     areas (each LOMO_PEER_SIGNAL_BYTES, IPC-mapped; sig_dev[rank] is own).
+ *   lomo_mc_barrier: sig_mc / sig_uc = a LOMO_PEER_SIGNAL_BYTES area at the
+ *     multicast / this rank's unicast address of a bound multicast object. */
+#define LOMO_PEER_MAX 16
+#define LOMO_PEER_CHANNELS 16
+#define LOMO_PEER_SIGNAL_BYTES (8 * LOMO_PEER_CHANNELS * LOMO_PEER_MAX)
+#define LOMO_E_UNSUPPORTED (-3) /* capability absent (e.g. no multicast) */
+size_t lomo_ipc_handle_bytes(void);
+int lomo_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out);
+int lomo_ipc_open(const void* handle, void** dev_ptr);
+int lomo_ipc_close(void* dev_ptr);
+int lomo_ipc_free(void* dev_ptr);
+int lomo_peer_barrier(void* const* sig_dev, int world, int rank, int channel, uint64_t epoch,
+                      int64_t timeout_ns, int* err_dev, void* stream);
+int lomo_mc_supported(int device);
+int lomo_mc_create(int world, size_t bytes, uint64_t* obj, size_t* granted_bytes, int* fd);
+int lomo_mc_import(int pid, int fd, size_t bytes, uint64_t* obj);
+int lomo_mc_add_device(uint64_t obj, int device);
+int lomo_mc_bind(uint64_t obj, int device, void** uc_ptr, void** mc_ptr);
+int lomo_mc_free(uint64_t obj);
+int lomo_mc_barrier(void* sig_mc, const void* sig_uc, int world, int channel, uint64_t epoch,
+                    int64_t timeout_ns, int* err_dev, void* stream);
 
 /* ---- row-sparse embedding gradient (K1 on the rows a batch touched) ---- */
 /* The reference's embedding VJP scatters dy into a dense [V, h] gradient;

@@ -22,6 +22,13 @@ USE_SCALE, USE_COEF, USE_SKIP, ACCUM_F64, LR_FROM_STATE = 0x1, 0x2, 0x4, 0x8, 0x
 DEFER_ROWS = 0x20
 PROBE_KEEP_GRAD = 0x40
 PROBE_BLOCKS_PER_SLOT = 8192
+E_ARG, E_SLOT, E_UNSUPPORTED = -1, -2, -3
+PEER_MAX, PEER_CHANNELS = 16, 16
+PEER_SIGNAL_BYTES = 8 * PEER_CHANNELS * PEER_MAX
+# lomo_state.error codes (sticky, surfaced by the step's status read)
+STATE_ERRORS = {1: "a probe kernel was given a norm slot outside [0, nslots) (LOMO_E_SLOT)",
+                2: "a peer barrier timed out: a rank did not reach the same collective point "
+                   "(sharded fused_rs mode)"}
 ABI_VERSION = 1
 
 # every symbol the header declares (checked by tests/test_native_abi.py)
@@ -54,6 +61,21 @@ EXPORTS = (
     "lomo_gemm_probe_finish",
     "lomo_rows_aggregate",
     "lomo_fused_update_rows",
+    "lomo_fused_mc_update",
+    "lomo_fused_mc_probe",
+    "lomo_ipc_handle_bytes",
+    "lomo_ipc_alloc",
+    "lomo_ipc_open",
+    "lomo_ipc_close",
+    "lomo_ipc_free",
+    "lomo_peer_barrier",
+    "lomo_mc_supported",
+    "lomo_mc_create",
+    "lomo_mc_import",
+    "lomo_mc_add_device",
+    "lomo_mc_bind",
+    "lomo_mc_free",
+    "lomo_mc_barrier",
 )
 
 # include/lomo_workload.h: the benchmark decoder's fused layers (not the LOMO path)
@@ -98,7 +120,7 @@ class LomoStatus(ctypes.Structure):
         ("ticket", ctypes.c_uint32),
         ("has_scaler", ctypes.c_int32),
         ("scale_f32", ctypes.c_float),
-        ("pad0", ctypes.c_int32),
+        ("error", ctypes.c_int32),
         ("grad_div", ctypes.c_double),
         ("lr", ctypes.c_double),
     ]
@@ -149,6 +171,22 @@ _SIGS = {
     "lomo_fused_update_rows": (_i32, [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _dbl, _dbl, _dbl,
                                       _u32, _vp, _vp]),
     "lomo_gemm_probe_finish": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
+    "lomo_fused_mc_update": (_i32, [_vp, _vp, _i64, _i32, _i32, _dbl, _dbl, _dbl, _u32, _vp, _vp]),
+    "lomo_fused_mc_probe": (_i32, [_vp, _i64, _i32, _i32, _u32, _vp, _vp]),
+    "lomo_ipc_handle_bytes": (ctypes.c_size_t, []),
+    "lomo_ipc_alloc": (_i32, [ctypes.c_size_t, ctypes.POINTER(_vp), _vp]),
+    "lomo_ipc_open": (_i32, [_vp, ctypes.POINTER(_vp)]),
+    "lomo_ipc_close": (_i32, [_vp]),
+    "lomo_ipc_free": (_i32, [_vp]),
+    "lomo_peer_barrier": (_i32, [_vp, _i32, _i32, _i32, ctypes.c_uint64, _i64, _vp, _vp]),
+    "lomo_mc_supported": (_i32, [_i32]),
+    "lomo_mc_create": (_i32, [_i32, ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint64),
+                              ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(_i32)]),
+    "lomo_mc_import": (_i32, [_i32, _i32, ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint64)]),
+    "lomo_mc_add_device": (_i32, [ctypes.c_uint64, _i32]),
+    "lomo_mc_bind": (_i32, [ctypes.c_uint64, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "lomo_mc_free": (_i32, [ctypes.c_uint64]),
+    "lomo_mc_barrier": (_i32, [_vp, _vp, _i32, _i32, ctypes.c_uint64, _i64, _vp, _vp]),
     "lomo_wl_rmsnorm_fwd": (_i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, ctypes.c_float, _vp]),
     "lomo_wl_rmsnorm_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp]),
     "lomo_wl_rmsnorm_partial_rows": (_i32, [_i64]),

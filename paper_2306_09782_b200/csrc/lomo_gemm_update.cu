@@ -5,7 +5,8 @@
 // only to apply p <- p - lr * coef * dW / scale (optim.py:52-54 with the
 // update_hook stages, stabilize.py:217-224).  Here that update is the GEMM's
 // epilogue: the tcgen05 tensor-core GEMM accumulates dW tile by tile in TMEM
-// and the epilogue writes  p <- alpha * acc + beta * p  with
+// and the epilogue writes  p <- alpha * round(acc) + beta * p  (round = to the
+// storage dtype, the gradient autograd / the reference tape would deliver) with
 // alpha = -lr * coef / scale and beta = 1 - lr * wd, so the gradient is never
 // materialised in HBM (K1 would have read it and p, and written p: 6 B/elem;
 // the fused epilogue moves 4 B/elem and needs no separate launch).
@@ -47,6 +48,30 @@ namespace lomo_gemm {
 
 using namespace cute;
 
+// fp32 accumulator -> the storage dtype's value (round to nearest even),
+// kept in fp32 for the update arithmetic
+template <typename Element>
+struct RoundToStorage {
+  template <class T>
+  struct Fn {
+    CUTLASS_HOST_DEVICE T operator()(T const& v) const { return v; }
+  };
+  template <int N>
+  struct Fn<cutlass::Array<float, N>> {
+    CUTLASS_DEVICE cutlass::Array<float, N> operator()(cutlass::Array<float, N> const& v) const {
+      cutlass::Array<float, N> out;
+      CUTLASS_PRAGMA_UNROLL
+      for (int i = 0; i < N; ++i) {
+        if constexpr (std::is_same<Element, cutlass::half_t>::value)
+          out[i] = __half2float(__float2half_rn(v[i]));
+        else
+          out[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+      }
+      return out;
+    }
+  };
+};
+
 // EpiN: epilogue sub-tile 128 x EpiN (0 = CUTLASS's choice).  128 x 32 keeps
 // more C-load / D-store stages in flight than the automatic 128 x 64: 4 %
 // faster over a 7B pass (profiles/r01_gemm_shapes.md)
@@ -68,8 +93,26 @@ struct FusedUpdateGemm {
   // (profiles/r01_gemm_shapes.md)
   using ClusterShape = Shape<_2, Int<ClusterN>, _1>;
 
-  using Fusion = cutlass::epilogue::fusion::LinearCombination<ElementC, ElementCompute, ElementC,
-                                                              ElementCompute>;
+  // D = fma(alpha, round_storage(acc), beta * C): the accumulator is first
+  // rounded to the storage dtype -- the gradient the reference's tape would
+  // deliver (tape.py:377, grad = self._round(grad)) and K1 would read --
+  // then the update of optim.py:52-54 with one rounding (beta == 1 exactly
+  // when there is no weight decay).
+  template <class T>
+  using RoundFn = typename RoundToStorage<Element>::template Fn<T>;
+  using Scalar = cutlass::epilogue::fusion::Sm90ScalarBroadcast<float, Stride<_0, _0, int64_t>>;
+  using RoundAcc = cutlass::epilogue::fusion::Sm90EVT<
+      cutlass::epilogue::fusion::Sm90Compute<RoundFn, float, float,
+                                             cutlass::FloatRoundStyle::round_to_nearest>,
+      cutlass::epilogue::fusion::Sm90AccFetch>;
+  using BetaC = cutlass::epilogue::fusion::Sm90EVT<
+      cutlass::epilogue::fusion::Sm90Compute<cutlass::multiplies, float, float,
+                                             cutlass::FloatRoundStyle::round_to_nearest>,
+      Scalar, cutlass::epilogue::fusion::Sm90SrcFetch<ElementC>>;
+  using Fusion = cutlass::epilogue::fusion::Sm90EVT<
+      cutlass::epilogue::fusion::Sm90Compute<cutlass::homogeneous_multiply_add, ElementC, float,
+                                             cutlass::FloatRoundStyle::round_to_nearest>,
+      Scalar, RoundAcc, BetaC>;
 
   using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
       cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
@@ -107,11 +150,18 @@ struct FusedUpdateGemm {
         cutlass::gemm::GemmUniversalMode::kGemm,
         {M, N, K, 1},
         {static_cast<const ElementA*>(dy), sA, static_cast<const ElementB*>(x), sB},
-        {{alpha, beta}, static_cast<const ElementC*>(p), sC, static_cast<ElementC*>(p), sD}};
-    if (coefs_dev != nullptr) {  // alpha/beta read by the epilogue at run time
-      args.epilogue.thread.alpha_ptr = coefs_dev;
-      args.epilogue.thread.beta_ptr = coefs_dev + 1;
+        {{}, static_cast<const ElementC*>(p), sC, static_cast<ElementC*>(p), sD}};
+    // tree arguments: children first, node last; alpha/beta from device
+    // memory at run time when coefs_dev is given (graph-capturable)
+    typename Scalar::Arguments a{}, b{};
+    a.scalars[0] = alpha;
+    b.scalars[0] = beta;
+    if (coefs_dev != nullptr) {
+      a.scalar_ptrs[0] = coefs_dev;
+      b.scalar_ptrs[0] = coefs_dev + 1;
     }
+    args.epilogue.thread = typename Fusion::Arguments{
+        a, typename RoundAcc::Arguments{{}, {}}, typename BetaC::Arguments{b, {}, {}}, {}};
     // persistent tile scheduler sized to the device (epilogue of tile i overlaps
     // the mainloop of tile i+1 through the double-buffered TMEM accumulator)
     args.hw_info = hw_info();

@@ -482,6 +482,17 @@ __device__ __forceinline__ double* partials_of(lomo_state* s, int slot) {
   return slots_of(s) + s->nslots + nblocks_words(s->nslots) +
          (size_t)slot * LOMO_PROBE_BLOCKS_PER_SLOT;
 }
+// One CTA's partial of norm slot `slot` (thread 0).  A slot outside
+// [0, nslots) writes nothing and raises the sticky state->error (the host
+// turns it into LOMO_E_SLOT at the step's status read).
+__device__ __forceinline__ void put_partial(lomo_state* st, int slot, double v, int nblocks) {
+  if ((unsigned)slot >= (unsigned)st->nslots) {
+    st->error = 1;
+    return;
+  }
+  partials_of(st, slot)[blockIdx.x] = v;
+  if (blockIdx.x == 0) nblocks_of(st)[slot] = nblocks;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -639,8 +650,7 @@ __global__ void __launch_bounds__(kThreads, 5)  // 48 registers: 5 CTAs per SM, 
   // order (deterministic, no atomics on the hot path)
   const double bsum = block_sum(acc, sm);
   if (threadIdx.x == 0) {
-    partials_of(st, slot)[blockIdx.x] = bsum;
-    if (blockIdx.x == 0) nblocks_of(st)[slot] = (int32_t)gridDim.x;
+    put_partial(st, slot, bsum, (int)gridDim.x);
   }
 }
 
@@ -673,8 +683,13 @@ __global__ void __launch_bounds__(kThreads)
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
   const double r = block_sum(acc, sm);
   if (threadIdx.x == 0) {
-    slots_of(st)[tab.slot[blockIdx.x]] = r;
-    nblocks_of(st)[tab.slot[blockIdx.x]] = 0;  // reduced in place
+    const int slot = tab.slot[blockIdx.x];
+    if ((unsigned)slot >= (unsigned)st->nslots) {
+      st->error = 1;
+    } else {
+      slots_of(st)[slot] = r;
+      nblocks_of(st)[slot] = 0;  // reduced in place
+    }
   }
 }
 
@@ -698,8 +713,7 @@ __global__ void __launch_bounds__(kThreads)
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
   const double bsum = block_sum(acc, sm);
   if (threadIdx.x == 0) {
-    partials_of(st, slot)[blockIdx.x] = bsum;
-    if (blockIdx.x == 0) nblocks_of(st)[slot] = (int32_t)gridDim.x;
+    put_partial(st, slot, bsum, (int)gridDim.x);
   }
 }
 
@@ -744,8 +758,7 @@ __global__ void __launch_bounds__(kThreads) k6_rows_multi(const __grid_constant_
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
   const double bsum = block_sum(acc, sm);
   if (threadIdx.x == 0) {
-    partials_of(st, tab.slot[e])[blockIdx.x] = bsum;
-    if (blockIdx.x == 0) nblocks_of(st)[tab.slot[e]] = (int32_t)tab.rows[e];
+    put_partial(st, tab.slot[e], bsum, (int)tab.rows[e]);
   }
 }
 
@@ -848,8 +861,69 @@ __global__ void __launch_bounds__(kThreads)
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
   const double bsum = block_sum(acc, sm);
   if (threadIdx.x == 0) {
-    partials_of(st, slot)[blockIdx.x] = bsum;
-    if (blockIdx.x == 0) nblocks_of(st)[slot] = (int32_t)gridDim.x;
+    put_partial(st, slot, bsum, (int)gridDim.x);
+  }
+}
+
+// NVLS form: one multimem.ld_reduce per 16-byte vector at the multicast
+// address -- the switch fetches the vector from every rank's copy and returns
+// the sum (fp32 accumulation for 16-bit storage, one rounding to storage, as
+// an NCCL reduce-scatter output would be), so each GPU's inbound NVLink
+// traffic is its slice once instead of once per peer.
+template <typename T>
+__device__ __forceinline__ uint4 mc_ld_reduce(const void* mc) {
+  uint4 r;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(mc) : "memory");
+  } else if constexpr (std::is_same<T, __half>::value) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(mc) : "memory");
+  } else {
+    static_assert(std::is_same<T, float>::value, "NVLS K4: f32, f16 or bf16 storage");
+    float x, y, z, w;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "l"(mc) : "memory");
+    r = make_uint4(__float_as_uint(x), __float_as_uint(y), __float_as_uint(z), __float_as_uint(w));
+  }
+  return r;
+}
+
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k4_mc_update(T* __restrict__ p, const T* __restrict__ mc, int64_t nvec, UpdArgs<M> a,
+                 unsigned flags, const lomo_state* st) {
+  pdl_enter();
+  const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (i >= nvec) return;
+  const uint4 gv = mc_ld_reduce<T>(reinterpret_cast<const uint4*>(mc) + i);
+  uint4* pv = reinterpret_cast<uint4*>(p);
+  const uint4 P = ld_stream_rw(pv + i);
+  if (!resolve_args(a, flags, st)) return;  // overlaps the loads above
+  st_stream(pv + i, upd_vec<T, M>(P, gv, a));
+}
+
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads)
+    k4_mc_probe(const T* __restrict__ mc, int64_t nvec, int64_t per_cta, int slot,
+                unsigned flags, void* state) {
+  __shared__ double sm[kThreads / 32];
+  pdl_wait();
+  pdl_launch_dependents();
+  lomo_state* st = hdr(state);
+  const bool use_scale = (flags & LOMO_USE_SCALE) != 0;
+  const M inv_scale = use_scale ? (M)st->inv_scale : (M)1;
+  double acc = 0.0;
+  bool bad = false;
+  const int64_t beg = (int64_t)blockIdx.x * per_cta;
+  const int64_t end = min(beg + per_cta, nvec);
+  const uint4* gv = reinterpret_cast<const uint4*>(mc);
+  for (int64_t i = beg + threadIdx.x; i < end; i += kThreads)
+    acc += vec_sumsq<T, M>(mc_ld_reduce<T>(gv + i), inv_scale, use_scale, bad);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
+  const double bsum = block_sum(acc, sm);
+  if (threadIdx.x == 0) {
+    put_partial(st, slot, bsum, (int)gridDim.x);
   }
 }
 
@@ -989,7 +1063,7 @@ __global__ void k_state_init(void* state, int nslots, double scale, int growth_i
     st->steps_applied = 0;
     st->steps_skipped = 0;
     st->ticket = 0;
-    st->pad0 = 0;
+    st->error = 0;
     st->lr = 0.0;
   }
   double* s = reinterpret_cast<double*>(reinterpret_cast<char*>(state) + sizeof(lomo_state));
@@ -1248,6 +1322,33 @@ int launch_rs_probe(const void* const* peers, int world, int64_t off, int64_t n,
                 state);
 }
 
+template <typename T, typename M>
+int launch_mc_update(void* p, const void* mc, int64_t n, double lr, double clip, double wd,
+                     unsigned flags, const void* state, cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  if (n % V != 0 || ((uintptr_t)mc & 15) != 0 || ((uintptr_t)p & 15) != 0) return LOMO_E_ARG;
+  const int64_t nvec = n / V;
+  const unsigned grid = (unsigned)((nvec + kThreads - 1) / kThreads);
+  return launch(k4_mc_update<T, M>, dim3(grid > 0 ? grid : 1), dim3(kThreads), s,
+                static_cast<T*>(p), static_cast<const T*>(mc), nvec,
+                make_args<M>(lr, clip, wd, flags), flags, static_cast<const lomo_state*>(state));
+}
+
+template <typename T, typename M>
+int launch_mc_probe(const void* mc, int64_t n, int slot, unsigned flags, void* state,
+                    cudaStream_t s) {
+  constexpr int V = 16 / sizeof(T);
+  if (n % V != 0 || ((uintptr_t)mc & 15) != 0) return LOMO_E_ARG;
+  const int64_t nvec = n / V;
+  int64_t per_cta = (nvec + LOMO_PROBE_BLOCKS_PER_SLOT - 1) / LOMO_PROBE_BLOCKS_PER_SLOT;
+  per_cta = (per_cta + kThreads - 1) / kThreads * kThreads;
+  if (per_cta < 4 * kThreads) per_cta = 4 * kThreads;
+  int64_t grid = (nvec + per_cta - 1) / per_cta;
+  if (grid < 1) grid = 1;
+  return launch(k4_mc_probe<T, M>, dim3((unsigned)grid), dim3(kThreads), s,
+                static_cast<const T*>(mc), nvec, per_cta, slot, flags, state);
+}
+
 }  // namespace lomo_k
 using namespace lomo_k;
 
@@ -1302,7 +1403,8 @@ int lomo_fused_update(void* p, const void* g, int64_t n, int dtype, int math, do
   if (n < 0) return LOMO_E_ARG;
   if (n == 0) return 0;
   if (p == nullptr || g == nullptr) return LOMO_E_ARG;
-  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP)) && state == nullptr)
+  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP | LOMO_LR_FROM_STATE)) &&
+      state == nullptr)
     return LOMO_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const bool f64 = math == LOMO_MATH_F64;
@@ -1335,7 +1437,8 @@ int lomo_fused_update_multi(void* const* p_list, const void* const* g_list,
     if (n_list[i] < 0) return LOMO_E_ARG;
     if (n_list[i] > 0 && (p_list[i] == nullptr || g_list[i] == nullptr)) return LOMO_E_ARG;
   }
-  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP)) && state == nullptr)
+  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP | LOMO_LR_FROM_STATE)) &&
+      state == nullptr)
     return LOMO_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const bool f64 = math == LOMO_MATH_F64;
@@ -1464,7 +1567,8 @@ int lomo_fused_rs_update(void* p_shard, const void* const* peer_bufs_dev, int wo
   if (n < 0 || offset < 0 || world < 1 || world > kMaxPeers) return LOMO_E_ARG;
   if (n == 0) return 0;
   if (p_shard == nullptr || peer_bufs_dev == nullptr) return LOMO_E_ARG;
-  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP)) && state == nullptr)
+  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP | LOMO_LR_FROM_STATE)) &&
+      state == nullptr)
     return LOMO_E_ARG;
   if (math != LOMO_MATH_F32 && math != LOMO_MATH_F64) return LOMO_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1498,6 +1602,49 @@ int lomo_fused_rs_probe(const void* const* peer_bufs_dev, int world, int64_t off
                  : launch_rs_probe<__nv_bfloat16, float>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
     case LOMO_F32: return launch_rs_probe<float, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
     case LOMO_F64: return launch_rs_probe<double, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
+  }
+  return LOMO_E_ARG;
+}
+
+int lomo_fused_mc_update(void* p_shard, const void* mc, int64_t n, int dtype, int math, double lr,
+                         double clip_value, double weight_decay, unsigned flags,
+                         const void* state, void* stream) {
+  if (n < 0) return LOMO_E_ARG;
+  if (n == 0) return 0;
+  if (p_shard == nullptr || mc == nullptr) return LOMO_E_ARG;
+  if ((flags & (LOMO_USE_SCALE | LOMO_USE_COEF | LOMO_USE_SKIP | LOMO_LR_FROM_STATE)) &&
+      state == nullptr)
+    return LOMO_E_ARG;
+  if (math != LOMO_MATH_F32 && math != LOMO_MATH_F64) return LOMO_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool f64 = math == LOMO_MATH_F64;
+#define LOMO_MCU(T, M) \
+  launch_mc_update<T, M>(p_shard, mc, n, lr, clip_value, weight_decay, flags, state, s)
+  switch (dtype) {
+    case LOMO_F16: return f64 ? LOMO_MCU(__half, double) : LOMO_MCU(__half, float);
+    case LOMO_BF16: return f64 ? LOMO_MCU(__nv_bfloat16, double) : LOMO_MCU(__nv_bfloat16, float);
+    case LOMO_F32: return f64 ? LOMO_MCU(float, double) : LOMO_MCU(float, float);
+  }
+#undef LOMO_MCU
+  return LOMO_E_ARG;  // f64 storage: no multimem f64 vector reduction; use the IPC form
+}
+
+int lomo_fused_mc_probe(const void* mc, int64_t n, int dtype, int slot, unsigned flags,
+                        void* state, void* stream) {
+  if (state == nullptr || n < 0) return LOMO_E_ARG;
+  if (slot < 0) return LOMO_E_SLOT;
+  if (n == 0) return 0;
+  if (mc == nullptr) return LOMO_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool f64 = (flags & LOMO_ACCUM_F64) != 0;
+  switch (dtype) {
+    case LOMO_F16:
+      return f64 ? launch_mc_probe<__half, double>(mc, n, slot, flags, state, s)
+                 : launch_mc_probe<__half, float>(mc, n, slot, flags, state, s);
+    case LOMO_BF16:
+      return f64 ? launch_mc_probe<__nv_bfloat16, double>(mc, n, slot, flags, state, s)
+                 : launch_mc_probe<__nv_bfloat16, float>(mc, n, slot, flags, state, s);
+    case LOMO_F32: return launch_mc_probe<float, double>(mc, n, slot, flags, state, s);
   }
   return LOMO_E_ARG;
 }

@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from .dispatch import HookDispatcher
-from .errors import ConfigError, ShapeError
+from .errors import ConfigError, NativeError, ShapeError
 
 DTYPE_CODE = {
     torch.float32: _lib.F32,
@@ -130,6 +130,18 @@ class CudaEngine:
                                                 slot, d.flags, self.ptr, self.stream()),
                    "lomo_fused_rs_probe")
 
+    # K4, NVLS form: `mc` = this rank's slice of the bucket at the multicast address
+    def mc_update(self, p_shard: torch.Tensor, mc: int) -> None:
+        d = self.dispatch
+        _lib.check(self.lib.lomo_fused_mc_update(
+            p_shard.data_ptr(), mc, p_shard.numel(), DTYPE_CODE[p_shard.dtype], self.math, d.lr,
+            d.clip, d.wd, d.flags, self.ptr, self.stream()), "lomo_fused_mc_update")
+
+    def mc_probe(self, mc: int, n: int, dtype: torch.dtype, slot: int) -> None:
+        d = self.dispatch
+        _lib.check(self.lib.lomo_fused_mc_probe(mc, n, DTYPE_CODE[dtype], slot, d.flags, self.ptr,
+                                                self.stream()), "lomo_fused_mc_probe")
+
     def finalize(self) -> None:
         _lib.check(self.lib.lomo_finalize_norm(self.ptr, self.stream()), "lomo_finalize_norm")
 
@@ -148,7 +160,16 @@ class CudaEngine:
         _lib.check(self.lib.lomo_read_status(self.ptr, self.status, self.stream()),
                    "lomo_read_status")
         torch.cuda.current_stream(self.device).synchronize()
+        if self.status.error:
+            raise NativeError(_lib.STATE_ERRORS.get(self.status.error,
+                                                    f"device error {self.status.error}"))
         return self.status
+
+    @property
+    def error_ptr(self) -> int:
+        """Device address of the state's sticky ``error`` word (peer barriers
+        report a timeout there, so the step's status read surfaces it)."""
+        return self.ptr + _lib.LomoStatus.error.offset
 
     @property
     def launches(self) -> int:

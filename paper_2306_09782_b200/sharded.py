@@ -30,22 +30,25 @@ GPUs of one box (north star (3)).
   one ``all_gather`` exchanges ``{sumsq, overflow}`` per rank, and K3a decides
   on the rank-ordered sum -- the same bits on every rank, no float atomics.
 * Gradient peak: one bucket (flat) instead of one tensor.
-* ``fused_rs=True`` (K4): the flat gradient buffers live in symmetric memory
-  (peer-mapped over NVLink, torch symmetric memory); when a bucket is complete
-  every rank runs ONE kernel that loads its slice from all peers' buffers,
-  sums in rank order and applies the update (or the probe) directly -- no
-  reduce-scatter output is ever written.  Two buffers alternate between
-  buckets; a device barrier before the kernel (all peers wrote the bucket) and
-  one before a buffer is refilled (all peers finished reading it) order the
-  ranks.  (Three buffers: autograd can interleave adjacent buckets.)
+* ``fused_rs`` (K4): the flat gradient buffers are peer-mapped (``peer.py``:
+  CUDA IPC, or an NVSwitch multicast object); when a bucket is complete every
+  rank runs ONE kernel that reduces its slice over all ranks' buffers -- P2P
+  loads summed in rank order (IPC), or ``multimem.ld_reduce`` (NVLS) -- and
+  applies the update (or the probe) directly: no reduce-scatter output is
+  ever written.  Three buffers rotate between buckets (autograd can
+  interleave adjacent buckets); a device barrier before the kernel (all ranks
+  wrote the bucket) and one before a buffer is refilled (all ranks finished
+  reading it) order the ranks.
 """
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 import torch.distributed as dist
 
+from . import peer as _peer
 from . import replay as _replay
 from .engine import CudaEngine, dtype_code
 from .errors import ConfigError
@@ -159,42 +162,21 @@ class _KeptShards:
         self.shards.clear()
 
 
-class _SymmRing:
-    """A few symmetric-memory gradient buffers per dtype.  Autograd can
-    interleave the gradients of adjacent buckets, so a buffer is owned by one
-    open bucket until its K4 launch; reuse waits for a device barrier (every
-    rank finished reading it).  Acquisition order follows the hook order,
-    which is identical on every rank."""
-
-    NBUF = 3
-
-    def __init__(self, numel: int, dtype, device, group):
-        import torch.distributed._symmetric_memory as symm
-        name = (group if group is not None else dist.group.WORLD).group_name
-        self.bufs, self.handles = [], []
-        for _ in range(self.NBUF):
-            t = symm.empty(numel, dtype=dtype, device=device)
-            self.handles.append(symm.rendezvous(t, name))
-            self.bufs.append(t)
-        self.owner = [None] * self.NBUF
-        self.read_pending = [False] * self.NBUF
-        self.k = 0
-
-    def acquire(self, bucket_idx: int) -> int:
-        for _ in range(self.NBUF):
-            k = self.k
-            self.k = (self.k + 1) % self.NBUF
-            if self.owner[k] is None:
-                if self.read_pending[k]:
-                    self.handles[k].barrier(channel=self.NBUF + k)  # peers done reading
-                    self.read_pending[k] = False
-                self.owner[k] = bucket_idx
-                return k
-        raise RuntimeError("more than {} buckets receive gradients at once".format(self.NBUF))
-
-    def release(self, k: int) -> None:
-        self.owner[k] = None
-        self.read_pending[k] = True
+def _pick_transport(fused_rs, device, group) -> str:
+    """fused_rs=True / "auto": NVLS when every rank has its own multicast-capable
+    GPU, else CUDA IPC; "ipc" / "nvls" force one."""
+    if fused_rs in ("ipc", "nvls"):
+        return fused_rs
+    if fused_rs not in (True, "auto"):
+        raise ConfigError(f"fused_rs must be False, True, 'auto', 'ipc' or 'nvls', got {fused_rs!r}")
+    world = dist.get_world_size(group)
+    props = torch.cuda.get_device_properties(device)
+    mine = (os.uname().nodename, str(getattr(props, "uuid", device)),
+            _peer.nvls_available(device))
+    everyone: list = [None] * world
+    dist.all_gather_object(everyone, mine, group=group)
+    distinct = len({(h, u) for h, u, _ in everyone}) == world
+    return "nvls" if distinct and all(ok for _, _, ok in everyone) else "ipc"
 
 
 class ShardedLOMO(_Protocol):
@@ -211,7 +193,9 @@ class ShardedLOMO(_Protocol):
             its forward (ZeRO-3); False keeps them resident (ZeRO-2-like).
         process_group: the data-parallel group (default: WORLD).
         fused_rs: K4 -- reduce over peer memory fused with the update instead
-            of NCCL reduce_scatter + K1/K2 (CUDA + NVLink peers only).
+            of NCCL reduce_scatter + K1/K2.  ``True``/``"auto"``: NVLS
+            multicast when every rank has its own multicast-capable GPU, else
+            CUDA IPC; ``"ipc"`` / ``"nvls"`` force a transport.
         direct_grads: weight gradients of the model's linears
             (``replay.linear`` / ``replay.matmul_in_out``) are computed by the
             linear's backward straight into the bucket's flat buffer
@@ -239,7 +223,7 @@ class ShardedLOMO(_Protocol):
                  loss_scale=None, *, clip_grad_value: float | None = None,
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
                  math: str = "f32", buckets=None, reshard_after_forward: bool = True,
-                 process_group=None, fused_rs: bool = False, direct_grads: bool = True,
+                 process_group=None, fused_rs: bool | str = False, direct_grads: bool = True,
                  replay: bool = False, keep_grads: bool = False, _engine=None):
         if not dist.is_initialized():
             raise ConfigError("ShardedLOMO needs torch.distributed to be initialised")
@@ -293,14 +277,20 @@ class ShardedLOMO(_Protocol):
             self.device, len(self.buckets), self.scaler, self.max_norm, math,
             grad_div=float(self.world))
         self._mode = 0
-        self.fused_rs = bool(fused_rs)
+        self.fused_rs = fused_rs is not False and fused_rs is not None
         self._rings: dict = {}
+        self.transport = None
         if self.fused_rs:
             if self.device.type != "cuda" or self.world > 16:
                 raise ConfigError("fused_rs needs CUDA peers (<= 16 ranks over NVLink)")
-            for dt in {b.dtype for b in self.buckets}:
+            self.transport = _pick_transport(fused_rs, self.device, process_group)
+            if self.transport == "nvls" and any(b.dtype == torch.float64 for b in self.buckets):
+                raise ConfigError("fused_rs='nvls' reduces f32/f16/bf16 buckets (multimem has no "
+                                  "f64 vector form); use fused_rs='ipc'")
+            for dt in sorted({b.dtype for b in self.buckets}, key=str):  # same order on every rank
                 n = max(b.padded for b in self.buckets if b.dtype == dt)
-                self._rings[dt] = _SymmRing(n, dt, self.device, process_group)
+                self._rings[dt] = _peer.PeerRing(n, dt, self.device, process_group,
+                                                 self.transport, err_ptr=self.engine.error_ptr)
         self._lin = None
         if direct_grads:
             self._lin = _replay.ReplayStash(keep=replay)
@@ -445,13 +435,11 @@ class ShardedLOMO(_Protocol):
             # K4: every rank has written the bucket -> reduce over peer memory
             # fused with the update / probe; nothing is written back
             ring = self._rings[b.dtype]
-            h = ring.handles[b.ring_k]
-            h.barrier(channel=b.ring_k)  # every rank has written this bucket
-            peers = h.buffer_ptrs_dev
+            ring.filled(b.ring_k)  # every rank has written this bucket
             if self._mode == _PROBE:
-                self.engine.rs_probe(peers, self.world, self.rank * b.S, b.S, b.dtype, b.idx)
+                ring.probe(self.engine, b.ring_k, self.rank * b.S, b.S, b.idx)
             else:
-                self.engine.rs_update(b.shard, peers, self.world, self.rank * b.S)
+                ring.update(self.engine, b.shard, b.ring_k, self.rank * b.S)
                 b.dirty = True
             ring.release(b.ring_k)
             b.gflat = None
@@ -597,6 +585,9 @@ class ShardedLOMO(_Protocol):
         for h in self._handles:
             h.remove()
         self._handles = []
+        for ring in self._rings.values():
+            ring.close()  # collective: every rank calls remove_hooks
+        self._rings = {}
 
     def gather_all(self) -> None:
         """Materialise every bucket's full parameters (e.g. for evaluation)."""

@@ -89,17 +89,28 @@ def test_sharded_with_checkpointing_world1(nccl_world):
     ob.remove_hooks()
 
 
+def _need_nvls(transport):
+    from paper_2306_09782_b200.peer import nvls_available
+    if transport == "nvls" and not nvls_available(torch.device("cuda", 0)):
+        pytest.skip("no NVLS multicast on this GPU (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 0)")
+
+
+@pytest.mark.parametrize("transport", ["ipc", "nvls"])
 @pytest.mark.parametrize("two_pass", [False, True])
-def test_fused_rs_world1_equals_nccl_path(nccl_world, two_pass):
-    """K4 over symmetric memory (world 1: the only peer is this GPU) gives the
-    same parameters as NCCL reduce_scatter + K1/K2."""
+def test_fused_rs_world1_equals_nccl_path(nccl_world, two_pass, transport):
+    """K4 over peer buffers (world 1: the only peer is this GPU) gives the
+    same parameters as NCCL reduce_scatter + K1/K2 -- over a CUDA-IPC
+    allocation, and over an NVLS multicast object (multimem.ld_reduce of one
+    copy is the copy)."""
     from paper_2306_09782_b200.sharded import ShardedLOMO
     from paper_2306_09782_b200.workloads import Llama
+    _need_nvls(transport)
     a = Llama(CFG, dtype=torch.bfloat16, device="cuda", seed=0)
     b = Llama(CFG, dtype=torch.bfloat16, device="cuda", seed=0)
     kw = dict(clip_grad_norm=0.5, loss_scale=2.0 ** 8) if two_pass else {}
     oa = ShardedLOMO(a, lr=0.05, **kw)
-    ob = ShardedLOMO(b, lr=0.05, fused_rs=True, **kw)
+    ob = ShardedLOMO(b, lr=0.05, fused_rs=transport, **kw)
+    assert ob.transport == transport
     g = torch.Generator(device="cuda").manual_seed(5)
     for step in range(3):
         d = torch.randint(0, CFG["vocab"], (2, 33), device="cuda", generator=g)
@@ -112,3 +123,47 @@ def test_fused_rs_world1_equals_nccl_path(nccl_world, two_pass):
         assert torch.equal(x, y)
     oa.remove_hooks()
     ob.remove_hooks()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float16, torch.bfloat16])
+def test_nvls_k4_kernels_world1(nccl_world, dtype):
+    """The NVLS K4 kernels on a one-device multicast object: ld_reduce over
+    the multicast address returns the one copy, so K4-mc equals K1/K2 on the
+    buffer itself (bit for bit; probe to fp32 summation order), and the
+    multimem.red barrier completes."""
+    from paper_2306_09782_b200 import _lib
+    from paper_2306_09782_b200.engine import CudaEngine
+    from paper_2306_09782_b200.peer import PeerRing
+    _need_nvls("nvls")
+    dev = torch.device("cuda", 0)
+    n = 3 * 8192 + 64
+    eng = CudaEngine(dev, 2, None, None, "f32")
+    ring = PeerRing(n, dtype, dev, None, "nvls", err_ptr=eng.error_ptr, timeout_s=10)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for rnd in range(4):
+        k = ring.acquire(rnd)
+        ring.bufs[k].copy_(torch.randn(n, generator=g, device=dev).to(dtype))
+        ring.filled(k)
+        p = torch.rand(n, generator=g, device=dev).to(dtype)
+        q = p.clone()
+        eng.configure(lr=0.125)
+        ring.update(eng, p, k, 0)
+        eng.update(q, ring.bufs[k])
+        eng.flush()
+        eng.configure(flags=0)
+        _lib.check(eng.lib.lomo_begin_step(eng.ptr, None, 0, eng.stream()), "begin")
+        ring.probe(eng, k, 0, n, 0)
+        eng.probe(ring.bufs[k], 1)
+        eng.flush()
+        _lib.check(eng.lib.lomo_local_norm_partial(eng.ptr, torch.zeros(2, dtype=torch.float64,
+                                                                      device=dev).data_ptr(),
+                                                   eng.stream()), "partial")
+        st = eng.read_status()  # raises on a barrier timeout
+        ring.release(k)
+        assert torch.equal(p, q), rnd
+        sl = torch.empty(2, dtype=torch.float64)
+        off = _lib.STATE_HEADER_BYTES
+        sl.copy_(eng.state[off:off + 16].view(torch.float64))
+        assert abs(sl[0] - sl[1]) <= 1e-6 * float(sl[1]), (rnd, sl)
+        assert not st.overflow
+    ring.close()
