@@ -1,13 +1,19 @@
 """K5: the weight-gradient GEMM with the LOMO update as its epilogue
 (csrc/lomo_gemm_update.cu, tcgen05 tensor cores), through the C-ABI.
 
-Reference: p_ref = round(beta * p + alpha * (dy^T x)) with the product in
-float64 (the reference's full-width update arithmetic, optim.py:52-54, on the
-exact gradient).  Tolerance (stated): within one ulp of the operands' scale,
-|got - ref| <= ulp(|p| + |alpha dy^T x|) -- the fp32 tensor-core
-accumulation error is far below that; where p and the update cancel the
-result's own ulp is tiny, so a result-ulp bound would be meaningless there.
-fp16 results are additionally within 1 result-ulp everywhere (measured).
+The epilogue first rounds the fp32 accumulator to the storage dtype -- the
+gradient the reference tape delivers to the hook (tape.py:377) and K1 reads
+-- then applies p <- fma(alpha, g, beta * p) (optim.py:52-54 with the
+update_hook factors folded into alpha, stabilize.py:217-224).
+
+* K5 == K6 (same tcgen05 mainloop, gradient kept) -> K1, BIT FOR BIT, when
+  alpha = -lr (identical gradients, identical arithmetic).
+* Against float64: p_ref = round(beta * p + alpha * round16(dy^T x)); within
+  TWO ulps of the operands' scale |p| + |alpha g| (stated tolerance): one for
+  the update's rounding, one because the fp32 accumulation can move the
+  16-bit gradient by one of its ulps near a rounding tie (alpha * ulp(g) is
+  at most one operand ulp).  Measured: max 2.0, mismatching elements
+  <= 8.4e-4.
 """
 import numpy as np
 import pytest
@@ -50,7 +56,7 @@ def test_gemm_update_matches_f64_reference(dtype, out_f, in_f, tokens):
     x = torch.randn(tokens, in_f, device="cuda", generator=g).to(dtype)
     alpha, beta = -0.05 * 0.7 / 1024.0 * 1024.0, 1.0
     p0 = p.double()
-    upd = alpha * (dy.double().t() @ x.double())
+    upd = alpha * (dy.double().t() @ x.double()).to(dtype).double()  # the rounded gradient
     want = O.round_to((beta * p0 + upd).cpu().numpy(), prec)
     assert _run(p, dy, x, alpha, beta) == 0
     torch.cuda.synchronize()
@@ -63,9 +69,40 @@ def test_gemm_update_matches_f64_reference(dtype, out_f, in_f, tokens):
     ulp = np.ldexp(1.0, np.maximum(e - 1, emin) - mant)
     print(f"{dtype} {out_f}x{in_f}x{tokens}: max result-ulp {d.max().item()}, "
           f"mismatch {frac:.2e}, max err/operand-ulp {np.max(err / ulp):.3f}")
-    assert np.all(err <= ulp)
-    if dtype == torch.float16:
-        assert d.max().item() <= 1
+    assert np.all(err <= 2 * ulp)
+    assert frac <= 2e-3
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("out_f,in_f,tokens", [(256, 128, 64), (4096, 4096, 1024),
+                                               (1000, 2816, 1000), (11008, 4096, 512)])
+def test_gemm_update_equals_k6_grad_then_k1(dtype, out_f, in_f, tokens):
+    """Identical gradients: K6 with LOMO_PROBE_KEEP_GRAD stores the rounded
+    accumulator of the same mainloop K5 runs; K1 (f32 math) on that gradient
+    must equal K5 bit for bit."""
+    from paper_2306_09782_b200.engine import CudaEngine
+    lib = U.lib()
+    dt = U.CODE[dtype]
+    g = torch.Generator(device="cuda").manual_seed(7 * out_f + tokens)
+    p = torch.empty(out_f, in_f, device="cuda").uniform_(-0.08, 0.08, generator=g).to(dtype)
+    dy = (torch.randn(tokens, out_f, device="cuda", generator=g) * 1e-2).to(dtype)
+    x = torch.randn(tokens, in_f, device="cuda", generator=g).to(dtype)
+    lr = 0.05 * 0.7
+    q = p.clone()
+    assert _run(p, dy, x, -lr, 1.0) == 0
+    st = CudaEngine(torch.device("cuda", 0), 1)
+    need = lib.lomo_gemm_probe_workspace(out_f, in_f, tokens, dt)
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device="cuda")
+    grad = torch.empty(out_f, in_f, dtype=dtype, device="cuda")
+    assert lib.lomo_gemm_probe(dy.data_ptr(), x.data_ptr(), grad.data_ptr(), out_f, in_f, tokens,
+                               dt, 0, _lib.PROBE_KEEP_GRAD, st.ptr, ws.data_ptr(), need,
+                               U.stream()) == 0
+    _lib.check(lib.lomo_fused_update(q.data_ptr(), grad.data_ptr(), q.numel(), dt, _lib.MATH_F32,
+                                     lr, 0.0, 0.0, 0, None, U.stream()), "K1")
+    torch.cuda.synchronize()
+    d = U.ulp_diff(p, q)
+    print(f"{dtype} {out_f}x{in_f}x{tokens}: K5 vs K6-grad->K1 max ulp {d.max().item()}")
+    assert torch.equal(p, q)
 
 
 def test_gemm_update_weight_decay_and_zero_alpha():
@@ -110,22 +147,17 @@ def test_lomo_replay_fused_gemm_matches_replay_k1(dtype):
     la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
     lb = ob.step(lambda: b.loss(d[:, :-1], d[:, 1:]), 0.05)
     assert oa.last_outcome == ob.last_outcome and la == lb
-    # K5 applies the fp32 accumulator; K1 applies dW rounded to 16 bits first
-    # (relative 2^-8 / 2^-11 of the step): same step up to that rounding
-    eps = 2.0 ** -7 if dtype == torch.bfloat16 else 2.0 ** -10
-    worst = 0.0
-    for (name, x), y, q in zip(a.named_parameters(), b.parameters(), p0):
-        xf, yf = x.detach().float(), y.detach().float()
-        quantum = 2.0 ** -24 if dtype == torch.float16 else 2.0 ** -133  # subnormal ulp
-        tol = eps * torch.maximum(xf.abs(), yf.abs()) + eps * (xf - q).abs() + quantum
-        r = (xf - yf).abs() / tol
-        if r.max().item() > worst:
-            i = r.argmax()
-            print(name, tuple(x.shape), "unfused", xf.flatten()[i].item(), "fused",
-                  yf.flatten()[i].item(), "p0", q.flatten()[i].item())
-        worst = max(worst, r.max().item())
-    print(f"{dtype}: fused vs unfused, max |diff| / tolerance = {worst:.3f}")
-    assert worst <= 1.0
+    # identical protocol; the gradients differ only by cuBLAS's vs the
+    # tcgen05 kernel's fp32 summation order before their rounding to 16 bits,
+    # and alpha folds lr * coef / scale into one fp32 constant: within one ulp
+    d = U.ulp_diff(torch.cat([x.detach().reshape(-1) for x in a.parameters()]),
+                   torch.cat([y.detach().reshape(-1) for y in b.parameters()]))
+    moved = torch.cat([(x.detach().float() - q).reshape(-1) != 0
+                       for x, q in zip(a.parameters(), p0)])
+    print(f"{dtype}: fused vs unfused max ulp {d.max().item()}, mean ulp "
+          f"{d.double().mean().item():.2e}, {int(moved.sum())} elements moved")
+    assert d.max().item() <= 1
+    assert d.double().mean().item() <= 1e-3
 
 
 # --- CUDA-graph capture of the replay step (graphs.py) -----------------------------

@@ -110,7 +110,9 @@ def test_c1_fixture_fp16_two_pass(c1_meta, c1_arrays, key, scaler, math_mode):
     print(f"fixture {key} fp16 ({math_mode} math): max ulp {u.max()}, mean ulp {u.mean():.4f}, "
           f">2ulp fraction {(u > 2).mean():.2e}, max loss rel {rel:.2e}")
     assert rel < 5e-3
-    assert u.mean() < 0.25 and u.max() <= 64
+    # measured (B200): max 15 / 9 ulp, mean 0.0154 / 0.0078 (f32 math);
+    # the error is the torch fp16 forward/backward ops', not the update's
+    assert u.mean() <= 0.02 and u.max() <= 16
 
 
 @pytest.mark.parametrize("replay", [True, False])
@@ -123,8 +125,8 @@ def test_c1_fixture_fp16_two_pass_fused_gemm(c1_meta, c1_arrays, key, scaler, re
     K5 applies every update inside its GEMM in pass 2 (replayed, or in the
     strict second backward).  Fixtures B (norm clip + growing scale) and C
     (forced fp16 overflows): skip decisions and the scale trajectory equal the
-    reference run's exactly; parameters differ only by K5 applying the fp32
-    accumulator instead of the fp16-rounded gradient (max / mean ulp printed)."""
+    reference run's exactly; parameters carry the same error profile as the
+    hook path (K5 rounds the accumulator to fp16 before the update)."""
     stab = Stabilizer(ClipMode.by_global_norm(1.0), LossScaler(
         scaler.scale, growth_interval=scaler.growth_interval, max_scale=scaler.max_scale))
     model, opt, losses, outcomes, scales = _run_c1(
@@ -140,7 +142,10 @@ def test_c1_fixture_fp16_two_pass_fused_gemm(c1_meta, c1_arrays, key, scaler, re
           f"max ulp {u.max()}, mean ulp {u.mean():.4f}, >2ulp fraction {(u > 2).mean():.2e}, "
           f"max loss rel {rel:.2e}")
     assert rel < 5e-3
-    assert u.mean() < 0.5 and u.max() <= 64
+    # measured (B200): max 12 / 9 ulp, mean 0.0154 / 0.0079 -- the same
+    # profile as the hook path (K5 rounds the accumulator to fp16 first,
+    # tape.py:377, as K1 receives it)
+    assert u.mean() <= 0.02 and u.max() <= 16
 
 
 def test_lomo_equals_sgd_bit_exact_fp64():
