@@ -870,37 +870,105 @@ def _sharded_world1(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(max_seconds=20.0, steps=None):
-    """The reference's update arithmetic (oracle port of optim.py:52-54 with
-    the fp16-emulated write-back, tensor.py:30-38) on one LLaMA-7B decoder
-    layer's tensors (9 tensors, 202,383,360 elements), all host cores."""
+def _import_reference():
+    """The reference package itself: baseline/_ref (pip-installed from
+    /root/reference, travels to the GPU box) or the read-only source tree.
+    Returns (fusedtrain modules, where) or (None, why)."""
+    import importlib
+    for where in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (where / "fusedtrain" / "optim.py").exists():
+            if str(where) not in sys.path:
+                sys.path.insert(0, str(where))
+            try:
+                mods = {m: importlib.import_module(f"fusedtrain.{m}")
+                        for m in ("optim", "tape", "tensor", "estimate")}
+                return mods, str(where.relative_to(ROOT) if where.is_relative_to(ROOT) else where)
+            except Exception as exc:  # noqa: BLE001
+                return None, f"import from {where} failed: {exc}"
+    return None, "reference package not found (baseline/_ref missing)"
+
+
+def cpu_baseline(max_seconds=20.0, steps=None, threads=None):
+    """The reference's own CPU update (fusedtrain.optim.apply_update,
+    optim.py:52-54, with Tensor.assign's binary16 write-back, tensor.py:30-38,
+    74-81) over LLaMA-7B layer 0's 9 parameter tensors (202,383,360 elements,
+    HALF_EMULATED = the reference's 16-bit path), imported from baseline/_ref.
+    (i) as shipped: one thread (numpy elementwise), one 4096x4096 tensor;
+    (ii) all host cores: the same function on disjoint row blocks of every
+    tensor, one thread per block (numpy releases the GIL in the ufuncs).
+    Falls back to the oracle restatement (kind "port") only when the
+    reference cannot be imported."""
     import numpy as np
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import lomo_oracle as O
+    from concurrent.futures import ThreadPoolExecutor
     from paper_2306_09782_b200.workloads import llama_param_shapes
+    ref, where = _import_reference()
+    cores = threads or os.cpu_count() or 1
     shapes = [s for name, s in llama_param_shapes("7b") if name.startswith("layers.0.")]
     rng = np.random.default_rng(0)
-    P = [O.round_through_half(rng.uniform(-0.08, 0.08, math.prod(s))) for s in shapes]
-    G = [O.round_through_half(rng.normal(0.0, 1e-3, math.prod(s))) for s in shapes]
-    elems = sum(p.size for p in P)
-    cores = os.cpu_count() or 1
-    O.update_pass_threads(P[:1], G[:1], 0.05, O.HALF, cores)  # warm the pool/pages
+    if ref is not None:
+        T, Prm, apply = ref["tensor"], ref["tape"].Parameter, ref["optim"].apply_update
+        half = T.Precision.HALF_EMULATED
+
+        def make(values):
+            return Prm("w", 0, T.Tensor(values, half))
+
+        def upd(pg):
+            apply(pg[0], pg[1], 0.05)
+        kind = "reference"
+    else:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import lomo_oracle as O
+
+        class _P:  # the oracle's restatement of apply_update on a holder
+            def __init__(self, v):
+                self.v = O.round_through_half(v)
+
+        def make(values):
+            return _P(values)
+
+        def upd(pg):
+            pg[0].v = O.apply_update(pg[0].v, pg[1], 0.05, O.HALF)
+        kind = "port"
+    # (i) as shipped: one tensor, one thread
+    n1 = 4096 * 4096
+    one = (make(rng.uniform(-0.08, 0.08, n1)), np.round(rng.normal(0.0, 1e-3, n1), 8))
+    upd(one)
+    t0 = time.perf_counter()
+    upd(one)
+    single = 6 * n1 / (time.perf_counter() - t0) / 1e9
+    del one
+    # (ii) all cores: disjoint row blocks of every layer-0 tensor
+    work = []
+    for s in shapes:
+        rows, cols = s[0], math.prod(s[1:]) if len(s) > 1 else 1
+        per = max(1, rows // max(1, (2 * cores * rows * cols) // sum(math.prod(x) for x in shapes)))
+        for r0 in range(0, rows, per):
+            m = (min(rows, r0 + per) - r0) * cols
+            work.append((make(rng.uniform(-0.08, 0.08, m)),
+                         make(rng.normal(0.0, 1e-3, m)).value.data if kind == "reference"
+                         else O.round_through_half(rng.normal(0.0, 1e-3, m))))
+    elems = sum(math.prod(s) for s in shapes)
     times = []
-    t_all = time.perf_counter()
-    while True:
-        t0 = time.perf_counter()
-        O.update_pass_threads(P, G, 0.05, O.HALF, cores)
-        times.append(time.perf_counter() - t0)
-        if steps is not None and len(times) >= steps:
-            break
-        if steps is None and (time.perf_counter() - t_all > max_seconds or len(times) >= 20):
-            break
+    with ThreadPoolExecutor(cores) as ex:
+        list(ex.map(upd, work[:cores]))  # warm the pool
+        t_all = time.perf_counter()
+        while True:
+            t0 = time.perf_counter()
+            list(ex.map(upd, work))
+            times.append(time.perf_counter() - t0)
+            if steps is not None and len(times) >= steps:
+                break
+            if steps is None and (time.perf_counter() - t_all > max_seconds or len(times) >= 20):
+                break
     t = sum(times) / len(times)
     return {"value": round(BYTES_PER_ELEM * elems / t / 1e9, 3), "unit": "GB/s", "cores": cores,
-            "kind": "port",
-            "sample": f"apply_update (optim.py:52-54, fp16 write-back) over LLaMA-7B layer-0's "
-                      f"9 tensors ({elems} elements) x {len(times)} passes, float64 buffers like "
-                      f"the reference, numpy on a {cores}-thread pool",
+            "kind": kind, "source": where if kind == "reference" else "oracle/lomo_oracle.py",
+            "sample": f"fusedtrain.optim.apply_update (optim.py:52-54, HALF_EMULATED write-back "
+                      f"tensor.py:30-38) over LLaMA-7B layer-0's 9 tensors ({elems} elements, "
+                      f"{len(work)} disjoint row blocks) x {len(times)} passes, float64 buffers "
+                      f"as the reference keeps them, {cores} host threads",
+            "as_shipped_1thread_gbs": round(single, 3),
+            "as_shipped_sample": "one 4096x4096 tensor, one thread (numpy elementwise, as shipped)",
             "seconds_per_pass": round(t, 3),
             "full_7b_pass_seconds_extrapolated": round(t * 6738415616 / elems, 1)}
 
@@ -958,7 +1026,8 @@ def main():
                 "data": "synthetic p~U(-0.08,0.08), g~N(0,1e-3)", "impl": "reference",
                 "config": {"workload": "reference apply_update over LLaMA-7B layer-0 tensors "
                                        "(bounded sample of config 2)"},
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                    "source", "as_shipped_1thread_gbs")},
                 "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
