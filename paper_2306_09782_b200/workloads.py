@@ -562,10 +562,14 @@ class LlamaLayer(nn.Module):
             m = F.silu(gu[..., :f]) * gu[..., f:]
         return x, rlinear(m, self.down)
 
-    def forward(self, x, cos, sin):
+    def forward(self, x, cos, sin, pending=None, stream: bool = False):
+        """``stream=True`` (stacked projections): the residual-stream form
+        ``forward_res`` -> (stream, MLP output).  Llama calls every layer
+        through ``Module.__call__`` so per-layer module hooks (ShardedLOMO's
+        ZeRO-3 gather / release / refresh wait) fire on both forms."""
         if self.fused_proj:
-            x, mlp = self.forward_res(x, None, cos, sin)
-            return x + mlp
+            x, mlp = self.forward_res(x, pending, cos, sin)
+            return (x, mlp) if stream else x + mlp
         b, s, h = x.shape
         nh, dh = self.nh, h // self.nh
         fused = self.input_layernorm.fused
@@ -634,9 +638,9 @@ class Llama(nn.Module):
             for layer in self.layers:
                 if self.checkpointing and self.training:
                     x, pending = torch.utils.checkpoint.checkpoint(
-                        layer.forward_res, x, pending, cos, sin, use_reentrant=False)
+                        layer, x, cos, sin, pending, True, use_reentrant=False)
                 else:
-                    x, pending = layer.forward_res(x, pending, cos, sin)
+                    x, pending = layer(x, cos, sin, pending, True)
             _, y = add_rms_norm(x, pending, self.norm.weight)
             return rlinear(y, self.lm_head)
         for layer in self.layers:

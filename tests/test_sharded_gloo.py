@@ -36,9 +36,9 @@ def _batches(step, world):
     return d[:, :-1], d[:, 1:]
 
 
-def _reference(steps, world, max_norm, lr, inf_step=None):
+def _reference(steps, world, max_norm, lr, inf_step=None, fused_proj=False):
     from paper_2306_09782_b200.workloads import Llama
-    model = Llama(CFG, dtype=torch.float64, device="cpu", seed=0)
+    model = Llama(CFG, dtype=torch.float64, device="cpu", seed=0, fused_proj=fused_proj)
     outcomes = []
     for step in range(steps):
         ids, tgt = _batches(step, world)
@@ -75,6 +75,8 @@ def _run(rank, world, port, mode, q):
     replay = mode.endswith("_replay")    # pass 2 from the stashed (x, dy)
     keep = mode.endswith("_keep")        # pass 2 from pass 1's reduced shards
     mode = mode.removesuffix("_copy").removesuffix("_replay").removesuffix("_keep")
+    fused_proj = mode.endswith("_fp")    # stacked projections (layers called as forward_res)
+    mode = mode.removesuffix("_fp")
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -84,7 +86,7 @@ def _run(rank, world, port, mode, q):
         from paper_2306_09782_b200.sharded import ShardedLOMO
         from paper_2306_09782_b200.workloads import Llama
         torch.manual_seed(1234 + rank)  # ranks start different: broadcast must fix it
-        model = Llama(CFG, dtype=torch.float64, device="cpu", seed=rank)
+        model = Llama(CFG, dtype=torch.float64, device="cpu", seed=rank, fused_proj=fused_proj)
         lr = 0.05
         max_norm = 0.5 if mode != "plain" else None
         stab = None
@@ -122,7 +124,8 @@ def _run(rank, world, port, mode, q):
 
 @pytest.mark.parametrize("mode", ["plain", "norm", "norm_scaler", "skip", "norm_scaler_copy",
                                   "norm_replay", "norm_scaler_replay", "skip_replay",
-                                  "norm_scaler_keep", "skip_keep"])
+                                  "norm_scaler_keep", "skip_keep", "norm_scaler_fp",
+                                  "norm_scaler_fp_keep"])
 def test_sharded_lomo_matches_full_batch_reference(mode):
     world = 2
     ctx = mp.get_context("spawn")
@@ -144,8 +147,11 @@ def test_sharded_lomo_matches_full_batch_reference(mode):
         assert p.exitcode == 0
     res.sort(key=lambda t: t[0])
     mode = mode.removesuffix("_copy").removesuffix("_replay").removesuffix("_keep")
+    fused_proj = mode.endswith("_fp")
+    mode = mode.removesuffix("_fp")
     max_norm = 0.5 if mode != "plain" else None
-    want, want_out = _reference(3, world, max_norm, 0.05, inf_step=1 if mode == "skip" else None)
+    want, want_out = _reference(3, world, max_norm, 0.05, inf_step=1 if mode == "skip" else None,
+                                fused_proj=fused_proj)
     for rank, released, outcomes, got in res:
         assert all(released), "layer buckets must be released after construction (ZeRO-3)"
         assert outcomes == want_out, (rank, outcomes, want_out)
