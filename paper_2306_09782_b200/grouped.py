@@ -129,7 +129,9 @@ class GroupedLOMO:
     def _gemm_probe(self, wid: int, w, x, dy) -> bool:
         """K6 from the linear's backward: the retained gradient and the group
         slot's sum of squares / overflow from one tensor-core GEMM."""
-        p = self._by_id[wid]
+        p = self._by_id.get(wid)
+        if p is None or wid not in self._slot:  # not a managed leaf: autograd's dW + hook
+            return False
         if p.dtype not in (torch.bfloat16, torch.float16) or p.dim() != 2:
             return False
         out_f, in_f = p.shape

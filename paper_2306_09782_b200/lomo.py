@@ -337,6 +337,18 @@ class LOMO(_Protocol):
         self._lin = self._stash if replay else (
             ReplayStash(keep=False) if (self.fuse_probe or self._fused_update) else None)
         self._by_id = {id(p): p for p in uniq}
+        if self._fused_update and hasattr(model, "named_parameters"):
+            # tied weights (one Parameter under several names): K5 would apply
+            # the linear's share in place before autograd delivered the rest,
+            # and a single pass cannot be rolled back -- refuse up front.
+            # (A weight reused by two linears without being registered twice
+            # is only seen during backward: ConfigError after that step.)
+            seen: set[int] = set()
+            for name, p in model.named_parameters(remove_duplicate=False):
+                if p.requires_grad and id(p) in seen:
+                    raise ConfigError(f"fuse_gemm without replay: {name} is a tied weight; "
+                                      "use replay=True or fuse_gemm=False")
+                seen.add(id(p))
         self._coefs = None
         self._lr_from_state = False  # graph capture: the state's lr, set per replay
         self._pws = {}         # K6 workspace per weight (its partial sums stay until
@@ -520,15 +532,22 @@ class LOMO(_Protocol):
             ws = self._pws[wid] = torch.empty(need, dtype=torch.uint8, device=w.device)
         if self._gscratch is None:  # K6's clipped by-product store: 16 bytes
             self._gscratch = torch.empty(256, dtype=torch.uint8, device=w.device)
-        slot = self._slot[wid]
+        slot = self._slot.get(wid)
+        if slot is None:  # not a managed leaf (e.g. w.to(dtype)): autograd's dW + hook
+            return False
         stream = self.engine.stream()
         if self.probe_stream:
-            # beside the rest of the backward: x/dy stay alive in the stash and
-            # the partial sums go to this weight's own workspace; joined in
-            # _finish_probes, before K3a
+            # beside the rest of the backward; the partial sums go to this
+            # weight's own workspace; joined in _finish_probes, before K3a.
+            # dy / x may be freed by autograd as soon as the linear's backward
+            # returns (strict protocol, checkpoint recompute): record_stream
+            # keeps the allocator from handing their blocks to the main stream
+            # before K6 has read them
             if self._pstream is None:
                 self._pstream = torch.cuda.Stream(w.device)
             self._pstream.wait_stream(torch.cuda.current_stream(w.device))
+            dy2.record_stream(self._pstream)
+            x2.record_stream(self._pstream)
             stream = self._pstream.cuda_stream
         rc = lib.lomo_gemm_probe(dy2.data_ptr(), x2.data_ptr(), self._gscratch.data_ptr(), out_f,
                                  in_f, dy2.shape[0], dt, slot,
@@ -557,7 +576,10 @@ class LOMO(_Protocol):
     def _gemm_update_bw(self, wid: int, w, x, dy) -> bool:
         """K5 from inside the update backward: the weight's update applied as
         the epilogue of its weight-gradient GEMM (alpha/beta from device)."""
-        if not self._gemm_update(self._by_id[wid], x, dy, 0.0, coefs=self._coefs):
+        p = self._by_id.get(wid)
+        if p is None:  # not a managed leaf (e.g. w.to(dtype)): autograd's dW + hook
+            return False
+        if not self._gemm_update(p, x, dy, 0.0, coefs=self._coefs):
             return False
         self.hook_calls += 1
         return True
