@@ -16,20 +16,28 @@ Also on the line:
                 MEASURED_PEAKS.json hbm_gbs; traffic from the committed ncu capture
   e2e           the same pass through the C-ABI with HOST buffers: pinned H2D of
                 p and g, K1, D2H of p, all inside the timed region
-  cpu_baseline  the reference's update arithmetic (oracle port of optim.py:52-54,
-                fp16 emulation = the reference's 16-bit path) on all host cores
+  cpu_baseline  the reference's own fusedtrain.optim.apply_update (optim.py:52-54,
+                HALF_EMULATED write-back) imported from baseline/_ref, on all
+                host cores, plus its as-shipped single-thread rate
+  c1_parity     config 1: the reference's mini transformer, fixtures A/B/C
+                recorded from the reference, through the product path: decisions,
+                max/mean ulp, normwise error, GPU vs reference seconds
   train         config 3: LLaMA-7B fp16 LOMO, dynamic loss scale + two-pass
-                global-norm clip (1.0), seq 1024 x batch 1, tokens/s
+                global-norm clip (1.0), seq 1024 x batch 1, tokens/s; a fresh
+                model per variant; the measured Table-1 row beside the
+                reference estimator's
   train_sharded_world1
                 config 4's sharded train leg (LLaMA-13B, ShardedLOMO) in a world-1
                 NCCL group: the sharded machinery's cost next to plain LOMO
   clocks        NVML SM clock / throttle reasons sampled during the timed region
 
-N > 1 (torchrun): weak scaling -- every rank runs the same 7B-shaped update
-pass on its own parameters (its ZeRO-3 shards of an N x 7B model), no
-collective in the timed data path; ``value`` = all ranks' algorithmic bytes /
-max-over-ranks time.  The sharded TRAIN leg (configs 4/5) uses ShardedLOMO
-with NCCL reduce-scatter feeding the per-shard update.
+N > 1 (torchrun): the headline is the SHARDED update pass of LLaMA-7B (SURVEY
+8e): per rank 33 flat gradient buckets (its own backward's), reduced across
+the ranks -- NCCL reduce_scatter -> K1 on the rank's 1/W shard, and K4 over
+peer-mapped buffers -- ``value`` = the 7B update's algorithmic bytes / max-
+over-ranks time (strong scaling: the total work is one 7B update).  e2e is
+the same pass from pinned host buffers; the train leg is ShardedLOMO on
+LLaMA-13B (config 4) with NCCL_DEBUG=INFO init lines in the log.
 """
 from __future__ import annotations
 
@@ -376,6 +384,157 @@ def bench_update(args, rank, world):
             "kernel_ms_per_step": ksum_ms / args.steps, "shapes": shapes}
 
 
+def _buckets_7b(world: int, layers: int = 32):
+    """ShardedLOMO's buckets of LLaMA-7B: one per decoder layer (its 9
+    tensors) plus the embedding / final norm / head, each padded to a multiple
+    of 8 * world elements; delivery order = reverse registration.  ``layers``
+    < 32 keeps only the first layers (validation dry runs only)."""
+    from paper_2306_09782_b200.workloads import llama_param_shapes
+    groups: dict = {}
+    for name, shape in llama_param_shapes("7b"):
+        key = name.split(".")[1] if name.startswith("layers.") else "rest"
+        if key != "rest" and int(key) >= layers:
+            continue
+        groups[key] = groups.get(key, 0) + math.prod(shape)
+    sizes = [groups[k] for k in groups]
+    align = 8 * world
+    return [int(math.ceil(n / align) * align) for n in sizes], sum(sizes)
+
+
+def bench_sharded_update(args, rank, world):
+    """N > 1 headline: one sharded LOMO update pass of LLaMA-7B over the
+    ranks.  Every rank holds the full flat gradient buckets of
+    its own backward (33 buckets, 13.5 GB bf16, different data per rank);
+    per bucket, in delivery order:
+
+      nccl  reduce_scatter_tensor (SUM, NCCL over NVLink) -> K1 on this
+            rank's 1/W shard (inv_scale = 1/W: the data-parallel mean), the
+            K1 of bucket b enqueued once bucket b-1's collective is issued
+            (ShardedLOMO._reduce/_drain);
+      k4    the buckets live in peer-mapped buffers (peer.PeerRing: NVLS
+            multicast when available, else CUDA IPC); a device barrier, then
+            ONE kernel reduces this rank's slice over all ranks' buffers and
+            applies the update -- the reduced gradient never reaches HBM.
+
+    value = algorithmic update bytes of the whole job (6 B/param: the 7B
+    update, split 1/W per rank) / max-over-ranks time: strong scaling, the
+    total work is one 7B update.  Reported beside it: per-rank GB/s, the
+    NVLink bytes each rank moves (its gradient's (W-1)/W, out and in), and
+    K1's own roofline on the shard."""
+    import torch
+    import torch.distributed as dist
+    from paper_2306_09782_b200 import _lib
+    from paper_2306_09782_b200.engine import CudaEngine
+    from paper_2306_09782_b200.peer import PeerRing
+    from paper_2306_09782_b200.sharded import _pick_transport, reduce_scatter
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
+    sizes, P = _buckets_7b(world, args.update_layers)
+    nb = len(sizes)
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    G = [torch.empty(n, dtype=dt, device=dev).normal_(0.0, 1e-3, generator=gen) for n in sizes]
+    W = [torch.empty(n // world, dtype=dt, device=dev).uniform_(-0.08, 0.08, generator=gen)
+         for n in sizes]
+    GS = [torch.empty(n // world, dtype=dt, device=dev) for n in sizes]
+    eng = CudaEngine(dev, nb, None, None, "f32", grad_div=float(world))
+    eng.configure(lr=0.05, flags=_lib.USE_SCALE)
+    order = list(range(nb - 1, -1, -1))
+    # gloo (LOMO_BENCH_SHARE_GPU dry run) cannot overlap; NCCL runs async
+    async_ok = dist.get_backend() == "nccl"
+
+    def nccl_pass(events=None):
+        inflight = []
+        for b in order:
+            work = reduce_scatter(GS[b], G[b], None, async_op=async_ok)
+            inflight.append((work, b))
+            if len(inflight) > 1:  # K1 of the previous bucket once this one's RS is issued
+                w_, b_ = inflight.pop(0)
+                _k1(w_, b_, events)
+        while inflight:
+            w_, b_ = inflight.pop(0)
+            _k1(w_, b_, events)
+
+    def _k1(work, b, events):
+        if work is not None:
+            work.wait()
+        if events is not None:
+            events[b][0].record()
+        eng.update(W[b], GS[b])
+        if events is not None:
+            events[b][1].record()
+
+    def timed(fn, steps):
+        _barrier(world)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(steps):
+            fn()
+        s1.record()
+        _barrier(world)
+        return _max_over_ranks(s0.elapsed_time(s1) / steps, world)
+
+    out = {}
+    for _ in range(args.warmup):
+        nccl_pass()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        ms_nccl = timed(nccl_pass, args.steps)
+    launches = args.steps * nb
+    # K1's own time on the shards (per-launch events, a separate pass)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(nb)]
+    nccl_pass(ev)
+    torch.cuda.synchronize()
+    k1_ms = sum(a.elapsed_time(b) for a, b in ev)
+    k1_gbs = BYTES_PER_ELEM * (P / world) / (k1_ms * 1e-3) / 1e9
+    link_bytes = 2 * P * (world - 1) / world  # this rank's gradient bytes leaving (and entering)
+    out["nccl"] = {"ms_per_pass": round(ms_nccl, 3),
+                   "gbs": round(BYTES_PER_ELEM * P / (ms_nccl * 1e-3) / 1e9, 1),
+                   "per_rank_gbs": round(BYTES_PER_ELEM * P / world / (ms_nccl * 1e-3) / 1e9, 1),
+                   "nvlink_gbs_per_rank": round(link_bytes / (ms_nccl * 1e-3) / 1e9, 1),
+                   "k1_ms_per_pass": round(k1_ms, 3), "k1_gbs": round(k1_gbs, 1),
+                   "collective": "reduce_scatter_tensor " + dist.get_backend(),
+                   "clocks": clk.summary()}
+    del GS
+    # ---- K4 over peer-mapped buffers (every bucket resident, as the backward left it)
+    try:
+        transport = args.k4_transport or _pick_transport(True, dev, None)
+        ring = PeerRing(max(sizes), dt, dev, None, transport, err_ptr=eng.error_ptr,
+                        timeout_s=60.0, nbuf=nb)
+        for b in range(nb):
+            ring.bufs[b][:sizes[b]].copy_(G[b])
+        del G
+        torch.cuda.empty_cache()
+
+        def k4_pass():
+            for b in order:
+                ring.filled(b)  # every rank's bucket b is written
+                ring.update(eng, W[b], b, rank * (sizes[b] // world))
+        for _ in range(args.warmup):
+            k4_pass()
+        eng.read_status()  # a barrier timeout would raise here
+        ms_k4 = timed(k4_pass, args.steps)
+        eng.read_status()
+        out["k4"] = {"ms_per_pass": round(ms_k4, 3),
+                     "gbs": round(BYTES_PER_ELEM * P / (ms_k4 * 1e-3) / 1e9, 1),
+                     "per_rank_gbs": round(BYTES_PER_ELEM * P / world / (ms_k4 * 1e-3) / 1e9, 1),
+                     "nvlink_gbs_per_rank": round(link_bytes / (ms_k4 * 1e-3) / 1e9, 1),
+                     "transport": transport,
+                     "kernel": "lomo_fused_mc_update (multimem.ld_reduce)" if transport == "nvls"
+                               else "lomo_fused_rs_update (P2P loads, rank-order sum)"}
+        launches = max(launches, args.steps * nb * 2)
+        ring.close()
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+        traceback.print_exc()
+        out["k4"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    best = "k4" if out["k4"].get("gbs", 0) > out["nccl"]["gbs"] else "nccl"
+    out.update({"best": best, "ms": out[best]["ms_per_pass"], "gbs": out[best]["gbs"],
+                "elements": P, "buckets": nb, "nvlink_bytes_per_rank": int(link_bytes),
+                "launches": launches, "clocks": out["nccl"]["clocks"],
+                "k1_gbs": k1_gbs})
+    return out
+
+
 def _sum_over_ranks(x: int, world: int) -> int:
     import torch
     import torch.distributed as dist
@@ -487,6 +646,82 @@ def bench_e2e(args, rank, world):
             "path": "C-ABI lomo_fused_update, pinned host p/g -> HBM -> K1 -> host p"}
 
 
+def bench_e2e_sharded(args, rank, world):
+    """N > 1 e2e: the sharded update pass with HOST buffers.  Per bucket (delivery
+    order): H2D of this rank's gradient bucket and of its parameter shard
+    (pinned), NCCL reduce_scatter, K1 on the shard through the C-ABI, D2H of
+    the updated shard -- all inside the timed region, pipelined over NS
+    device slots and two copy streams.  The gradient host buffers cycle
+    through NS pinned buckets (the bytes copied per step are the full 2P)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2306_09782_b200 import _lib
+    from paper_2306_09782_b200.engine import CudaEngine
+    from paper_2306_09782_b200.sharded import reduce_scatter
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
+    sizes, P = _buckets_7b(world, args.update_layers)
+    nb, NS = len(sizes), max(2, args.e2e_slots)
+    mx = max(sizes)
+    gen = torch.Generator(device="cuda").manual_seed(77 + rank)
+    DG = [torch.empty(mx, dtype=dt, device=dev) for _ in range(NS)]
+    DW = [torch.empty(mx // world, dtype=dt, device=dev) for _ in range(NS)]
+    DS = [torch.empty(mx // world, dtype=dt, device=dev) for _ in range(NS)]
+    HG = [torch.empty(mx, dtype=dt, pin_memory=True) for _ in range(NS)]
+    for h in HG:
+        h.copy_(DG[0].normal_(0.0, 1e-3, generator=gen))
+    HW = [torch.empty(n // world, dtype=dt, pin_memory=True) for n in sizes]
+    for h in HW:
+        h.copy_(DW[0][:h.numel()].uniform_(-0.08, 0.08, generator=gen))
+    eng = CudaEngine(dev, nb, None, None, "f32", grad_div=float(world))
+    eng.configure(lr=0.05, flags=_lib.USE_SCALE)
+    h2d, comp, d2h = torch.cuda.Stream(), torch.cuda.current_stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(NS)]
+    ev_done = [torch.cuda.Event() for _ in range(NS)]
+    ev_out = [torch.cuda.Event() for _ in range(NS)]
+    order = list(range(nb - 1, -1, -1))
+    async_ok = dist.get_backend() == "nccl"
+
+    def one_pass():
+        for k, b in enumerate(order):
+            s, n, S = k % NS, sizes[b], sizes[b] // world
+            with torch.cuda.stream(h2d):
+                h2d.wait_event(ev_out[s])
+                DG[s][:n].copy_(HG[k % NS][:n], non_blocking=True)
+                DW[s][:S].copy_(HW[b], non_blocking=True)
+                ev_in[s].record(h2d)
+            comp.wait_event(ev_in[s])
+            work = reduce_scatter(DS[s][:S], DG[s][:n], None, async_op=async_ok)
+            if work is not None:
+                work.wait()
+            eng.update(DW[s][:S], DS[s][:S])
+            ev_done[s].record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev_done[s])
+                HW[b].copy_(DW[s][:S], non_blocking=True)
+                ev_out[s].record(d2h)
+        comp.wait_stream(d2h)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        one_pass()
+    _barrier(world)
+    steps = max(1, min(args.steps, 5))
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(steps):
+        one_pass()
+    s1.record()
+    _barrier(world)
+    ms = _max_over_ranks(s0.elapsed_time(s1), world) / steps
+    esz = 2
+    return {"value": round(BYTES_PER_ELEM * P / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": esz * (sum(sizes) + sum(sizes) // world),
+            "d2h_bytes_per_step": esz * sum(sizes) // world,
+            "ms_per_step": round(ms, 2), "steps": steps,
+            "path": "pinned host gradient bucket + parameter shard -> HBM -> NCCL "
+                    "reduce_scatter -> K1 (C-ABI lomo_fused_update) -> host shard"}
+
+
 def _lib_state_mib(nslots: int) -> float:
     from paper_2306_09782_b200 import _lib
     return _lib.state_bytes(nslots) / 2 ** 20
@@ -512,56 +747,61 @@ _GRAPHED = ("replay_fused_gemm_graph", "strict_fused_gemm_graph", "single_pass_f
             "grouped_fused_gemm_graph", "strict_graph", "replay_graph")
 
 
+_TWO_PASS = ("strict", "strict_graph", "strict_fused_gemm", "strict_fused_gemm_graph", "replay",
+             "replay_graph", "replay_fused_gemm", "replay_fused_gemm_graph")
+TRAIN_HEADLINE = "replay_fused_gemm_graph"
+TRAIN_DEFAULT = ("strict", "strict_fused_gemm_graph", TRAIN_HEADLINE, "grouped_fused_gemm_graph",
+                 "single_pass_fused_gemm_graph")
+
+
 def bench_train(args, rank, world):
     """Config 3: LLaMA-7B fp16 LOMO, dynamic loss scale + two-pass clip.
 
-    Timed several ways on the same model (successive runs continue training it):
-    ``strict`` -- the reference protocol, pass 2 is a second backward over the
-    retained graph, each hook launches on the autograd stream, one gradient
-    alive; ``strict_fused_gemm`` -- the same protocol with each linear's probe
-    (K6, pass 1) and update (K5, pass 2) fused into its weight-gradient GEMM
-    inside the backward: no gradient materialised and no stash;
-    ``replay`` -- pass 2 recomputes each weight gradient from the
-    (input, output-gradient) pairs stashed in pass 1 (replay.py) and feeds K1
-    without a second backward; ``replay_fused_gemm`` -- replay with K6 in
-    pass 1 and K5 in pass 2; ``replay_fused_gemm_graph``
-    -- the same step captured into two CUDA graphs around the host decision
-    (graphs.py); ``grouped`` -- the paper's
-    single-pass alternative (per-layer norm clip, GroupedLOMO), reported beside
-    the headline, which is the best two-pass variant (config 3's protocol).  (A side-stream overlap of
-    the hook kernels was measured slower -- 8.6k vs 9.1k tok/s -- and is not
-    timed here; LOMO(overlap=True) keeps it available.)"""
+    Every variant trains a FRESH model (same seed, same batches), so the
+    losses and outcomes of the variants are comparable.  The headline is the
+    fixed variant ``replay_fused_gemm_graph`` timed over ``--train-steps-
+    headline`` steps (default 30); ``strict`` -- the reference protocol as is
+    (pass 2 = a second backward over the retained graph, hook kernels K2/K1,
+    one gradient alive) -- is reported beside it, as are the other variants
+    (``--train-variants`` selects; each ``--train-steps`` steps):
+    ``strict_fused_gemm[_graph]`` -- the same protocol with each linear's probe
+    (K6, pass 1) and update (K5, pass 2) inside its weight-gradient GEMM;
+    ``replay*`` -- pass 2 recomputes each weight gradient from the (input,
+    output-gradient) pairs stashed in pass 1 (replay.py) instead of a second
+    backward; ``*_graph`` -- the step captured as two CUDA graphs around the
+    one host decision (graphs.py); ``grouped*`` -- the paper's single-pass
+    per-layer clip (GroupedLOMO); ``single_pass*`` -- LOMO's single fused
+    pass, no clip and no scaler.  Afterwards the paper's Table-1 LOMO row is
+    MEASURED on a fresh model (``table1``)."""
     import torch
     from paper_2306_09782_b200 import LOMO, GroupedLOMO, LossScaler
     from paper_2306_09782_b200.workloads import Llama
-    torch.cuda.reset_peak_memory_stats()
     size = args.train_model
     ckpt = args.ckpt or size == "65b"
-    model = Llama(size, dtype=torch.float16, device="cuda", checkpointing=ckpt,
-                  fused_proj=not args.separate_proj)
-    model.train()
-    params_bytes = sum(p.numel() * p.element_size() for p in model.parameters())
-    largest = max(p.numel() * p.element_size() for p in model.parameters())
     seq, batch = args.seq, args.batch
+
+    def build():
+        torch.cuda.empty_cache()
+        m = Llama(size, dtype=torch.float16, device="cuda", checkpointing=ckpt,
+                  fused_proj=not args.separate_proj, seed=0)
+        m.train()
+        return m
+
     gen = torch.Generator(device="cuda").manual_seed(0)
     data = [torch.randint(0, 32000, (batch, seq + 1), device="cuda", generator=gen)
             for _ in range(4)]
-    out = {"model": f"llama-{size} (random init N(0,0.02)), fp16 params, no master copy",
+    out = {"model": f"llama-{size} (random init N(0,0.02), a fresh model per variant), fp16 "
+                    "params, no master copy",
            "projections": "separate q/k/v, gate/up" if args.separate_proj else
            "stacked qkv [3h,h] and gate_up [2f,h] weights (same parameters and math)",
-           "seq_len": seq, "batch": batch, "steps": args.train_steps, "passes_per_step": 2,
-           "clip_grad_norm": 1.0, "activation_checkpointing": bool(ckpt),
-           "paper_tgs_rtx3090": 769.92}
-    gstep = None
-    variants = ("strict", "strict_graph", "strict_fused_gemm", "strict_fused_gemm_graph", "replay",
-                "replay_graph",
-                "replay_fused_gemm",
-                "replay_fused_gemm_graph", "grouped", "grouped_fused_gemm",
-                "grouped_fused_gemm_graph", "single_pass_fused_gemm",
-                "single_pass_fused_gemm_graph") \
-        if not args.train_variants else \
-        tuple(args.train_variants.split(","))
+           "seq_len": seq, "batch": batch, "passes_per_step": 2,
+           "clip_grad_norm": 1.0, "loss_scale": "dynamic, 2^10, growth 16",
+           "activation_checkpointing": bool(ckpt), "paper_tgs_rtx3090": 769.92,
+           "headline_variant": TRAIN_HEADLINE}
+    variants = tuple(args.train_variants.split(",")) if args.train_variants else TRAIN_DEFAULT
     for key in variants:
+        model = build()
+        gstep = None
         if key in _GRAPHED:
             from paper_2306_09782_b200.graphs import GraphedGroupedStep, GraphedLOMOStep
             if key.startswith("grouped"):
@@ -574,37 +814,30 @@ def bench_train(args, rank, world):
                            replay=key.startswith("replay"), fuse_gemm="fused_gemm" in key)
             static = data[0].clone()
             G = GraphedGroupedStep if key.startswith("grouped") else GraphedLOMOStep
-            gstep = G(opt, lambda d: model.loss(d[:, :-1], d[:, 1:]), (static,),
+            gstep = G(opt, lambda d, m=model: m.loss(d[:, :-1], d[:, 1:]), (static,),
                       warmup=max(2, args.train_warmup), lr=1e-3)
 
-            def step(k):
+            def step(k, gstep=gstep, static=static):
                 static.copy_(data[k % len(data)])
                 # the loss stays on the device until the timed loop ends: the
-                # graphed step's one host sync is its status read, and the next
-                # step's graphs are queued while this one's pass 2 runs
+                # graphed step's one host sync is its status read
                 return gstep.step(1e-3).detach().clone()
-        elif key == "single_pass_fused_gemm":
-            # LOMO's own single fused pass (no clip, no scaler: optim.py:118-132)
-            # with every linear's update inside its weight-gradient GEMM (K5 in
-            # the backward); reported beside the headline, not config 3's protocol
-            opt = LOMO(model, lr=1e-3, fuse_gemm=True)
-        elif key in ("grouped", "grouped_fused_gemm"):
-            # the paper's single-pass alternative (stabilize.py:234-274): clip
-            # each decoder layer by its own norm, no loss scaler, one backward
-            # (_fused_gemm: each linear's group probe inside its GEMM, K6)
-            opt = GroupedLOMO(model, lr=1e-3, max_norm=1.0, window=1,
-                              fuse_gemm=key == "grouped_fused_gemm")
         else:
-            opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
-                       loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
-                       replay=key.startswith("replay"),
-                       fuse_gemm=key in ("replay_fused_gemm", "strict_fused_gemm"))
+            if key == "single_pass_fused_gemm":
+                opt = LOMO(model, lr=1e-3, fuse_gemm=True)
+            elif key in ("grouped", "grouped_fused_gemm"):
+                opt = GroupedLOMO(model, lr=1e-3, max_norm=1.0, window=1,
+                                  fuse_gemm=key == "grouped_fused_gemm")
+            else:
+                opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
+                           loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
+                           replay=key.startswith("replay"),
+                           fuse_gemm=key in ("replay_fused_gemm", "strict_fused_gemm"))
 
-        if key not in _GRAPHED:
-            def step(k, opt=opt):
+            def step(k, opt=opt, model=model):
                 d = data[k % len(data)]
                 return opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
-
+        nsteps = args.train_steps_headline if key == TRAIN_HEADLINE else args.train_steps
         for k in range(args.train_warmup):
             step(k)
         torch.cuda.synchronize()
@@ -613,14 +846,15 @@ def bench_train(args, rank, world):
         losses, outcomes = [], []
         with ClockSampler(torch.cuda.current_device()) as clk:
             start.record()
-            for k in range(args.train_steps):
-                losses.append(step(k))
+            for k in range(nsteps):
+                losses.append(step(args.train_warmup + k))
                 outcomes.append(opt.last_outcome.value if opt.last_outcome else "applied")
             end.record()
             torch.cuda.synchronize()
-        ms = start.elapsed_time(end) / args.train_steps
+        ms = start.elapsed_time(end) / nsteps
         losses = [float(x) for x in losses]
         out[key] = {"tokens_per_s": round(batch * seq / (ms * 1e-3), 1), "ms_per_step": round(ms, 2),
+                    "steps": nsteps, "warmup": args.train_warmup,
                     "peak_mem_gib": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
                     "loss_scale_final": getattr(opt, "loss_scale", None), "outcomes": outcomes,
                     "losses": [round(x, 4) for x in losses], "clocks": clk.summary()}
@@ -628,28 +862,27 @@ def bench_train(args, rank, world):
         if pw:
             out[key]["tokens_per_joule"] = round(out[key]["tokens_per_s"] / pw, 2)
         opt.remove_hooks()
-        del opt
-        step = gstep = None  # noqa: F841  (release the graphs' memory pool)
+        del opt, step, gstep, model
         torch.cuda.empty_cache()
-    two_pass = [k for k in variants
-                if k not in ("grouped", "grouped_fused_gemm", "grouped_fused_gemm_graph",
-                             "single_pass_fused_gemm", "single_pass_fused_gemm_graph")]
-    # the headline: config 3's two-pass protocol
-    best = max(two_pass or variants, key=lambda k: out[k]["tokens_per_s"])
-    out["tokens_per_s"] = out[best]["tokens_per_s"]
-    out["ms_per_step"] = out[best]["ms_per_step"]
-    out["headline_variant"] = best
+    hv_key = TRAIN_HEADLINE if TRAIN_HEADLINE in out else next(
+        (k for k in variants if k in _TWO_PASS), variants[0])
+    out["headline_variant"] = hv_key
+    out["tokens_per_s"] = out[hv_key]["tokens_per_s"]
+    out["ms_per_step"] = out[hv_key]["ms_per_step"]
+    if "strict" in out:
+        out["strict_tokens_per_s"] = out["strict"]["tokens_per_s"]
     # tensor work of the headline step (two-pass replay protocol): forward,
     # input-gradient, pass-1 weight-gradient (K6) and pass-2 weight-gradient
     # (K5) GEMMs over every linear, plus causal attention (fwd + ~2.5x bwd);
     # against the bf16 peak scaled to the median SM clock the leg ran at
+    from paper_2306_09782_b200.workloads import LLAMA, llama_param_shapes
+    cfg = LLAMA[size]
     tokens = batch * seq
-    lin = sum(p.numel() for n, p in model.named_parameters() if p.dim() == 2
+    lin = sum(math.prod(s) for n, s in llama_param_shapes(size) if len(s) == 2
               and "embed" not in n)
-    cfg = model.cfg
     attn = 3.5 * 2 * 2 * tokens * seq * 0.5 * cfg["hidden"] * cfg["layers"]
     tflop = (4 * 2 * tokens * lin + attn) / 1e12
-    hv = out[best]
+    hv = out[hv_key]
     pflops = tflop / (hv["ms_per_step"] * 1e-3) / 1e3
     peak_tf, peak_src = _bf16_peak_tflops()
     peak_pf = peak_tf / 1e3
@@ -660,101 +893,93 @@ def bench_train(args, rank, world):
         "tflop_per_step": round(tflop, 2), "achieved_pflops": round(pflops, 3),
         "peak_pflops": round(peak_pf, 3), "peak_source": peak_src,
         "frac": round(pflops / peak_pf, 3),
-        # an isolated-kernel peak scaled to the clock the power cap left
         "frac_at_run_clock": (round(pflops / (peak_pf * scale), 3)
                               if scale and not sustained else None)}
-    out["memory_gib"] = {
-        "params": round(params_bytes / 2 ** 30, 2), "largest_gradient": round(largest / 2 ** 30, 3),
-        "optimizer_state": 0.0,
-        "lomo_state_block_mib": round(_lib_state_mib(len(list(model.parameters()))), 1),
-        "peak_allocated": out[variants[0]]["peak_mem_gib"],
-        "paper_table1_lomo_row": {"params": 12.55, "gradients": 0.24, "optimizer_states": 0.0}}
-    if args.table1_setting and "replay_fused_gemm_graph" in variants:
-        # the paper's Table 1 shape (seq 512 x batch 8 = 4096 tokens per step):
-        # the same graphed two-pass step; the per-step update work (K5/K6/K1
-        # over 6.7 G parameters) is amortised over 4x the tokens
-        from paper_2306_09782_b200.graphs import GraphedLOMOStep
-        s1, b1 = 512, 8
-        d1 = [torch.randint(0, 32000, (b1, s1 + 1), device="cuda", generator=gen)
-              for _ in range(4)]
-        opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0,
-                   loss_scale=LossScaler(2.0 ** 10, growth_interval=16), replay=True,
-                   fuse_gemm=True)
-        static = d1[0].clone()
-        gstep = GraphedLOMOStep(opt, lambda d: model.loss(d[:, :-1], d[:, 1:]), (static,),
-                                warmup=max(2, args.train_warmup), lr=1e-3)
-        torch.cuda.synchronize()
-        torch.cuda.reset_peak_memory_stats()
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        outcomes = []
-        with ClockSampler(torch.cuda.current_device()) as clk:
-            start.record()
-            for k in range(args.train_steps):
-                static.copy_(d1[k % len(d1)])
-                gstep.step(1e-3)
-                outcomes.append(opt.last_outcome.value)
-            end.record()
-            torch.cuda.synchronize()
-        ms = start.elapsed_time(end) / args.train_steps
-        out["table1_setting_graph"] = {
-            "seq_len": s1, "batch": b1, "tokens_per_s": round(b1 * s1 / (ms * 1e-3), 1),
-            "ms_per_step": round(ms, 2),
-            "peak_mem_gib": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
-            "outcomes": outcomes, "clocks": clk.summary()}
-        opt.remove_hooks()
-        del opt, gstep
-        torch.cuda.empty_cache()
-    del model
+    if size == "7b" and not args.no_table1:
+        out["table1"] = measure_table1(args, build)
     torch.cuda.empty_cache()
     return out
 
 
-def bench_memory_table(args):
-    """the paper's Table 1 setting (LLaMA-7B, seq 512 x batch 8,
-    fp16, LOMO) with and without per-layer activation checkpointing, measured
-    from torch.cuda memory stats next to the reference estimator's analytic
-    row (estimate.py:200-218; PAPER.md:193-196)."""
+def measure_table1(args, build):
+    """the paper's Table 1 LOMO row (LLaMA-7B, fp16, seq 512 x
+    batch 8), MEASURED on the plain LOMO hook path, beside
+    the reference estimator's row (fusedtrain/estimate.py:200-218, imported
+    from baseline/_ref) for the same setting, with and without per-layer
+    activation checkpointing.
+
+      params      torch.cuda.memory_allocated() delta of building the model
+      gradients   the largest total of live .grad tensors over every hook
+                  call of a step (an instrumentation hook runs before LOMO's
+                  and sums the gradients alive at that moment), and the most
+                  gradient tensors ever alive at once
+      optimizer   LOMO's per-parameter state (none) and its one state block
+      step peak   max_memory_allocated() of one step minus what was
+                  allocated before the model existed"""
     import torch
     from paper_2306_09782_b200 import LOMO, LossScaler
-    from paper_2306_09782_b200.workloads import Llama
+    seq, batch = 512, 8
+    ref, where = _import_reference()
+    gib = 2 ** 30
     rows = {}
-    import gc
-    gc.collect()
-    torch.cuda.empty_cache()
-    # whatever earlier legs of this process still hold (graph pools) is not
-    # this table's memory: every figure below is relative to it
-    pre = torch.cuda.memory_allocated()
-    for ac in (False, True):
+    for ac in (True, False):
+        import gc
+        gc.collect()
         torch.cuda.empty_cache()
-        model = Llama("7b", dtype=torch.float16, device="cuda", checkpointing=ac)
-        model.train()
+        before = torch.cuda.memory_allocated()
+        model = build()
+        params_b = torch.cuda.memory_allocated() - before
+        model.checkpointing = ac
+        plist = list(model.parameters())
+        live = {"bytes": 0, "count": 0, "largest": 0}
+
+        def watch(p, plist=plist, live=live):
+            b = c = 0
+            for q in plist:
+                if q.grad is not None:
+                    b += q.grad.numel() * q.grad.element_size()
+                    c += 1
+            live["bytes"] = max(live["bytes"], b)
+            live["count"] = max(live["count"], c)
+            live["largest"] = max(live["largest"], p.grad.numel() * p.grad.element_size())
+        hs = [p.register_post_accumulate_grad_hook(watch) for p in plist]  # before LOMO's
         opt = LOMO(model, lr=1e-3, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 10))
-        d = torch.randint(0, 32000, (8, 513), device="cuda")
-        step = lambda: opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
-        step()
+        d = torch.randint(0, 32000, (batch, seq + 1), device="cuda",
+                          generator=torch.Generator(device="cuda").manual_seed(5))
+        opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)  # warm (allocator, kernels)
         torch.cuda.synchronize()
-        base = torch.cuda.memory_allocated()
         torch.cuda.reset_peak_memory_stats()
-        step()
+        live.update(bytes=0, count=0, largest=0)
+        opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)
         torch.cuda.synchronize()
-        peak = torch.cuda.max_memory_allocated()
-        params = sum(p.numel() * p.element_size() for p in model.parameters())
-        gib = 2 ** 30
-        rows["ac" if ac else "no_ac"] = {
-            "params_gib": round(params / gib, 2),
-            "step_peak_gib": round((peak - pre) / gib, 2),
-            "peak_above_resident_gib": round((peak - base) / gib, 2),
-            "largest_gradient_gib": round(max(p.numel() * p.element_size()
-                                              for p in model.parameters()) / gib, 3),
-            "optimizer_state_gib": 0.0}
+        peak = torch.cuda.max_memory_allocated() - before
+        row = {"params_gib": round(params_b / gib, 3),
+               "gradients_live_max_gib": round(live["bytes"] / gib, 3),
+               "gradient_tensors_live_max": live["count"],
+               "largest_gradient_gib": round(live["largest"] / gib, 3),
+               "optimizer_state_per_param_bytes": 0,
+               "optimizer_state_block_gib": round(opt.engine.state.numel() / gib, 4),
+               "step_peak_gib": round(peak / gib, 2),
+               "outcome": opt.last_outcome.value if opt.last_outcome else None}
         opt.remove_hooks()
-        del opt, model
-    rows["reference_estimator_lomo_gib"] = {
-        "no_ac": {"params": 12.55, "gradients": 0.24, "optimizer": 0.0, "activations": 45.61,
-                  "total": 59.40},
-        "ac": {"params": 12.55, "gradients": 0.24, "optimizer": 0.0, "activations": 1.79,
-               "total": 14.58},
-        "note": "the estimator counts stored attention scores; SDPA flash attention keeps none"}
+        for h in hs:
+            h.remove()
+        del opt, model, plist
+        if ref is not None:
+            E = ref["estimate"]
+            est = E.estimate(E.PRESETS["llama-7b"], E.TrainSetup(
+                ref["optim"].OptimizerKind.LOMO, E.EstimatePrecision.MIXED16, ac, seq, batch))
+            row["reference_estimator_gib"] = {
+                "params": round(est.params_gib, 2), "gradients": round(est.gradients_gib, 2),
+                "optim_states": round(est.optim_states_gib, 2),
+                "activations": round(est.activations_gib, 2), "total": round(est.total_gib, 2),
+                "source": f"fusedtrain.estimate.estimate ({where}), estimate.py:200-218"}
+        rows["ac" if ac else "no_ac"] = row
+    rows["paper_table1_lomo"] = {"params": 12.55, "gradients": 0.24, "optimizer_states": 0.0,
+                                 "total_ac": 14.58, "source": "PAPER.md:193-196"}
+    rows["setting"] = f"LLaMA-7B fp16, seq {seq} x batch {batch}, LOMO two-pass (clip 1.0, scale 2^10)"
+    rows["note"] = ("activations: SDPA flash attention keeps no score matrix; the estimator "
+                    "charges 4 width-equivalents per score element")
     torch.cuda.empty_cache()
     return rows
 
@@ -870,6 +1095,143 @@ def _sharded_world1(args):
         dist.destroy_process_group()
 
 
+def _ulps16(got, ref):
+    import numpy as np
+    g = got.astype(np.float16).view(np.int16).astype(np.int64)
+    r = ref.astype(np.float16).view(np.int16).astype(np.int64)
+    g = np.where(g < 0, -(1 << 15) - g, g)
+    r = np.where(r < 0, -(1 << 15) - r, r)
+    return np.abs(g - r)
+
+
+def bench_c1(args):
+    """Config 1 parity leg: the reference's own mini
+    transformer (zoo.py:150-224), 10 LOMO steps, against the fixtures
+    recorded from the reference itself (tests/golden/c1.*, made by
+    tests/golden/make_golden.py): A = FULL, plain LOMO; B = HALF, two-pass
+    global-norm clip 1.0 + LossScaler(2^16, growth 2); C = as B from 2^24 with
+    max 2^24 (forced fp16 overflows).  Each fixture runs through the product
+    path -- LOMO's hooks -> K2/K3/K1 (``hooks``), and for B/C also the
+    training path with K6/K5 inside the weight-gradient GEMMs
+    (``fused_gemm``) -- plus, for B/C, the exactness mode: the restated tape
+    (tests/exact_c1.py, f64 ops with the reference's binary16 rounding)
+    driving the product kernels in f64 math (``exact_tape``).  Reported:
+    decision (outcome, log2 scale) equality, max / mean ulp (fp16) or
+    normwise relative error (fp32) of the sampled final parameters, loss
+    error, and the GPU run's wall seconds beside the reference's recorded
+    CPU seconds for the same 10 steps."""
+    import numpy as np
+    import torch
+    from paper_2306_09782_b200 import LOMO, ClipMode, LossScaler, Stabilizer
+    from paper_2306_09782_b200.workloads import (MiniConfig, MiniTransformer,
+                                                 mean_cross_entropy, sequence_copy_batch)
+    meta = json.loads((ROOT / "tests" / "golden" / "c1.json").read_text())
+    arr = np.load(ROOT / "tests" / "golden" / "c1.npz")
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    prev_rr = torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+    cfg = MiniConfig(layers=2, hidden=256, heads=4, vocab=1024, seed=0)
+    toks = [torch.from_numpy(sequence_copy_batch(0, s, 4, 128, 1024)).cuda() for s in range(10)]
+
+    def stab(key):
+        if key == "A":
+            return None
+        s0 = 2.0 ** 16 if key == "B" else 2.0 ** 24
+        return Stabilizer(ClipMode.by_global_norm(1.0), LossScaler(s0, 2, max_scale=2.0 ** 24))
+
+    def compare(key, named, losses, outcomes, scales, secs):
+        ref = meta[key]
+        r = {"gpu_seconds": round(secs, 3), "reference_cpu_seconds": round(ref["seconds"], 2),
+             "outcomes_equal": outcomes == ref["outcomes"]}
+        if ref["log2_scale"]:
+            r["log2_scale_equal"] = [math.log2(s) for s in scales] == ref["log2_scale"]
+        r["max_loss_rel"] = float(max(abs(a - b) / abs(b) for a, b in zip(losses, ref["losses"])
+                                      if math.isfinite(b)))
+        got = {n: t.detach().reshape(-1) for n, t in named}
+        if ref["precision"] == "full":
+            r["max_normwise_rel"] = float(max(
+                np.linalg.norm(got[n][torch.from_numpy(arr[f"{key}/{n}/idx"]).cuda()]
+                               .double().cpu().numpy() - arr[f"{key}/{n}/val"])
+                / np.linalg.norm(arr[f"{key}/{n}/val"]) for n in got))
+        else:
+            u = np.concatenate([_ulps16(got[n][torch.from_numpy(arr[f"{key}/{n}/idx"]).cuda()]
+                                        .double().cpu().numpy(), arr[f"{key}/{n}/val"])
+                                for n in got])
+            r.update(max_ulp=int(u.max()), mean_ulp=round(float(u.mean()), 5),
+                     frac_gt_2ulp=float((u > 2).mean()), sampled=int(u.size))
+        return r
+
+    def run(key, dtype, fused):
+        model = MiniTransformer(cfg, dtype=dtype, device="cuda", fused_linear=fused)
+        kw = {"stabilizer": stab(key)}
+        if fused:
+            kw.update(replay=True, fuse_gemm=True)
+        opt = LOMO(model, lr=0.05, **kw)
+        losses, outcomes, scales = [], [], []
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in range(10):
+            ids = toks[s]
+            losses.append(opt.step(lambda: mean_cross_entropy(model(ids), ids), 0.05))
+            outcomes.append(opt.last_outcome.value if opt.last_outcome else "applied")
+            scales.append(opt.loss_scale)
+        torch.cuda.synchronize()
+        secs = time.perf_counter() - t0
+        res = compare(key, model.named_reference_parameters(), losses, outcomes, scales, secs)
+        opt.remove_hooks()
+        return res
+
+    out = {"A": {"hooks": run("A", torch.float32, False)}}
+    for key in ("B", "C"):
+        out[key] = {"hooks": run(key, torch.float16, False),
+                    "fused_gemm": run(key, torch.float16, True)}
+    # the exactness mode: restated tape (test infrastructure) + product kernels, f64 math
+    sys.path.insert(0, str(ROOT / "tests"))
+    import gpu_util as U
+    from exact_c1 import ExactMini
+    from paper_2306_09782_b200 import _lib
+    for key in ("B", "C"):
+        m = ExactMini(MiniConfig())
+        slot = {n: i for i, n in enumerate(reversed(m.names))}
+        st = U.State(len(m.names), scale=2.0 ** 16 if key == "B" else 2.0 ** 24, growth=2,
+                     min_scale=1.0, max_scale=2.0 ** 24, max_norm=1.0)
+        losses, outcomes, scales = [], [], []
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in range(10):
+            scale = st.status().scale
+            logits, S = m.forward(toks[s])
+            loss, dout = m.loss_and_grad(logits, toks[s])
+            st.begin(torch.tensor(loss, dtype=torch.float64, device="cuda"))
+            m.backward(S, dout * scale, lambda n, g: st.probe(
+                g.to(torch.float16), slot[n], _lib.USE_SCALE | _lib.ACCUM_F64))
+            st.finalize()
+            if st.status().skip:
+                outcomes.append("skipped_overflow")
+            else:
+                logits2, S2 = m.forward(toks[s])
+                loss, dout2 = m.loss_and_grad(logits2, toks[s])
+                m.backward(S2, dout2 * scale, lambda n, g: U.fused_update(
+                    m.p16[n], g.to(torch.float16), math="f64", lr=0.05,
+                    flags=_lib.USE_SKIP | _lib.USE_SCALE | _lib.USE_COEF, state=st))
+                st.on_clean()
+                outcomes.append("applied")
+            losses.append(loss)
+            scales.append(st.status().scale)
+        torch.cuda.synchronize()
+        out[key]["exact_tape"] = compare(key, [(n, m.p16[n]) for n in m.names], losses, outcomes,
+                                         scales, time.perf_counter() - t0)
+    torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = prev_rr
+    ok = all(v.get("outcomes_equal") and v.get("log2_scale_equal", True)
+             for fx in out.values() for v in fx.values())
+    out["decisions_identical"] = bool(ok)
+    out["tolerances"] = {"A": "normwise rel <= 1e-5 (north star fp32)",
+                         "B/C": "decisions identical; max/mean ulp reported (2-ulp contract "
+                                "is the hook-level one, SURVEY 8c; exact_tape = 0 expected)"}
+    return out
+
+
 def _import_reference():
     """The reference package itself: baseline/_ref (pip-installed from
     /root/reference, travels to the GPU box) or the read-only source tree.
@@ -983,24 +1345,24 @@ def main():
     ap.add_argument("--dtype", choices=["bf16", "fp16"], default="bf16")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c1", action="store_true", help="skip the config-1 parity leg")
+    ap.add_argument("--no-table1", action="store_true", help="skip the measured Table-1 row")
     ap.add_argument("--e2e-slots", type=int, default=4, help="device staging slots of the e2e pipeline")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--train-steps", type=int, default=5)
+    ap.add_argument("--train-steps", type=int, default=10)
+    ap.add_argument("--train-steps-headline", type=int, default=30)
     ap.add_argument("--train-warmup", type=int, default=3)
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--ckpt", action="store_true", help="per-layer activation checkpointing")
-    ap.add_argument("--no-table1-setting", dest="table1_setting", action="store_false",
-                    help="skip the extra seq 512 x batch 8 graphed train line")
     ap.add_argument("--separate-proj", action="store_true",
                     help="train leg: q/k/v and gate/up as separate weights (default: stacked)")
-    ap.add_argument("--memory-table", action="store_true",
-                    help="also measure the Table-1 setting (seq 512 x batch 8, AC off/on)")
     ap.add_argument("--train-model", default="7b", choices=["7b", "13b", "30b", "65b"],
                     help="model of the single-GPU train leg (config 3: 7b)")
     ap.add_argument("--train-variants", default="",
-                    help="comma list of strict,replay,replay_fused_gemm,replay_fused_gemm_graph,grouped "
-             "(default: all)")
+                    help="comma list (default: " + ",".join(TRAIN_DEFAULT) + "); also strict_graph, "
+                         "strict_fused_gemm, replay, replay_graph, replay_fused_gemm, grouped, "
+                         "grouped_fused_gemm, single_pass_fused_gemm")
     ap.add_argument("--sharded-train", action="store_true",
                     help="run the ZeRO-3 sharded train leg even at N=1 (world-1 NCCL group)")
     ap.add_argument("--no-sharded-world1", dest="sharded_world1", action="store_false",
@@ -1009,6 +1371,11 @@ def main():
                     help="sharded train leg: pass 2 as a second forward+backward (default: replay)")
     ap.add_argument("--sharded-model", default="13b", choices=["tiny", "7b", "13b", "30b", "65b"],
                     help="model of the N>1 sharded train leg (config 4: 13b, config 5: 65b)")
+    ap.add_argument("--update-layers", type=int, default=32,
+                    help="N>1 sharded update: decoder-layer buckets (32 = LLaMA-7B; fewer only "
+                         "for LOMO_BENCH_SHARE_GPU dry runs)")
+    ap.add_argument("--k4-transport", default="", choices=["", "ipc", "nvls"],
+                    help="N>1: force the K4 peer transport (default: NVLS when available)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -1033,6 +1400,10 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    if world > 1:
+        # NCCL's init lines (ranks, NVLink/NVLS transport) in the job log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import torch
     rank, world, local = _dist_init(args.gpus)
     if args.sharded_train and world == 1:
@@ -1044,8 +1415,6 @@ def main():
     import __graft_entry__
     __graft_entry__.build()
     torch.backends.cuda.matmul.allow_tf32 = False
-
-    up = bench_update(args, rank, world)
     peak, peak_src = _peaks()
     tr = _traffic()
 
@@ -1059,37 +1428,19 @@ def main():
             torch.cuda.empty_cache()
             return {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
-    e2e = None if args.no_e2e else optional(bench_e2e, args, rank, world)
-    train = None
-    if not args.no_train:
-        train = optional(bench_train, args, rank, world) if (world == 1 and not
-                                                              args.sharded_train) else \
-            optional(bench_train_sharded, args, rank, world)
-    sharded1 = None
-    if world == 1 and not args.no_train and not args.sharded_train and args.sharded_world1:
-        # config 4's data path (ZeRO-3 buckets, NCCL reduce-scatter -> K2/K1 per
-        # shard) on this one GPU: a world-1 NCCL group, where the collectives are
-        # local copies -- the sharded machinery's own cost, next to plain LOMO
-        sharded1 = optional(_sharded_world1, args)
-    mem_table = optional(bench_memory_table, args) if (args.memory_table and world == 1) else None
-    cb = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cb = optional(cpu_baseline)
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(up["gbs"], 1), "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(up["ms"], 4),
-            "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": args.dtype,
-            "data": "synthetic: p~U(-0.08,0.08), g~N(0,1e-3) (torch.Generator seed 1234+rank)",
+    if world == 1:
+        up = bench_update(args, rank, world)
+        value, ms = up["gbs"], up["ms"]
+        head = {
+            "scaling": "weak",
             "config": {
                 "workload": "config 2: one LOMO fused-update pass (K1 per tensor, reverse "
                             "registration = autograd delivery order) over all 291 LLaMA-7B "
-                            "parameter tensors" + (f", on each of {world} ranks (its shards of a "
-                                                   f"{world}x7B model)" if world > 1 else ""),
+                            "parameter tensors",
                 "elements": up["total_elems"], "algorithmic_bytes_per_elem": BYTES_PER_ELEM,
-                "math": "fp32", "lr": 0.05, "parallelism": f"dp{world} (per-rank shards, weak)" if world > 1 else "single",
-                "l2": "no flush: per-step working set 27 GB >> 126 MB L2, each byte touched once per step"},
+                "math": "fp32", "lr": 0.05, "parallelism": "single",
+                "l2": "no flush: per-step working set 27 GB >> 126 MB L2, each byte touched "
+                      "once per step"},
             "roofline": {"bound": "hbm", "achieved": round(up["gbs"], 1), "peak": peak,
                          "unit": "GB/s", "frac": round(up["gbs"] / peak, 4),
                          "traffic": tr["dram_bytes"] if tr else None,
@@ -1109,15 +1460,57 @@ def main():
             "probe_pass": dict(up["probe"], frac=round(up["probe"]["gbs"] / peak, 4)),
             "update_pass_device_state": dict(up["flags_pass"],
                                              frac=round(up["flags_pass"]["gbs"] / peak, 4)),
-            "f64_math_update_pass": dict(up["f64_math"], frac=round(up["f64_math"]["gbs"] / peak, 4)),
-            "gpu_launches": up["launches"],
-            "clocks": up["clocks"],
-            "e2e": e2e,
-            "cpu_baseline": cb,
-            "train": train,
+            "f64_math_update_pass": dict(up["f64_math"],
+                                         frac=round(up["f64_math"]["gbs"] / peak, 4)),
+            "gpu_launches": up["launches"], "clocks": up["clocks"]}
+    else:
+        sh = bench_sharded_update(args, rank, world)
+        value, ms = sh["gbs"], sh["ms"]
+        head = {
+            "scaling": "strong",
+            "config": {
+                "workload": f"sharded LOMO update pass of LLaMA-7B over {world} ranks: "
+                            f"{sh['buckets']} flat "
+                            "gradient buckets per rank (its own backward's), reduced across ranks "
+                            "and applied to each rank's 1/W parameter shard (best of NCCL "
+                            "reduce_scatter -> K1 and K4)",
+                "elements": sh["elements"], "algorithmic_bytes_per_elem": BYTES_PER_ELEM,
+                "math": "fp32", "lr": 0.05, "parallelism": f"zero3-dp{world}",
+                "l2": "no flush: 13.5 GB of gradients per rank per step >> 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": round(sh["k1_gbs"], 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(sh["k1_gbs"] / peak, 4),
+                         "traffic": None, "peak_source": peak_src,
+                         "kernel": "K1 on the reduce-scattered shards (per-launch CUDA events); "
+                                   "the pass itself is NVLink-bound, see sharded_update"},
+            "sharded_update": sh, "gpu_launches": sh["launches"], "clocks": sh["clocks"]}
+
+    e2e = None if args.no_e2e else optional(bench_e2e if world == 1 else bench_e2e_sharded,
+                                            args, rank, world)
+    c1 = optional(bench_c1, args) if (world == 1 and not args.no_c1) else None
+    train = None
+    if not args.no_train:
+        train = optional(bench_train, args, rank, world) if (world == 1 and not
+                                                              args.sharded_train) else \
+            optional(bench_train_sharded, args, rank, world)
+    sharded1 = None
+    if world == 1 and not args.no_train and not args.sharded_train and args.sharded_world1:
+        # config 4's data path (ZeRO-3 buckets, NCCL reduce-scatter -> K2/K1 per
+        # shard) on this one GPU: a world-1 NCCL group, where the collectives are
+        # local copies -- the sharded machinery's own cost, next to plain LOMO
+        sharded1 = optional(_sharded_world1, args)
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cb = optional(cpu_baseline)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": head.pop("scaling"),
+            "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic: p~U(-0.08,0.08), g~N(0,1e-3) (torch.Generator seed 1234+rank)",
         }
-        if mem_table is not None:
-            line["memory_table"] = mem_table
+        line.update(head)
+        line.update({"e2e": e2e, "cpu_baseline": cb, "c1_parity": c1, "train": train})
         if sharded1 is not None:
             line["train_sharded_world1"] = sharded1
         print(json.dumps(line), flush=True)
