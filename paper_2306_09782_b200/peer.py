@@ -70,9 +70,14 @@ class PeerRing:
     NBUF = 3
 
     def __init__(self, numel: int, dtype: torch.dtype, device: torch.device, group,
-                 transport: str = "ipc", err_ptr: int = 0, timeout_s: float = 120.0):
+                 transport: str = "ipc", err_ptr: int = 0, timeout_s: float = 120.0,
+                 nbuf: int | None = None):
         if transport not in ("ipc", "nvls"):
             raise ConfigError(f"peer transport must be 'ipc' or 'nvls', got {transport!r}")
+        if nbuf is not None:
+            if nbuf < 1:
+                raise ConfigError("nbuf must be >= 1")
+            self.NBUF = int(nbuf)
         self.lib = _lib.load()
         self.group = group
         self.world = dist.get_world_size(group)
@@ -183,7 +188,7 @@ class PeerRing:
             self.k = (self.k + 1) % self.NBUF
             if self.owner[k] is None:
                 if self.read_pending[k]:
-                    self.barrier(self.NBUF + k)  # every rank's K4 finished reading k
+                    self.barrier(self._free_ch(k))  # every rank's K4 finished reading k
                     self.read_pending[k] = False
                 self.owner[k] = bucket_idx
                 return k
@@ -207,9 +212,20 @@ class PeerRing:
                                           self.timeout_ns, self.err_ptr, s)
         _lib.check(rc, "peer barrier")
 
+    # Channels name epoch counters: buffer k's "filled" barriers use channel
+    # k mod 8, its "free" barriers 8 + k mod 8.  Buffers may share a channel --
+    # every rank issues the same sequence of barriers, so the epochs agree.
+    _HALF = _lib.PEER_CHANNELS // 2
+
+    def _filled_ch(self, k: int) -> int:
+        return k % self._HALF
+
+    def _free_ch(self, k: int) -> int:
+        return self._HALF + k % self._HALF
+
     def filled(self, k: int) -> None:
         """Every rank has written buffer k (before its K4)."""
-        self.barrier(k)
+        self.barrier(self._filled_ch(k))
 
     # ------------------------------------------------------------------ K4
     def update(self, engine, p_shard: torch.Tensor, k: int, offset: int) -> None:
