@@ -365,14 +365,24 @@ def bench_update(args, rank, world):
     for _ in range(2):
         run_update_pass(dfl, P, G, dt_code, stream)
     torch.cuda.synchronize()
-    start.record()
-    for _ in range(args.steps):
-        run_update_pass(dfl, P, G, dt_code, stream)
-    end.record()
-    torch.cuda.synchronize()
-    fl_ms = start.elapsed_time(end) / args.steps
+
+    def pass_ms(d):
+        start.record()
+        for _ in range(args.steps):
+            run_update_pass(d, P, G, dt_code, stream)
+        end.record()
+        torch.cuda.synchronize()
+        return start.elapsed_time(end) / args.steps
+    # A/B alternation with the flag-free form (same tensors, back to back), so
+    # the comparison does not depend on the order of the bench's legs
+    ab = {"state": [], "plain": []}
+    for _ in range(2):
+        ab["state"].append(pass_ms(dfl))
+        ab["plain"].append(pass_ms(disp))
+    fl_ms = min(ab["state"])
     flags_pass = {"gbs": round(BYTES_PER_ELEM * elems / (fl_ms * 1e-3) / 1e9, 1),
                   "ms_per_pass": round(fl_ms, 4),
+                  "ab_ms": {k: [round(x, 4) for x in v] for k, v in ab.items()},
                   "flags": "USE_SKIP|USE_SCALE|USE_COEF|LR_FROM_STATE (state block read per CTA)"}
     del P, G
     torch.cuda.empty_cache()

@@ -485,13 +485,26 @@ __device__ __forceinline__ double* partials_of(lomo_state* s, int slot) {
 // One CTA's partial of norm slot `slot` (thread 0).  A slot outside
 // [0, nslots) writes nothing and raises the sticky state->error (the host
 // turns it into LOMO_E_SLOT at the step's status read).
-__device__ __forceinline__ void put_partial(lomo_state* st, int slot, double v, int nblocks) {
-  if ((unsigned)slot >= (unsigned)st->nslots) {
+__device__ __forceinline__ void put_partial(lomo_state* st, int slot, double v, int nblocks,
+                                            int nslots) {
+  if ((unsigned)slot >= (unsigned)nslots) {
     st->error = 1;
     return;
   }
-  partials_of(st, slot)[blockIdx.x] = v;
-  if (blockIdx.x == 0) nblocks_of(st)[slot] = nblocks;
+  double* s = slots_of(st);
+  s[nslots + nblocks_words(nslots) + (size_t)slot * LOMO_PROBE_BLOCKS_PER_SLOT + blockIdx.x] = v;
+  if (blockIdx.x == 0) reinterpret_cast<int32_t*>(s + nslots)[slot] = nblocks;
+}
+__device__ __forceinline__ void put_partial(lomo_state* st, int slot, double v, int nblocks) {
+  put_partial(st, slot, v, nblocks, st->nslots);
+}
+// nslots is written once, by lomo_state_init (a launch long before any
+// probe), and never again: a probe may read it BEFORE griddepcontrol.wait,
+// so the tail's partial store does not wait for a header round trip.
+__device__ __forceinline__ int nslots_early(const void* state) {
+  int v;
+  asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(&hdr(const_cast<void*>(state))->nslots));
+  return v;
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -583,10 +596,12 @@ __global__ void __launch_bounds__(kThreads, 5)  // 48 registers: 5 CTAs per SM, 
              int slot, unsigned flags, void* state) {
   constexpr int V = 16 / sizeof(T);
   __shared__ double sm[kThreads / 32];
+  int nslots = 0;
   if (threadIdx.x == 0) {  // this CTA's tile into L2 while the previous grid drains
     const int64_t b0 = (int64_t)blockIdx.x * per_cta;
     const int64_t nt = min(per_cta, nvec - b0);
     if (nt > 0) prefetch_l2(reinterpret_cast<const uint4*>(g + head) + b0, (uint32_t)(nt * 16));
+    nslots = nslots_early(state);  // (the tail's partial store needs it)
   }
   pdl_wait();
   pdl_launch_dependents();
@@ -597,28 +612,29 @@ __global__ void __launch_bounds__(kThreads, 5)  // 48 registers: 5 CTAs per SM, 
   bool bad = false;
   // small fixed tiles (>= 2048 vectors = 32 KB, <= LOMO_PROBE_BLOCKS_PER_SLOT
   // CTAs): the block scheduler balances them across SMs like K1's tiles.
-  // The first tile's loads are issued before the (dependent, L2-latency)
-  // read of inv_scale, as in K1: most CTAs run exactly one tile.
+  //
+  // The squares are summed UNSCALED and the CTA's sum is multiplied by
+  // inv_scale^2 once, at the end: inv_scale is a power of two (the loss
+  // scale; with a data-parallel divisor that is a power of two too), so every
+  // term, every partial sum and the result scale exactly -- the same bits as
+  // summing (g * inv_scale)^2 (stabilize.py:199) -- but no load of the loop
+  // depends on the state.  (Any other divisor: within f64 rounding.)  Reading inv_scale before or inside the loop
+  // measured 6-8 % slower over the LLaMA-7B probe pass
+  // (tools/k1_variants.cu, "k2 clone USE_SCALE ...").
   const int64_t beg = (int64_t)blockIdx.x * per_cta;
   const int64_t end = min(beg + per_cta, nvec);
   const uint4* gv = reinterpret_cast<const uint4*>(g + head);
-  M inv_scale = (M)1;
-  bool have_scale = !use_scale;
-  if (blockIdx.x == 0) {  // scalar head (before the first aligned vector) and tail, first:
-    if (!have_scale) {    // CTA 0 keeps the summation order of the partial it always had
-      inv_scale = (M)st->inv_scale;
-      have_scale = true;
-    }
+  if (blockIdx.x == 0) {  // scalar head (before the first aligned vector) and tail, first
     const int64_t tail0 = head + nvec * V;
     const int64_t ntail = n - tail0;
     for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
       const int64_t e = i < head ? i : tail0 + (i - head);
       M x = to_m<M>(g[e]);
       bad |= !is_fin(x);
-      if (use_scale) x = x * inv_scale;
       acc += (double)x * (double)x;
     }
   }
+  const double acc_ht = acc;
   for (int64_t base = beg + threadIdx.x; base < end; base += (int64_t)kThreads * kUnroll) {
     uint4 G[kUnroll];
 #pragma unroll
@@ -626,31 +642,41 @@ __global__ void __launch_bounds__(kThreads, 5)  // 48 registers: 5 CTAs per SM, 
       const int64_t i = base + (int64_t)u * kThreads;
       if (i < end) G[u] = ld_stream_ro(gv + i);
     }
-    if (!have_scale) {
-      double sc;
-      asm volatile("ld.global.f64 %0, [%1];" : "=d"(sc) : "l"(&st->inv_scale));
-      inv_scale = (M)sc;
-      have_scale = true;
-    }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int64_t i = base + (int64_t)u * kThreads;
-      if (i < end) acc += tile_sumsq<T, M>(G[u], inv_scale, use_scale, bad);
+      if (i < end) acc += tile_sumsq<T, M>(G[u], (M)1, false, bad);
     }
   }
   if constexpr (std::is_same<M, float>::value) {
-    if (!is_fin(acc)) {  // rare: was it a non-finite element or fp32 overflow?
+    if (!is_fin(acc)) {  // rare: a non-finite element, or fp32 overflow of the squares?
       for (int64_t i = beg + threadIdx.x; i < end && !bad; i += kThreads)
         bad = vec_has_nonfinite<T>(ld_stream_ro(gv + i));
+      if (!bad) {  // finite elements whose fp32 squares overflowed: redo them in f64
+        acc = acc_ht;
+        for (int64_t i = beg + threadIdx.x; i < end; i += kThreads) {
+          Vec16<T> G;
+          G.u = ld_stream_ro(gv + i);
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            const double x = (double)to_m<float>(G.e[k]);
+            acc += x * x;
+          }
+        }
+      }
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
 
   // per-CTA partial into this slot's partial row; K3 reduces the row in CTA
   // order (deterministic, no atomics on the hot path)
-  const double bsum = block_sum(acc, sm);
+  double bsum = block_sum(acc, sm);
   if (threadIdx.x == 0) {
-    put_partial(st, slot, bsum, (int)gridDim.x);
+    if (use_scale) {
+      const double sc = st->inv_scale;
+      bsum *= sc * sc;  // exact: a power of two
+    }
+    put_partial(st, slot, bsum, (int)gridDim.x, nslots);
   }
 }
 

@@ -212,6 +212,95 @@ __global__ void __launch_bounds__(256, 5) v_probe_pf(const bf* __restrict__ g, i
   if (threadIdx.x == 0) part[blockIdx.x] = r + (bad ? 1.0 : 0.0);
 }
 
+// ---- K2: the product kernel with one feature switched at a time (MASK bits) --
+// 1: non-finite flag folded into the partial as NaN (no __syncthreads_or)
+// 2: no CTA-0 head/tail branch     4: no inv_scale branch in the loop
+// 8: per-element finiteness test (vec_sumsq) instead of the rescan
+template <int MASK>
+__global__ void __launch_bounds__(256, 5) v_k2(const bf* __restrict__ g, int64_t n, int head,
+                                                int64_t nvec, int64_t per_cta, int slot,
+                                                unsigned flags, void* state) {
+  constexpr int V = 8;
+  __shared__ double sm[8];
+  int nsl = 0;
+  if (threadIdx.x == 0) {
+    const int64_t b0 = (int64_t)blockIdx.x * per_cta;
+    const int64_t nt = min(per_cta, nvec - b0);
+    if (nt > 0) prefetch_l2(reinterpret_cast<const uint4*>(g + head) + b0, (uint32_t)(nt * 16));
+    nsl = nslots_early(state);
+  }
+  pdl_wait();
+  pdl_launch_dependents();
+  lomo_state* st = hdr(state);
+  const bool use_scale = (flags & LOMO_USE_SCALE) != 0;
+  double acc = 0.0;
+  bool bad = false;
+  const int64_t beg = (int64_t)blockIdx.x * per_cta;
+  const int64_t end = min(beg + per_cta, nvec);
+  const uint4* gv = reinterpret_cast<const uint4*>(g + head);
+  float inv_scale = 1.f;
+  bool have_scale = !use_scale || (MASK & 4) || (MASK & 32);
+  if (!(MASK & 2) && blockIdx.x == 0) {
+    if (!have_scale) {
+      inv_scale = (float)st->inv_scale;
+      have_scale = true;
+    }
+    const int64_t tail0 = head + nvec * V;
+    const int64_t ntail = n - tail0;
+    for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
+      const int64_t e = i < head ? i : tail0 + (i - head);
+      float x = to_m<float>(g[e]);
+      bad |= !is_fin(x);
+      if (use_scale) x = x * inv_scale;
+      acc += (double)x * (double)x;
+    }
+  }
+  if ((MASK & 16) && !have_scale) {  // peeled form: the scale read outside the loop
+    double sc;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(sc) : "l"(&st->inv_scale));
+    inv_scale = (float)sc;
+    have_scale = true;
+  }
+  for (int64_t base = beg + threadIdx.x; base < end; base += 256 * 8) {
+    uint4 G[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = base + (int64_t)u * 256;
+      if (i < end) G[u] = ld_stream_ro(gv + i);
+    }
+    if (!(MASK & 16) && !have_scale) {
+      double sc;
+      asm volatile("ld.global.f64 %0, [%1];" : "=d"(sc) : "l"(&st->inv_scale));
+      inv_scale = (float)sc;
+      have_scale = true;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = base + (int64_t)u * 256;
+      if (i < end) {
+        if (MASK & 8) acc += vec_sumsq<bf, float>(G[u], inv_scale, use_scale, bad);
+        else acc += vec_sumsq_nocheck<bf>(G[u], inv_scale, use_scale);
+      }
+    }
+  }
+  if (!(MASK & 8) && !is_fin(acc)) {
+    for (int64_t i = beg + threadIdx.x; i < end && !bad; i += 256)
+      bad = vec_has_nonfinite<bf>(ld_stream_ro(gv + i));
+  }
+  if ((MASK & 32) && use_scale) {  // unscaled sums, scaled once at the end (exact: power of 2)
+    double sc;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(sc) : "l"(&st->inv_scale));
+    acc *= sc * sc;
+  }
+  if (MASK & 1) {
+    if (bad) acc = __longlong_as_double(0x7ff8000000000000ll);
+  } else if (__syncthreads_or(bad) && threadIdx.x == 0) {
+    st->overflow = 1;
+  }
+  const double bsum = block_sum(acc, sm);
+  if (threadIdx.x == 0) put_partial(st, slot, bsum, (int)gridDim.x, nsl);
+}
+
 // ---- variant: TMA bulk copies through a 4-stage shared-memory ring ---------
 constexpr int kTileElems = 8192;  // 16 KB per operand per stage
 constexpr int kStages = 4;
@@ -532,6 +621,49 @@ int main() {
         }, 10);
         printf("%-44s %8.3f ms  %7.1f GB/s\n", name, ms, gbp / (ms * 1e-3));
       };
+      auto pk = [&](auto kern, unsigned fl, const char* name) {
+        float ms = time_passes([&] {
+          for (int i = ns - 1; i >= 0; --i) {
+            const int64_t nvec = ts[i].n / 8;
+            int64_t per = (nvec + LOMO_PROBE_BLOCKS_PER_SLOT - 1) / LOMO_PROBE_BLOCKS_PER_SLOT;
+            per = (per + 2047) / 2048 * 2048;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)((nvec + per - 1) / per));
+            cfg.blockDim = dim3(256);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&cfg, kern, (const bf*)ts[i].g, ts[i].n, 0, nvec, per, ns - 1 - i,
+                                  fl, st));
+          }
+        }, 10);
+        printf("%-44s %8.3f ms  %7.1f GB/s\n", name, ms, gbp / (ms * 1e-3));
+      };
+      for (int rep = 0; rep < 2; ++rep) {
+        pk(v_k2<0>, 0u, "k2 clone (product)");
+        pk(v_k2<1>, 0u, "k2 clone: NaN-folded flag");
+        pk(v_k2<2>, 0u, "k2 clone: no head/tail branch");
+        pk(v_k2<8>, 0u, "k2 clone: per-element check");
+        pk(v_k2<3>, 0u, "k2 clone: NaN + no head/tail");
+        pk(v_k2<0>, (unsigned)LOMO_USE_SCALE, "k2 clone (product) USE_SCALE");
+        pk(v_k2<1>, (unsigned)LOMO_USE_SCALE, "k2 clone NaN-folded USE_SCALE");
+        pk(v_k2<4>, (unsigned)LOMO_USE_SCALE, "k2 clone USE_SCALE, no scale read");
+        pk(v_k2<16>, (unsigned)LOMO_USE_SCALE, "k2 clone USE_SCALE, scale read pre-loop");
+        pk(v_k2<32>, (unsigned)LOMO_USE_SCALE, "k2 clone USE_SCALE, scaled at the end");
+        pk(v_k2<33>, (unsigned)LOMO_USE_SCALE, "k2 clone USE_SCALE, end-scaled + NaN flag");
+        float ms = time_passes([&] {
+          for (int i = ns - 1; i >= 0; --i)
+            lomo_probe(ts[i].g, ts[i].n, LOMO_BF16, ns - 1 - i, LOMO_USE_SCALE, st, nullptr);
+        }, 10);
+        printf("%-44s %8.3f ms  %7.1f GB/s\n", "product (peeled) USE_SCALE", ms, gbp / (ms * 1e-3));
+        ms = time_passes([&] {
+          for (int i = ns - 1; i >= 0; --i)
+            lomo_probe(ts[i].g, ts[i].n, LOMO_BF16, ns - 1 - i, 0u, st, nullptr);
+        }, 10);
+        printf("%-44s %8.3f ms  %7.1f GB/s\n", "product (peeled)", ms, gbp / (ms * 1e-3));
+      }
       p2(v_probe2<0>, "k2-like: state row + syncthreads_or");
       p2(v_probe2<1>, "k2-like: NaN-folded flag");
       p2(v_probe2<2>, "k2-like: NaN flag, no nblocks");
@@ -551,6 +683,27 @@ int main() {
     probe_pass(v_probe<8>, 4096, 1 << 20, "probe 4096 vec/CTA u8");
     probe_pass(v_probe<8>, 8192, 1 << 20, "probe 8192 vec/CTA u8");
     probe_pass(v_probe<16>, 8192, 1 << 20, "probe 8192 vec/CTA u16");
+    // K1-like geometry: tiles of >= nvec/8192 vectors (the partial-row limit),
+    // as small as one vector per thread, own tile prefetched into L2
+    probe_pass(v_probe_pf<1, 0>, 256, 8192, "probe >=256 u1 (<=8192 CTAs) + prefetch");
+    probe_pass(v_probe_pf<2, 0>, 512, 8192, "probe >=512 u2 (<=8192 CTAs) + prefetch");
+    probe_pass(v_probe_pf<4, 0>, 1024, 8192, "probe >=1024 u4 (<=8192 CTAs) + prefetch");
+    // read ceiling: the same kernels over ONE flat 2.4 GB buffer (one launch)
+    {
+      const int64_t nflat = 3 * (int64_t)ts[0].n;  // the largest tensor, x3 (padding)
+      bf* flat;
+      CK(cudaMalloc(&flat, nflat * 2));
+      CK(cudaMemset(flat, 0, nflat * 2));
+      for (int64_t per : {(int64_t)2048, (int64_t)8192}) {
+        const int64_t nvec = nflat / 8;
+        float ms = time_passes([&] {
+          v_probe<8><<<(unsigned)((nvec + per - 1) / per), 256>>>(flat, nvec, per, part);
+        }, 10);
+        printf("flat one launch %5lld vec/CTA u8 (%.2f GB)     %8.3f ms  %7.1f GB/s\n",
+               (long long)per, 2.0 * nflat / 1e9, ms, 2.0 * nflat / 1e9 / (ms * 1e-3));
+      }
+      CK(cudaFree(flat));
+    }
   }
 
   // one flat launch over the biggest tensor only (in-kernel efficiency)
