@@ -265,6 +265,25 @@ def bench_update(args, rank, world):
     total_elems = _sum_over_ranks(elems, world)
     gbs = BYTES_PER_ELEM * total_elems * args.steps / (ms * 1e-3) / 1e9
 
+    # host cost of enqueueing one pass, measured from an empty launch queue (a
+    # sync before each pass: the host never blocks on a full queue), for the
+    # C++ dispatcher the hooks use and for its Python/ctypes form
+    def enqueue_ms(d, reps=7):
+        out = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            run_update_pass(d, P, G, dt_code, stream)
+            out.append((time.perf_counter() - t) * 1e3)
+        torch.cuda.synchronize()
+        return statistics.median(out)
+    pyd = HookDispatcher(lib, None, _lib.MATH_F32, use_cpp=False)
+    pyd.configure(lr=0.05)
+    host_enqueue = {"dispatcher": "C++ (csrc/lomo_dispatch.cpp)" if disp._cpp is not None
+                    else "python/ctypes", "ms_per_pass": round(enqueue_ms(disp), 3),
+                    "python_ctypes_ms_per_pass": round(enqueue_ms(pyd), 3),
+                    "launches_per_pass": len([p for p in P if p.numel() > disp.small]) + 2}
+
     # instrumented replay with per-launch events (same steps) -> kernel roofline
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in P]
     kt = [0.0] * len(P)
@@ -389,7 +408,8 @@ def bench_update(args, rank, world):
     return {"gbs": gbs, "ms": ms / args.steps, "probe": probe, "f64_math": f64,
             "flags_pass": flags_pass,
             "graphed_gbs": BYTES_PER_ELEM * elems / (upd_graph_ms * 1e-3) / 1e9,
-            "host_ms": host_ms, "elems_per_rank": elems, "total_elems": total_elems,
+            "host_ms": host_ms, "host_enqueue": host_enqueue,
+            "elems_per_rank": elems, "total_elems": total_elems,
             "launches": launches, "clocks": clk.summary(), "kernel_gbs": achieved,
             "kernel_ms_per_step": ksum_ms / args.steps, "shapes": shapes}
 
@@ -1462,7 +1482,9 @@ def main():
                                    "on one stream, bracketed by CUDA events; achieved = 6 B/elem x "
                                    "elements / their time",
                          "avg_launch_us": round(1e3 * up["ms"] / (up["launches"] / args.steps), 2),
-                         "host_ms_per_pass": round(up["host_ms"], 3),
+                         "host_ms_per_pass": up["host_enqueue"]["ms_per_pass"],
+                         "host_enqueue": up["host_enqueue"],
+                         "host_ms_timed_loop": round(up["host_ms"], 3),
                          "graphed_pass_gbs": round(up["graphed_gbs"], 1),
                          "per_shape_instrumented": up["shapes"],
                          "per_shape_note": "per-launch event pairs (separate replay) break the PDL "

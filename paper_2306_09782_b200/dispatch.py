@@ -14,10 +14,29 @@ largest single tensor plus the parked tiny ones.
 from __future__ import annotations
 
 import ctypes
+import importlib.util
 
 from . import _lib
 
 SMALL_NUMEL = 1 << 16
+
+_CPP = None
+
+
+def cpp_dispatch():
+    """The C++ form of this dispatcher (csrc/lomo_dispatch.cpp, built in-tree
+    by __graft_entry__.build() next to liblomo_b200.so), or None if absent."""
+    global _CPP
+    if _CPP is None:
+        import sysconfig
+        path = _lib.LIB_PATH.parent / ("_lomo_dispatch" + sysconfig.get_config_var("EXT_SUFFIX"))
+        _CPP = False
+        if path.exists():
+            spec = importlib.util.spec_from_file_location("_lomo_dispatch", path)
+            mod = importlib.util.module_from_spec(spec)
+            spec.loader.exec_module(mod)
+            _CPP = mod
+    return _CPP or None
 
 
 class HookDispatcher:
@@ -34,15 +53,20 @@ class HookDispatcher:
     """
 
     def __init__(self, lib, state_ptr: int | None, math_code: int,
-                 small_numel: int = SMALL_NUMEL, side_stream=None):
+                 small_numel: int = SMALL_NUMEL, side_stream=None, use_cpp: bool = True):
         self.lib = lib
         self.state_ptr = state_ptr
         self.math = math_code
         self.small = small_numel
         self._upd = {}    # dtype code -> [(p, g)]
         self._prb = {}    # dtype code -> [(g, slot)]
-        self.launches = 0
+        self._launches = 0
         self.side = side_stream
+        # the same launches from C++ (one pybind call + the CUDA launch per
+        # gradient, no ctypes argument conversion); the side-stream mode
+        # stays in Python
+        mod = cpp_dispatch() if (use_cpp and side_stream is None) else None
+        self._cpp = mod.Dispatcher(state_ptr or 0, math_code, small_numel) if mod else None
         if side_stream is not None:
             import torch
             self._events = [torch.cuda.Event() for _ in range(32)]
@@ -71,6 +95,20 @@ class HookDispatcher:
     def configure(self, lr: float = 0.0, clip: float = 0.0, wd: float = 0.0, flags: int = 0):
         """Per-pass constants (the same for every tensor of one backward)."""
         self.lr, self.clip, self.wd, self.flags = float(lr), float(clip), float(wd), int(flags)
+        if self._cpp is not None:
+            self._cpp.configure(self.lr, self.clip, self.wd, self.flags)
+            self.update = self._cpp_update
+            self.probe = self._cpp_probe
+
+    @property
+    def launches(self) -> int:
+        return self._launches + (self._cpp.launches if self._cpp is not None else 0)
+
+    def _cpp_update(self, p, g, dt: int, stream: int) -> None:
+        self._cpp.update(p, g, stream)
+
+    def _cpp_probe(self, g, dt: int, slot: int, stream: int) -> None:
+        self._cpp.probe(g, slot, stream)
 
     # ------------------------------------------------------------ K1 / K2
     def update(self, p, g, dt: int, stream: int) -> None:
@@ -86,7 +124,7 @@ class HookDispatcher:
                                         self.clip, self.wd, self.flags, self.state_ptr, stream)
         if rc:
             _lib.check(rc, "lomo_fused_update")
-        self.launches += 1
+        self._launches += 1
 
     def probe(self, g, dt: int, slot: int, stream: int) -> None:
         n = g.numel()
@@ -100,7 +138,7 @@ class HookDispatcher:
         rc = self.lib.lomo_probe(g.data_ptr(), n, dt, slot, self.flags, self.state_ptr, stream)
         if rc:
             _lib.check(rc, "lomo_probe")
-        self.launches += 1
+        self._launches += 1
 
     # ------------------------------------------------------------ flushing
     def _flush_upd(self, dt, stream):
@@ -116,7 +154,7 @@ class HookDispatcher:
                                                     self.clip, self.wd, self.flags,
                                                     self.state_ptr, stream),
                    "lomo_fused_update_multi")
-        self.launches += (k + 63) // 64
+        self._launches += (k + 63) // 64
 
     def _flush_prb(self, dt, stream):
         lst = self._prb.pop(dt, [])
@@ -129,11 +167,13 @@ class HookDispatcher:
         ss = (ctypes.c_int * k)(*[s for _, s in lst])
         _lib.check(self.lib.lomo_probe_multi(gs, ns, ss, k, dt, self.flags, self.state_ptr, stream),
                    "lomo_probe_multi")
-        self.launches += (k + 63) // 64
+        self._launches += (k + 63) // 64
 
     def flush(self, stream: int) -> None:
         """Launch everything parked; the parked gradients are released after
         their kernel is enqueued (stream-ordered reuse by the allocator)."""
+        if self._cpp is not None:
+            self._cpp.flush(stream)
         for dt in list(self._upd):
             self._flush_upd(dt, stream)
         for dt in list(self._prb):
@@ -141,4 +181,5 @@ class HookDispatcher:
         self.join()
 
     def pending(self) -> int:
-        return sum(map(len, self._upd.values())) + sum(map(len, self._prb.values()))
+        return (sum(map(len, self._upd.values())) + sum(map(len, self._prb.values())) +
+                (self._cpp.pending() if self._cpp is not None else 0))

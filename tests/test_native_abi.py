@@ -114,3 +114,16 @@ def test_product_path_has_no_cpu_fallback():
 def test_package_does_not_import_the_oracle():
     for p in (ROOT / "paper_2306_09782_b200").rglob("*.py"):
         assert "lomo_oracle" not in p.read_text(), p
+
+
+def test_cpp_dispatcher_extension_loads():
+    """The C++ hook dispatcher (csrc/lomo_dispatch.cpp) is built in-tree next
+    to liblomo_b200.so and exposes the HookDispatcher surface (no launches
+    without a GPU)."""
+    from paper_2306_09782_b200.dispatch import cpp_dispatch
+    mod = cpp_dispatch()
+    assert mod is not None, "the _lomo_dispatch extension was not built"
+    assert mod.abi_version() == _lib.ABI_VERSION
+    d = mod.Dispatcher(0, _lib.MATH_F32, 1 << 16)
+    d.configure(0.05, 0.0, 0.0, 0)
+    assert (d.lr, d.flags, d.launches, d.pending()) == (0.05, 0, 0, 0)
