@@ -103,6 +103,10 @@ class _Protocol:
                            and st.clip.kind is ClipKind.BY_VALUE else 0.0)
         self.passes = st.backward_passes_per_step if st is not None else 1
         self._pending = None          # None | "apply" | "skip" after grad_norm
+        # two-pass mode: read the loss's finiteness on the host before pass 1,
+        # so a non-finite loss runs no backward (the reference's order,
+        # stabilize.py:185-189); graphs.py turns it off inside its captures
+        self.check_loss_first = True
         self.last_outcome: StepOutcome | None = None
         self.clip_coef: float | None = None
         self.last_norm: float | None = None
@@ -132,10 +136,16 @@ class _Protocol:
         """
         if self.passes != 2:
             raise TapeStateError("grad_norm is only needed with clip_grad_norm or loss_scale")
-        self.engine.begin(self._check_loss(loss))
+        checked = self._check_loss(loss)
+        self.engine.begin(checked)
         self.engine.configure(flags=self._flags(_PROBE))
-        self._run_backward(self._scaled(loss), _PROBE, retain_graph)
-        self._decide()
+        # stabilize.py:185-189: a non-finite loss skips the step BEFORE any
+        # backward.  The device flag alone (begin_step) gives the same
+        # decision, but the backward would still run; the host check costs
+        # one sync after the forward (the graphed step keeps the device flag)
+        if not (self.check_loss_first and not bool(torch.isfinite(checked.detach()).all())):
+            self._run_backward(self._scaled(loss), _PROBE, retain_graph)
+        self._decide()  # K3a: skip (overflow set by begin_step) + LossScaler.on_overflow
         st = self.engine.read_status()  # the one host sync of the step
         if st.underflow:
             raise ScaleUnderflowError(

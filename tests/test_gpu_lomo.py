@@ -250,6 +250,26 @@ def test_non_finite_loss_aborts_without_touching_params():
     assert not all(torch.equal(a, b) for a, b in zip(before, model.parameters()))
 
 
+@pytest.mark.parametrize("check_first", [True, False])
+def test_two_pass_non_finite_loss_skips_before_backward(check_first):
+    """stabilize.py:185-189: a non-finite loss skips the step (halving the
+    scale) before any backward.  With the host check (the default) no hook
+    runs; with the device flag alone the decision is the same."""
+    cfg = MiniConfig(layers=1, hidden=64, heads=2, vocab=128, seed=0)
+    model = MiniTransformer(cfg, dtype=torch.float16, device="cuda")
+    before = [p.detach().clone() for p in model.parameters()]
+    opt = LOMO(model, lr=0.05, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 10))
+    opt.check_loss_first = check_first
+    ids = torch.from_numpy(sequence_copy_batch(0, 0, 2, 8, 128)).cuda()
+    opt.step(lambda: mean_cross_entropy(model(ids), ids) * float("nan"), 0.05)
+    assert opt.last_outcome == StepOutcome.SKIPPED_OVERFLOW
+    assert opt.loss_scale == 2.0 ** 9
+    assert (opt.hook_calls == 0) == check_first
+    for a, b in zip(before, model.parameters()):
+        assert torch.equal(a, b)
+    assert all(p.grad is None for p in model.parameters())
+
+
 def test_overflow_skip_leaves_params_byte_identical_and_halves_scale():
     """test_stabilize.py:233-240 / criterion 6."""
     cfg = MiniConfig(layers=1, hidden=64, heads=2, vocab=128, seed=0)
