@@ -67,6 +67,20 @@ def _peaks():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
+def _pass_traffic():
+    """DRAM bytes of one WHOLE update pass (ncu range replay, every launch's
+    write-back included) against its algorithmic bytes: profiles/r02_pass_dram.json."""
+    p = ROOT / "profiles" / "r02_pass_dram.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    u = d["update_pass_k1"]
+    return {"dram_bytes": u["dram_bytes_read"] + u["dram_bytes_write"],
+            "algorithmic_bytes": 6 * d["elements_per_pass"], "bytes_per_elem": u["bytes_per_elem"],
+            "probe_pass_bytes_per_elem": d["probe_pass_k2"]["bytes_per_elem"],
+            "source": "profiles/r02_pass_dram.json"}
+
+
 def _traffic():
     """DRAM bytes of one K1 launch (the largest shape) from the committed ncu
     --set full capture, with that launch's algorithmic bytes."""
@@ -1476,7 +1490,8 @@ def main():
                          "traffic": tr["dram_bytes"] if tr else None,
                          "traffic_algorithmic": tr["algorithmic_bytes"] if tr else None,
                          "traffic_launch": tr["launch"] if tr else None,
-                         "traffic_source": tr["source"] if tr else None, "peak_source": peak_src,
+                         "traffic_source": tr["source"] if tr else None,
+                         "traffic_whole_pass": _pass_traffic(), "peak_source": peak_src,
                          "kernel": "k1_update<bf16,f32>: the timed region holds only K1 launches "
                                    "(226 per-tensor + 2 k1_update_multi for the 65 [4096] tensors) "
                                    "on one stream, bracketed by CUDA events; achieved = 6 B/elem x "
