@@ -107,7 +107,11 @@ typedef struct lomo_state {
                          /*      2: a peer barrier timed out (sharded K4)        */
   double grad_div;       /* 112: data-parallel gradient divisor (world size; 1)      */
   double lr;             /* 120: learning rate read under LOMO_LR_FROM_STATE          */
-  /* followed by: double  sumsq[nslots];                      (per-slot totals)
+  /* followed by: 32 bytes at offset 128: the pass-2 record {int32 skip; float
+   *              inv_scale, clip_coef, lr} (fp32 copies the state kernels
+   *              republish whenever they change a field; the fp32-math K1
+   *              reads it with one 16-byte load, internal);
+   *              double  sumsq[nslots];  at LOMO_STATE_SLOTS_OFFSET (per-slot totals)
    *              int32_t nblocks[nslots], padded to 8 bytes;  (K2 CTAs per slot)
    *              double  partials[nslots][LOMO_PROBE_BLOCKS_PER_SLOT];
    * K2 writes one partial per CTA (no atomics); K3a reduces each row in CTA
@@ -115,6 +119,7 @@ typedef struct lomo_state {
 } lomo_state;
 
 #define LOMO_PROBE_BLOCKS_PER_SLOT 8192
+#define LOMO_STATE_SLOTS_OFFSET 160 /* sizeof(lomo_state) + the 32-byte pass-2 record */
 
 /* 128-byte host snapshot of the state header (lomo_read_status). */
 typedef lomo_state lomo_status;

@@ -128,6 +128,8 @@ class LomoStatus(ctypes.Structure):
 
 assert ctypes.sizeof(LomoStatus) == 128
 STATE_HEADER_BYTES = 128
+K1_RECORD_BYTES = 32  # the pass-2 record between the header and sumsq[]
+SLOTS_OFFSET = STATE_HEADER_BYTES + K1_RECORD_BYTES  # LOMO_STATE_SLOTS_OFFSET
 SCALE_F32_OFFSET = LomoStatus.scale_f32.offset
 
 _vp = ctypes.c_void_p
@@ -241,4 +243,4 @@ def check(rc: int, what: str) -> None:
 def state_bytes(nslots: int) -> int:
     # pure arithmetic restated so it works without loading (must equal the C side)
     n = int(nslots)
-    return STATE_HEADER_BYTES + 8 * (n + (n + 1) // 2 + n * PROBE_BLOCKS_PER_SLOT)
+    return SLOTS_OFFSET + 8 * (n + (n + 1) // 2 + n * PROBE_BLOCKS_PER_SLOT)

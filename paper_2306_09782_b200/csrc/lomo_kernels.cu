@@ -251,17 +251,71 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 // with one 4 KB tile per CTA that cost K1 a third of its bandwidth whenever
 // a state flag was set (9.7 vs 6.2 ms over the LLaMA-7B pass,
 // tools/k1_context.py).
+// The pass-2 record: fp32 copies of skip / 1/scale / clip coefficient / lr,
+// 32 bytes right after the 128-byte header (include/lomo_b200.h).  Every
+// state kernel that changes one of those fields republishes it
+// (publish_rec), so the fp32-math kernels read their four step constants
+// with ONE 16-byte load per warp.  The values are exactly the (float) casts
+// the f64 fields would get, so the update's bits are unchanged.
+struct K1Rec {
+  int32_t skip;
+  float inv_scale, coef, lr;
+};
+constexpr size_t kRecBytes = 32;
+static_assert(sizeof(lomo_state) + kRecBytes == LOMO_STATE_SLOTS_OFFSET, "state layout");
+__host__ __device__ __forceinline__ const K1Rec* rec_of(const lomo_state* s) {
+  return reinterpret_cast<const K1Rec*>(reinterpret_cast<const char*>(s) + sizeof(lomo_state));
+}
+__device__ __forceinline__ void publish_rec(lomo_state* s) {
+  K1Rec* r = const_cast<K1Rec*>(rec_of(s));
+  r->skip = s->skip;
+  r->inv_scale = (float)s->inv_scale;
+  r->coef = (float)s->clip_coef;
+  r->lr = (float)s->lr;
+}
+
+// Step-state scalars (skip, 1/scale, clip coefficient, lr).  Kernels issue
+// their data loads BEFORE calling this: the loads do not depend on the
+// state, so the state read's L2 latency overlaps them.  Reading the state
+// first put one dependent L2 round trip in front of every CTA's loads --
+// with one 4 KB tile per CTA that cost K1 a third of its bandwidth whenever
+// a state flag was set (9.7 vs 6.2 ms over the LLaMA-7B pass,
+// tools/k1_context.py).
 template <typename M>
 __device__ __forceinline__ bool resolve_args(UpdArgs<M>& a, unsigned flags,
                                              const lomo_state* st) {
-  if (st != nullptr) {
-    // four independent plain loads from one 128-byte line, all in flight
-    // together (the state was written by an earlier kernel: after the PDL
-    // wait, no volatile/strong access is needed -- a volatile read of `skip`
-    // compiled to LDG.STRONG.SYS and serialised a second round trip)
-    // One lane per warp loads, the warp shares by shuffle: four loads per
-    // thread would triple K1's load instructions (one 16-byte vector of p
-    // and of g per thread) and cost ~7 % of its bandwidth.
+  if (st == nullptr) return true;
+  if constexpr (std::is_same<M, float>::value) {
+    // fp32 math: lane 0 loads the 16-byte pass-2 record, the warp shares it
+    // by four 32-bit shuffles (tools/k1_state_ab.cu: 6.11 ms per LLaMA-7B
+    // pass vs 6.20 for four f64 header loads + f64 shuffles, 6.08 flag-free)
+    uint4 r = make_uint4(0u, 0u, 0u, 0u);
+    if ((threadIdx.x & 31) == 0)
+      asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                   : "l"(rec_of(st)));
+    r.x = __shfl_sync(0xffffffffu, r.x, 0);
+    r.y = __shfl_sync(0xffffffffu, r.y, 0);
+    r.z = __shfl_sync(0xffffffffu, r.z, 0);
+    r.w = __shfl_sync(0xffffffffu, r.w, 0);
+    if ((flags & LOMO_USE_SKIP) && r.x) return false;
+    if (flags & LOMO_USE_SCALE) a.inv_scale = __uint_as_float(r.y);
+    if (flags & LOMO_USE_COEF) a.coef = __uint_as_float(r.z);
+    if (flags & LOMO_LR_FROM_STATE) {
+      a.lr = __uint_as_float(r.w);
+      if (a.has_wd) {  // decay from the f64 lr, as the f64 path computes it
+        double lr;
+        asm volatile("ld.global.f64 %0, [%1];" : "=d"(lr) : "l"(&st->lr));
+        a.decay = (float)(1.0 - lr * (double)a.wd);
+      }
+    }
+    return true;
+  } else {
+    // f64 math: four independent plain loads from one 128-byte line, all in
+    // flight together (the state was written by an earlier kernel: after the
+    // PDL wait, no volatile/strong access is needed -- a volatile read of
+    // `skip` compiled to LDG.STRONG.SYS and serialised a second round trip).
+    // One lane per warp loads, the warp shares by shuffle.
     int32_t skip = 0;
     double inv_scale = 0.0, coef = 0.0, lr = 0.0;
     if ((threadIdx.x & 31) == 0) {
@@ -281,8 +335,8 @@ __device__ __forceinline__ bool resolve_args(UpdArgs<M>& a, unsigned flags,
       a.lr = (M)lr;
       a.decay = (M)(1.0 - lr * (double)a.wd);
     }
+    return true;
   }
-  return true;
 }
 
 template <typename M>
@@ -473,7 +527,7 @@ __host__ __device__ __forceinline__ size_t nblocks_words(int nslots) {
   return (size_t)(nslots + 1) / 2;  // int32 pairs -> 8-byte words
 }
 __device__ __forceinline__ double* slots_of(lomo_state* s) {
-  return reinterpret_cast<double*>(reinterpret_cast<char*>(s) + sizeof(lomo_state));
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(s) + LOMO_STATE_SLOTS_OFFSET);
 }
 __device__ __forceinline__ int32_t* nblocks_of(lomo_state* s) {
   return reinterpret_cast<int32_t*>(slots_of(s) + s->nslots);
@@ -990,6 +1044,7 @@ __device__ void decide(lomo_state* st, double total) {
     st->steps_skipped += 1;
     scaler_on_overflow(st);  // _skip, stabilize.py:155-159
   }
+  publish_rec(st);
 }
 
 // K3a: CTA c reduces slots c, c+grid, ... (each slot's K2 partials in CTA
@@ -1060,6 +1115,7 @@ __global__ void k3_on_clean(void* state) {
     st->inv_scale = 1.0 / (st->scale * st->grad_div);
     st->scale_f32 = (float)st->scale;
     st->clean_steps = 0;
+    publish_rec(st);
   }
 }
 
@@ -1092,14 +1148,18 @@ __global__ void k_state_init(void* state, int nslots, double scale, int growth_i
     st->error = 0;
     st->lr = 0.0;
   }
-  double* s = reinterpret_cast<double*>(reinterpret_cast<char*>(state) + sizeof(lomo_state));
+  if (threadIdx.x == 0) publish_rec(st);
+  double* s = slots_of(st);
   const size_t words = (size_t)nslots + nblocks_words(nslots);  // partials need no init
   for (size_t i = threadIdx.x; i < words; i += blockDim.x) s[i] = 0.0;
 }
 
 __global__ void k_set_lr(void* state, double lr) {
   pdl_wait();
-  if (threadIdx.x == 0) hdr(state)->lr = lr;
+  if (threadIdx.x == 0) {
+    hdr(state)->lr = lr;
+    publish_rec(hdr(state));
+  }
 }
 
 __global__ void k_update_coefs(const void* state, double wd, unsigned flags, float* out) {
@@ -1148,6 +1208,7 @@ __global__ void k_begin_step(void* state, const void* loss, int loss_dtype) {
       st->overflow = 1;  // optim.py:63-65 / stabilize.py:188-189
       st->skip = 1;
     }
+    publish_rec(st);
   }
 }
 
@@ -1387,7 +1448,7 @@ int lomo_abi_version(void) { return LOMO_ABI_VERSION; }
 
 size_t lomo_state_bytes(int nslots) {
   if (nslots < 0) nslots = 0;
-  return sizeof(lomo_state) +
+  return LOMO_STATE_SLOTS_OFFSET +
          sizeof(double) * ((size_t)nslots + nblocks_words(nslots) +
                            (size_t)nslots * LOMO_PROBE_BLOCKS_PER_SLOT);
 }

@@ -70,6 +70,9 @@ class State:
             setattr(st, k, v)
         raw = bytes(ctypes.string_at(ctypes.addressof(st), ctypes.sizeof(st)))
         self.buf[:128].copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
+        # the fp32 kernels read the pass-2 record the state kernels republish
+        # from the header; lomo_set_lr (same lr) is one of them
+        _lib.check(lib().lomo_set_lr(self.ptr, st.lr, stream()), "lomo_set_lr")
         torch.cuda.synchronize()
 
     def begin(self, loss: torch.Tensor | None = None):
@@ -95,7 +98,8 @@ class State:
         tmp = torch.zeros(2, dtype=torch.float64, device="cuda")
         _lib.check(lib().lomo_local_norm_partial(self.ptr, tmp.data_ptr(), stream()), "partial")
         torch.cuda.synchronize()
-        return self.buf[128:128 + 8 * n].view(torch.float64).cpu().numpy()
+        o = _lib.SLOTS_OFFSET
+        return self.buf[o:o + 8 * n].view(torch.float64).cpu().numpy()
 
 
 def fused_update(p, g, math="f32", lr=0.05, clip=0.0, wd=0.0, flags=0, state=None):

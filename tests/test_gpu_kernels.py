@@ -130,6 +130,47 @@ def test_k1_all_stages(prec, math_mode):
             assert d.max().item() <= 1, (wd, d.max().item())
 
 
+def _record(st):
+    """The 16-byte pass-2 record after the header: (skip, inv_scale, coef, lr) as fp32."""
+    torch.cuda.synchronize()
+    raw = st.buf[_lib.STATE_HEADER_BYTES:_lib.STATE_HEADER_BYTES + 16].cpu()
+    skip = int(raw[:4].view(torch.int32).item())
+    f = raw[4:16].view(torch.float32).numpy()
+    return skip, float(f[0]), float(f[1]), float(f[2])
+
+
+def _want_record(h):
+    return (h.skip, float(np.float32(h.inv_scale)), float(np.float32(h.clip_coef)),
+            float(np.float32(h.lr)))
+
+
+def test_pass2_record_is_republished_by_every_state_kernel():
+    """The fp32 K1 reads skip / 1/scale / coef / lr from the record; every
+    kernel that changes one of those header fields must republish it."""
+    st = U.State(2, scale=2.0 ** 10, growth=1, max_norm=1.0)
+    assert _record(st) == _want_record(st.status())                    # init
+    _lib.check(U.lib().lomo_set_lr(st.ptr, 0.0123, U.stream()), "lr")
+    assert _record(st) == _want_record(st.status()) and _record(st)[3] == np.float32(0.0123)
+    g = torch.full((1000,), 3.0, dtype=torch.float16, device="cuda") * 2 ** 10
+    st.begin()
+    st.probe(g, 0, _lib.USE_SCALE)
+    st.finalize()                                                      # coef < 1
+    h = st.status()
+    assert 0 < h.clip_coef < 1 and _record(st) == _want_record(h)
+    st.on_clean()                                                      # growth: scale x2
+    h = st.status()
+    assert h.scale == 2.0 ** 11 and _record(st) == _want_record(h)
+    st.begin(torch.tensor(float("inf"), device="cuda"))                # non-finite loss
+    h = st.status()
+    assert h.skip == 1 and _record(st) == _want_record(h)
+    st.begin()
+    g[3] = float("nan")
+    st.probe(g, 1, _lib.USE_SCALE)
+    st.finalize()                                                      # overflow: halve, skip
+    h = st.status()
+    assert h.skip == 1 and h.scale == 2.0 ** 10 and _record(st) == _want_record(h)
+
+
 def test_k1_skip_flag_is_a_noop():
     rng = np.random.default_rng(3)
     p0, g0 = _draw(50000, "half", rng)

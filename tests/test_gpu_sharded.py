@@ -162,7 +162,7 @@ def test_nvls_k4_kernels_world1(nccl_world, dtype):
         ring.release(k)
         assert torch.equal(p, q), rnd
         sl = torch.empty(2, dtype=torch.float64)
-        off = _lib.STATE_HEADER_BYTES
+        off = _lib.SLOTS_OFFSET
         sl.copy_(eng.state[off:off + 16].view(torch.float64))
         assert abs(sl[0] - sl[1]) <= 1e-6 * float(sl[1]), (rnd, sl)
         assert not st.overflow
