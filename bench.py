@@ -416,6 +416,7 @@ def bench_update(args, rank, world):
     flags_pass = {"gbs": round(BYTES_PER_ELEM * elems / (fl_ms * 1e-3) / 1e9, 1),
                   "ms_per_pass": round(fl_ms, 4),
                   "ab_ms": {k: [round(x, 4) for x in v] for k, v in ab.items()},
+                  "vs_flag_free_ab": round(min(ab["plain"]) / fl_ms, 4),
                   "flags": "USE_SKIP|USE_SCALE|USE_COEF|LR_FROM_STATE (state block read per CTA)"}
     del P, G
     torch.cuda.empty_cache()

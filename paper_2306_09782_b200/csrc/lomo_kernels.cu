@@ -36,7 +36,12 @@
 namespace lomo_k {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 8;  // K2: 16-byte loads in flight per thread (tools/k1_variants.cu)
+// K2: 16-byte loads in flight per thread; the tile is kThreads x kUnroll
+// vectors (16 KB).  tools/k1_state_ab.cu, LLaMA-7B probe pass, 8 alternating
+// rounds: 16 KB tiles 6.12 TB/s against 5.86-5.93 for 32 KB tiles (8 loads
+// per thread) -- smaller tiles spread each 32-90 MB gradient over more CTAs,
+// so the grid's last wave is shorter.
+constexpr int kUnroll = 4;
 
 // --------------------------------------------------------------------------
 // device info (grid sizing)
@@ -552,15 +557,6 @@ __device__ __forceinline__ void put_partial(lomo_state* st, int slot, double v, 
 __device__ __forceinline__ void put_partial(lomo_state* st, int slot, double v, int nblocks) {
   put_partial(st, slot, v, nblocks, st->nslots);
 }
-// nslots is written once, by lomo_state_init (a launch long before any
-// probe), and never again: a probe may read it BEFORE griddepcontrol.wait,
-// so the tail's partial store does not wait for a header round trip.
-__device__ __forceinline__ int nslots_early(const void* state) {
-  int v;
-  asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(&hdr(const_cast<void*>(state))->nslots));
-  return v;
-}
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -644,27 +640,108 @@ __device__ __forceinline__ double tile_sumsq(const uint4& gv, M inv_scale, bool 
   }
 }
 
+// Fixed-order CTA sum for a CTA that reduces once: one barrier (block_sum's
+// second barrier only protects `sm` for reuse).  Result valid in thread 0.
+__device__ __forceinline__ double block_sum_once(double v, double* sm) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < kThreads / 32; ++i) r += sm[i];
+  }
+  return r;
+}
+
+// K2's cold paths, kept out of line so the hot kernel carries none of their
+// registers or instructions (each cost 1-3 % of the probe pass inline,
+// tools/k1_state_ab.cu "k2p -..." ablations).  Both return NaN when they see
+// a non-finite gradient element (probe_hook's overflow, stabilize.py:196-197).
+//
+// The scalar head (before the first aligned vector) and tail (CTA 0).
 template <typename T, typename M>
-__global__ void __launch_bounds__(kThreads, 5)  // 48 registers: 5 CTAs per SM, no spills
+__device__ __noinline__ double k2_head_tail(const T* g, int64_t n, int head, int64_t nvec) {
+  constexpr int V = 16 / sizeof(T);
+  const int64_t tail0 = head + nvec * V;
+  const int64_t ntail = n - tail0;
+  double acc = 0.0;
+  bool bad = false;
+  for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
+    const int64_t e = i < head ? i : tail0 + (i - head);
+    M x = to_m<M>(g[e]);
+    bad |= !is_fin(x);
+    acc += (double)x * (double)x;
+  }
+  return bad ? __longlong_as_double(0x7ff8000000000000ll) : acc;
+}
+// A thread whose fp32 running sum came out non-finite: a non-finite element
+// (NaN result), or finite elements whose fp32 squares overflowed (the sum
+// redone in f64 from `acc0`).
+template <typename T>
+__device__ __noinline__ double k2_rescan(const uint4* gv, int64_t beg, int64_t end, double acc0) {
+  constexpr int V = 16 / sizeof(T);
+  for (int64_t i = beg + threadIdx.x; i < end; i += kThreads)
+    if (vec_has_nonfinite<T>(ld_stream_ro(gv + i))) return __longlong_as_double(0x7ff8000000000000ll);
+  double acc = acc0;
+  for (int64_t i = beg + threadIdx.x; i < end; i += kThreads) {
+    Vec16<T> G;
+    G.u = ld_stream_ro(gv + i);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      const double x = (double)to_m<float>(G.e[k]);
+      acc += x * x;
+    }
+  }
+  return acc;
+}
+
+// One tile of K2: kUnroll 16-byte vectors per thread, all loads issued
+// before the first square.
+template <typename T, typename M>
+__device__ __forceinline__ double k2_tile(const uint4* __restrict__ gv, int64_t base, int64_t end,
+                                          bool& bad) {
+  uint4 G[kUnroll];
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const int64_t i = base + (int64_t)u * kThreads;
+    if (i < end) G[u] = ld_stream_ro(gv + i);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u) {
+    const int64_t i = base + (int64_t)u * kThreads;
+    if (i < end) acc += tile_sumsq<T, M>(G[u], (M)1, false, bad);
+  }
+  return acc;
+}
+
+template <typename T, typename M>
+__global__ void __launch_bounds__(kThreads, 6)
     k2_probe(const T* __restrict__ g, int64_t n, int head, int64_t nvec, int64_t per_cta,
              int slot, unsigned flags, void* state) {
-  constexpr int V = 16 / sizeof(T);
   __shared__ double sm[kThreads / 32];
-  int nslots = 0;
-  if (threadIdx.x == 0) {  // this CTA's tile into L2 while the previous grid drains
-    const int64_t b0 = (int64_t)blockIdx.x * per_cta;
-    const int64_t nt = min(per_cta, nvec - b0);
-    if (nt > 0) prefetch_l2(reinterpret_cast<const uint4*>(g + head) + b0, (uint32_t)(nt * 16));
-    nslots = nslots_early(state);  // (the tail's partial store needs it)
-  }
+  const int64_t beg = (int64_t)blockIdx.x * per_cta;
+  const int64_t end = min(beg + per_cta, nvec);
+  const uint4* gv = reinterpret_cast<const uint4*>(g + head);
+  if (threadIdx.x == 0 && end > beg)  // this CTA's tile into L2 while the previous grid drains
+    prefetch_l2(gv + beg, (uint32_t)((end - beg) * 16));
   pdl_wait();
   pdl_launch_dependents();
   lomo_state* st = hdr(state);
-  const bool use_scale = (flags & LOMO_USE_SCALE) != 0;
+  // 1/scale and nslots for the CTA's partial, loaded now (after the wait: an
+  // earlier step's K3 may have changed the scale) and consumed at the end, so
+  // the L2 round trip hides behind the tile's loads instead of extending the
+  // CTA's life (tools/k1_state_ab.cu: 2.20 vs 2.24 ms per pass read at the end)
+  double sc = 1.0;
+  int nslots = 0;
+  if (threadIdx.x == 0) {
+    if (flags & LOMO_USE_SCALE)
+      asm volatile("ld.global.f64 %0, [%1];" : "=d"(sc) : "l"(&st->inv_scale));
+    asm volatile("ld.global.s32 %0, [%1];" : "=r"(nslots) : "l"(&st->nslots));
+  }
 
-  double acc = 0.0;
-  bool bad = false;
-  // small fixed tiles (>= 2048 vectors = 32 KB, <= LOMO_PROBE_BLOCKS_PER_SLOT
+  // small fixed tiles (>= 1024 vectors = 16 KB, <= LOMO_PROBE_BLOCKS_PER_SLOT
   // CTAs): the block scheduler balances them across SMs like K1's tiles.
   //
   // The squares are summed UNSCALED and the CTA's sum is multiplied by
@@ -672,64 +749,41 @@ __global__ void __launch_bounds__(kThreads, 5)  // 48 registers: 5 CTAs per SM, 
   // scale; with a data-parallel divisor that is a power of two too), so every
   // term, every partial sum and the result scale exactly -- the same bits as
   // summing (g * inv_scale)^2 (stabilize.py:199) -- but no load of the loop
-  // depends on the state.  (Any other divisor: within f64 rounding.)  Reading inv_scale before or inside the loop
-  // measured 6-8 % slower over the LLaMA-7B probe pass
-  // (tools/k1_variants.cu, "k2 clone USE_SCALE ...").
-  const int64_t beg = (int64_t)blockIdx.x * per_cta;
-  const int64_t end = min(beg + per_cta, nvec);
-  const uint4* gv = reinterpret_cast<const uint4*>(g + head);
-  if (blockIdx.x == 0) {  // scalar head (before the first aligned vector) and tail, first
-    const int64_t tail0 = head + nvec * V;
-    const int64_t ntail = n - tail0;
-    for (int64_t i = threadIdx.x; i < head + ntail; i += blockDim.x) {
-      const int64_t e = i < head ? i : tail0 + (i - head);
-      M x = to_m<M>(g[e]);
-      bad |= !is_fin(x);
-      acc += (double)x * (double)x;
-    }
+  // depends on the state.  (Any other divisor: within f64 rounding.)
+  bool bad = false;
+  double acc = 0.0;
+  if (blockIdx.x == 0) {
+    acc = k2_head_tail<T, M>(g, n, head, nvec);
+    bad = acc != acc;  // (the NaN then flows into the partial, as before)
   }
   const double acc_ht = acc;
-  for (int64_t base = beg + threadIdx.x; base < end; base += (int64_t)kThreads * kUnroll) {
-    uint4 G[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t i = base + (int64_t)u * kThreads;
-      if (i < end) G[u] = ld_stream_ro(gv + i);
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t i = base + (int64_t)u * kThreads;
-      if (i < end) acc += tile_sumsq<T, M>(G[u], (M)1, false, bad);
-    }
+  // One 16 KB tile per CTA (every launch but the largest tensors'): straight
+  // -line code, all of the tile's loads in flight before the first square.
+  // Larger per-CTA ranges loop over tiles (no outer unroll: the compiler
+  // otherwise software-pipelines the loop so a tile's loads are no longer all
+  // in flight at once -- 5.37 vs 6.1 TB/s).
+  if (per_cta == (int64_t)kThreads * kUnroll) {
+    acc += k2_tile<T, M>(gv, beg + threadIdx.x, end, bad);
+  } else {
+#pragma unroll 1
+    for (int64_t base = beg + threadIdx.x; base < end; base += (int64_t)kThreads * kUnroll)
+      acc += k2_tile<T, M>(gv, base, end, bad);
   }
   if constexpr (std::is_same<M, float>::value) {
-    if (!is_fin(acc)) {  // rare: a non-finite element, or fp32 overflow of the squares?
-      for (int64_t i = beg + threadIdx.x; i < end && !bad; i += kThreads)
-        bad = vec_has_nonfinite<T>(ld_stream_ro(gv + i));
-      if (!bad) {  // finite elements whose fp32 squares overflowed: redo them in f64
-        acc = acc_ht;
-        for (int64_t i = beg + threadIdx.x; i < end; i += kThreads) {
-          Vec16<T> G;
-          G.u = ld_stream_ro(gv + i);
-#pragma unroll
-          for (int k = 0; k < V; ++k) {
-            const double x = (double)to_m<float>(G.e[k]);
-            acc += x * x;
-          }
-        }
-      }
+    if (!is_fin(acc)) {  // rare
+      acc = k2_rescan<T>(gv, beg, end, acc_ht);
+      if (acc != acc) bad = true;
     }
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
+  // any thread that saw a non-finite element raises the flag (all store 1:
+  // no barrier needed, K3 reads it after this grid completes)
+  if (bad) st->overflow = 1;
 
   // per-CTA partial into this slot's partial row; K3 reduces the row in CTA
   // order (deterministic, no atomics on the hot path)
-  double bsum = block_sum(acc, sm);
+  double bsum = block_sum_once(acc, sm);
   if (threadIdx.x == 0) {
-    if (use_scale) {
-      const double sc = st->inv_scale;
-      bsum *= sc * sc;  // exact: a power of two
-    }
+    if (flags & LOMO_USE_SCALE) bsum *= sc * sc;  // exact: a power of two
     put_partial(st, slot, bsum, (int)gridDim.x, nslots);
   }
 }

@@ -143,7 +143,8 @@ float time_passes(F&& one_pass, int reps) {
   return ms / reps;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const bool ncu_mode = argc > 1;
   std::vector<int64_t> sizes;
   sizes.push_back(32000LL * 4096);
   for (int l = 0; l < 32; ++l) {
@@ -193,11 +194,24 @@ int main() {
       }
     }, 10);
   };
+  if (ncu_mode) {  // a few launches of each probe form, for ncu --set full
+    double* part;
+    CK(cudaMalloc(&part, sizeof(double) * 65536));
+    for (int i = (int)ts.size() - 2; i >= (int)ts.size() - 4; --i) {
+      const int64_t nvec = ts[i].n / 8;
+      lomo_probe(ts[i].g, ts[i].n, LOMO_BF16, i, LOMO_USE_SCALE, state, nullptr);
+      launch(k2v<4, 5, true, 1, 2>, dim3((unsigned)((nvec + 1023) / 1024)), dim3(256),
+             (cudaStream_t)0, (const bf*)ts[i].g, nvec, (int64_t)1024, part,
+             (const double*)((char*)state + 8));
+    }
+    CK(cudaDeviceSynchronize());
+    return 0;
+  }
   const char* names[] = {"plain (no state)", "product state (lane0 4 ld + f64 shfl)",
                          "record: all lanes ld.v4", "record: lane0 ld.v4 + 4 shfl",
                          "record: all lanes before wait (unsafe)"};
   double sum[5] = {0};
-  const int rounds = 4;
+  const int rounds = 1;
   for (int r = 0; r < rounds; ++r) {
     float ms[5] = {product(false), product(true), variant(k1_rec<1>), variant(k1_rec<2>),
                    variant(k1_rec<3>)};
@@ -237,31 +251,27 @@ int main() {
   };
   std::vector<PV> pv = {
       {"K2 product (USE_SCALE)", probe_product},
-      {"k2v u8 t2048 5/SM pf (product shape)", [&] { return probe_v(k2v<8, 5, true, 1>, 2048); }},
-      {"k2v u8 t2048 5/SM pf scale@end", [&] { return probe_v(k2v<8, 5, true, 1, 1>, 2048); }},
-      {"k2v u4 t1024 5/SM pf", [&] { return probe_v(k2v<4, 5, true, 1>, 1024); }},
-      {"k2v u4 t1024 5/SM pf scale@end", [&] { return probe_v(k2v<4, 5, true, 1, 1>, 1024); }},
       {"k2v u4 t1024 5/SM pf scale early", [&] { return probe_v(k2v<4, 5, true, 1, 2>, 1024); }},
-      {"k2v u4 t1024 6/SM pf", [&] { return probe_v(k2v<4, 6, true, 1>, 1024); }},
-      {"k2v u4 t1024 4/SM pf", [&] { return probe_v(k2v<4, 4, true, 1>, 1024); }},
-      {"k2v u4 t1024 5/SM no-pf", [&] { return probe_v(k2v<4, 5, false, 1>, 1024); }},
-      {"k2v u2 t512 8/SM pf", [&] { return probe_v(k2v<2, 8, true, 1>, 512); }},
-      {"k2v u2 t512 5/SM pf", [&] { return probe_v(k2v<2, 5, true, 1>, 512); }},
-      {"k2v u2 t1024 8/SM pf", [&] { return probe_v(k2v<2, 8, true, 1>, 1024); }},
-      {"k2v u4 t1536 5/SM pf", [&] { return probe_v(k2v<4, 5, true, 1>, 1536); }},
-      {"k2v u1 t256 8/SM pf", [&] { return probe_v(k2v<1, 8, true, 1>, 256); }},
+      {"k2v u8 t2048 5/SM pf scale early", [&] { return probe_v(k2v<8, 5, true, 1, 2>, 2048); }},
   };
 
+
+
+
+
+
   std::vector<double> psum(pv.size(), 0.0);
-  for (int r = 0; r < 3; ++r)
-    for (size_t v = 0; v < pv.size(); ++v) {
+  const int prounds = 4;
+  for (int r = 0; r < prounds; ++r)
+    for (size_t vi = 0; vi < pv.size(); ++vi) {
+      const size_t v = (r & 1) ? pv.size() - 1 - vi : vi;
       const float ms = pv[v].f();
       psum[v] += ms;
       printf("round %d %-44s %7.3f ms %7.1f GB/s\n", r, pv[v].name, ms, gbp / (ms * 1e-3));
     }
   for (size_t v = 0; v < pv.size(); ++v)
-    printf("mean  %-44s %7.3f ms %7.1f GB/s\n", pv[v].name, psum[v] / 3,
-           gbp / (psum[v] / 3 * 1e-3));
+    printf("mean  %-44s %7.3f ms %7.1f GB/s\n", pv[v].name, psum[v] / prounds,
+           gbp / (psum[v] / prounds * 1e-3));
   // flat read ceiling: one launch over the 32000x4096 head (262 MB)
   {
     const int64_t nvec = ts[0].n / 8;
