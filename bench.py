@@ -1042,7 +1042,8 @@ def bench_train_sharded(args, rank, world):
     size = args.sharded_model
     ckpt = args.ckpt or size == "65b"
     spec = dict(hidden=512, layers=4, heads=8, ffn=1408, vocab=32000) if size == "tiny" else size
-    model = Llama(spec, dtype=torch.float16, device="cuda", checkpointing=ckpt)
+    model = Llama(spec, dtype=torch.float16, device="cuda", checkpointing=ckpt,
+                  fused_proj=not args.separate_proj)
     model.train()
     # 180 GB per GPU: when the gathered model takes under 40 % of HBM, the layer
     # buckets stay gathered between forward and backward (parameters are still
@@ -1082,8 +1083,13 @@ def bench_train_sharded(args, rank, world):
         end.record()
         _barrier(world)
     ms = _max_over_ranks(start.elapsed_time(end), world) / args.train_steps
+    eager_peak = torch.cuda.max_memory_allocated()
+    graphed = None
+    if not reshard and not args.sharded_strict and not args.no_sharded_graph:
+        graphed = _graphed_sharded(args, opt, model, data, world)
     out = {"model": f"llama-{size} (random init), fp16, parameters sharded over {world} GPUs "
-                    f"({'ZeRO-3: layers freed after use' if reshard else 'layers kept gathered'})",
+                    f"({'ZeRO-3: layers freed after use' if reshard else 'layers kept gathered'})"
+                    + ("" if args.separate_proj else "; stacked qkv / gate_up weights"),
            "tokens_per_s": round(world * batch * seq / (ms * 1e-3), 1),
            "tokens_per_gpu_per_s": round(batch * seq / (ms * 1e-3), 1),
            "ms_per_step": round(ms, 2), "seq_len": seq, "batch_per_rank": batch,
@@ -1094,12 +1100,74 @@ def bench_train_sharded(args, rank, world):
            "pass2": "second forward + backward" if args.sharded_strict else
                     (f"K1 over pass 1's reduced gradient shards ({pbytes / world / 2**30:.1f} GiB "
                      "kept per rank)" if keep else "replay of the stashed (x, dy) into the buckets"),
-           "peak_mem_gib_rank0": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
+           "peak_mem_gib_rank0": round(eager_peak / 2 ** 30, 2),
            "paper_tgs_rtx3090": {"13b": 66.19, "30b": 11.61, "65b": 4.93}.get(size)}
+    if graphed is not None:
+        out["graphed"] = graphed
+        if "tokens_per_s" in graphed:
+            out["eager_tokens_per_s"] = out["tokens_per_s"]
+            if graphed["tokens_per_s"] > out["tokens_per_s"]:
+                out["tokens_per_s"] = graphed["tokens_per_s"]
+                out["tokens_per_gpu_per_s"] = graphed["tokens_per_gpu_per_s"]
+                out["ms_per_step"] = graphed["ms_per_step"]
+                out["headline_variant"] = "graphed (GraphedShardedStep)"
+                out["tensor_roofline"] = _sharded_roofline(model, batch, seq, graphed["ms_per_step"],
+                                                           keep, False, ckpt, graphed["clocks"])
+            else:
+                out["headline_variant"] = "eager"
     opt.remove_hooks()
     del opt, model
     torch.cuda.empty_cache()
     return out
+
+
+def _graphed_sharded(args, opt, model, data, world):
+    """The same ShardedLOMO step captured as two CUDA graphs
+    (``GraphedShardedStep``: refresh all-gathers, reduce-scatters, K2/K3/K1
+    and the rank exchange inside the graphs; the status read between them).
+    Continues training the eager leg's model (throughput, not a fresh run)."""
+    import torch
+    from paper_2306_09782_b200.graphs import GraphedShardedStep
+    try:
+        torch.cuda.empty_cache()
+        static = data[0].clone()
+        gs = GraphedShardedStep(opt, lambda d: model.loss(d[:, :-1], d[:, 1:]), [static],
+                                warmup=max(2, args.train_warmup), lr=1e-3)
+        for k in range(2):
+            static.copy_(data[k % len(data)])
+            gs.step(1e-3)
+        torch.cuda.synchronize()
+        _barrier(world)
+        torch.cuda.reset_peak_memory_stats()
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        outcomes = []
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            start.record()
+            for k in range(args.train_steps):
+                static.copy_(data[k % len(data)])
+                gs.step(1e-3)
+                outcomes.append(opt.last_outcome.value)
+            end.record()
+            _barrier(world)
+        ms = _max_over_ranks(start.elapsed_time(end), world) / args.train_steps
+        seq, batch = args.seq, args.batch
+        res = {"tokens_per_s": round(world * batch * seq / (ms * 1e-3), 1),
+               "tokens_per_gpu_per_s": round(batch * seq / (ms * 1e-3), 1),
+               "ms_per_step": round(ms, 2), "steps": args.train_steps, "outcomes": outcomes,
+               "clocks": clk.summary(),
+               "peak_mem_gib_rank0": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
+               "note": "same model as the eager leg, continued. In a world-1 group NCCL "
+                       "runs its captured collectives as copy kernels on the SMs (eager: "
+                       "copy-engine DMA), so at N=1 the graphed step is slower; at N>1 both "
+                       "forms run NCCL's kernels and the graph removes the eager step's "
+                       "host gaps (tools/sharded_profile.py: 3.7-5.3 ms idle per step)"}
+        del gs
+        torch.cuda.empty_cache()
+        return res
+    except Exception as exc:  # noqa: BLE001 -- a secondary leg must not cost the line
+        import traceback
+        traceback.print_exc()
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
 
 def _sharded_roofline(model, batch, seq, ms, keep, strict, ckpt, clk):
@@ -1412,6 +1480,8 @@ def main():
                     help="run the ZeRO-3 sharded train leg even at N=1 (world-1 NCCL group)")
     ap.add_argument("--no-sharded-world1", dest="sharded_world1", action="store_false",
                     help="skip the N=1 run of the sharded train leg (world-1 NCCL group)")
+    ap.add_argument("--no-sharded-graph", action="store_true",
+                    help="sharded train leg: skip the GraphedShardedStep timing")
     ap.add_argument("--sharded-strict", action="store_true",
                     help="sharded train leg: pass 2 as a second forward+backward (default: replay)")
     ap.add_argument("--sharded-model", default="13b", choices=["tiny", "7b", "13b", "30b", "65b"],

@@ -1,7 +1,8 @@
 """CUDA-graph capture of a whole LOMO step: the two-pass replay step (below),
 the strict two-pass step (pass 2 a second backward over the retained autograd
 graph, with or without the fused GEMMs), the single fused pass, and
-GroupedLOMO's single pass (``GraphedGroupedStep``).
+GroupedLOMO's single pass (``GraphedGroupedStep``), and ShardedLOMO's
+two-pass step with its NCCL collectives (``GraphedShardedStep``).
 
 A LLaMA-7B step issues ~3,000 kernels -- autograd's, the hook kernels, K5 --
 and at seq 1024 the host cannot launch them as fast as the B200 runs them.
@@ -213,5 +214,106 @@ class GraphedGroupedStep:
         skipped = st.steps_skipped > opt._skipped_before
         opt._skipped_before = st.steps_skipped
         opt.last_outcome = StepOutcome.SKIPPED_OVERFLOW if skipped else StepOutcome.APPLIED
+        self.steps += 1
+        return self.loss
+
+
+class GraphedShardedStep:
+    """:class:`~paper_2306_09782_b200.sharded.ShardedLOMO`'s two-pass step
+    captured as two CUDA graphs, NCCL collectives included (one process per
+    GPU; every rank captures and replays the same sequence):
+
+    * graph 1: the refresh all-gathers of the updated parameter shards (each
+      layer's forward waits for its own bucket), the forward, the cross-rank
+      loss sum and ``begin_step``, the pass-1 backward -- per bucket the
+      asynchronous ``reduce_scatter_tensor`` and K2 on this rank's shard --,
+      then the local K3 partial, the ``all_gather`` of ``{sumsq, overflow}``
+      and K3a on the rank-ordered sum;
+    * host: the one status read (stabilize.py:204-205);
+    * graph 2: pass 2 -- K1 over pass 1's kept gradient shards
+      (``keep_grads``), or the replayed buckets' reduce-scatter + K1
+      (``replay``) -- with the learning rate from the device state, and K3b.
+
+    The host-side step (``ShardedLOMO.step``) launches ~2,000 kernels and
+    ~80 collectives per step; replaying the graphs removes that host cost.
+    Needs the layers kept gathered (``reshard_after_forward=False``: ZeRO-3's
+    per-layer free and re-gather resize storage, which a graph cannot) and
+    the NCCL reduce-scatter (not ``fused_rs``: K4's peer barriers count
+    epochs on the host).  Numerics are those of the eager step.
+
+    Args as :class:`GraphedLOMOStep`.
+    """
+
+    def __init__(self, opt, loss_fn: Callable[..., torch.Tensor],
+                 static_inputs: Sequence[torch.Tensor], warmup: int = 2, lr: float = 1e-3):
+        from .sharded import ShardedLOMO, _KeptShards
+        if not isinstance(opt, ShardedLOMO) or opt.passes != 2:
+            raise ConfigError("GraphedShardedStep needs a two-pass ShardedLOMO "
+                              "(clip_grad_norm and/or loss_scale)")
+        if opt.fused_rs:
+            raise ConfigError("GraphedShardedStep: fused_rs counts its peer-barrier epochs on "
+                              "the host; capture the NCCL reduce-scatter form")
+        if any(not b.persistent for b in opt.buckets):
+            raise ConfigError("GraphedShardedStep needs reshard_after_forward=False (ZeRO-3's "
+                              "per-layer free/re-gather resizes storage inside the step)")
+        if opt._stash is None:
+            raise ConfigError("GraphedShardedStep needs keep_grads=True or replay=True (pass 2 "
+                              "without a second forward/backward)")
+        if opt.clip_value:
+            raise ConfigError("value clipping is a single-pass mode")
+        self.opt, self.loss_fn, self.inputs = opt, loss_fn, tuple(static_inputs)
+        self.keep = isinstance(opt._stash, _KeptShards)
+        dev = opt.device
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(max(1, warmup)):
+                opt.step(lambda: loss_fn(*self.inputs), lr)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        for b in opt.buckets:
+            b.wait()
+        eng = opt.engine
+        pool = torch.cuda.graph_pool_handle()
+        self.g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g1, pool=pool):
+            # the refresh gathers of every bucket (captured unconditionally:
+            # after a skipped step they re-gather unchanged shards)
+            for b in opt.buckets:
+                b.dirty = True
+            opt._refresh()
+            self.loss = loss_fn(*self.inputs)
+            eng.begin(opt._check_loss(self.loss))
+            eng.configure(flags=opt._flags(_PROBE))
+            opt._run_backward(opt._scaled(self.loss), _PROBE, False)
+            opt._decide()
+        self.g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g2, pool=pool):
+            eng.configure(0.0, 0.0, opt.weight_decay, opt._flags(_UPDATE) | _lib.LR_FROM_STATE)
+            opt._replay_pass(0.0)
+            eng.on_clean()
+        for b in opt.buckets:
+            b.dirty = False  # the refresh lives in graph 1
+        self.steps = 0
+
+    def step(self, lr: float) -> torch.Tensor:
+        """One captured sharded step; returns the (device) loss tensor."""
+        opt, eng = self.opt, self.opt.engine
+        _lib.check(eng.lib.lomo_set_lr(eng.ptr, float(lr), eng.stream()), "lomo_set_lr")
+        self.g1.replay()
+        st = eng.read_status()          # the one host sync of the step
+        if st.underflow:
+            raise ScaleUnderflowError(
+                f"loss scale would fall below {st.min_scale}; training diverged")
+        opt.last_norm, opt.clip_coef = float(st.total_norm), float(st.clip_coef)
+        if st.skip:
+            opt.last_outcome = StepOutcome.SKIPPED_OVERFLOW
+        else:
+            self.g2.replay()
+            opt.last_outcome = StepOutcome.APPLIED
+            for b in opt.buckets:
+                # the next graph-1 replay re-gathers them; an eager refresh
+                # before that (gather_all, an eager step) must too
+                b.dirty = True
         self.steps += 1
         return self.loss

@@ -1,7 +1,10 @@
 """Profile ShardedLOMO (config 4's path) in a world-1 NCCL group: GPU time by
 kernel family, idle time between kernels, and the largest gaps.
 
-    python tools/sharded_profile.py [--model 7b] [--mode keep|replay|strict]
+    python tools/sharded_profile.py [--model 7b] [--mode keep|replay|strict] [--graph]
+                                    [--separate-proj]
+
+--graph profiles the GraphedShardedStep replay of the same step.
 """
 import argparse
 import os
@@ -20,17 +23,24 @@ from paper_2306_09782_b200.workloads import Llama  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="7b")
 ap.add_argument("--mode", default="keep", choices=["keep", "replay", "strict"])
+ap.add_argument("--graph", action="store_true")
+ap.add_argument("--separate-proj", action="store_true")
 a = ap.parse_args()
 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
 os.environ.setdefault("MASTER_PORT", "29571")
 torch.cuda.set_device(0)
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-model = Llama(a.model, dtype=torch.float16, device="cuda", fused_proj=True)
+model = Llama(a.model, dtype=torch.float16, device="cuda", fused_proj=not a.separate_proj)
 opt = ShardedLOMO(model, lr=1e-3, clip_grad_norm=1.0, loss_scale=LossScaler(2.0 ** 10),
                   reshard_after_forward=False, replay=a.mode == "replay",
                   keep_grads=a.mode == "keep")
 d = torch.randint(0, 32000, (1, 1025), device="cuda")
 step = lambda: opt.step(lambda: model.loss(d[:, :-1], d[:, 1:]), 1e-3)  # noqa: E731
+if a.graph:
+    from paper_2306_09782_b200.graphs import GraphedShardedStep  # noqa: E402
+    gs = GraphedShardedStep(opt, lambda x: model.loss(x[:, :-1], x[:, 1:]), [d], warmup=2,
+                            lr=1e-3)
+    step = lambda: gs.step(1e-3)  # noqa: E731
 for _ in range(3):
     step()
 torch.cuda.synchronize()
