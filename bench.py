@@ -1085,7 +1085,9 @@ def bench_train_sharded(args, rank, world):
     ms = _max_over_ranks(start.elapsed_time(end), world) / args.train_steps
     eager_peak = torch.cuda.max_memory_allocated()
     graphed = None
-    if not reshard and not args.sharded_strict and not args.no_sharded_graph:
+    import torch.distributed as dist
+    if not reshard and not args.sharded_strict and not args.no_sharded_graph and \
+            dist.get_backend() == "nccl":  # (not the gloo LOMO_BENCH_SHARE_GPU dry run)
         graphed = _graphed_sharded(args, opt, model, data, world)
     out = {"model": f"llama-{size} (random init), fp16, parameters sharded over {world} GPUs "
                     f"({'ZeRO-3: layers freed after use' if reshard else 'layers kept gathered'})"
