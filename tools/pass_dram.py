@@ -1,6 +1,6 @@
 """Whole-pass DRAM bytes of the LLaMA-7B update pass (K1) and probe pass (K2).
 
-    ncu --replay-mode app-range --profile-from-start off --clock-control none \
+    ncu --replay-mode app-range --clock-control none \
         --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
         python tools/pass_dram.py
 
