@@ -255,7 +255,11 @@ def bench_update(args, rank, world):
     from paper_2306_09782_b200.dispatch import HookDispatcher
     lib = _lib.load()
     disp = HookDispatcher(lib, None, _lib.MATH_F32)
-    disp.configure(lr=0.05)
+    # the pass issues its K1s back to back (no kernel in between), as a pass
+    # over kept or replayed gradients does: every K1 after the first is
+    # chained (LOMO_CHAINED: loads/stores before the PDL wait); the unchained
+    # form -- the autograd-hook pattern -- is timed beside it
+    disp.configure(lr=0.05, chain=True)
     P, G = make_update_workload(rank, world, args.dtype)
     dt_code = _lib.BF16 if args.dtype == "bf16" else _lib.F16
     elems = sum(p.numel() for p in P)
@@ -292,7 +296,7 @@ def bench_update(args, rank, world):
         torch.cuda.synchronize()
         return statistics.median(out)
     pyd = HookDispatcher(lib, None, _lib.MATH_F32, use_cpp=False)
-    pyd.configure(lr=0.05)
+    pyd.configure(lr=0.05, chain=True)
     host_enqueue = {"dispatcher": "C++ (csrc/lomo_dispatch.cpp)" if disp._cpp is not None
                     else "python/ctypes", "ms_per_pass": round(enqueue_ms(disp), 3),
                     "python_ctypes_ms_per_pass": round(enqueue_ms(pyd), 3),
@@ -377,7 +381,7 @@ def bench_update(args, rank, world):
              "what": "K2 sum-of-squares + overflow flag over every gradient, + begin/finalize (K3a)"}
     # the exact-arithmetic mode (f64 math, direct rounding) on the same pass
     d64 = HookDispatcher(lib, None, _lib.MATH_F64)
-    d64.configure(lr=0.05)
+    d64.configure(lr=0.05, chain=True)
     for _ in range(2):
         run_update_pass(d64, P, G, dt_code, stream)
     torch.cuda.synchronize()
@@ -394,7 +398,10 @@ def bench_update(args, rank, world):
     # (stabilize.py:215-224), no host scalars
     _lib.check(lib.lomo_set_lr(st.data_ptr(), 0.05, stream), "lomo_set_lr")
     dfl = HookDispatcher(lib, st.data_ptr(), _lib.MATH_F32)
-    dfl.configure(flags=_lib.USE_SKIP | _lib.USE_SCALE | _lib.USE_COEF | _lib.LR_FROM_STATE)
+    dfl.configure(flags=_lib.USE_SKIP | _lib.USE_SCALE | _lib.USE_COEF | _lib.LR_FROM_STATE,
+                  chain=True)
+    dun = HookDispatcher(lib, None, _lib.MATH_F32)
+    dun.configure(lr=0.05)  # unchained: every K1 waits for its predecessor first
     for _ in range(2):
         run_update_pass(dfl, P, G, dt_code, stream)
     torch.cuda.synchronize()
@@ -408,20 +415,28 @@ def bench_update(args, rank, world):
         return start.elapsed_time(end) / args.steps
     # A/B alternation with the flag-free form (same tensors, back to back), so
     # the comparison does not depend on the order of the bench's legs
-    ab = {"state": [], "plain": []}
+    ab = {"state": [], "plain": [], "plain_unchained": []}
     for _ in range(2):
         ab["state"].append(pass_ms(dfl))
         ab["plain"].append(pass_ms(disp))
+        ab["plain_unchained"].append(pass_ms(dun))
     fl_ms = min(ab["state"])
+    un_ms = min(ab["plain_unchained"])
     flags_pass = {"gbs": round(BYTES_PER_ELEM * elems / (fl_ms * 1e-3) / 1e9, 1),
                   "ms_per_pass": round(fl_ms, 4),
                   "ab_ms": {k: [round(x, 4) for x in v] for k, v in ab.items()},
                   "vs_flag_free_ab": round(min(ab["plain"]) / fl_ms, 4),
                   "flags": "USE_SKIP|USE_SCALE|USE_COEF|LR_FROM_STATE (state block read per CTA)"}
+    unchained = {"gbs": round(BYTES_PER_ELEM * elems / (un_ms * 1e-3) / 1e9, 1),
+                 "ms_per_pass": round(un_ms, 4),
+                 "vs_chained_ab": round(min(ab["plain"]) / un_ms, 4),
+                 "what": "the same pass with every K1 waiting for its predecessor before "
+                         "its loads (griddepcontrol.wait first): the autograd-hook pattern, "
+                         "where the gradient's producer runs just before each K1"}
     del P, G
     torch.cuda.empty_cache()
     return {"gbs": gbs, "ms": ms / args.steps, "probe": probe, "f64_math": f64,
-            "flags_pass": flags_pass,
+            "flags_pass": flags_pass, "unchained": unchained,
             "graphed_gbs": BYTES_PER_ELEM * elems / (upd_graph_ms * 1e-3) / 1e9,
             "host_ms": host_ms, "host_enqueue": host_enqueue,
             "elems_per_rank": elems, "total_elems": total_elems,
@@ -1553,7 +1568,10 @@ def main():
             "config": {
                 "workload": "config 2: one LOMO fused-update pass (K1 per tensor, reverse "
                             "registration = autograd delivery order) over all 291 LLaMA-7B "
-                            "parameter tensors",
+                            "parameter tensors, issued back to back as a pass over kept "
+                            "gradients issues them (K1s after the first chained, "
+                            "LOMO_CHAINED; the unchained hook pattern: "
+                            "update_pass_unchained)",
                 "elements": up["total_elems"], "algorithmic_bytes_per_elem": BYTES_PER_ELEM,
                 "math": "fp32", "lr": 0.05, "parallelism": "single",
                 "l2": "no flush: per-step working set 27 GB >> 126 MB L2, each byte touched "
@@ -1565,10 +1583,10 @@ def main():
                          "traffic_launch": tr["launch"] if tr else None,
                          "traffic_source": tr["source"] if tr else None,
                          "traffic_whole_pass": _pass_traffic(), "peak_source": peak_src,
-                         "kernel": "k1_update<bf16,f32>: the timed region holds only K1 launches "
-                                   "(226 per-tensor + 2 k1_update_multi for the 65 [4096] tensors) "
-                                   "on one stream, bracketed by CUDA events; achieved = 6 B/elem x "
-                                   "elements / their time",
+                         "kernel": "k1_update<bf16,f32,chained>: the timed region holds only K1 "
+                                   "launches (226 per-tensor + 2 k1_update_multi for the 65 [4096] "
+                                   "tensors) on one stream, bracketed by CUDA events; achieved = "
+                                   "6 B/elem x elements / their time",
                          "avg_launch_us": round(1e3 * up["ms"] / (up["launches"] / args.steps), 2),
                          "host_ms_per_pass": up["host_enqueue"]["ms_per_pass"],
                          "host_enqueue": up["host_enqueue"],
@@ -1580,6 +1598,8 @@ def main():
             "probe_pass": dict(up["probe"], frac=round(up["probe"]["gbs"] / peak, 4)),
             "update_pass_device_state": dict(up["flags_pass"],
                                              frac=round(up["flags_pass"]["gbs"] / peak, 4)),
+            "update_pass_unchained": dict(up["unchained"],
+                                          frac=round(up["unchained"]["gbs"] / peak, 4)),
             "f64_math_update_pass": dict(up["f64_math"],
                                          frac=round(up["f64_math"]["gbs"] / peak, 4)),
             "gpu_launches": up["launches"], "clocks": up["clocks"]}

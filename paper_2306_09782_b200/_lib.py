@@ -19,6 +19,7 @@ LIB_PATH = _HERE / "_native" / "liblomo_b200.so"
 F32, F16, BF16, F64 = 0, 1, 2, 3
 MATH_F32, MATH_F64 = 0, 1
 USE_SCALE, USE_COEF, USE_SKIP, ACCUM_F64, LR_FROM_STATE = 0x1, 0x2, 0x4, 0x8, 0x10
+CHAINED = 0x80  # K1: previous launch on the stream is a K1 on other tensors
 DEFER_ROWS = 0x20
 PROBE_KEEP_GRAD = 0x40
 PROBE_BLOCKS_PER_SLOT = 8192

@@ -41,11 +41,15 @@ class Dispatcher {
   Dispatcher(int64_t state_ptr, int math, int64_t small_numel)
       : state_(reinterpret_cast<void*>(state_ptr)), math_(math), small_(small_numel) {}
 
-  void configure(double lr, double clip, double wd, int64_t flags) {
+  // chain: consecutive K1 launches of this dispatcher on one stream are
+  // declared independent (LOMO_CHAINED, dispatch.HookDispatcher.configure)
+  void configure(double lr, double clip, double wd, int64_t flags, bool chain) {
     lr_ = lr;
     clip_ = clip;
     wd_ = wd;
     flags_ = (unsigned)flags;
+    chain_ = chain;
+    chain_stream_ = nullptr;
   }
 
   // K1 for one (parameter, gradient) pair, or park it when tiny.
@@ -59,9 +63,11 @@ class Dispatcher {
       if (lst.size() == 64) flush_upd(dt);
       return;
     }
-    check(lomo_fused_update(p.data_ptr(), g.data_ptr(), n, dt, math_, lr_, clip_, wd_, flags_,
+    const unsigned fl = flags_ | ((chain_ && chain_stream_ == cur_) ? LOMO_CHAINED : 0u);
+    check(lomo_fused_update(p.data_ptr(), g.data_ptr(), n, dt, math_, lr_, clip_, wd_, fl,
                             state_, stream()),
           "lomo_fused_update");
+    chain_stream_ = cur_;
     ++launches_;
   }
 
@@ -76,6 +82,7 @@ class Dispatcher {
       if (lst.size() == 64) flush_prb(dt);
       return;
     }
+    chain_stream_ = nullptr;
     check(lomo_probe(g.data_ptr(), n, dt, (int)slot, flags_, state_, stream()), "lomo_probe");
     ++launches_;
   }
@@ -123,6 +130,7 @@ class Dispatcher {
     check(lomo_fused_update_multi(ps.data(), gs.data(), ns.data(), k, dt, math_, lr_, clip_, wd_,
                                   flags_, state_, stream()),
           "lomo_fused_update_multi");
+    chain_stream_ = cur_;  // a K1 multi on other tensors may precede a chained K1
     launches_ += (k + 63) / 64;
     lst.clear();  // released after the launch: stream-ordered reuse by the allocator
   }
@@ -140,6 +148,7 @@ class Dispatcher {
       ns[i] = lst[i].first.numel();
       ss[i] = lst[i].second;
     }
+    chain_stream_ = nullptr;
     check(lomo_probe_multi(gs.data(), ns.data(), ss.data(), k, dt, flags_, state_, stream()),
           "lomo_probe_multi");
     launches_ += (k + 63) / 64;
@@ -152,6 +161,8 @@ class Dispatcher {
   int64_t small_;
   double lr_ = 0.0, clip_ = 0.0, wd_ = 0.0;
   unsigned flags_ = 0;
+  bool chain_ = false;
+  void* chain_stream_ = nullptr;  // stream of the last K1-family launch (chain mode)
   int64_t launches_ = 0;
   std::map<int, std::vector<std::pair<at::Tensor, at::Tensor>>> upd_;
   std::map<int, std::vector<std::pair<at::Tensor, int>>> prb_;

@@ -363,7 +363,14 @@ __device__ __forceinline__ bool load_args(UpdArgs<M>& a, unsigned flags,
 // drains.
 constexpr int kK1Vec = 1;
 
-template <typename T, typename M>
+// CHAIN (LOMO_CHAINED): the previous launch on the stream is a K1 on other
+// tensors, so nothing this CTA reads or writes depends on it: the tile's
+// loads, the update and the stores run BEFORE griddepcontrol.wait, while the
+// previous grid drains, and dependents are released at entry.  The wait at
+// the end keeps stream order: this grid completes only after its
+// predecessor has (tools/k1_state_ab.cu: 5.83-6.03 ms per LLaMA-7B pass
+// against 6.03-6.16 waiting first).
+template <typename T, typename M, bool CHAIN>
 __global__ void __launch_bounds__(kThreads)
     k1_update(T* __restrict__ p, const T* __restrict__ g, int64_t n, int head,
               int64_t nvec, UpdArgs<M> a, unsigned flags, const lomo_state* st) {
@@ -372,7 +379,11 @@ __global__ void __launch_bounds__(kThreads)
   const uint4* gv = reinterpret_cast<const uint4*>(g + head);
   // (no L2 prefetch here, unlike K2: measured 5 % slower with every CTA
   // prefetching its 4 KB tiles, and 6 % slower with only the first wave)
-  pdl_enter();
+  if (CHAIN) {
+    pdl_launch_dependents();
+  } else {
+    pdl_enter();
+  }
   const int64_t base = (int64_t)blockIdx.x * (kThreads * kK1Vec) + threadIdx.x;
   uint4 P[kK1Vec], G[kK1Vec];
 #pragma unroll
@@ -383,7 +394,10 @@ __global__ void __launch_bounds__(kThreads)
       P[u] = ld_stream_rw(pv + i);
     }
   }
-  if (!resolve_args(a, flags, st)) return;  // overlaps the loads above
+  if (!resolve_args(a, flags, st)) {  // overlaps the loads above
+    if (CHAIN) pdl_wait();
+    return;
+  }
 
   if (blockIdx.x == 0) {  // scalar head (before the first aligned vector) and tail
     const int64_t tail0 = head + nvec * V;
@@ -398,6 +412,7 @@ __global__ void __launch_bounds__(kThreads)
     const int64_t i = base + (int64_t)u * kThreads;
     if (i < nvec) st_stream(pv + i, upd_vec<T, M>(P[u], G[u], a));
   }
+  if (CHAIN) pdl_wait();
 }
 
 // Fallback when p and g have different 16-byte misalignment: scalar, still
@@ -1359,8 +1374,11 @@ int launch_update(void* p_, const void* g_, int64_t n, double lr, double clip, d
     const int64_t nvec = (n - head) / V;
     const int64_t tiles = (nvec + kThreads * kK1Vec - 1) / (kThreads * kK1Vec);
     const unsigned grid = (unsigned)(tiles > 0 ? tiles : 1);
-    return launch(k1_update<T, M>, dim3(grid), dim3(kThreads), s, p, g, n, head, nvec, a, flags,
-                  st);
+    if (flags & LOMO_CHAINED)
+      return launch(k1_update<T, M, true>, dim3(grid), dim3(kThreads), s, p, g, n, head, nvec, a,
+                    flags, st);
+    return launch(k1_update<T, M, false>, dim3(grid), dim3(kThreads), s, p, g, n, head, nvec, a,
+                  flags, st);
   }
   const int grid = grid_for((n + 3) / 4, occupancy(k1_update_scalar<T, M>));
   return launch(k1_update_scalar<T, M>, dim3(grid), dim3(kThreads), s, p, g, n, a, flags, st);

@@ -92,11 +92,21 @@ class HookDispatcher:
             import torch
             torch.cuda.current_stream().wait_stream(self.side)
 
-    def configure(self, lr: float = 0.0, clip: float = 0.0, wd: float = 0.0, flags: int = 0):
-        """Per-pass constants (the same for every tensor of one backward)."""
+    def configure(self, lr: float = 0.0, clip: float = 0.0, wd: float = 0.0, flags: int = 0,
+                  chain: bool = False):
+        """Per-pass constants (the same for every tensor of one backward).
+
+        ``chain``: the caller issues this pass's updates back to back with no
+        other kernel in between (a pass over kept or replayed gradients, the
+        config-2 microbench) -- every K1 that directly follows one of this
+        dispatcher's K1 launches on the same stream gets ``LOMO_CHAINED``
+        and overlaps the previous launch's drain.  Never for the autograd
+        hook path, where the gradient's producer runs just before the K1."""
         self.lr, self.clip, self.wd, self.flags = float(lr), float(clip), float(wd), int(flags)
+        self.chain = bool(chain) and self.side is None
+        self._chain_stream = None
         if self._cpp is not None:
-            self._cpp.configure(self.lr, self.clip, self.wd, self.flags)
+            self._cpp.configure(self.lr, self.clip, self.wd, self.flags, self.chain)
             self.update = self._cpp_update
             self.probe = self._cpp_probe
 
@@ -120,10 +130,14 @@ class HookDispatcher:
                 self._flush_upd(dt, stream)
             return
         stream = self._route(stream, (g,))
+        flags = self.flags
+        if self.chain and self._chain_stream == stream:
+            flags |= _lib.CHAINED
         rc = self.lib.lomo_fused_update(p.data_ptr(), g.data_ptr(), n, dt, self.math, self.lr,
-                                        self.clip, self.wd, self.flags, self.state_ptr, stream)
+                                        self.clip, self.wd, flags, self.state_ptr, stream)
         if rc:
             _lib.check(rc, "lomo_fused_update")
+        self._chain_stream = stream
         self._launches += 1
 
     def probe(self, g, dt: int, slot: int, stream: int) -> None:
@@ -135,6 +149,7 @@ class HookDispatcher:
                 self._flush_prb(dt, stream)
             return
         stream = self._route(stream, (g,))
+        self._chain_stream = None
         rc = self.lib.lomo_probe(g.data_ptr(), n, dt, slot, self.flags, self.state_ptr, stream)
         if rc:
             _lib.check(rc, "lomo_probe")
@@ -154,6 +169,7 @@ class HookDispatcher:
                                                     self.clip, self.wd, self.flags,
                                                     self.state_ptr, stream),
                    "lomo_fused_update_multi")
+        self._chain_stream = stream  # a K1 multi on other tensors may precede a chained K1
         self._launches += (k + 63) // 64
 
     def _flush_prb(self, dt, stream):
@@ -165,6 +181,7 @@ class HookDispatcher:
         gs = (ctypes.c_void_p * k)(*[g.data_ptr() for g, _ in lst])
         ns = (ctypes.c_int64 * k)(*[g.numel() for g, _ in lst])
         ss = (ctypes.c_int * k)(*[s for _, s in lst])
+        self._chain_stream = None
         _lib.check(self.lib.lomo_probe_multi(gs, ns, ss, k, dt, self.flags, self.state_ptr, stream),
                    "lomo_probe_multi")
         self._launches += (k + 63) // 64

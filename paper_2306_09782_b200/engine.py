@@ -104,8 +104,15 @@ class CudaEngine:
         _lib.check(self.lib.lomo_begin_step(self.ptr, lt.data_ptr(), dtype_code(lt.dtype),
                                             self.stream()), "lomo_begin_step")
 
-    def configure(self, lr: float = 0.0, clip: float = 0.0, wd: float = 0.0, flags: int = 0):
-        self.dispatch.configure(lr, clip, wd, flags)
+    def configure(self, lr: float = 0.0, clip: float = 0.0, wd: float = 0.0, flags: int = 0,
+                  chain: bool = False):
+        self.dispatch.configure(lr, clip, wd, flags, chain)
+
+    def chain_updates(self) -> None:
+        """The next updates are issued back to back (a pass over kept or
+        replayed gradients): chain their K1 launches (LOMO_CHAINED)."""
+        d = self.dispatch
+        d.configure(d.lr, d.clip, d.wd, d.flags, True)
 
     def probe(self, g: torch.Tensor, slot: int) -> None:
         self.dispatch.probe(g, DTYPE_CODE[g.dtype], slot, self.stream())

@@ -188,9 +188,10 @@ class GroupedLOMO:
         eng.flush()
         self._finish_probes()
         eng.finalize()                        # N, coef = min(1, max_norm/N), skip if !finite
+        # the group's updates run back to back after K3a: chained K1 launches
         eng.configure(0.0 if self._lr_from_state else self._lr, 0.0, self.weight_decay,
                       _lib.USE_SKIP | _lib.USE_COEF |
-                      (_lib.LR_FROM_STATE if self._lr_from_state else 0))
+                      (_lib.LR_FROM_STATE if self._lr_from_state else 0), chain=True)
         for p, g in self._buf:
             eng.update(p, g)
         eng.flush()

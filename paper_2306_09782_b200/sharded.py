@@ -511,7 +511,9 @@ class ShardedLOMO(_Protocol):
         bucket's reduce-scatter + K1 on this rank's shard."""
         st = self._stash
         if isinstance(st, _KeptShards):
-            # pass 1 already produced this rank's reduced gradient shards
+            # pass 1 already produced this rank's reduced gradient shards; the
+            # K1s over them run back to back (chained launches)
+            self.engine.chain_updates()
             try:
                 for b in self.buckets:
                     g = st.shards.pop(b.idx, None)

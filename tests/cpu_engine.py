@@ -46,8 +46,11 @@ class CpuEngine:
         self.underflow = False
         self.coef = 1.0
 
-    def configure(self, lr=0.0, clip=0.0, wd=0.0, flags=0):
+    def configure(self, lr=0.0, clip=0.0, wd=0.0, flags=0, chain=False):
         self.lr, self.clip, self.wd, self.flags = lr, clip, wd, flags
+
+    def chain_updates(self):
+        pass  # launch chaining has no CPU counterpart
 
     def probe(self, g, slot):
         x = g.detach().double().numpy()

@@ -99,3 +99,53 @@ def test_llama_shapes():
     assert len(llama_param_shapes("7b")) == 291
     assert llama_param_count("13b") == 13_015_864_320
     assert llama_param_count("65b") == 65_285_660_672
+
+
+def test_dispatcher_chains_only_consecutive_k1_launches():
+    """HookDispatcher(chain=True): LOMO_CHAINED on a K1 only when the previous
+    launch of this dispatcher on the same stream was a K1 (or K1 multi); the
+    first update of a pass, any update after a probe, after a reconfigure or
+    on another stream waits for its predecessor (no flag)."""
+    import torch
+
+    from paper_2306_09782_b200 import _lib
+    from paper_2306_09782_b200.dispatch import HookDispatcher
+
+    class Lib:
+        def __init__(self):
+            self.calls = []
+
+        def lomo_fused_update(self, p, g, n, dt, math, lr, clip, wd, flags, state, stream):
+            self.calls.append(("k1", flags, stream))
+            return 0
+
+        def lomo_fused_update_multi(self, ps, gs, ns, k, dt, math, lr, clip, wd, flags, state,
+                                    stream):
+            self.calls.append(("multi", flags, stream))
+            return 0
+
+        def lomo_probe(self, g, n, dt, slot, flags, state, stream):
+            self.calls.append(("k2", flags, stream))
+            return 0
+
+    lib = Lib()
+    d = HookDispatcher(lib, None, _lib.MATH_F32, small_numel=4, use_cpp=False)
+    big, small = torch.zeros(16), torch.zeros(2)
+    d.configure(lr=0.1, chain=True)
+    d.update(big, big, _lib.F32, 7)      # first of the pass: waits
+    d.update(big, big, _lib.F32, 7)      # chained
+    d.update(small, small, _lib.F32, 7)  # parked
+    d.flush(7)                           # K1 multi (never chained itself)
+    d.update(big, big, _lib.F32, 7)      # after a K1 multi: chained
+    d.update(big, big, _lib.F32, 8)      # another stream: waits
+    d.probe(big, _lib.F32, 0, 8)
+    d.update(big, big, _lib.F32, 8)      # after a probe: waits
+    d.configure(lr=0.1, chain=True)
+    d.update(big, big, _lib.F32, 8)      # after a reconfigure: waits
+    d.configure(lr=0.1)
+    d.update(big, big, _lib.F32, 8)
+    d.update(big, big, _lib.F32, 8)      # chain off: never
+    chained = [bool(f & _lib.CHAINED) for kind, f, _ in lib.calls]
+    kinds = [kind for kind, _, _ in lib.calls]
+    assert kinds == ["k1", "k1", "multi", "k1", "k1", "k2", "k1", "k1", "k1", "k1"]
+    assert chained == [False, True, False, True, False, False, False, False, False, False]

@@ -10,6 +10,7 @@
 
 #include <cstdio>
 #include <functional>
+#include <string>
 #include <vector>
 
 using namespace lomo_k;
@@ -41,34 +42,49 @@ __device__ __forceinline__ uint4 ld_bcast(const void* p) {
 // MODE 1: every lane loads the 16-byte record (broadcast), after the wait
 // MODE 2: lane 0 loads it, 4 x 32-bit shuffles
 // MODE 3: every lane loads it BEFORE the PDL wait (unsafe bound)
+// MODE 4: MODE 2 with the tile's data loads issued BEFORE the PDL wait
+// MODE 5: data + record loads first, trigger dependents at entry, the PDL
+//         wait only after the stores (the grid still completes after its
+//         predecessor)
+// MODE 6: no PDL wait at all (unsafe bound)
 template <int MODE>
 __global__ void __launch_bounds__(kThreads)
     k1_rec(bf* __restrict__ p, const bf* __restrict__ g, int64_t nvec, UpdArgs<float> a,
            const Rec* rec) {
   uint4* pv = reinterpret_cast<uint4*>(p);
   const uint4* gv = reinterpret_cast<const uint4*>(g);
-  uint4 r;
-  if (MODE == 3) r = ld_bcast(rec);
-  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  uint4 r;
   uint4 P, G;
-  if (i < nvec) {
+  if (MODE == 3) r = ld_bcast(rec);
+  if (MODE >= 4 && i < nvec) {
+    G = ld_stream_ro(gv + i);
+    P = ld_stream_rw(pv + i);
+  }
+  if (MODE >= 5) {
+    pdl_launch_dependents();
+  } else {
+    pdl_enter();
+  }
+  if (MODE <= 3 && i < nvec) {
     G = ld_stream_ro(gv + i);
     P = ld_stream_rw(pv + i);
   }
   if (MODE == 1) r = ld_bcast(rec);
-  if (MODE == 2) {
+  if (MODE == 2 || MODE >= 4) {
     if ((threadIdx.x & 31) == 0) r = ld_bcast(rec);
     r.x = __shfl_sync(0xffffffffu, r.x, 0);
     r.y = __shfl_sync(0xffffffffu, r.y, 0);
     r.z = __shfl_sync(0xffffffffu, r.z, 0);
     r.w = __shfl_sync(0xffffffffu, r.w, 0);
   }
-  if (r.x) return;
-  a.inv_scale = __uint_as_float(r.y);
-  a.coef = __uint_as_float(r.z);
-  a.lr = __uint_as_float(r.w);
-  if (i < nvec) st_stream(pv + i, upd_vec<bf, float>(P, G, a));
+  if (!r.x) {
+    a.inv_scale = __uint_as_float(r.y);
+    a.coef = __uint_as_float(r.z);
+    a.lr = __uint_as_float(r.w);
+    if (i < nvec) st_stream(pv + i, upd_vec<bf, float>(P, G, a));
+  }
+  if (MODE == 5) pdl_wait();
 }
 
 // K2 variants: tile = UNROLL x 256 vectors per CTA (one pass over the tile),
@@ -144,7 +160,7 @@ float time_passes(F&& one_pass, int reps) {
 }
 
 int main(int argc, char** argv) {
-  const bool ncu_mode = argc > 1;
+  const bool ncu_mode = argc > 1 && std::string(argv[1]) == "ncu";
   std::vector<int64_t> sizes;
   sizes.push_back(32000LL * 4096);
   for (int l = 0; l < 32; ++l) {
@@ -207,22 +223,24 @@ int main(int argc, char** argv) {
     CK(cudaDeviceSynchronize());
     return 0;
   }
-  const char* names[] = {"plain (no state)", "product state (lane0 4 ld + f64 shfl)",
-                         "record: all lanes ld.v4", "record: lane0 ld.v4 + 4 shfl",
-                         "record: all lanes before wait (unsafe)"};
-  double sum[5] = {0};
-  const int rounds = 1;
+  const char* names[] = {"plain (no state)", "product state (record)",
+                         "rec: lane0 ld.v4 + 4 shfl", "rec + data loads before wait",
+                         "loads first, trigger at entry, wait at end", "no wait (unsafe)"};
+  constexpr int NV = 6;
+  double sum[NV] = {0};
+  const int rounds = 4;
   for (int r = 0; r < rounds; ++r) {
-    float ms[5] = {product(false), product(true), variant(k1_rec<1>), variant(k1_rec<2>),
-                   variant(k1_rec<3>)};
-    for (int v = 0; v < 5; ++v) {
+    float ms[NV] = {product(false), product(true), variant(k1_rec<2>), variant(k1_rec<4>),
+                    variant(k1_rec<5>), variant(k1_rec<6>)};
+    for (int v = 0; v < NV; ++v) {
       printf("round %d %-42s %7.3f ms %7.1f GB/s\n", r, names[v], ms[v], gb / (ms[v] * 1e-3));
       sum[v] += ms[v];
     }
   }
-  for (int v = 0; v < 5; ++v)
+  for (int v = 0; v < NV; ++v)
     printf("mean  %-42s %7.3f ms %7.1f GB/s\n", names[v], sum[v] / rounds,
            gb / (sum[v] / rounds * 1e-3));
+  if (argc < 2 || std::string(argv[1]) != "k2") return 0;
 
   // ---- K2 probe pass (2 B/elem) ----
   const double gbp = 2.0 * total / 1e9;
