@@ -26,7 +26,7 @@ P, G = bench.make_update_workload(0, 1, "bf16")
 elems = sum(p.numel() for p in P)
 s = torch.cuda.current_stream().cuda_stream
 disp = HookDispatcher(lib, None, _lib.MATH_F32)
-disp.configure(lr=0.05)
+disp.configure(lr=0.05, chain=True)  # as the bench pass
 st = torch.zeros(_lib.state_bytes(len(P)), dtype=torch.uint8, device="cuda")
 _lib.check(lib.lomo_state_init(st.data_ptr(), len(P), 1024.0, 16, 1.0, 2.0 ** 24, 1.0, 1.0, s),
            "init")
