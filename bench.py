@@ -333,13 +333,15 @@ def bench_update(args, rank, world):
     _lib.check(lib.lomo_state_init(st.data_ptr(), len(P), 1024.0, 16, 1.0, 2.0 ** 24, 1.0, 1.0,
                                    stream), "init")
     pdisp = HookDispatcher(lib, st.data_ptr(), _lib.MATH_F32)
-    pdisp.configure(flags=_lib.USE_SCALE)
+    pdisp.configure(flags=_lib.USE_SCALE, chain=True)  # K2s after the first chained
+    pdun = HookDispatcher(lib, st.data_ptr(), _lib.MATH_F32)
+    pdun.configure(flags=_lib.USE_SCALE)               # the hook pattern
 
-    def probe_pass(s=stream):
+    def probe_pass(s=stream, d=pdisp):
         lib.lomo_begin_step(st.data_ptr(), None, 0, s)
         for i in range(len(G) - 1, -1, -1):
-            pdisp.probe(G[i], dt_code, len(G) - 1 - i, s)
-        pdisp.flush(s)
+            d.probe(G[i], dt_code, len(G) - 1 - i, s)
+        d.flush(s)
         lib.lomo_finalize_norm(st.data_ptr(), s)
     for _ in range(args.warmup):
         probe_pass()
@@ -352,6 +354,12 @@ def bench_update(args, rank, world):
     host_probe_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     torch.cuda.synchronize()
     probe_ms = start.elapsed_time(end) / args.steps
+    start.record()
+    for _ in range(args.steps):
+        probe_pass(d=pdun)
+    end.record()
+    torch.cuda.synchronize()
+    probe_un_ms = start.elapsed_time(end) / args.steps
     # the same launches captured in a CUDA graph (as GraphedLOMOStep runs them):
     # removes the host launch cost, leaving the kernels' own time
     def graphed(fn):
@@ -376,9 +384,12 @@ def bench_update(args, rank, world):
     upd_graph_ms = graphed(lambda s: run_update_pass(disp, P, G, dt_code, s))
     probe = {"gbs": round(2 * elems / (probe_ms * 1e-3) / 1e9, 1), "ms_per_pass": round(probe_ms, 4),
              "graphed_gbs": round(2 * elems / (probe_graph_ms * 1e-3) / 1e9, 1),
+             "unchained_gbs": round(2 * elems / (probe_un_ms * 1e-3) / 1e9, 1),
              "host_ms_per_pass": round(host_probe_ms, 3),
              "algorithmic_bytes_per_elem": 2,
-             "what": "K2 sum-of-squares + overflow flag over every gradient, + begin/finalize (K3a)"}
+             "what": "K2 sum-of-squares + overflow flag over every gradient (back to back, "
+                     "K2s after the first chained; unchained_gbs: the hook pattern), + "
+                     "begin/finalize (K3a)"}
     # the exact-arithmetic mode (f64 math, direct rounding) on the same pass
     d64 = HookDispatcher(lib, None, _lib.MATH_F64)
     d64.configure(lr=0.05, chain=True)

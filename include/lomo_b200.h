@@ -73,15 +73,16 @@ typedef enum {
                               /* lomo_gemm_probe_finish reduces a batch of them  */
 #define LOMO_PROBE_KEEP_GRAD 0x40u /* K6: grad_out receives dW in the storage  */
                                    /* dtype (else a 16-byte scratch)           */
-#define LOMO_CHAINED 0x80u /* K1: the kernel launched just before this one on   */
-                           /* the stream is a K1 (or K1 multi) on OTHER tensors, */
+#define LOMO_CHAINED 0x80u /* K1 / K2: the kernel launched just before this one */
+                           /* on the stream is a K1 (or K1 multi) -- for K2 a K2 */
+                           /* (or K2 multi) on another slot -- on OTHER tensors, */
                            /* as in a run of updates over kept or replayed       */
-                           /* gradients; K1 then loads and stores before the PDL */
-                           /* wait and waits only at its end, overlapping the    */
-                           /* previous launch's drain.  UNSAFE when the previous */
-                           /* kernel writes this p or g (e.g. the same tensor    */
-                           /* twice in a row) or is a producer that triggers its */
-                           /* dependents before its writes complete.             */
+                           /* gradients; the kernel then loads and stores before */
+                           /* the PDL wait and waits only at its end, overlapping */
+                           /* the previous launch's drain.  UNSAFE when the      */
+                           /* previous kernel writes this p or g (e.g. the same  */
+                           /* tensor twice in a row) or is a producer that       */
+                           /* triggers its dependents before its writes complete. */
 #define LOMO_ACCUM_F64 0x8u /* K2: accumulate every square in f64 (the reference's */
                             /* float64 dot, stabilize.py:199); default for 16-bit   */
                             /* storage: exact fp32 squares summed per 16-byte      */

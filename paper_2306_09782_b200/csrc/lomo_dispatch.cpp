@@ -49,6 +49,7 @@ class Dispatcher {
     wd_ = wd;
     flags_ = (unsigned)flags;
     chain_ = chain;
+    chain_kind_ = 0;
     chain_stream_ = nullptr;
   }
 
@@ -63,11 +64,10 @@ class Dispatcher {
       if (lst.size() == 64) flush_upd(dt);
       return;
     }
-    const unsigned fl = flags_ | ((chain_ && chain_stream_ == cur_) ? LOMO_CHAINED : 0u);
-    check(lomo_fused_update(p.data_ptr(), g.data_ptr(), n, dt, math_, lr_, clip_, wd_, fl,
-                            state_, stream()),
+    check(lomo_fused_update(p.data_ptr(), g.data_ptr(), n, dt, math_, lr_, clip_, wd_,
+                            flags_ | chained('u'), state_, stream()),
           "lomo_fused_update");
-    chain_stream_ = cur_;
+    mark('u');
     ++launches_;
   }
 
@@ -82,8 +82,9 @@ class Dispatcher {
       if (lst.size() == 64) flush_prb(dt);
       return;
     }
-    chain_stream_ = nullptr;
-    check(lomo_probe(g.data_ptr(), n, dt, (int)slot, flags_, state_, stream()), "lomo_probe");
+    check(lomo_probe(g.data_ptr(), n, dt, (int)slot, flags_ | chained('p'), state_, stream()),
+          "lomo_probe");
+    mark('p');
     ++launches_;
   }
 
@@ -114,6 +115,16 @@ class Dispatcher {
   // the raw cudaStream_t the caller passed (the hook's stream)
   void* stream() const { return cur_; }
 
+  // LOMO_CHAINED when this dispatcher's previous launch on this stream was of
+  // the same family ('u': K1 / K1 multi, 'p': K2 / K2 multi)
+  unsigned chained(char kind) const {
+    return (chain_ && chain_kind_ == kind && chain_stream_ == cur_) ? LOMO_CHAINED : 0u;
+  }
+  void mark(char kind) {
+    chain_kind_ = kind;
+    chain_stream_ = cur_;
+  }
+
   void flush_upd(int dt) {
     auto it = upd_.find(dt);
     if (it == upd_.end() || it->second.empty()) return;
@@ -130,7 +141,7 @@ class Dispatcher {
     check(lomo_fused_update_multi(ps.data(), gs.data(), ns.data(), k, dt, math_, lr_, clip_, wd_,
                                   flags_, state_, stream()),
           "lomo_fused_update_multi");
-    chain_stream_ = cur_;  // a K1 multi on other tensors may precede a chained K1
+    mark('u');  // a K1 multi on other tensors may precede a chained K1
     launches_ += (k + 63) / 64;
     lst.clear();  // released after the launch: stream-ordered reuse by the allocator
   }
@@ -148,9 +159,9 @@ class Dispatcher {
       ns[i] = lst[i].first.numel();
       ss[i] = lst[i].second;
     }
-    chain_stream_ = nullptr;
     check(lomo_probe_multi(gs.data(), ns.data(), ss.data(), k, dt, flags_, state_, stream()),
           "lomo_probe_multi");
+    mark('p');
     launches_ += (k + 63) / 64;
     lst.clear();
   }
@@ -162,7 +173,8 @@ class Dispatcher {
   double lr_ = 0.0, clip_ = 0.0, wd_ = 0.0;
   unsigned flags_ = 0;
   bool chain_ = false;
-  void* chain_stream_ = nullptr;  // stream of the last K1-family launch (chain mode)
+  char chain_kind_ = 0;           // family and stream of the last launch (chain mode)
+  void* chain_stream_ = nullptr;
   int64_t launches_ = 0;
   std::map<int, std::vector<std::pair<at::Tensor, at::Tensor>>> upd_;
   std::map<int, std::vector<std::pair<at::Tensor, int>>> prb_;

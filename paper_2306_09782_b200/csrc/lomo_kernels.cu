@@ -731,7 +731,10 @@ __device__ __forceinline__ double k2_tile(const uint4* __restrict__ gv, int64_t 
   return acc;
 }
 
-template <typename T, typename M>
+// CHAIN (LOMO_CHAINED): the previous launch is a K2 on another gradient and
+// slot, so the CTA runs entirely before griddepcontrol.wait (its tile's loads
+// need no L2 prefetch) and waits at its end, as chained K1 does.
+template <typename T, typename M, bool CHAIN>
 __global__ void __launch_bounds__(kThreads, 6)
     k2_probe(const T* __restrict__ g, int64_t n, int head, int64_t nvec, int64_t per_cta,
              int slot, unsigned flags, void* state) {
@@ -739,10 +742,14 @@ __global__ void __launch_bounds__(kThreads, 6)
   const int64_t beg = (int64_t)blockIdx.x * per_cta;
   const int64_t end = min(beg + per_cta, nvec);
   const uint4* gv = reinterpret_cast<const uint4*>(g + head);
-  if (threadIdx.x == 0 && end > beg)  // this CTA's tile into L2 while the previous grid drains
-    prefetch_l2(gv + beg, (uint32_t)((end - beg) * 16));
-  pdl_wait();
-  pdl_launch_dependents();
+  if (CHAIN) {
+    pdl_launch_dependents();
+  } else {
+    if (threadIdx.x == 0 && end > beg)  // this CTA's tile into L2 while the previous grid drains
+      prefetch_l2(gv + beg, (uint32_t)((end - beg) * 16));
+    pdl_wait();
+    pdl_launch_dependents();
+  }
   lomo_state* st = hdr(state);
   // 1/scale and nslots for the CTA's partial, loaded now (after the wait: an
   // earlier step's K3 may have changed the scale) and consumed at the end, so
@@ -801,6 +808,7 @@ __global__ void __launch_bounds__(kThreads, 6)
     if (flags & LOMO_USE_SCALE) bsum *= sc * sc;  // exact: a power of two
     put_partial(st, slot, bsum, (int)gridDim.x, nslots);
   }
+  if (CHAIN) pdl_wait();
 }
 
 // Multi-tensor probe: one CTA per (small) tensor, which writes its slot
@@ -1446,7 +1454,10 @@ int launch_probe(const void* g_, int64_t n, int slot, unsigned flags, void* stat
   if (per_cta < tile) per_cta = tile;
   int64_t grid = (nvec + per_cta - 1) / per_cta;
   if (grid < 1) grid = 1;
-  return launch(k2_probe<T, M>, dim3((unsigned)grid), dim3(kThreads), s, g, n, head, nvec,
+  if (flags & LOMO_CHAINED)
+    return launch(k2_probe<T, M, true>, dim3((unsigned)grid), dim3(kThreads), s, g, n, head, nvec,
+                  per_cta, slot, flags, state);
+  return launch(k2_probe<T, M, false>, dim3((unsigned)grid), dim3(kThreads), s, g, n, head, nvec,
                 per_cta, slot, flags, state);
 }
 

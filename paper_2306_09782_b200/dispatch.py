@@ -99,12 +99,13 @@ class HookDispatcher:
         ``chain``: the caller issues this pass's updates back to back with no
         other kernel in between (a pass over kept or replayed gradients, the
         config-2 microbench) -- every K1 that directly follows one of this
-        dispatcher's K1 launches on the same stream gets ``LOMO_CHAINED``
-        and overlaps the previous launch's drain.  Never for the autograd
+        dispatcher's K1 launches on the same stream (every K2 that directly
+        follows one of its K2 launches) gets ``LOMO_CHAINED`` and overlaps
+        the previous launch's drain.  Never for the autograd
         hook path, where the gradient's producer runs just before the K1."""
         self.lr, self.clip, self.wd, self.flags = float(lr), float(clip), float(wd), int(flags)
         self.chain = bool(chain) and self.side is None
-        self._chain_stream = None
+        self._chain = None  # (family, stream) of the last launch: "u" K1, "p" K2
         if self._cpp is not None:
             self._cpp.configure(self.lr, self.clip, self.wd, self.flags, self.chain)
             self.update = self._cpp_update
@@ -130,14 +131,12 @@ class HookDispatcher:
                 self._flush_upd(dt, stream)
             return
         stream = self._route(stream, (g,))
-        flags = self.flags
-        if self.chain and self._chain_stream == stream:
-            flags |= _lib.CHAINED
+        flags = self.flags | (_lib.CHAINED if self.chain and self._chain == ("u", stream) else 0)
         rc = self.lib.lomo_fused_update(p.data_ptr(), g.data_ptr(), n, dt, self.math, self.lr,
                                         self.clip, self.wd, flags, self.state_ptr, stream)
         if rc:
             _lib.check(rc, "lomo_fused_update")
-        self._chain_stream = stream
+        self._chain = ("u", stream)
         self._launches += 1
 
     def probe(self, g, dt: int, slot: int, stream: int) -> None:
@@ -149,8 +148,9 @@ class HookDispatcher:
                 self._flush_prb(dt, stream)
             return
         stream = self._route(stream, (g,))
-        self._chain_stream = None
-        rc = self.lib.lomo_probe(g.data_ptr(), n, dt, slot, self.flags, self.state_ptr, stream)
+        flags = self.flags | (_lib.CHAINED if self.chain and self._chain == ("p", stream) else 0)
+        rc = self.lib.lomo_probe(g.data_ptr(), n, dt, slot, flags, self.state_ptr, stream)
+        self._chain = ("p", stream)
         if rc:
             _lib.check(rc, "lomo_probe")
         self._launches += 1
@@ -169,7 +169,7 @@ class HookDispatcher:
                                                     self.clip, self.wd, self.flags,
                                                     self.state_ptr, stream),
                    "lomo_fused_update_multi")
-        self._chain_stream = stream  # a K1 multi on other tensors may precede a chained K1
+        self._chain = ("u", stream)  # a K1 multi on other tensors may precede a chained K1
         self._launches += (k + 63) // 64
 
     def _flush_prb(self, dt, stream):
@@ -181,9 +181,9 @@ class HookDispatcher:
         gs = (ctypes.c_void_p * k)(*[g.data_ptr() for g, _ in lst])
         ns = (ctypes.c_int64 * k)(*[g.numel() for g, _ in lst])
         ss = (ctypes.c_int * k)(*[s for _, s in lst])
-        self._chain_stream = None
         _lib.check(self.lib.lomo_probe_multi(gs, ns, ss, k, dt, self.flags, self.state_ptr, stream),
                    "lomo_probe_multi")
+        self._chain = ("p", stream)
         self._launches += (k + 63) // 64
 
     def flush(self, stream: int) -> None:

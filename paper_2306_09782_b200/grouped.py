@@ -181,7 +181,7 @@ class GroupedLOMO:
         if not self._buf:
             return
         eng = self.engine
-        eng.configure(flags=self._probe_flags)
+        eng.configure(flags=self._probe_flags, chain=True)  # the group's K2s back to back
         for p, g in self._buf:
             if id(p) not in self._probed:
                 eng.probe(g, self._slot[id(p)])

@@ -629,3 +629,37 @@ def test_chained_k1_pass_equals_unchained(use_cpp, state_flags):
     torch.cuda.synchronize()
     for k, (a, b) in enumerate(zip(P, Q)):
         assert torch.equal(a, b), k
+
+
+@pytest.mark.parametrize("use_cpp", [True, False])
+def test_chained_k2_pass_equals_unchained(use_cpp):
+    """Chained K2 launches (LOMO_CHAINED) give the same per-slot partials,
+    sums and overflow decision as waiting ones, over 40 ragged gradients."""
+    from paper_2306_09782_b200.dispatch import HookDispatcher
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    sizes = [(1 << 20) + 13 * k for k in range(30)] + [3000 + k for k in range(8)] + [5, 7]
+    G = [torch.empty(n, dtype=torch.bfloat16, device="cuda").normal_(0, 1e-2, generator=gen) * 64
+         for n in sizes]
+    res = []
+    for chain in (False, True, True):
+        st = U.State(len(G), scale=64.0, max_norm=1.0)
+        d = HookDispatcher(U.lib(), st.ptr, _lib.MATH_F32, small_numel=4096, use_cpp=use_cpp)
+        d.configure(flags=_lib.USE_SCALE, chain=chain)
+        st.begin()
+        for k, g in enumerate(G):
+            d.probe(g, _lib.BF16, k, U.stream())
+        d.flush(U.stream())
+        st.finalize()
+        h = st.status()
+        res.append((st.slots(len(G)).tolist(), h.total_norm, h.overflow, h.skip))
+    assert res[0] == res[1] == res[2]
+    G[17][5] = float("nan")
+    st = U.State(len(G), scale=64.0, max_norm=1.0)
+    d = HookDispatcher(U.lib(), st.ptr, _lib.MATH_F32, small_numel=4096, use_cpp=use_cpp)
+    d.configure(flags=_lib.USE_SCALE, chain=True)
+    st.begin()
+    for k, g in enumerate(G):
+        d.probe(g, _lib.BF16, k, U.stream())
+    d.flush(U.stream())
+    st.finalize()
+    assert st.status().overflow == 1 and st.status().skip == 1

@@ -102,10 +102,11 @@ def test_llama_shapes():
 
 
 def test_dispatcher_chains_only_consecutive_k1_launches():
-    """HookDispatcher(chain=True): LOMO_CHAINED on a K1 only when the previous
-    launch of this dispatcher on the same stream was a K1 (or K1 multi); the
-    first update of a pass, any update after a probe, after a reconfigure or
-    on another stream waits for its predecessor (no flag)."""
+    """HookDispatcher(chain=True): LOMO_CHAINED on a K1 (K2) only when the
+    previous launch of this dispatcher on the same stream was a K1 or K1
+    multi (a K2 or K2 multi); the first launch of a pass, any launch after
+    one of the other family, after a reconfigure or on another stream waits
+    for its predecessor (no flag)."""
     import torch
 
     from paper_2306_09782_b200 import _lib
@@ -138,7 +139,8 @@ def test_dispatcher_chains_only_consecutive_k1_launches():
     d.flush(7)                           # K1 multi (never chained itself)
     d.update(big, big, _lib.F32, 7)      # after a K1 multi: chained
     d.update(big, big, _lib.F32, 8)      # another stream: waits
-    d.probe(big, _lib.F32, 0, 8)
+    d.probe(big, _lib.F32, 0, 8)         # after a K1: waits
+    d.probe(big, _lib.F32, 1, 8)         # after a K2: chained
     d.update(big, big, _lib.F32, 8)      # after a probe: waits
     d.configure(lr=0.1, chain=True)
     d.update(big, big, _lib.F32, 8)      # after a reconfigure: waits
@@ -147,5 +149,5 @@ def test_dispatcher_chains_only_consecutive_k1_launches():
     d.update(big, big, _lib.F32, 8)      # chain off: never
     chained = [bool(f & _lib.CHAINED) for kind, f, _ in lib.calls]
     kinds = [kind for kind, _, _ in lib.calls]
-    assert kinds == ["k1", "k1", "multi", "k1", "k1", "k2", "k1", "k1", "k1", "k1"]
-    assert chained == [False, True, False, True, False, False, False, False, False, False]
+    assert kinds == ["k1", "k1", "multi", "k1", "k1", "k2", "k2", "k1", "k1", "k1", "k1"]
+    assert chained == [False, True, False, True, False, False, True, False, False, False, False]
