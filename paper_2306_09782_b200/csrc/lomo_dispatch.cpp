@@ -186,7 +186,8 @@ PYBIND11_MODULE(TORCH_EXTENSION_NAME, m) {
   m.doc() = "C++ hook dispatcher for the LOMO C-ABI (K1/K2 launches)";
   pybind11::class_<Dispatcher>(m, "Dispatcher")
       .def(pybind11::init<int64_t, int, int64_t>())
-      .def("configure", &Dispatcher::configure)
+      .def("configure", &Dispatcher::configure, pybind11::arg("lr"), pybind11::arg("clip"),
+           pybind11::arg("wd"), pybind11::arg("flags"), pybind11::arg("chain") = false)
       .def("update", &Dispatcher::update)
       .def("probe", &Dispatcher::probe)
       .def("flush", &Dispatcher::flush)
