@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define LOMO_ABI_VERSION 1
+#define LOMO_ABI_VERSION 2 /* 2: the pass-2 record at offset 128 moved sumsq[] to 160; LOMO_CHAINED */
 
 /* storage dtype of p and g (reference: Precision, tensor.py:19-21;
  * FULL == float64 storage, HALF_EMULATED == binary16; bf16 is new). */

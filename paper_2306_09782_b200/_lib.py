@@ -30,7 +30,7 @@ PEER_SIGNAL_BYTES = 8 * PEER_CHANNELS * PEER_MAX
 STATE_ERRORS = {1: "a probe kernel was given a norm slot outside [0, nslots) (LOMO_E_SLOT)",
                 2: "a peer barrier timed out: a rank did not reach the same collective point "
                    "(sharded fused_rs mode)"}
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # every symbol the header declares (checked by tests/test_native_abi.py)
 EXPORTS = (
