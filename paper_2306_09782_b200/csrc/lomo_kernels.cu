@@ -930,28 +930,32 @@ __global__ void __launch_bounds__(kThreads) k6_rows_multi(const __grid_constant_
 // reduced gradient is never written to HBM.  Requires 16-byte aligned slices
 // (ShardedLOMO pads buckets to 8*world elements).
 constexpr int kMaxPeers = 16;
+// Peers are read in chunks of kPeerChunk: a chunk's loads are all in flight
+// before its adds, and only one chunk is live in registers.  A fully
+// unrolled 16-peer array held 64 registers of loads (92 / 138 registers per
+// thread for update / probe, 2 / 1 CTAs per SM); tools/k4_local.py.
+constexpr int kPeerChunk = 4;
 
-template <typename T>
-__device__ __forceinline__ void peer_load_vec(const T* const* __restrict__ peers, int world,
-                                              int64_t idx, uint4 (&buf)[kMaxPeers]) {
-#pragma unroll
-  for (int r = 0; r < kMaxPeers; ++r)  // all loads in flight before the adds
-    if (r < world) buf[r] = ld_stream_ro(reinterpret_cast<const uint4*>(peers[r]) + idx);
-}
-
+// acc[k] = sum over ranks r = 0..world-1, in rank order, of peer r's vector idx
 template <typename T, typename M>
-__device__ __forceinline__ void peer_add_vec(const uint4 (&buf)[kMaxPeers], int world,
-                                             M (&acc)[16 / sizeof(T)]) {
+__device__ __forceinline__ void peer_sum_vec(const T* const* __restrict__ peers, int world,
+                                             int64_t idx, M (&acc)[16 / sizeof(T)]) {
   constexpr int V = 16 / sizeof(T);
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = (M)0;
+  for (int r0 = 0; r0 < world; r0 += kPeerChunk) {
+    uint4 buf[kPeerChunk];
 #pragma unroll
-  for (int r = 0; r < kMaxPeers; ++r) {
-    if (r < world) {
-      Vec16<T> G;
-      G.u = buf[r];
+    for (int j = 0; j < kPeerChunk; ++j)  // the chunk's loads in flight before the adds
+      if (r0 + j < world) buf[j] = ld_stream_ro(reinterpret_cast<const uint4*>(peers[r0 + j]) + idx);
 #pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] += to_m<M>(G.e[k]);
+    for (int j = 0; j < kPeerChunk; ++j) {
+      if (r0 + j < world) {
+        Vec16<T> G;
+        G.u = buf[j];
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] += to_m<M>(G.e[k]);
+      }
     }
   }
 }
@@ -968,43 +972,47 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (i >= nvec) return;
-  uint4 buf[kMaxPeers];
-  peer_load_vec<T>(peers, world, i, buf);
   uint4* pv = reinterpret_cast<uint4*>(p);
   Vec16<T> P, O;
-  P.u = ld_stream_rw(pv + i);
-  if (!resolve_args(a, flags, st)) return;  // overlaps the loads above
+  P.u = ld_stream_rw(pv + i);  // in flight with the first chunk of peer loads
   M g[V];
-  peer_add_vec<T, M>(buf, world, g);
+  peer_sum_vec<T, M>(peers, world, i, g);
+  if (!resolve_args(a, flags, st)) return;
 #pragma unroll
   for (int k = 0; k < V; ++k) O.e[k] = from_m<T, M>(upd_elem(to_m<M>(P.e[k]), g[k], a));
   st_stream(pv + i, O.u);
 }
 
+// The peer table is written once when the ring is set up (never by a kernel
+// of the step), so it is read before the PDL wait; each peer's slice of the
+// CTA's tile is bulk-prefetched into L2 while the previous grid drains (as
+// K2 does).
 template <typename T, typename M>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 5)
     k4_rs_probe(const T* const* __restrict__ peers_dev, int world, int64_t off, int64_t nvec,
                 int64_t per_cta, int slot, unsigned flags, void* state) {
   constexpr int V = 16 / sizeof(T);
   __shared__ double sm[kThreads / 32];
   __shared__ const T* peers[kMaxPeers];
+  const int64_t beg = (int64_t)blockIdx.x * per_cta;
+  const int64_t end = min(beg + per_cta, nvec);
+  if (threadIdx.x < kMaxPeers) {
+    const T* q = threadIdx.x < world ? peers_dev[threadIdx.x] + off : nullptr;
+    peers[threadIdx.x] = q;
+    if (q != nullptr && end > beg)
+      prefetch_l2(reinterpret_cast<const uint4*>(q) + beg, (uint32_t)((end - beg) * 16));
+  }
   pdl_wait();
   pdl_launch_dependents();
   lomo_state* st = hdr(state);
-  if (threadIdx.x < kMaxPeers)
-    peers[threadIdx.x] = threadIdx.x < world ? peers_dev[threadIdx.x] + off : nullptr;
   __syncthreads();
   const bool use_scale = (flags & LOMO_USE_SCALE) != 0;
   const M inv_scale = use_scale ? (M)st->inv_scale : (M)1;
   double acc = 0.0;
   bool bad = false;
-  const int64_t beg = (int64_t)blockIdx.x * per_cta;
-  const int64_t end = min(beg + per_cta, nvec);
   for (int64_t i = beg + threadIdx.x; i < end; i += kThreads) {
-    uint4 buf[kMaxPeers];
-    peer_load_vec<T>(peers, world, i, buf);
     M g[V];
-    peer_add_vec<T, M>(buf, world, g);
+    peer_sum_vec<T, M>(peers, world, i, g);
     M part = 0;
 #pragma unroll
     for (int k = 0; k < V; ++k) {
@@ -1015,8 +1023,8 @@ __global__ void __launch_bounds__(kThreads)
     }
     acc += (double)part;
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
-  const double bsum = block_sum(acc, sm);
+  if (bad) st->overflow = 1;  // any thread (all store 1)
+  const double bsum = block_sum_once(acc, sm);
   if (threadIdx.x == 0) {
     put_partial(st, slot, bsum, (int)gridDim.x);
   }
