@@ -455,6 +455,72 @@ def bench_update(args, rank, world):
             "kernel_ms_per_step": ksum_ms / args.steps, "shapes": shapes}
 
 
+def bench_k4_local(args, world_sim: int = 8):
+    """K4 (reduce-scatter fused with the update / probe) on this one GPU with
+    simulated peers: rank 0 of ``world_sim`` ranks, its slice of every
+    LLaMA-7B bucket read from ``world_sim`` distinct local buffers (at N > 1
+    they are the peers' buffers over NVLink).  The kernel's HBM roofline:
+    (2W + 4) B/elem for the update, 2W for the probe (tools/k4_local.py)."""
+    import ctypes
+
+    import torch
+    from paper_2306_09782_b200 import _lib
+    lib = _lib.load()
+    W = world_sim
+    sizes, _ = _buckets_7b(W)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    shards, keep, tabs = [], [], []
+    for n in sizes:
+        S = n // W
+        shards.append(torch.empty(S, dtype=torch.bfloat16, device="cuda").uniform_(
+            -0.08, 0.08, generator=gen))
+        bufs = [torch.empty(S, dtype=torch.bfloat16, device="cuda").normal_(0, 1e-3, generator=gen)
+                for _ in range(W)]
+        keep.append(bufs)
+        tabs.append(torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda"))
+    elems = sum(x.numel() for x in shards)
+    st = torch.zeros(_lib.state_bytes(len(sizes)), dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.lomo_state_init(st.data_ptr(), len(sizes), 0.0, 16, 1.0, 2.0 ** 24, 0.0, 1.0,
+                                   s), "init")
+
+    def upd():
+        for k in range(len(shards) - 1, -1, -1):
+            _lib.check(lib.lomo_fused_rs_update(
+                shards[k].data_ptr(), ctypes.c_void_p(tabs[k].data_ptr()), W, 0,
+                shards[k].numel(), _lib.BF16, _lib.MATH_F32, 0.05, 0.0, 0.0, 0, None, s),
+                "rs_update")
+
+    def prb():
+        lib.lomo_begin_step(st.data_ptr(), None, 0, s)
+        for k in range(len(shards) - 1, -1, -1):
+            _lib.check(lib.lomo_fused_rs_probe(ctypes.c_void_p(tabs[k].data_ptr()), W, 0,
+                                               shards[k].numel(), _lib.BF16, k, 0,
+                                               st.data_ptr(), s), "rs_probe")
+
+    peak, _ = _peaks()
+    out = {"world_simulated": W, "buckets": len(sizes), "shard_elements": elems,
+           "what": "rank 0's K4 over its 1/W slice of every LLaMA-7B bucket, the W peer "
+                   "buffers local (HBM in place of NVLink): the kernel's own roofline"}
+    for name, fn, bpe in (("update", upd, 2 * W + 4), ("probe", prb, 2 * W)):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        gbs = bpe * elems / (ms * 1e-3) / 1e9
+        out[name] = {"ms_per_pass": round(ms, 4), "gbs": round(gbs, 1),
+                     "algorithmic_bytes_per_elem": bpe, "frac": round(gbs / peak, 4)}
+    del keep, tabs, shards
+    torch.cuda.empty_cache()
+    return out
+
+
 def _buckets_7b(world: int, layers: int = 32):
     """ShardedLOMO's buckets of LLaMA-7B: one per decoder layer (its 9
     tensors) plus the embedding / final norm / head, each padded to a multiple
@@ -1638,6 +1704,7 @@ def main():
     e2e = None if args.no_e2e else optional(bench_e2e if world == 1 else bench_e2e_sharded,
                                             args, rank, world)
     c1 = optional(bench_c1, args) if (world == 1 and not args.no_c1) else None
+    k4l = optional(bench_k4_local, args) if world == 1 else None
     train = None
     if not args.no_train:
         train = optional(bench_train, args, rank, world) if (world == 1 and not
@@ -1662,6 +1729,8 @@ def main():
         }
         line.update(head)
         line.update({"e2e": e2e, "cpu_baseline": cb, "c1_parity": c1, "train": train})
+        if k4l is not None:
+            line["k4_simulated_peers"] = k4l
         if sharded1 is not None:
             line["train_sharded_world1"] = sharded1
         print(json.dumps(line), flush=True)
