@@ -1150,7 +1150,8 @@ def bench_train_sharded(args, rank, world):
     opt = ShardedLOMO(model, lr=1e-3, clip_grad_norm=1.0,
                       loss_scale=LossScaler(2.0 ** 10, growth_interval=16),
                       reshard_after_forward=reshard,
-                      replay=not args.sharded_strict and not keep, keep_grads=keep)
+                      replay=not args.sharded_strict and not keep, keep_grads=keep,
+                      fused_rs=args.sharded_fused_rs or False)
     torch.cuda.empty_cache()
     seq, batch = args.seq, args.batch
     gen = torch.Generator(device="cuda").manual_seed(rank)
@@ -1179,6 +1180,7 @@ def bench_train_sharded(args, rank, world):
     graphed = None
     import torch.distributed as dist
     if not reshard and not args.sharded_strict and not args.no_sharded_graph and \
+            not args.sharded_fused_rs and \
             dist.get_backend() == "nccl":  # (not the gloo LOMO_BENCH_SHARE_GPU dry run)
         graphed = _graphed_sharded(args, opt, model, data, world)
     out = {"model": f"llama-{size} (random init), fp16, parameters sharded over {world} GPUs "
@@ -1189,6 +1191,7 @@ def bench_train_sharded(args, rank, world):
            "ms_per_step": round(ms, 2), "seq_len": seq, "batch_per_rank": batch,
            "activation_checkpointing": ckpt, "passes_per_step": 2, "outcomes": outcomes,
            "reshard_after_forward": reshard, "clocks": clk.summary(),
+           "reduction": f"K4 over {opt.transport}" if opt.fused_rs else "NCCL reduce_scatter",
            "tensor_roofline": _sharded_roofline(model, batch, seq, ms, keep,
                                                 args.sharded_strict, ckpt, clk.summary()),
            "pass2": "second forward + backward" if args.sharded_strict else
@@ -1574,6 +1577,9 @@ def main():
                     help="run the ZeRO-3 sharded train leg even at N=1 (world-1 NCCL group)")
     ap.add_argument("--no-sharded-world1", dest="sharded_world1", action="store_false",
                     help="skip the N=1 run of the sharded train leg (world-1 NCCL group)")
+    ap.add_argument("--sharded-fused-rs", default="", choices=["", "auto", "ipc", "nvls"],
+                    help="sharded train leg: K4 over peer memory instead of the NCCL "
+                         "reduce-scatter (with kept shards: the K4 probe keeps the reduced slice)")
     ap.add_argument("--no-sharded-graph", action="store_true",
                     help="sharded train leg: skip the GraphedShardedStep timing")
     ap.add_argument("--sharded-strict", action="store_true",

@@ -215,6 +215,15 @@ int lomo_fused_rs_update(void* p_shard, const void* const* peer_bufs_dev, int wo
 int lomo_fused_rs_probe(const void* const* peer_bufs_dev, int world, int64_t offset,
                         int64_t n, int dtype, int slot, unsigned flags, void* state,
                         void* stream);
+/* K4 probe that also KEEPS the reduced slice: `out` (n elements of `dtype`,
+ * 16-byte aligned) receives the rank-ordered sum rounded to the storage dtype
+ * -- what a reduce-scatter would have written -- and the squares are taken of
+ * those rounded values.  Pass 2 then updates from `out` with K1 (ShardedLOMO
+ * keep_grads over K4: no second reduction).  probe_hook stabilize.py:193-200
+ * on the reduced gradient. */
+int lomo_fused_rs_probe_keep(const void* const* peer_bufs_dev, int world, int64_t offset,
+                             int64_t n, int dtype, int slot, unsigned flags, void* state,
+                             void* out, void* stream);
 /* NVLS form of K4: `mc` is this rank's slice [offset, offset+n) of the bucket
  * at a MULTICAST address (lomo_mc_bind); every 16-byte vector is fetched with
  * multimem.ld_reduce.add (the NVSwitch sums the `world` copies in flight, fp32
@@ -227,6 +236,10 @@ int lomo_fused_mc_update(void* p_shard, const void* mc, int64_t n, int dtype, in
                          const void* state, void* stream);
 int lomo_fused_mc_probe(const void* mc, int64_t n, int dtype, int slot, unsigned flags,
                         void* state, void* stream);
+/* NVLS form of lomo_fused_rs_probe_keep: `out` receives the switch's sum
+ * (already rounded to the storage dtype by multimem.ld_reduce). */
+int lomo_fused_mc_probe_keep(const void* mc, int64_t n, int dtype, int slot, unsigned flags,
+                             void* state, void* out, void* stream);
 
 /* ---- peer memory for K4 (transport; one process per GPU) --------------- */
 /* The reduce-over-peers kernels need the ranks' bucket buffers mapped into

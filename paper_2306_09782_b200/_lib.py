@@ -64,6 +64,8 @@ EXPORTS = (
     "lomo_fused_update_rows",
     "lomo_fused_mc_update",
     "lomo_fused_mc_probe",
+    "lomo_fused_rs_probe_keep",
+    "lomo_fused_mc_probe_keep",
     "lomo_ipc_handle_bytes",
     "lomo_ipc_alloc",
     "lomo_ipc_open",
@@ -176,6 +178,8 @@ _SIGS = {
     "lomo_gemm_probe_finish": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
     "lomo_fused_mc_update": (_i32, [_vp, _vp, _i64, _i32, _i32, _dbl, _dbl, _dbl, _u32, _vp, _vp]),
     "lomo_fused_mc_probe": (_i32, [_vp, _i64, _i32, _i32, _u32, _vp, _vp]),
+    "lomo_fused_rs_probe_keep": (_i32, [_vp, _i32, _i64, _i64, _i32, _i32, _u32, _vp, _vp, _vp]),
+    "lomo_fused_mc_probe_keep": (_i32, [_vp, _i64, _i32, _i32, _u32, _vp, _vp, _vp]),
     "lomo_ipc_handle_bytes": (ctypes.c_size_t, []),
     "lomo_ipc_alloc": (_i32, [ctypes.c_size_t, ctypes.POINTER(_vp), _vp]),
     "lomo_ipc_open": (_i32, [_vp, ctypes.POINTER(_vp)]),

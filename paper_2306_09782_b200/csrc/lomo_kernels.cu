@@ -987,10 +987,14 @@ __global__ void __launch_bounds__(kThreads)
 // of the step), so it is read before the PDL wait; each peer's slice of the
 // CTA's tile is bulk-prefetched into L2 while the previous grid drains (as
 // K2 does).
-template <typename T, typename M>
+// KEEP (lomo_fused_rs_probe_keep): the reduced slice, rounded to the storage
+// dtype as a reduce-scatter output is, is also written to `out` and the
+// squares are taken of those rounded values -- the gradient pass 2 then
+// applies (ShardedLOMO keep_grads over K4).
+template <typename T, typename M, bool KEEP>
 __global__ void __launch_bounds__(kThreads, 5)
     k4_rs_probe(const T* const* __restrict__ peers_dev, int world, int64_t off, int64_t nvec,
-                int64_t per_cta, int slot, unsigned flags, void* state) {
+                int64_t per_cta, int slot, unsigned flags, void* state, T* __restrict__ out) {
   constexpr int V = 16 / sizeof(T);
   __shared__ double sm[kThreads / 32];
   __shared__ const T* peers[kMaxPeers];
@@ -1013,6 +1017,15 @@ __global__ void __launch_bounds__(kThreads, 5)
   for (int64_t i = beg + threadIdx.x; i < end; i += kThreads) {
     M g[V];
     peer_sum_vec<T, M>(peers, world, i, g);
+    if (KEEP) {
+      Vec16<T> O;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        O.e[k] = from_m<T, M>(g[k]);
+        g[k] = to_m<M>(O.e[k]);
+      }
+      reinterpret_cast<uint4*>(out)[i] = O.u;
+    }
     M part = 0;
 #pragma unroll
     for (int k = 0; k < V; ++k) {
@@ -1071,7 +1084,7 @@ __global__ void __launch_bounds__(kThreads)
 template <typename T, typename M>
 __global__ void __launch_bounds__(kThreads)
     k4_mc_probe(const T* __restrict__ mc, int64_t nvec, int64_t per_cta, int slot,
-                unsigned flags, void* state) {
+                unsigned flags, void* state, T* __restrict__ out) {
   __shared__ double sm[kThreads / 32];
   pdl_wait();
   pdl_launch_dependents();
@@ -1083,8 +1096,11 @@ __global__ void __launch_bounds__(kThreads)
   const int64_t beg = (int64_t)blockIdx.x * per_cta;
   const int64_t end = min(beg + per_cta, nvec);
   const uint4* gv = reinterpret_cast<const uint4*>(mc);
-  for (int64_t i = beg + threadIdx.x; i < end; i += kThreads)
-    acc += vec_sumsq<T, M>(mc_ld_reduce<T>(gv + i), inv_scale, use_scale, bad);
+  for (int64_t i = beg + threadIdx.x; i < end; i += kThreads) {
+    const uint4 r = mc_ld_reduce<T>(gv + i);  // the switch's sum, rounded to T
+    if (out != nullptr) reinterpret_cast<uint4*>(out)[i] = r;  // keep: the reduced slice
+    acc += vec_sumsq<T, M>(r, inv_scale, use_scale, bad);
+  }
   if (__syncthreads_or(bad) && threadIdx.x == 0) st->overflow = 1;
   const double bsum = block_sum(acc, sm);
   if (threadIdx.x == 0) {
@@ -1486,7 +1502,7 @@ int launch_rs_update(void* p, const void* const* peers, int world, int64_t off, 
 
 template <typename T, typename M>
 int launch_rs_probe(const void* const* peers, int world, int64_t off, int64_t n, int slot,
-                    unsigned flags, void* state, cudaStream_t s) {
+                    unsigned flags, void* state, cudaStream_t s, void* out = nullptr) {
   constexpr int V = 16 / sizeof(T);
   if (n % V != 0 || (off * (int64_t)sizeof(T)) % 16 != 0) return LOMO_E_ARG;
   const int64_t nvec = n / V;
@@ -1495,9 +1511,15 @@ int launch_rs_probe(const void* const* peers, int world, int64_t off, int64_t n,
   if (per_cta < 4 * kThreads) per_cta = 4 * kThreads;
   int64_t grid = (nvec + per_cta - 1) / per_cta;
   if (grid < 1) grid = 1;
-  return launch(k4_rs_probe<T, M>, dim3((unsigned)grid), dim3(kThreads), s,
+  if (out != nullptr) {
+    if (((uintptr_t)out & 15) != 0) return LOMO_E_ARG;
+    return launch(k4_rs_probe<T, M, true>, dim3((unsigned)grid), dim3(kThreads), s,
+                  reinterpret_cast<const T* const*>(peers), world, off, nvec, per_cta, slot, flags,
+                  state, static_cast<T*>(out));
+  }
+  return launch(k4_rs_probe<T, M, false>, dim3((unsigned)grid), dim3(kThreads), s,
                 reinterpret_cast<const T* const*>(peers), world, off, nvec, per_cta, slot, flags,
-                state);
+                state, static_cast<T*>(nullptr));
 }
 
 template <typename T, typename M>
@@ -1514,9 +1536,9 @@ int launch_mc_update(void* p, const void* mc, int64_t n, double lr, double clip,
 
 template <typename T, typename M>
 int launch_mc_probe(const void* mc, int64_t n, int slot, unsigned flags, void* state,
-                    cudaStream_t s) {
+                    cudaStream_t s, void* out = nullptr) {
   constexpr int V = 16 / sizeof(T);
-  if (n % V != 0 || ((uintptr_t)mc & 15) != 0) return LOMO_E_ARG;
+  if (n % V != 0 || ((uintptr_t)mc & 15) != 0 || ((uintptr_t)out & 15) != 0) return LOMO_E_ARG;
   const int64_t nvec = n / V;
   int64_t per_cta = (nvec + LOMO_PROBE_BLOCKS_PER_SLOT - 1) / LOMO_PROBE_BLOCKS_PER_SLOT;
   per_cta = (per_cta + kThreads - 1) / kThreads * kThreads;
@@ -1524,7 +1546,7 @@ int launch_mc_probe(const void* mc, int64_t n, int slot, unsigned flags, void* s
   int64_t grid = (nvec + per_cta - 1) / per_cta;
   if (grid < 1) grid = 1;
   return launch(k4_mc_probe<T, M>, dim3((unsigned)grid), dim3(kThreads), s,
-                static_cast<const T*>(mc), nvec, per_cta, slot, flags, state);
+                static_cast<const T*>(mc), nvec, per_cta, slot, flags, state, static_cast<T*>(out));
 }
 
 }  // namespace lomo_k
@@ -1763,25 +1785,36 @@ int lomo_fused_rs_update(void* p_shard, const void* const* peer_bufs_dev, int wo
   return LOMO_E_ARG;
 }
 
-int lomo_fused_rs_probe(const void* const* peer_bufs_dev, int world, int64_t offset, int64_t n,
-                        int dtype, int slot, unsigned flags, void* state, void* stream) {
+static int rs_probe_impl(const void* const* peers, int world, int64_t offset, int64_t n, int dtype,
+                         int slot, unsigned flags, void* state, void* out, void* stream) {
   if (state == nullptr || n < 0 || offset < 0 || world < 1 || world > kMaxPeers) return LOMO_E_ARG;
   if (slot < 0) return LOMO_E_SLOT;
   if (n == 0) return 0;
-  if (peer_bufs_dev == nullptr) return LOMO_E_ARG;
+  if (peers == nullptr) return LOMO_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const bool f64 = (flags & LOMO_ACCUM_F64) != 0;
+#define LOMO_RSP(T, M) launch_rs_probe<T, M>(peers, world, offset, n, slot, flags, state, s, out)
   switch (dtype) {
-    case LOMO_F16:
-      return f64 ? launch_rs_probe<__half, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s)
-                 : launch_rs_probe<__half, float>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
-    case LOMO_BF16:
-      return f64 ? launch_rs_probe<__nv_bfloat16, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s)
-                 : launch_rs_probe<__nv_bfloat16, float>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
-    case LOMO_F32: return launch_rs_probe<float, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
-    case LOMO_F64: return launch_rs_probe<double, double>(peer_bufs_dev, world, offset, n, slot, flags, state, s);
+    case LOMO_F16: return f64 ? LOMO_RSP(__half, double) : LOMO_RSP(__half, float);
+    case LOMO_BF16: return f64 ? LOMO_RSP(__nv_bfloat16, double) : LOMO_RSP(__nv_bfloat16, float);
+    case LOMO_F32: return LOMO_RSP(float, double);
+    case LOMO_F64: return LOMO_RSP(double, double);
   }
+#undef LOMO_RSP
   return LOMO_E_ARG;
+}
+
+int lomo_fused_rs_probe(const void* const* peer_bufs_dev, int world, int64_t offset, int64_t n,
+                        int dtype, int slot, unsigned flags, void* state, void* stream) {
+  return rs_probe_impl(peer_bufs_dev, world, offset, n, dtype, slot, flags, state, nullptr,
+                       stream);
+}
+
+int lomo_fused_rs_probe_keep(const void* const* peer_bufs_dev, int world, int64_t offset,
+                             int64_t n, int dtype, int slot, unsigned flags, void* state,
+                             void* out, void* stream) {
+  if (out == nullptr && n > 0) return LOMO_E_ARG;
+  return rs_probe_impl(peer_bufs_dev, world, offset, n, dtype, slot, flags, state, out, stream);
 }
 
 int lomo_fused_mc_update(void* p_shard, const void* mc, int64_t n, int dtype, int math, double lr,
@@ -1807,24 +1840,33 @@ int lomo_fused_mc_update(void* p_shard, const void* mc, int64_t n, int dtype, in
   return LOMO_E_ARG;  // f64 storage: no multimem f64 vector reduction; use the IPC form
 }
 
-int lomo_fused_mc_probe(const void* mc, int64_t n, int dtype, int slot, unsigned flags,
-                        void* state, void* stream) {
+static int mc_probe_impl(const void* mc, int64_t n, int dtype, int slot, unsigned flags,
+                         void* state, void* out, void* stream) {
   if (state == nullptr || n < 0) return LOMO_E_ARG;
   if (slot < 0) return LOMO_E_SLOT;
   if (n == 0) return 0;
   if (mc == nullptr) return LOMO_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   const bool f64 = (flags & LOMO_ACCUM_F64) != 0;
+#define LOMO_MCP(T, M) launch_mc_probe<T, M>(mc, n, slot, flags, state, s, out)
   switch (dtype) {
-    case LOMO_F16:
-      return f64 ? launch_mc_probe<__half, double>(mc, n, slot, flags, state, s)
-                 : launch_mc_probe<__half, float>(mc, n, slot, flags, state, s);
-    case LOMO_BF16:
-      return f64 ? launch_mc_probe<__nv_bfloat16, double>(mc, n, slot, flags, state, s)
-                 : launch_mc_probe<__nv_bfloat16, float>(mc, n, slot, flags, state, s);
-    case LOMO_F32: return launch_mc_probe<float, double>(mc, n, slot, flags, state, s);
+    case LOMO_F16: return f64 ? LOMO_MCP(__half, double) : LOMO_MCP(__half, float);
+    case LOMO_BF16: return f64 ? LOMO_MCP(__nv_bfloat16, double) : LOMO_MCP(__nv_bfloat16, float);
+    case LOMO_F32: return LOMO_MCP(float, double);
   }
+#undef LOMO_MCP
   return LOMO_E_ARG;
+}
+
+int lomo_fused_mc_probe(const void* mc, int64_t n, int dtype, int slot, unsigned flags,
+                        void* state, void* stream) {
+  return mc_probe_impl(mc, n, dtype, slot, flags, state, nullptr, stream);
+}
+
+int lomo_fused_mc_probe_keep(const void* mc, int64_t n, int dtype, int slot, unsigned flags,
+                             void* state, void* out, void* stream) {
+  if (out == nullptr && n > 0) return LOMO_E_ARG;
+  return mc_probe_impl(mc, n, dtype, slot, flags, state, out, stream);
 }
 
 int lomo_probe_rows(const float* partials_dev, int64_t rows, int64_t ld, int64_t cols, int slot,

@@ -131,8 +131,14 @@ class CudaEngine:
             self.math, d.lr, d.clip, d.wd, d.flags, self.ptr, self.stream()), "lomo_fused_rs_update")
 
     def rs_probe(self, peers_dev: int, world: int, offset: int, n: int, dtype: torch.dtype,
-                 slot: int) -> None:
+                 slot: int, out: torch.Tensor | None = None) -> None:
+        """K4 probe; ``out``: also keep the reduced slice (lomo_fused_rs_probe_keep)."""
         d = self.dispatch
+        if out is not None:
+            _lib.check(self.lib.lomo_fused_rs_probe_keep(
+                peers_dev, world, offset, n, DTYPE_CODE[dtype], slot, d.flags, self.ptr,
+                out.data_ptr(), self.stream()), "lomo_fused_rs_probe_keep")
+            return
         _lib.check(self.lib.lomo_fused_rs_probe(peers_dev, world, offset, n, DTYPE_CODE[dtype],
                                                 slot, d.flags, self.ptr, self.stream()),
                    "lomo_fused_rs_probe")
@@ -144,8 +150,14 @@ class CudaEngine:
             p_shard.data_ptr(), mc, p_shard.numel(), DTYPE_CODE[p_shard.dtype], self.math, d.lr,
             d.clip, d.wd, d.flags, self.ptr, self.stream()), "lomo_fused_mc_update")
 
-    def mc_probe(self, mc: int, n: int, dtype: torch.dtype, slot: int) -> None:
+    def mc_probe(self, mc: int, n: int, dtype: torch.dtype, slot: int,
+                 out: torch.Tensor | None = None) -> None:
         d = self.dispatch
+        if out is not None:
+            _lib.check(self.lib.lomo_fused_mc_probe_keep(mc, n, DTYPE_CODE[dtype], slot, d.flags,
+                                                         self.ptr, out.data_ptr(), self.stream()),
+                       "lomo_fused_mc_probe_keep")
+            return
         _lib.check(self.lib.lomo_fused_mc_probe(mc, n, DTYPE_CODE[dtype], slot, d.flags, self.ptr,
                                                 self.stream()), "lomo_fused_mc_probe")
 

@@ -234,12 +234,14 @@ class PeerRing:
         else:
             engine.mc_update(p_shard, self.mc_base + k * self.buf_bytes + offset * self.esize)
 
-    def probe(self, engine, k: int, offset: int, n: int, slot: int) -> None:
+    def probe(self, engine, k: int, offset: int, n: int, slot: int, out=None) -> None:
+        """K4 probe of this rank's slice; ``out``: also keep the reduced slice."""
         if self.transport == "ipc":
-            engine.rs_probe(self.peers_dev[k].data_ptr(), self.world, offset, n, self.dtype, slot)
+            engine.rs_probe(self.peers_dev[k].data_ptr(), self.world, offset, n, self.dtype, slot,
+                            out=out)
         else:
             engine.mc_probe(self.mc_base + k * self.buf_bytes + offset * self.esize, n,
-                            self.dtype, slot)
+                            self.dtype, slot, out=out)
 
     # ----------------------------------------------------------------- close
     def close(self) -> None:

@@ -214,7 +214,8 @@ class ShardedLOMO(_Protocol):
             HBM holds them) -- pass 2 is K1 over the kept shards, with no
             gradient recompute and no second reduce-scatter.  The update is
             the same as the strict protocol's (pass 1's reduced gradient IS
-            pass 2's).  Not with ``fused_rs`` (K4 never materialises a shard).
+            pass 2's).  With ``fused_rs`` the K4 probe writes the reduced
+            slice as it sums it (``lomo_fused_rs_probe_keep``).
     """
 
     _always_scale = True  # inv_scale carries the 1/world of the data-parallel mean
@@ -233,9 +234,8 @@ class ShardedLOMO(_Protocol):
             clip_grad_norm, clip_grad_value, loss_scale)
         self._init_protocol(st, lr, weight_decay)
         # option checks before the parameters are moved into buckets
-        if keep_grads and (fused_rs or replay):
-            raise ConfigError("keep_grads replaces replay and needs the NCCL reduce-scatter "
-                              "(not fused_rs)")
+        if keep_grads and replay:
+            raise ConfigError("keep_grads replaces replay (pass 2 updates from the kept shards)")
         if keep_grads and self.passes != 2:
             raise ConfigError("keep_grads replaces the second pass: it needs clip_grad_norm "
                               "or loss_scale")
@@ -437,7 +437,14 @@ class ShardedLOMO(_Protocol):
             ring = self._rings[b.dtype]
             ring.filled(b.ring_k)  # every rank has written this bucket
             if self._mode == _PROBE:
-                ring.probe(self.engine, b.ring_k, self.rank * b.S, b.S, b.idx)
+                if isinstance(self._stash, _KeptShards):
+                    # keep_grads over K4: the probe also writes the reduced
+                    # slice (rounded to storage), pass 2's K1 input
+                    gshard = torch.empty(b.S, dtype=b.dtype, device=b.device)
+                    ring.probe(self.engine, b.ring_k, self.rank * b.S, b.S, b.idx, out=gshard)
+                    self._stash.shards[b.idx] = gshard
+                else:
+                    ring.probe(self.engine, b.ring_k, self.rank * b.S, b.S, b.idx)
             else:
                 ring.update(self.engine, b.shard, b.ring_k, self.rank * b.S)
                 b.dirty = True

@@ -554,6 +554,42 @@ def test_k4_fused_reduce_update_matches_oracle(prec, math_mode, world):
     assert abs(got - want_sq) <= (1e-12 if math_mode == "f64" else 1e-6) * want_sq
 
 
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("world", [1, 3, 8])
+def test_k4_probe_keep_writes_the_reduced_slice(prec, world):
+    """lomo_fused_rs_probe_keep: `out` = the rank-ordered sum of the peers'
+    slices (f64 with ACCUM_F64) rounded to the storage dtype (what a
+    reduce-scatter writes), and the slot's sum of squares is taken of those rounded values
+    (f64 accumulation: 1e-12); a NaN in one peer raises the overflow flag."""
+    rng = np.random.default_rng(40 + world)
+    S = 8 * 1500
+    total = S * world
+    dt = U.TORCH_DT[prec]
+    bufs0 = [O.round_to(rng.normal(0, 1e-2, total), prec) for _ in range(world)]
+    bufs = [U.to_dev(b, dt) for b in bufs0]
+    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    off = (world // 2) * S
+    out = torch.empty(S, dtype=dt, device="cuda")
+    st = U.State(2)
+    st.begin()
+    _lib.check(U.lib().lomo_fused_rs_probe_keep(peers.data_ptr(), world, off, S, U.CODE[dt], 1,
+                                                _lib.ACCUM_F64, st.ptr, out.data_ptr(),
+                                                U.stream()), "rs_probe_keep")
+    acc = np.zeros(S)
+    for b in bufs0:  # ACCUM_F64: f64 accumulation in rank order
+        acc = acc + b[off:off + S]
+    want = O.round_to(acc, prec)
+    assert np.array_equal(out.double().cpu().numpy(), want)
+    sq = float(np.dot(want, want))
+    assert abs(st.slots(2)[1] - sq) <= 1e-12 * sq
+    assert st.status().overflow == 0
+    bufs[-1][off + 17] = float("nan")
+    st.begin()
+    _lib.check(U.lib().lomo_fused_rs_probe_keep(peers.data_ptr(), world, off, S, U.CODE[dt], 0,
+                                                0, st.ptr, out.data_ptr(), U.stream()), "keep")
+    assert st.status().overflow == 1
+
+
 def test_k4_rejects_misaligned_slices():
     b = torch.zeros(64, dtype=torch.bfloat16, device="cuda")
     peers = torch.tensor([b.data_ptr()], dtype=torch.int64, device="cuda")

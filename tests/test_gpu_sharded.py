@@ -96,20 +96,22 @@ def _need_nvls(transport):
 
 
 @pytest.mark.parametrize("transport", ["ipc", "nvls"])
-@pytest.mark.parametrize("two_pass", [False, True])
+@pytest.mark.parametrize("two_pass", [False, True, "keep"])
 def test_fused_rs_world1_equals_nccl_path(nccl_world, two_pass, transport):
     """K4 over peer buffers (world 1: the only peer is this GPU) gives the
     same parameters as NCCL reduce_scatter + K1/K2 -- over a CUDA-IPC
     allocation, and over an NVLS multicast object (multimem.ld_reduce of one
-    copy is the copy)."""
+    copy is the copy); "keep": keep_grads on both, the K4 probe writing the
+    reduced slice pass 2 updates from."""
     from paper_2306_09782_b200.sharded import ShardedLOMO
     from paper_2306_09782_b200.workloads import Llama
     _need_nvls(transport)
     a = Llama(CFG, dtype=torch.bfloat16, device="cuda", seed=0)
     b = Llama(CFG, dtype=torch.bfloat16, device="cuda", seed=0)
     kw = dict(clip_grad_norm=0.5, loss_scale=2.0 ** 8) if two_pass else {}
-    oa = ShardedLOMO(a, lr=0.05, **kw)
-    ob = ShardedLOMO(b, lr=0.05, fused_rs=transport, **kw)
+    keep = two_pass == "keep"
+    oa = ShardedLOMO(a, lr=0.05, keep_grads=keep, **kw)
+    ob = ShardedLOMO(b, lr=0.05, fused_rs=transport, keep_grads=keep, **kw)
     assert ob.transport == transport
     g = torch.Generator(device="cuda").manual_seed(5)
     for step in range(3):

@@ -35,7 +35,7 @@ def _batch(step, world):
 
 
 def _worker(rank, world, port, mode, q):
-    fused_rs = "ipc" if mode == "fused_rs" else False
+    fused_rs = "ipc" if mode.startswith("fused_rs") else False
     try:
         import torch.distributed as dist
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -47,7 +47,7 @@ def _worker(rank, world, port, mode, q):
         model = Llama(CFG, dtype=torch.float64, device="cuda", seed=rank)  # rank 0 broadcast
         opt = ShardedLOMO(model, lr=0.05, clip_grad_norm=0.5, loss_scale=2.0 ** 8, math="f64",
                           fused_rs=fused_rs, replay=mode == "replay",
-                          keep_grads=mode == "keep_grads")
+                          keep_grads=mode.endswith("keep_grads"))
         outs = []
         for step in range(3):
             ids, tgt = _batch(step, world)
@@ -81,7 +81,8 @@ def _reference(world):
     return {n: p.detach().cpu().numpy() for n, p in model.named_parameters()}
 
 
-@pytest.mark.parametrize("mode", ["nccl_path", "fused_rs", "replay", "keep_grads"])
+@pytest.mark.parametrize("mode", ["nccl_path", "fused_rs", "replay", "keep_grads",
+                                  "fused_rs_keep_grads"])
 def test_sharded_two_ranks_real_kernels(mode):
     if not torch.cuda.is_available():
         pytest.skip("needs CUDA")
