@@ -498,11 +498,22 @@ def bench_k4_local(args, world_sim: int = 8):
                                                shards[k].numel(), _lib.BF16, k, 0,
                                                st.data_ptr(), s), "rs_probe")
 
+    kept = torch.empty(max(x.numel() for x in shards), dtype=torch.bfloat16, device="cuda")
+
+    def prb_keep():
+        lib.lomo_begin_step(st.data_ptr(), None, 0, s)
+        for k in range(len(shards) - 1, -1, -1):
+            _lib.check(lib.lomo_fused_rs_probe_keep(ctypes.c_void_p(tabs[k].data_ptr()), W, 0,
+                                                    shards[k].numel(), _lib.BF16, k, 0,
+                                                    st.data_ptr(), kept.data_ptr(), s),
+                       "rs_probe_keep")
+
     peak, _ = _peaks()
     out = {"world_simulated": W, "buckets": len(sizes), "shard_elements": elems,
            "what": "rank 0's K4 over its 1/W slice of every LLaMA-7B bucket, the W peer "
                    "buffers local (HBM in place of NVLink): the kernel's own roofline"}
-    for name, fn, bpe in (("update", upd, 2 * W + 4), ("probe", prb, 2 * W)):
+    for name, fn, bpe in (("update", upd, 2 * W + 4), ("probe", prb, 2 * W),
+                          ("probe_keep", prb_keep, 2 * W + 2)):
         for _ in range(3):
             fn()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -516,7 +527,7 @@ def bench_k4_local(args, world_sim: int = 8):
         gbs = bpe * elems / (ms * 1e-3) / 1e9
         out[name] = {"ms_per_pass": round(ms, 4), "gbs": round(gbs, 1),
                      "algorithmic_bytes_per_elem": bpe, "frac": round(gbs / peak, 4)}
-    del keep, tabs, shards
+    del keep, tabs, shards, kept
     torch.cuda.empty_cache()
     return out
 

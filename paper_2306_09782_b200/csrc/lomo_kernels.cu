@@ -1508,7 +1508,7 @@ int launch_rs_probe(const void* const* peers, int world, int64_t off, int64_t n,
   const int64_t nvec = n / V;
   int64_t per_cta = (nvec + LOMO_PROBE_BLOCKS_PER_SLOT - 1) / LOMO_PROBE_BLOCKS_PER_SLOT;
   per_cta = (per_cta + kThreads - 1) / kThreads * kThreads;
-  if (per_cta < 4 * kThreads) per_cta = 4 * kThreads;
+  if (per_cta < kThreads) per_cta = kThreads;  // one vector per thread where the slot allows (tools/k4_local.py)
   int64_t grid = (nvec + per_cta - 1) / per_cta;
   if (grid < 1) grid = 1;
   if (out != nullptr) {
