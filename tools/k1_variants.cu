@@ -227,7 +227,9 @@ __global__ void __launch_bounds__(256, 5) v_k2(const bf* __restrict__ g, int64_t
     const int64_t b0 = (int64_t)blockIdx.x * per_cta;
     const int64_t nt = min(per_cta, nvec - b0);
     if (nt > 0) prefetch_l2(reinterpret_cast<const uint4*>(g + head) + b0, (uint32_t)(nt * 16));
-    nsl = nslots_early(state);
+    // (the round-1 product read nslots before the wait with ld.global.nc;
+    // the round-2 kernel loads it after the wait)
+    asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(nsl) : "l"(&hdr(state)->nslots));
   }
   pdl_wait();
   pdl_launch_dependents();
