@@ -1190,8 +1190,11 @@ def bench_train_sharded(args, rank, world):
     eager_peak = torch.cuda.max_memory_allocated()
     graphed = None
     import torch.distributed as dist
+    # the graphed form: at world 1 by default; at N > 1 only with --sharded-graph
+    # (multi-rank NCCL capture has not run on a multi-GPU box yet, and a hung
+    # capture would cost the whole line)
     if not reshard and not args.sharded_strict and not args.no_sharded_graph and \
-            not args.sharded_fused_rs and \
+            not args.sharded_fused_rs and (world == 1 or args.sharded_graph) and \
             dist.get_backend() == "nccl":  # (not the gloo LOMO_BENCH_SHARE_GPU dry run)
         graphed = _graphed_sharded(args, opt, model, data, world)
     out = {"model": f"llama-{size} (random init), fp16, parameters sharded over {world} GPUs "
@@ -1591,6 +1594,8 @@ def main():
     ap.add_argument("--sharded-fused-rs", default="", choices=["", "auto", "ipc", "nvls"],
                     help="sharded train leg: K4 over peer memory instead of the NCCL "
                          "reduce-scatter (with kept shards: the K4 probe keeps the reduced slice)")
+    ap.add_argument("--sharded-graph", action="store_true",
+                    help="N>1: also time the GraphedShardedStep form of the sharded train leg")
     ap.add_argument("--no-sharded-graph", action="store_true",
                     help="sharded train leg: skip the GraphedShardedStep timing")
     ap.add_argument("--sharded-strict", action="store_true",
