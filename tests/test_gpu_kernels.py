@@ -296,7 +296,8 @@ def test_k3_scaler_replay_matches_reference_fixture():
     seqs = json.loads((GOLDEN / "scaler_replay.json").read_text())
     inf = torch.tensor(float("inf"), device="cuda")
     zero = torch.tensor(0.5, device="cuda")
-    for s in seqs[:120]:
+    assert len(seqs) == 300
+    for s in seqs:  # every recorded replay
         st = U.State(1, scale=2.0 ** 6, growth=s["growth"], min_scale=1.0, max_scale=2.0 ** 10)
         trace = []
         for ok in s["outcomes"]:
