@@ -1,7 +1,10 @@
 """K1 inside the LLaMA-7B grouped training step vs K1 in the isolated update
 pass: event-timed K1 sections, plus nvidia-smi clocks/power under load.
 
-    python tools/k1_in_train.py
+    python tools/k1_in_train.py [--unchained]
+
+The instrumented flush mirrors GroupedLOMO._flush (chained K2s, K3a, chained
+K1s); --unchained times every launch waiting for its predecessor.
 """
 import subprocess
 import sys
@@ -15,6 +18,7 @@ import torch  # noqa: E402
 from paper_2306_09782_b200 import GroupedLOMO  # noqa: E402
 from paper_2306_09782_b200.workloads import Llama  # noqa: E402
 
+CHAIN = "--unchained" not in sys.argv
 torch.cuda.set_device(0)
 model = Llama("7b", dtype=torch.float16, device="cuda")
 opt = GroupedLOMO(model, lr=1e-3, max_norm=1.0, window=1)
@@ -35,14 +39,14 @@ def flush_timed():
         return
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     eng.begin(None)
-    eng.configure(flags=opt._probe_flags)
+    eng.configure(flags=opt._probe_flags, chain=CHAIN)
     e[0].record()
     for p, g in opt._buf:
         eng.probe(g, opt._slot[id(p)])
     eng.flush()
     e[1].record()
     eng.finalize()
-    eng.configure(opt._lr, 0.0, opt.weight_decay, _lib.USE_SKIP | _lib.USE_COEF)
+    eng.configure(opt._lr, 0.0, opt.weight_decay, _lib.USE_SKIP | _lib.USE_COEF, chain=CHAIN)
     e[2].record()
     n = 0
     for p, g in opt._buf:
