@@ -1457,11 +1457,12 @@ def bench_c1(args):
 
 
 def _import_reference():
-    """The reference package itself: baseline/_ref (pip-installed from
-    /root/reference, travels to the GPU box) or the read-only source tree.
-    Returns (fusedtrain modules, where) or (None, why)."""
+    """The reference package itself: baseline/_ref (pip-installed from a copy
+    of /root/reference/pkg; git-ignored, travels to the GPU box).  The bench
+    never reads /root/reference at run time.  Returns (fusedtrain modules,
+    where) or (None, why)."""
     import importlib
-    for where in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+    for where in (ROOT / "baseline" / "_ref",):
         if (where / "fusedtrain" / "optim.py").exists():
             if str(where) not in sys.path:
                 sys.path.insert(0, str(where))
