@@ -154,6 +154,63 @@ def test_f32_math_full_llama7b(work):
     assert worst <= 1, worst
 
 
+def test_fp16_two_pass_full_llama7b():
+    """Config 3's storage dtype at config 2's size: fp16 parameters and
+    gradients scaled by 2^10 (pass 1 sees the scaled gradient), f32 math:
+    every slot within 2e-6 of its float64 sum, the clip coefficient from the
+    device norm, and sampled elements <= 1 ulp from the oracle's
+    update_hook."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 * 2 ** 30:
+        pytest.skip("needs 40 GiB of free device memory")
+    gen = torch.Generator(device="cuda").manual_seed(12)
+    shapes = [math.prod(s) for _, s in llama_param_shapes("7b")]
+    P = [torch.empty(n, dtype=torch.float16, device="cuda").uniform_(-0.08, 0.08, generator=gen)
+         for n in shapes]
+    G = [(torch.empty(n, dtype=torch.float32, device="cuda").normal_(0.0, 1e-3, generator=gen)
+          * SCALE).half() for n in shapes]
+    rng = np.random.default_rng(1)
+    idx = [torch.from_numpy(np.unique(np.concatenate([[0, n - 1], rng.integers(0, n, NSAMP)]))
+                            ).cuda() for n in shapes]
+    lib = U.lib()
+    st = U.State(len(P), scale=SCALE, max_norm=MAX_NORM)
+    d = HookDispatcher(lib, st.ptr, _lib.MATH_F32)
+    d.configure(flags=_lib.USE_SCALE)
+    st.begin()
+    for i in range(len(G) - 1, -1, -1):
+        d.probe(G[i], _lib.F16, len(G) - 1 - i, U.stream())
+    d.flush(U.stream())
+    st.finalize()
+    h = st.status()
+    assert not h.skip
+    got = st.slots(len(P))
+    for s, i in enumerate(range(len(G) - 1, -1, -1)):
+        want = _sq64(G[i])
+        assert abs(got[s] - want) <= 2e-6 * want, (s, got[s], want)
+    p0 = [P[i][idx[i]].double().cpu().numpy() for i in range(len(P))]
+    g0 = [G[i][idx[i]].double().cpu().numpy() for i in range(len(P))]
+    _lib.check(lib.lomo_set_lr(st.ptr, LR, U.stream()), "lr")
+    _update_pass_dt(lib, st, P, G, _lib.F16)
+    for i in range(len(P)):
+        want_p = O.update_hook(p0[i], g0[i], LR, SCALE, None, h.clip_coef, "half")
+        dd = U.ulp_diff(P[i][idx[i]], U.to_dev(want_p, torch.float16))
+        assert int(dd.max()) <= 1, (i, int(dd.max()))
+    del P, G
+    torch.cuda.empty_cache()
+
+
+def _update_pass_dt(lib, st, P, G, dt):
+    d = HookDispatcher(lib, st.ptr, _lib.MATH_F32)
+    d.configure(flags=_lib.USE_SKIP | _lib.USE_SCALE | _lib.USE_COEF | _lib.LR_FROM_STATE,
+                chain=True)
+    for i in range(len(P) - 1, -1, -1):
+        d.update(P[i], G[i], dt, U.stream())
+    d.flush(U.stream())
+    torch.cuda.synchronize()
+
+
 def test_overflow_skip_full_llama7b(work):
     P, G, _ = work
     lib = U.lib()

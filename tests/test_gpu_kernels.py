@@ -635,9 +635,11 @@ def test_k1_k2_beyond_2_31_elements():
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("dtype,math_mode", [(torch.bfloat16, "f32"), (torch.float16, "f32"),
+                                             (torch.float32, "f32"), (torch.float16, "f64")])
 @pytest.mark.parametrize("use_cpp", [True, False])
 @pytest.mark.parametrize("state_flags", [False, True])
-def test_chained_k1_pass_equals_unchained(use_cpp, state_flags):
+def test_chained_k1_pass_equals_unchained(use_cpp, state_flags, dtype, math_mode):
     """LOMO_CHAINED (loads and stores before the PDL wait, the wait at the
     end) over a pass of 40 independent tensors -- ragged sizes, one
     misaligned pair (scalar fallback), small parked ones -- gives the same
@@ -645,23 +647,23 @@ def test_chained_k1_pass_equals_unchained(use_cpp, state_flags):
     from paper_2306_09782_b200.dispatch import HookDispatcher
     gen = torch.Generator(device="cuda").manual_seed(9)
     sizes = [(1 << 20) + 13 * k for k in range(30)] + [3000 + k for k in range(8)] + [5, 7]
-    P = [torch.empty(n, dtype=torch.bfloat16, device="cuda").uniform_(-0.08, 0.08, generator=gen)
+    P = [torch.empty(n, dtype=dtype, device="cuda").uniform_(-0.08, 0.08, generator=gen)
          for n in sizes]
-    G = [torch.empty(n, dtype=torch.bfloat16, device="cuda").normal_(0, 1e-2, generator=gen)
+    G = [torch.empty(n, dtype=dtype, device="cuda").normal_(0, 1e-2, generator=gen)
          for n in sizes]
-    G[3] = torch.cat([torch.zeros(1, dtype=torch.bfloat16, device="cuda"), G[3]])[1:]  # misaligned
+    G[3] = torch.cat([torch.zeros(1, dtype=dtype, device="cuda"), G[3]])[1:]  # misaligned
     Q = [p.clone() for p in P]
     st = U.State(1, scale=4.0, max_norm=1.0)
     st.write_header(clip_coef=0.5, lr=0.05)
     flags = (_lib.USE_SKIP | _lib.USE_SCALE | _lib.USE_COEF | _lib.LR_FROM_STATE
              if state_flags else 0)
     for chain, T in ((False, P), (True, Q)):
-        d = HookDispatcher(U.lib(), st.ptr if state_flags else None, _lib.MATH_F32,
+        d = HookDispatcher(U.lib(), st.ptr if state_flags else None, U.MATH[math_mode],
                            small_numel=4096, use_cpp=use_cpp)
         d.configure(lr=0.0 if state_flags else 0.05, flags=flags, chain=chain)
         for _ in range(3):  # three passes back to back
             for p, g in zip(T, G):
-                d.update(p, g, _lib.BF16, U.stream())
+                d.update(p, g, U.CODE[dtype], U.stream())
             d.flush(U.stream())
     torch.cuda.synchronize()
     for k, (a, b) in enumerate(zip(P, Q)):
