@@ -1194,7 +1194,7 @@ def bench_train_sharded(args, rank, world):
     # (multi-rank NCCL capture has not run on a multi-GPU box yet, and a hung
     # capture would cost the whole line)
     if not reshard and not args.sharded_strict and not args.no_sharded_graph and \
-            not args.sharded_fused_rs and (world == 1 or args.sharded_graph) and \
+            (world == 1 or args.sharded_graph) and \
             dist.get_backend() == "nccl":  # (not the gloo LOMO_BENCH_SHARE_GPU dry run)
         graphed = _graphed_sharded(args, opt, model, data, world)
     out = {"model": f"llama-{size} (random init), fp16, parameters sharded over {world} GPUs "

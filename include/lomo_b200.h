@@ -291,6 +291,15 @@ int lomo_mc_bind(uint64_t obj, int device, void** uc_ptr, void** mc_ptr);
 int lomo_mc_free(uint64_t obj);
 int lomo_mc_barrier(void* sig_mc, const void* sig_uc, int world, int channel, uint64_t epoch,
                     int64_t timeout_ns, int* err_dev, void* stream);
+/* The same barriers with the epoch kept on the device: `epochs_dev` holds one
+ * uint64 counter per channel (zero-initialised, this rank's own memory); the
+ * barrier uses counter+1 and stores it back.  Every rank issues the same
+ * sequence, so the counters agree -- and a CUDA graph that captured the
+ * barrier advances them on every replay (GraphedShardedStep with K4). */
+int lomo_peer_barrier_dev(void* const* sig_dev, uint64_t* epochs_dev, int world, int rank,
+                          int channel, int64_t timeout_ns, int* err_dev, void* stream);
+int lomo_mc_barrier_dev(void* sig_mc, const void* sig_uc, uint64_t* epochs_dev, int world,
+                        int channel, int64_t timeout_ns, int* err_dev, void* stream);
 
 /* ---- row-sparse embedding gradient (K1 on the rows a batch touched) ---- */
 /* The reference's embedding VJP scatters dy into a dense [V, h] gradient;

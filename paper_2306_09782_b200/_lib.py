@@ -72,6 +72,7 @@ EXPORTS = (
     "lomo_ipc_close",
     "lomo_ipc_free",
     "lomo_peer_barrier",
+    "lomo_peer_barrier_dev",
     "lomo_mc_supported",
     "lomo_mc_create",
     "lomo_mc_import",
@@ -79,6 +80,7 @@ EXPORTS = (
     "lomo_mc_bind",
     "lomo_mc_free",
     "lomo_mc_barrier",
+    "lomo_mc_barrier_dev",
 )
 
 # include/lomo_workload.h: the benchmark decoder's fused layers (not the LOMO path)
@@ -186,6 +188,7 @@ _SIGS = {
     "lomo_ipc_close": (_i32, [_vp]),
     "lomo_ipc_free": (_i32, [_vp]),
     "lomo_peer_barrier": (_i32, [_vp, _i32, _i32, _i32, ctypes.c_uint64, _i64, _vp, _vp]),
+    "lomo_peer_barrier_dev": (_i32, [_vp, _vp, _i32, _i32, _i32, _i64, _vp, _vp]),
     "lomo_mc_supported": (_i32, [_i32]),
     "lomo_mc_create": (_i32, [_i32, ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint64),
                               ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(_i32)]),
@@ -194,6 +197,7 @@ _SIGS = {
     "lomo_mc_bind": (_i32, [ctypes.c_uint64, _i32, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
     "lomo_mc_free": (_i32, [ctypes.c_uint64]),
     "lomo_mc_barrier": (_i32, [_vp, _vp, _i32, _i32, ctypes.c_uint64, _i64, _vp, _vp]),
+    "lomo_mc_barrier_dev": (_i32, [_vp, _vp, _vp, _i32, _i32, _i64, _vp, _vp]),
     "lomo_wl_rmsnorm_fwd": (_i32, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, ctypes.c_float, _vp]),
     "lomo_wl_rmsnorm_bwd": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp]),
     "lomo_wl_rmsnorm_partial_rows": (_i32, [_i64]),

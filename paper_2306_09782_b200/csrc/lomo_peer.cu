@@ -52,9 +52,16 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 // ([channel][t]) reaches `epoch`.  The kernel runs after every earlier kernel
 // of the stream completed (no PDL on this launch); the system-scope fence
 // then the release store publish those kernels' writes to the peers.
+//
+// `epochs` (non-null, the *_dev entry points): the epoch is this rank's
+// device counter for the channel plus one, written back at the end -- every
+// rank issues the same barrier sequence, so the counters agree, and a CUDA
+// graph replaying the barrier advances them (a host epoch would be frozen
+// into the graph).
 __global__ void k_peer_barrier(uint64_t* const* sig, int world, int rank, int channel,
-                               uint64_t epoch, int64_t timeout_ns, int* err) {
+                               uint64_t epoch, int64_t timeout_ns, int* err, uint64_t* epochs) {
   const int t = threadIdx.x;
+  if (epochs != nullptr) epoch = epochs[channel] + 1;
   if (t < world) {
     asm volatile("fence.acq_rel.sys;" ::: "memory");
     st_release_sys(sig[t] + channel * LOMO_PEER_MAX + rank, epoch);
@@ -69,14 +76,16 @@ __global__ void k_peer_barrier(uint64_t* const* sig, int world, int rank, int ch
     }
   }
   __syncthreads();
+  if (epochs != nullptr && t == 0) epochs[channel] = epoch;
 }
 
 // NVLS barrier: one multimem.red.add per rank on the channel's counter -- the
 // switch applies it to every rank's copy -- then wait for this GPU's copy to
 // reach epoch * world.
 __global__ void k_mc_barrier(uint64_t* mc, const uint64_t* uc, int world, int channel,
-                             uint64_t epoch, int64_t timeout_ns, int* err) {
+                             uint64_t epoch, int64_t timeout_ns, int* err, uint64_t* epochs) {
   if (threadIdx.x != 0) return;
+  if (epochs != nullptr) epoch = epochs[channel] + 1;
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   asm volatile("multimem.red.release.sys.global.add.u64 [%0], %1;" ::"l"(mc + channel),
                "l"((uint64_t)1)
@@ -90,6 +99,7 @@ __global__ void k_mc_barrier(uint64_t* mc, const uint64_t* uc, int world, int ch
     }
     __nanosleep(128);
   }
+  if (epochs != nullptr) epochs[channel] = epoch;
 }
 
 // ---------------------------------------------------------------- multicast
@@ -232,7 +242,19 @@ int lomo_peer_barrier(void* const* sig_dev, int world, int rank, int channel, ui
     return LOMO_E_ARG;
   k_peer_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<uint64_t* const*>(const_cast<void**>(sig_dev)), world, rank, channel, epoch,
-      timeout_ns, err_dev);
+      timeout_ns, err_dev, nullptr);
+  return (int)cudaGetLastError();
+}
+
+int lomo_peer_barrier_dev(void* const* sig_dev, uint64_t* epochs_dev, int world, int rank,
+                          int channel, int64_t timeout_ns, int* err_dev, void* stream) {
+  if (sig_dev == nullptr || epochs_dev == nullptr || err_dev == nullptr || world < 1 ||
+      world > LOMO_PEER_MAX || rank < 0 || rank >= world || channel < 0 ||
+      channel >= LOMO_PEER_CHANNELS)
+    return LOMO_E_ARG;
+  k_peer_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<uint64_t* const*>(const_cast<void**>(sig_dev)), world, rank, channel, 0,
+      timeout_ns, err_dev, epochs_dev);
   return (int)cudaGetLastError();
 }
 
@@ -394,7 +416,18 @@ int lomo_mc_barrier(void* sig_mc, const void* sig_uc, int world, int channel, ui
     return LOMO_E_ARG;
   k_mc_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(static_cast<uint64_t*>(sig_mc),
                                                      static_cast<const uint64_t*>(sig_uc), world,
-                                                     channel, epoch, timeout_ns, err_dev);
+                                                     channel, epoch, timeout_ns, err_dev, nullptr);
+  return (int)cudaGetLastError();
+}
+
+int lomo_mc_barrier_dev(void* sig_mc, const void* sig_uc, uint64_t* epochs_dev, int world,
+                        int channel, int64_t timeout_ns, int* err_dev, void* stream) {
+  if (sig_mc == nullptr || sig_uc == nullptr || epochs_dev == nullptr || err_dev == nullptr ||
+      world < 1 || world > LOMO_PEER_MAX || channel < 0 || channel >= LOMO_PEER_CHANNELS)
+    return LOMO_E_ARG;
+  k_mc_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(static_cast<uint64_t*>(sig_mc),
+                                                     static_cast<const uint64_t*>(sig_uc), world,
+                                                     channel, 0, timeout_ns, err_dev, epochs_dev);
   return (int)cudaGetLastError();
 }
 

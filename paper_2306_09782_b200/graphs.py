@@ -237,9 +237,11 @@ class GraphedShardedStep:
     The host-side step (``ShardedLOMO.step``) launches ~2,000 kernels and
     ~80 collectives per step; replaying the graphs removes that host cost.
     Needs the layers kept gathered (``reshard_after_forward=False``: ZeRO-3's
-    per-layer free and re-gather resize storage, which a graph cannot) and
-    the NCCL reduce-scatter (not ``fused_rs``: K4's peer barriers count
-    epochs on the host).  Numerics are those of the eager step.
+    per-layer free and re-gather resize storage, which a graph cannot).  With
+    ``fused_rs`` the K4 kernels and their device barriers are captured too
+    (the barriers' epochs are device counters the replays advance; the peer
+    ring's buffer rotation is the captured one, identical on every rank).
+    Numerics are those of the eager step.
 
     Args as :class:`GraphedLOMOStep`.
     """
@@ -250,9 +252,6 @@ class GraphedShardedStep:
         if not isinstance(opt, ShardedLOMO) or opt.passes != 2:
             raise ConfigError("GraphedShardedStep needs a two-pass ShardedLOMO "
                               "(clip_grad_norm and/or loss_scale)")
-        if opt.fused_rs:
-            raise ConfigError("GraphedShardedStep: fused_rs counts its peer-barrier epochs on "
-                              "the host; capture the NCCL reduce-scatter form")
         if any(not b.persistent for b in opt.buckets):
             raise ConfigError("GraphedShardedStep needs reshard_after_forward=False (ZeRO-3's "
                               "per-layer free/re-gather resizes storage inside the step)")
@@ -273,6 +272,10 @@ class GraphedShardedStep:
         torch.cuda.synchronize(dev)
         for b in opt.buckets:
             b.wait()
+        for ring in opt._rings.values():
+            # every buffer's first use in the captured sequence waits for the
+            # peers to finish reading it (its previous use is the previous replay)
+            ring.read_pending = [True] * ring.NBUF
         eng = opt.engine
         pool = torch.cuda.graph_pool_handle()
         self.g1 = torch.cuda.CUDAGraph()

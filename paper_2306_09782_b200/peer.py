@@ -99,7 +99,9 @@ class PeerRing:
             self._own_err = torch.zeros(1, dtype=torch.int32, device=device)
             err_ptr = self._own_err.data_ptr()
         self.err_ptr = err_ptr
-        self.epoch = [0] * _lib.PEER_CHANNELS
+        # per-channel epoch counters in device memory (lomo_*_barrier_dev): a
+        # CUDA graph replaying a barrier advances them, so K4 can be captured
+        self.epochs_dev = torch.zeros(_lib.PEER_CHANNELS, dtype=torch.int64, device=device)
         self.owner = [None] * self.NBUF
         self.read_pending = [False] * self.NBUF
         self.k = 0
@@ -199,17 +201,18 @@ class PeerRing:
         self.read_pending[k] = True
 
     def barrier(self, channel: int) -> None:
-        """Device barrier over the ranks, stream-ordered on the current stream."""
-        self.epoch[channel] += 1
+        """Device barrier over the ranks, stream-ordered on the current stream;
+        the channel's epoch is a device counter (graph-capturable)."""
         s = torch.cuda.current_stream(self.device).cuda_stream
         if self.transport == "ipc":
-            rc = self.lib.lomo_peer_barrier(self.sig_dev.data_ptr(), self.world, self.rank,
-                                            channel, self.epoch[channel], self.timeout_ns,
-                                            self.err_ptr, s)
+            rc = self.lib.lomo_peer_barrier_dev(self.sig_dev.data_ptr(), self.epochs_dev.data_ptr(),
+                                                self.world, self.rank, channel, self.timeout_ns,
+                                                self.err_ptr, s)
         else:
-            rc = self.lib.lomo_mc_barrier(self.mc_base + self.sig_off, self._base + self.sig_off,
-                                          self.world, channel, self.epoch[channel],
-                                          self.timeout_ns, self.err_ptr, s)
+            rc = self.lib.lomo_mc_barrier_dev(self.mc_base + self.sig_off,
+                                              self._base + self.sig_off,
+                                              self.epochs_dev.data_ptr(), self.world, channel,
+                                              self.timeout_ns, self.err_ptr, s)
         _lib.check(rc, "peer barrier")
 
     # Channels name epoch counters: buffer k's "filled" barriers use channel

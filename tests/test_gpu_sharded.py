@@ -171,9 +171,10 @@ def test_nvls_k4_kernels_world1(nccl_world, dtype):
     ring.close()
 
 
+@pytest.mark.parametrize("fused", [False, "ipc"])
 @pytest.mark.parametrize("mode", ["keep", "replay"])
 @pytest.mark.parametrize("dtype,scale", [(torch.float32, 2.0 ** 8), (torch.float16, 2.0 ** 20)])
-def test_graphed_sharded_step_equals_eager(nccl_world, mode, dtype, scale):
+def test_graphed_sharded_step_equals_eager(nccl_world, mode, dtype, scale, fused):
     """GraphedShardedStep (refresh all-gathers, reduce-scatters, K2/K3/K1 and
     the rank exchange captured in two CUDA graphs) == the eager ShardedLOMO
     step bit for bit, including overflow-skipped steps (fp16 at 2^20)."""
@@ -189,7 +190,7 @@ def test_graphed_sharded_step_equals_eager(nccl_world, mode, dtype, scale):
         return ShardedLOMO(m, lr=0.05, clip_grad_norm=0.5,
                            loss_scale=LossScaler(scale, growth_interval=2),
                            reshard_after_forward=False, keep_grads=mode == "keep",
-                           replay=mode == "replay")
+                           replay=mode == "replay", fused_rs=fused)
     oa, ob = make(a), make(b)
     g = torch.Generator(device="cuda").manual_seed(3)
     batches = [torch.randint(0, CFG["vocab"], (2, 33), device="cuda", generator=g)
