@@ -65,8 +65,9 @@ def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group, async_op: bool 
     ``async_op``: returns the NCCL work handle (gloo completes, None)."""
     if _backend(group) == "nccl":
         return dist.all_gather_into_tensor(out, inp, group=group, async_op=async_op)
-    # gloo (CPU tests): list form
-    dist.all_gather(list(out.chunk(dist.get_world_size(group))), inp, group=group)
+    # gloo (CPU tests): list form; the input may be this rank's chunk of
+    # `out` (persistent buckets gather in place), so it is copied first
+    dist.all_gather(list(out.chunk(dist.get_world_size(group))), inp.clone(), group=group)
     return None
 
 
@@ -113,7 +114,13 @@ class _Bucket:
                 p.data = full[off:off + n].view(p.shape)  # frees the original storage
         dist.broadcast(full, src=dist.get_global_rank(group, 0) if group is not None else 0,
                        group=group)  # every rank starts from rank 0's weights
-        self.shard = full[rank * self.S:(rank + 1) * self.S].clone()
+        # a persistent bucket's shard IS its slice of the full buffer: the
+        # update writes the gathered parameters in place and the refresh
+        # all-gather runs in place (no copy of this rank's own slice; at
+        # world 1 no copy at all).  A ZeRO-3 bucket frees `full` after use, so
+        # its shard is its own allocation.
+        sl = full[rank * self.S:(rank + 1) * self.S]
+        self.shard = sl if persistent else sl.clone()
         self.full = full
         self.nbytes = self.padded * full.element_size()
         self.gathered = True
