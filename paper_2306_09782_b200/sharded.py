@@ -466,7 +466,13 @@ class ShardedLOMO(_Protocol):
         # to NCCL (or at the end of the pass), so the compute stream never
         # waits on the collective it could overlap
         self._drain(keep=0)
-        gshard = torch.empty(b.S, dtype=b.dtype, device=b.device)
+        if isinstance(self._stash, _KeptShards) and self._mode == _PROBE and self.world > 1:
+            # a kept shard outlives the step: its own compact allocation
+            gshard = torch.empty(b.S, dtype=b.dtype, device=b.device)
+        else:
+            # in place: this rank's slice of the flat buffer receives the sum
+            # (NCCL's in-place reduce-scatter; no copy at all at world 1)
+            gshard = b.gflat[self.rank * b.S:(self.rank + 1) * b.S]
         work = reduce_scatter(gshard, b.gflat, self.group, async_op=True)
         self._inflight.append((work, gshard, b, self._mode))
         b.gflat = None
