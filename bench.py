@@ -1267,11 +1267,8 @@ def _graphed_sharded(args, opt, model, data, world):
                "ms_per_step": round(ms, 2), "steps": args.train_steps, "outcomes": outcomes,
                "clocks": clk.summary(),
                "peak_mem_gib_rank0": round(torch.cuda.max_memory_allocated() / 2 ** 30, 2),
-               "note": "same model as the eager leg, continued. In a world-1 group NCCL "
-                       "runs its captured collectives as copy kernels on the SMs (eager: "
-                       "copy-engine DMA), so at N=1 the graphed step is slower; at N>1 both "
-                       "forms run NCCL's kernels and the graph removes the eager step's "
-                       "host gaps (tools/sharded_profile.py: 3.7-5.3 ms idle per step)"}
+               "note": "same model as the eager leg, continued; the graph removes the eager "
+                       "step's host gaps (tools/sharded_profile.py)"}
         del gs
         torch.cuda.empty_cache()
         return res
