@@ -1154,7 +1154,9 @@ def bench_train_sharded(args, rank, world):
     # otherwise (65B) ZeRO-3 frees each layer after its forward and re-gathers it
     pbytes = sum(p.numel() * p.element_size() for p in model.parameters())
     hbm = torch.cuda.get_device_properties(0).total_memory
-    reshard = pbytes > 0.4 * hbm
+    # (at world 1 a ZeRO-3 shard is the whole model: freeing the gathered
+    # layers saves nothing and costs a gather per use, so never reshard)
+    reshard = world > 1 and pbytes > 0.4 * hbm
     # pass 2: K1 over pass 1's reduced gradient shards when 1/world of the
     # gradients fits in 15 % of HBM, else replay of the stashed (x, dy)
     keep = not args.sharded_strict and pbytes / world < 0.15 * hbm
