@@ -152,6 +152,7 @@ class GraphedLOMOStep:
             self.steps += 1
             return self.loss
         st = eng.read_status()          # the one host sync of the step
+        opt._mirror_scaler(st)
         if st.underflow:
             raise ScaleUnderflowError(
                 f"loss scale would fall below {st.min_scale}; training diverged")
@@ -160,6 +161,7 @@ class GraphedLOMOStep:
             opt.last_outcome = StepOutcome.SKIPPED_OVERFLOW
         else:
             self.g2.replay()
+            opt._scaler_clean()
             opt.last_outcome = StepOutcome.APPLIED
         self.steps += 1
         return self.loss
@@ -305,6 +307,7 @@ class GraphedShardedStep:
         _lib.check(eng.lib.lomo_set_lr(eng.ptr, float(lr), eng.stream()), "lomo_set_lr")
         self.g1.replay()
         st = eng.read_status()          # the one host sync of the step
+        opt._mirror_scaler(st)
         if st.underflow:
             raise ScaleUnderflowError(
                 f"loss scale would fall below {st.min_scale}; training diverged")
@@ -313,6 +316,7 @@ class GraphedShardedStep:
             opt.last_outcome = StepOutcome.SKIPPED_OVERFLOW
         else:
             self.g2.replay()
+            opt._scaler_clean()
             opt.last_outcome = StepOutcome.APPLIED
             for b in opt.buckets:
                 # the next graph-1 replay re-gathers them; an eager refresh

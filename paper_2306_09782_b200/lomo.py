@@ -147,6 +147,7 @@ class _Protocol:
             self._run_backward(self._scaled(loss), _PROBE, retain_graph)
         self._decide()  # K3a: skip (overflow set by begin_step) + LossScaler.on_overflow
         st = self.engine.read_status()  # the one host sync of the step
+        self._mirror_scaler(st)
         if st.underflow:
             raise ScaleUnderflowError(
                 f"loss scale would fall below {st.min_scale}; training diverged")
@@ -186,6 +187,7 @@ class _Protocol:
             else:
                 self._run_backward(self._scaled(loss), _UPDATE, False)
             self.engine.on_clean()
+            self._scaler_clean()
             self._after_update()
             self.last_outcome = StepOutcome.APPLIED
             return
@@ -208,6 +210,18 @@ class _Protocol:
 
     def _after_update(self) -> None:
         pass
+
+    def _mirror_scaler(self, st) -> None:
+        """The user's LossScaler object reads as the reference's: the device
+        state machine's scale / clean_steps at this step's status read."""
+        if self.scaler is not None:
+            self.scaler._mirror(st)
+
+    def _scaler_clean(self) -> None:
+        """After an applied step K3b ran LossScaler.on_clean on the device;
+        the host mirror applies the same arithmetic (no extra sync)."""
+        if self.scaler is not None:
+            self.scaler.on_clean()
 
     def _drop_stash(self) -> None:
         st = getattr(self, "_stash", None)

@@ -6,8 +6,10 @@ the reference's names, argument meaning and validation errors, so code
 written against the reference keeps working:
 
 * ``ClipMode``      stabilize.py:45-74   (none / by_value / by_global_norm / by_group_norm)
-* ``LossScaler``    stabilize.py:94-127  (power-of-two dynamic scale; the state
-                    machine itself runs on device, see ``LOMO.loss_scale``)
+* ``LossScaler``    stabilize.py:94-127  (power-of-two dynamic scale: the
+                    reference's live object -- ``scale``, ``clean_steps``,
+                    ``on_overflow()``, ``on_clean()``; under LOMO the state
+                    machine runs on device and the optimizer mirrors it here)
 * ``Stabilizer``    stabilize.py:130-153 (pass count; scaler + group clip rejected)
 * ``StepOutcome``   stabilize.py:77-79
 """
@@ -17,7 +19,7 @@ import math
 from dataclasses import dataclass
 from enum import Enum
 
-from .errors import ConfigError
+from .errors import ConfigError, ScaleUnderflowError
 
 
 class ClipKind(Enum):
@@ -72,28 +74,59 @@ def is_power_of_two(x: float) -> bool:
     return x > 0 and mantissa == 0.5
 
 
-@dataclass(frozen=True)
 class LossScaler:
-    """Dynamic loss-scale configuration (stabilize.py:94-113).
+    """Dynamic loss-scale state machine; the scale is always a power of two
+    (stabilize.py:94-127): the reference's names, validation, live
+    attributes and methods.
 
-    Validation is the reference's; the halve/double state machine
-    (stabilize.py:115-127) runs on device inside K3a/K3b.
+    Under :class:`~paper_2306_09782_b200.LOMO` the halve/double state machine
+    runs on the device (K3a halves on overflow, K3b counts clean steps); the
+    optimizer copies the device's ``scale`` and ``clean_steps`` into this
+    object at each step's status read and applies ``on_clean()`` after an
+    applied step (the same arithmetic K3b ran), so ``scaler.scale`` reads as
+    the reference's does -- without an extra host sync.
     """
 
-    scale: float = 2.0 ** 10
-    growth_interval: int = 16
-    min_scale: float = 1.0
-    max_scale: float = 2.0 ** 24
-
-    def __post_init__(self):
-        for name, value in (("scale", self.scale), ("min_scale", self.min_scale),
-                            ("max_scale", self.max_scale)):
+    def __init__(self, scale: float = 2.0 ** 10, growth_interval: int = 16,
+                 min_scale: float = 1.0, max_scale: float = 2.0 ** 24):
+        for name, value in (("scale", scale), ("min_scale", min_scale),
+                            ("max_scale", max_scale)):
             if not is_power_of_two(value):
                 raise ConfigError(f"{name} must be a positive power of two, got {value}")
-        if not (self.min_scale <= self.scale <= self.max_scale):
-            raise ConfigError(f"scale {self.scale} outside [{self.min_scale}, {self.max_scale}]")
-        if self.growth_interval < 1:
-            raise ConfigError(f"growth_interval must be >= 1, got {self.growth_interval}")
+        if not (min_scale <= scale <= max_scale):
+            raise ConfigError(f"scale {scale} outside [{min_scale}, {max_scale}]")
+        if growth_interval < 1:
+            raise ConfigError(f"growth_interval must be >= 1, got {growth_interval}")
+        self.scale = float(scale)
+        self.growth_interval = int(growth_interval)
+        self.min_scale = float(min_scale)
+        self.max_scale = float(max_scale)
+        self.clean_steps = 0
+
+    def on_overflow(self) -> None:
+        """stabilize.py:115-121: halve, or raise when below min_scale."""
+        if self.scale / 2.0 < self.min_scale:
+            raise ScaleUnderflowError(
+                f"loss scale would fall below {self.min_scale}; training diverged")
+        self.scale /= 2.0
+        self.clean_steps = 0
+
+    def on_clean(self) -> None:
+        """stabilize.py:123-127: double after growth_interval clean steps."""
+        self.clean_steps += 1
+        if self.clean_steps >= self.growth_interval:
+            self.scale = min(self.scale * 2.0, self.max_scale)
+            self.clean_steps = 0
+
+    def _mirror(self, status) -> None:
+        """Copy the device state machine's values (a lomo_status snapshot)."""
+        self.scale = float(status.scale)
+        self.clean_steps = int(status.clean_steps)
+
+    def __repr__(self) -> str:
+        return (f"LossScaler(scale={self.scale}, growth_interval={self.growth_interval}, "
+                f"min_scale={self.min_scale}, max_scale={self.max_scale}, "
+                f"clean_steps={self.clean_steps})")
 
 
 @dataclass(frozen=True)

@@ -122,7 +122,8 @@ class CpuEngine:
         self.scale_view.fill_(self.scale)
 
     def read_status(self):
-        return SimpleNamespace(scale=self.scale, inv_scale=self.inv_scale, skip=int(self.skip),
+        return SimpleNamespace(scale=self.scale, clean_steps=self.clean,
+                               inv_scale=self.inv_scale, skip=int(self.skip),
                                underflow=int(self.underflow),
                                overflow=int(self.overflow), total_norm=self.total_norm,
                                clip_coef=self.coef, min_scale=self.min_scale)

@@ -99,6 +99,9 @@ def _ulps16(got, ref):
                                         ("C", LossScaler(2.0 ** 24, 2, max_scale=2.0 ** 24))])
 @pytest.mark.parametrize("math_mode", ["f32", "f64"])
 def test_c1_fixture_fp16_two_pass(c1_meta, c1_arrays, key, scaler, math_mode):
+    # a fresh scaler per run: LossScaler is the reference's live state
+    # machine, and the optimizer mirrors the device's scale into it
+    scaler = LossScaler(scaler.scale, scaler.growth_interval, max_scale=scaler.max_scale)
     stab = Stabilizer(ClipMode.by_global_norm(1.0), scaler)
     model, opt, losses, outcomes, scales = _run_c1(torch.float16, {"stabilizer": stab},
                                                    math_mode=math_mode)
@@ -454,3 +457,34 @@ def test_replay_refuses_tied_weights():
     ids = torch.randint(0, 64, (2, 8), device="cuda")
     with pytest.raises(ConfigError):
         opt.step(lambda: mean_cross_entropy(m(ids), ids), 0.05)
+
+
+@pytest.mark.parametrize("graphed", [False, True])
+def test_loss_scaler_object_mirrors_the_device_state(graphed):
+    """After every step the user's LossScaler reads as the reference's would:
+    scale and clean_steps equal the device state machine's (halved on the
+    forced overflows, doubled after growth_interval clean steps), without an
+    extra host sync; eager and CUDA-graphed steps."""
+    from paper_2306_09782_b200.graphs import GraphedLOMOStep
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=64, layers=2, heads=4, ffn=128, vocab=128)
+    m = Llama(cfg, dtype=torch.float16, device="cuda", seed=0)
+    sc = LossScaler(2.0 ** 22, growth_interval=2, max_scale=2.0 ** 24)
+    opt = LOMO(m, lr=0.01, clip_grad_norm=1.0, loss_scale=sc, replay=graphed)
+    assert opt.scaler is sc
+    d = torch.randint(0, 128, (2, 33), device="cuda",
+                      generator=torch.Generator(device="cuda").manual_seed(2))
+    static = d.clone()
+    if graphed:
+        g = GraphedLOMOStep(opt, lambda x: m.loss(x[:, :-1], x[:, 1:]), (static,), warmup=1,
+                            lr=0.01)
+        step = lambda: g.step(0.01)  # noqa: E731
+    else:
+        step = lambda: opt.step(lambda: m.loss(static[:, :-1], static[:, 1:]), 0.01)  # noqa: E731
+    seen = set()
+    for _ in range(12):
+        step()
+        seen.add(opt.last_outcome)
+        st = opt.read_status()
+        assert (sc.scale, sc.clean_steps) == (st.scale, st.clean_steps)
+    assert StepOutcome.SKIPPED_OVERFLOW in seen and StepOutcome.APPLIED in seen

@@ -151,3 +151,34 @@ def test_dispatcher_chains_only_consecutive_k1_launches():
     kinds = [kind for kind, _, _ in lib.calls]
     assert kinds == ["k1", "k1", "multi", "k1", "k1", "k2", "k2", "k1", "k1", "k1", "k1"]
     assert chained == [False, True, False, True, False, False, True, False, False, False, False]
+
+
+def test_loss_scaler_host_state_machine_matches_reference_replays():
+    """LossScaler is the reference's live object (stabilize.py:94-127):
+    on_overflow / on_clean over the 300 recorded reference replays give the
+    recorded scale trace, underflow raises ScaleUnderflowError."""
+    import json
+
+    from conftest import GOLDEN
+
+    from paper_2306_09782_b200 import LossScaler
+    from paper_2306_09782_b200.errors import ScaleUnderflowError
+    seqs = json.loads((GOLDEN / "scaler_replay.json").read_text())
+    assert len(seqs) == 300
+    for s in seqs:
+        sc = LossScaler(scale=2.0 ** 6, growth_interval=s["growth"], min_scale=1.0,
+                        max_scale=2.0 ** 10)
+        trace = []
+        for ok in s["outcomes"]:
+            try:
+                sc.on_clean() if ok else sc.on_overflow()
+            except ScaleUnderflowError:
+                trace.append(None)
+                break
+            trace.append(sc.scale)
+        assert trace == s["trace"]
+    sc = LossScaler(scale=1024.0, growth_interval=4)
+    sc.on_clean()
+    assert sc.clean_steps == 1
+    sc.on_overflow()
+    assert sc.scale == 512.0 and sc.clean_steps == 0
