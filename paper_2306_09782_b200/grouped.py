@@ -78,6 +78,7 @@ class GroupedLOMO:
                 raise ConfigError("all parameters must live on one CUDA device")
             dtype_code(p.dtype)
         self.params = params
+        self._model = model
         self.lr = float(lr)
         self.weight_decay = float(weight_decay)
         self.layer = layer_of if layer_of is not None else infer_layers(model)
@@ -233,7 +234,9 @@ class GroupedLOMO:
                               "use GroupedLOMO(fuse_gemm=False)")
 
     def step(self, closure: Callable[[], torch.Tensor], lr: float | None = None) -> float:
-        loss = closure()
+        """closure() -> loss, or the reference's step(batch, lr) (see LOMO.step)."""
+        from .lomo import _as_closure
+        loss = _as_closure(self, closure)()
         self.fused_backward(loss, lr)
         return float(loss.detach())
 

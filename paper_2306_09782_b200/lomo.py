@@ -78,6 +78,19 @@ def trainable_params(model) -> list[torch.Tensor]:
     return uniq
 
 
+def _as_closure(opt, closure):
+    """step(closure) or the reference's step(batch) with batch = (inputs, targets)."""
+    if callable(closure):
+        return closure
+    model = getattr(opt, "_model", None)
+    if model is None or not callable(getattr(model, "loss", None)):
+        raise TypeError("step(batch, lr) needs a model with .loss(inputs, targets) (the "
+                        "reference's _forward_loss, optim.py:57-60); otherwise pass a closure "
+                        "returning the loss")
+    inputs, targets = closure
+    return lambda: model.loss(inputs, targets)
+
+
 class _Protocol:
     """The two-pass / single-pass step protocol shared by LOMO and ShardedLOMO
     (stabilize.py:148-230), over a CudaEngine and a backward driver.
@@ -232,11 +245,15 @@ class _Protocol:
              recompute_forward: bool = False) -> float:
         """The reference step protocol (optim.py:118-132, stabilize.py:148-230).
 
-        ``closure()`` runs the forward and returns the scalar loss.  Two-pass
-        mode reuses the pass-1 graph for pass 2 (identical values: pass 1
-        does not touch parameters); ``recompute_forward=True`` re-runs the
-        forward instead, as stabilize.py:226 does.  Returns the loss as a float.
+        ``closure()`` runs the forward and returns the scalar loss; the
+        reference's own form ``step(batch, lr)`` with ``batch = (inputs,
+        targets)`` is accepted too (``model.loss(inputs, targets)``, its
+        ``_forward_loss``, optim.py:57-60).  Two-pass mode reuses the pass-1
+        graph for pass 2 (identical values: pass 1 does not touch
+        parameters); ``recompute_forward=True`` re-runs the forward instead,
+        as stabilize.py:226 does.  Returns the loss as a float.
         """
+        closure = _as_closure(self, closure)
         loss = closure()
         if self.passes == 2:
             replay = getattr(self, "_stash", None) is not None
@@ -316,6 +333,7 @@ class LOMO(_Protocol):
         st = stabilizer if stabilizer is not None else stabilizer_from_args(
             clip_grad_norm, clip_grad_value, loss_scale)
         self._init_protocol(st, lr, weight_decay)
+        self._model = model
         uniq = trainable_params(model)
         dev = uniq[0].device
         if dev.type != "cuda":

@@ -279,6 +279,7 @@ class ShardedLOMO(_Protocol):
             for j, (p, off, n) in enumerate(zip(b.params, b.offsets, b.numels)):
                 self._loc[id(p)] = (b, off, n, j)
         self.params = params
+        self._model = model
         self.device = params[0].device
         self.engine = _engine if _engine is not None else CudaEngine(
             self.device, len(self.buckets), self.scaler, self.max_norm, math,

@@ -488,3 +488,33 @@ def test_loss_scaler_object_mirrors_the_device_state(graphed):
         st = opt.read_status()
         assert (sc.scale, sc.clean_steps) == (st.scale, st.clean_steps)
     assert StepOutcome.SKIPPED_OVERFLOW in seen and StepOutcome.APPLIED in seen
+
+
+def test_reference_style_step_batch_form():
+    """step((inputs, targets), lr) -- the reference's LOMO.step(batch, lr)
+    (optim.py:118-132, _forward_loss optim.py:57-60) -- equals
+    step(closure, lr) bit for bit, single and two-pass."""
+    from paper_2306_09782_b200 import GroupedLOMO
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=64, layers=2, heads=4, ffn=128, vocab=128)
+    d = torch.randint(0, 128, (2, 33), device="cuda",
+                      generator=torch.Generator(device="cuda").manual_seed(4))
+    for kw in ({}, {"clip_grad_norm": 1.0, "loss_scale": LossScaler(2.0 ** 8)}, "grouped"):
+        a = Llama(cfg, dtype=torch.float32, device="cuda", seed=0)
+        b = Llama(cfg, dtype=torch.float32, device="cuda", seed=0)
+        if kw == "grouped":
+            oa, ob = (GroupedLOMO(m, lr=0.05, max_norm=1.0, window=1) for m in (a, b))
+        else:
+            oa = LOMO(a, lr=0.05, **kw)
+            ob = LOMO(b, lr=0.05, **{k: (LossScaler(2.0 ** 8) if k == "loss_scale" else v)
+                                     for k, v in kw.items()})
+        for _ in range(2):
+            la = oa.step(lambda: a.loss(d[:, :-1], d[:, 1:]), 0.05)
+            lb = ob.step((d[:, :-1], d[:, 1:]), 0.05)
+            assert la == lb
+        for x, y in zip(a.parameters(), b.parameters()):
+            assert torch.equal(x, y)
+        oa.remove_hooks()
+        ob.remove_hooks()
+    with pytest.raises(TypeError):
+        LOMO(torch.nn.Linear(4, 4).cuda(), lr=0.1).step((d, d), 0.1)
