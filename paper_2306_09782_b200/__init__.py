@@ -10,10 +10,12 @@ from .errors import (ConfigError, FusedTrainError, NativeError, NonFiniteLossErr
                      ScaleUnderflowError, ShapeError, TapeStateError)
 from .grouped import GroupedLOMO
 from .lomo import LOMO, lomo_step
-from .stabilize import ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome
+from .stabilize import (ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome, clip_by_value,
+                        grouped_norm_clip_step, scaled_step, two_pass_norm_clip_step)
 
 __all__ = [
     "LOMO", "GroupedLOMO", "lomo_step", "ClipKind", "ClipMode", "LossScaler", "Stabilizer", "StepOutcome",
+    "clip_by_value", "two_pass_norm_clip_step", "grouped_norm_clip_step", "scaled_step",
     "ConfigError", "FusedTrainError", "NativeError", "NonFiniteLossError",
     "ScaleUnderflowError", "ShapeError", "TapeStateError",
 ]

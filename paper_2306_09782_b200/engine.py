@@ -84,6 +84,14 @@ class CudaEngine:
                 float(scaler.max_scale) if scaler else 1.0,
                 float(max_norm) if max_norm else 0.0, float(grad_div), self.stream()),
                 "lomo_state_init")
+            clean = int(getattr(scaler, "clean_steps", 0) or 0) if scaler else 0
+            if clean:
+                # a scaler handed over mid-count continues it, as the
+                # reference's live object does (stabilize.py:123-127); K3b
+                # republishes nothing for clean_steps, so a plain header write
+                off = _lib.LomoStatus.clean_steps.offset
+                self.state[off:off + 4].copy_(
+                    torch.tensor([clean], dtype=torch.int32).view(torch.uint8))
         side = torch.cuda.Stream(device) if overlap else None
         self.dispatch = HookDispatcher(self.lib, self.ptr, self.math, side_stream=side)
 

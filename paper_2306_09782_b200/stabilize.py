@@ -147,3 +147,53 @@ class Stabilizer:
     def backward_passes_per_step(self) -> int:
         two = self.scaler is not None or self.clip.kind is ClipKind.BY_GLOBAL_NORM
         return 2 if two else 1
+
+    def run_step(self, model, batch, lr: float, **lomo_kwargs):
+        """One stabilised fused step (stabilize.py:148-153): ``batch`` is
+        ``(inputs, targets)`` for ``model.loss`` or a closure returning the
+        loss.  Returns ``(loss, StepOutcome)``; the scaler object carries its
+        state from step to step, as the reference's does.  (A thin wrapper:
+        hooks are registered for this one step -- long loops keep one
+        :class:`~paper_2306_09782_b200.LOMO`.)"""
+        from .grouped import GroupedLOMO
+        from .lomo import LOMO
+        if self.clip.kind is ClipKind.BY_GROUP_NORM:
+            opt = GroupedLOMO(model, lr, max_norm=self.clip.max_norm, window=self.clip.window,
+                              **lomo_kwargs)
+        else:
+            opt = LOMO(model, lr, stabilizer=self, **lomo_kwargs)
+        try:
+            loss = opt.step(batch, lr)
+            outcome = opt.last_outcome
+            return loss, (StepOutcome.APPLIED if outcome is None else outcome)
+        finally:
+            opt.remove_hooks()
+
+
+def clip_by_value(grad, threshold: float):
+    """stabilize.py:82-86: clamp every element to [-threshold, threshold]
+    (NaN stays NaN, as np.clip); K1's ``clip_value`` applies it in place."""
+    if threshold <= 0:
+        raise ConfigError(f"clip threshold must be positive, got {threshold}")
+    return grad.clamp(-threshold, threshold)
+
+
+def two_pass_norm_clip_step(model, batch, lr: float, max_norm: float, **lomo_kwargs) -> float:
+    """stabilize.py:277-280: global-norm-clipped fused step (two passes)."""
+    loss, _ = Stabilizer(ClipMode.by_global_norm(max_norm)).run_step(model, batch, lr,
+                                                                     **lomo_kwargs)
+    return loss
+
+
+def grouped_norm_clip_step(model, batch, lr: float, max_norm: float, window: int,
+                           **lomo_kwargs) -> float:
+    """stabilize.py:283-289: single-pass step with per-layer-window clipping."""
+    loss, _ = Stabilizer(ClipMode.by_group_norm(max_norm, window)).run_step(model, batch, lr,
+                                                                            **lomo_kwargs)
+    return loss
+
+
+def scaled_step(model, batch, lr: float, scaler: LossScaler, clip: ClipMode = ClipMode(),
+                **lomo_kwargs):
+    """stabilize.py:292-295: loss-scaled fused step under the two-pass protocol."""
+    return Stabilizer(clip, scaler).run_step(model, batch, lr, **lomo_kwargs)

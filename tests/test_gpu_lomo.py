@@ -518,3 +518,40 @@ def test_reference_style_step_batch_form():
         ob.remove_hooks()
     with pytest.raises(TypeError):
         LOMO(torch.nn.Linear(4, 4).cuda(), lr=0.1).step((d, d), 0.1)
+
+
+def test_stabilizer_run_step_carries_the_scaler_like_the_reference():
+    """Stabilizer.run_step(model, batch, lr) (stabilize.py:148-153) and the
+    reference's helpers (scaled_step, two_pass_norm_clip_step,
+    grouped_norm_clip_step): a fresh optimizer per call, the scaler object
+    carrying scale AND clean_steps between calls -- so a run of run_step
+    calls equals one long-lived LOMO bit for bit, growth and skips included."""
+    from paper_2306_09782_b200 import (grouped_norm_clip_step, scaled_step,
+                                       two_pass_norm_clip_step)
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=64, layers=2, heads=4, ffn=128, vocab=128)
+    a = Llama(cfg, dtype=torch.float16, device="cuda", seed=0)
+    b = Llama(cfg, dtype=torch.float16, device="cuda", seed=0)
+    sa = LossScaler(2.0 ** 21, growth_interval=2, max_scale=2.0 ** 24)
+    sb = LossScaler(2.0 ** 21, growth_interval=2, max_scale=2.0 ** 24)
+    oa = LOMO(a, lr=0.01, stabilizer=Stabilizer(ClipMode.by_global_norm(1.0), sa))
+    stab_b = Stabilizer(ClipMode.by_global_norm(1.0), sb)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    outs = []
+    for _ in range(8):
+        d = torch.randint(0, 128, (2, 33), device="cuda", generator=g)
+        la = oa.step((d[:, :-1], d[:, 1:]), 0.01)
+        lb, ob = stab_b.run_step(b, (d[:, :-1], d[:, 1:]), 0.01)
+        assert la == lb and ob == oa.last_outcome
+        assert (sa.scale, sa.clean_steps) == (sb.scale, sb.clean_steps)
+        outs.append(ob)
+    assert StepOutcome.APPLIED in outs
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)
+    oa.remove_hooks()
+    d = torch.randint(0, 128, (2, 33), device="cuda", generator=g)
+    c = Llama(cfg, dtype=torch.float32, device="cuda", seed=0)
+    assert math.isfinite(two_pass_norm_clip_step(c, (d[:, :-1], d[:, 1:]), 0.01, 1.0))
+    assert math.isfinite(grouped_norm_clip_step(c, (d[:, :-1], d[:, 1:]), 0.01, 1.0, 1))
+    loss, outcome = scaled_step(c, (d[:, :-1], d[:, 1:]), 0.01, LossScaler(2.0 ** 4))
+    assert math.isfinite(loss) and outcome is StepOutcome.APPLIED

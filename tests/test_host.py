@@ -182,3 +182,18 @@ def test_loss_scaler_host_state_machine_matches_reference_replays():
     assert sc.clean_steps == 1
     sc.on_overflow()
     assert sc.scale == 512.0 and sc.clean_steps == 0
+
+
+def test_clip_by_value_kat_and_validation():
+    """stabilize.py:82-86: KAT [1.3, 0.8] @ 1.0 -> [1.0, 0.8]; NaN stays NaN;
+    a non-positive threshold is a ConfigError."""
+    import math
+
+    import torch
+
+    from paper_2306_09782_b200 import ConfigError, clip_by_value
+    out = clip_by_value(torch.tensor([1.3, 0.8, -2.5, float("nan")], dtype=torch.float64), 1.0)
+    assert out[:3].tolist() == [1.0, 0.8, -1.0] and math.isnan(out[3].item())
+    for t in (0.0, -1.0):
+        with pytest.raises(ConfigError):
+            clip_by_value(torch.zeros(2), t)
