@@ -8,13 +8,14 @@ unscale, overflow detection, clipping, weight decay and ``p -= lr*g``.
 """
 from .errors import (ConfigError, FusedTrainError, NativeError, NonFiniteLossError,
                      ScaleUnderflowError, ShapeError, TapeStateError)
+from .engine import apply_update
 from .grouped import GroupedLOMO
 from .lomo import LOMO, lomo_step
 from .stabilize import (ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome, clip_by_value,
                         grouped_norm_clip_step, scaled_step, two_pass_norm_clip_step)
 
 __all__ = [
-    "LOMO", "GroupedLOMO", "lomo_step", "ClipKind", "ClipMode", "LossScaler", "Stabilizer", "StepOutcome",
+    "LOMO", "GroupedLOMO", "lomo_step", "apply_update", "ClipKind", "ClipMode", "LossScaler", "Stabilizer", "StepOutcome",
     "clip_by_value", "two_pass_norm_clip_step", "grouped_norm_clip_step", "scaled_step",
     "ConfigError", "FusedTrainError", "NativeError", "NonFiniteLossError",
     "ScaleUnderflowError", "ShapeError", "TapeStateError",

@@ -38,6 +38,26 @@ def dtype_code(dtype: torch.dtype) -> int:
         raise ConfigError(f"unsupported parameter dtype {dtype}") from None
 
 
+def apply_update(param: torch.Tensor, grad: torch.Tensor, lr: float, math: str = "f64") -> None:
+    """optim.py:52-54 on the device: ``param <- round(param - lr * grad)`` in
+    place with one K1 launch on the current stream (``math="f64"``: the
+    reference's float64 arithmetic and direct rounding, bit-exact; "f32": the
+    fp32 hot path).  Both tensors on one CUDA device, same dtype and shape."""
+    if param.device.type != "cuda" or grad.device != param.device:
+        raise ConfigError("apply_update needs both tensors on one CUDA device (no CPU path)")
+    if grad.shape != param.shape:  # tensor.py:77-78
+        raise ShapeError("assign", f"shape {tuple(grad.shape)} != tensor shape {tuple(param.shape)}")
+    if grad.dtype != param.dtype or not (param.is_contiguous() and grad.is_contiguous()):
+        raise ConfigError("apply_update needs contiguous tensors of one dtype")
+    if math not in MATH_CODE:
+        raise ConfigError(f"math must be 'f32' or 'f64', got {math!r}")
+    idx = param.device.index if param.device.index is not None else torch.cuda.current_device()
+    _lib.check(_lib.load().lomo_fused_update(param.data_ptr(), grad.data_ptr(), param.numel(),
+                                             dtype_code(param.dtype), MATH_CODE[math],
+                                             float(lr), 0.0, 0.0, 0, None, _raw_stream(idx)),
+               "lomo_fused_update")
+
+
 class CudaEngine:
     """State block + K1/K2/K3 launches for one optimizer on one device.
 

@@ -702,3 +702,19 @@ def test_chained_k2_pass_equals_unchained(use_cpp):
     d.flush(U.stream())
     st.finalize()
     assert st.status().overflow == 1 and st.status().skip == 1
+
+
+@pytest.mark.parametrize("prec", PRECS)
+def test_apply_update_python_entry_matches_reference_kats(prec):
+    """paper_2306_09782_b200.apply_update (optim.py:52-54 as a device call):
+    f64 math is bit-exact against the oracle (the reference's float64
+    arithmetic + write-back rounding); shape mismatch -> ShapeError."""
+    from paper_2306_09782_b200 import ShapeError, apply_update
+    rng = np.random.default_rng(17)
+    p0, g0 = _draw(100003, prec, rng)
+    dt = U.TORCH_DT[prec]
+    p, g = U.to_dev(p0, dt), U.to_dev(g0, dt)
+    apply_update(p, g, 0.05)
+    assert np.array_equal(p.double().cpu().numpy(), O.apply_update(p0, g0, 0.05, prec))
+    with pytest.raises(ShapeError):
+        apply_update(p, g[:-1], 0.05)
