@@ -293,7 +293,12 @@ class LOMO(_Protocol):
             :class:`LossScaler` (dynamic scaling, two passes).
         clip_grad_value: value clip threshold (single pass, stabilize.py:163-176).
         weight_decay: decoupled decay ``p *= 1 - lr*wd`` (0 = the reference).
-        stabilizer: alternatively, the reference's :class:`Stabilizer`.
+        stabilizer: alternatively, the reference's :class:`Stabilizer`; the
+            reference's positional form ``LOMO(model, stabilizer)`` works too
+            (optim.py:108-112: the learning rate is then ``step``'s).
+        ledger: accepted for the reference's signature and ignored (the
+            memory ledger is outside this path; ``torch.cuda`` memory stats
+            report the same quantities).
         math: ``"f32"`` (fp32 arithmetic, the hot path) or ``"f64"`` (the
             reference's float64 arithmetic, rounded directly to storage).
         overlap: launch the hook kernels on a side stream so each update
@@ -327,7 +332,11 @@ class LOMO(_Protocol):
                  weight_decay: float = 0.0, stabilizer: Stabilizer | None = None,
                  math: str = "f32", overlap: bool = False, replay: bool = False,
                  fuse_gemm: bool = False, fuse_probe: bool | None = None,
-                 gemm_streams: int = 1, probe_stream: bool = False):
+                 gemm_streams: int = 1, probe_stream: bool = False, ledger=None):
+        if isinstance(lr, Stabilizer):  # the reference's LOMO(model, stabilizer)
+            if stabilizer is not None:
+                raise ConfigError("stabilizer given twice")
+            stabilizer, lr = lr, 1e-3
         if stabilizer is not None and (clip_grad_norm or clip_grad_value or loss_scale):
             raise ConfigError("pass either a Stabilizer or the clip/loss_scale arguments")
         st = stabilizer if stabilizer is not None else stabilizer_from_args(

@@ -555,3 +555,20 @@ def test_stabilizer_run_step_carries_the_scaler_like_the_reference():
     assert math.isfinite(grouped_norm_clip_step(c, (d[:, :-1], d[:, 1:]), 0.01, 1.0, 1))
     loss, outcome = scaled_step(c, (d[:, :-1], d[:, 1:]), 0.01, LossScaler(2.0 ** 4))
     assert math.isfinite(loss) and outcome is StepOutcome.APPLIED
+
+
+def test_reference_constructor_form():
+    """LOMO(model, stabilizer) -- the reference's positional signature
+    (optim.py:108-112), lr given to step -- equals the keyword form."""
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=64, layers=2, heads=4, ffn=128, vocab=128)
+    a = Llama(cfg, dtype=torch.float32, device="cuda", seed=0)
+    b = Llama(cfg, dtype=torch.float32, device="cuda", seed=0)
+    oa = LOMO(a, Stabilizer(ClipMode.by_global_norm(1.0)), ledger=None)
+    ob = LOMO(b, lr=0.05, clip_grad_norm=1.0)
+    d = torch.randint(0, 128, (2, 33), device="cuda")
+    assert oa.step((d[:, :-1], d[:, 1:]), 0.05) == ob.step((d[:, :-1], d[:, 1:]), 0.05)
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)
+    with pytest.raises(Exception):
+        LOMO(a, Stabilizer(), stabilizer=Stabilizer())
