@@ -718,3 +718,59 @@ def test_apply_update_python_entry_matches_reference_kats(prec):
     assert np.array_equal(p.double().cpu().numpy(), O.apply_update(p0, g0, 0.05, prec))
     with pytest.raises(ShapeError):
         apply_update(p, g[:-1], 0.05)
+
+
+def test_empty_and_tiny_inputs_everywhere():
+    """Empty tensors through every entry point the hooks use: K2 of an empty
+    gradient adds nothing to its slot, multi-tensor lists with empty and
+    1-element members update exactly the non-empty ones, K4 of an empty
+    slice is a no-op, and a model with an empty parameter trains."""
+    import ctypes
+    from paper_2306_09782_b200 import LOMO
+    e = torch.empty(0, dtype=torch.bfloat16, device="cuda")
+    st = U.State(3, max_norm=1.0)
+    st.begin()
+    st.probe(e, 0, 0)
+    st.probe(torch.ones(8, dtype=torch.bfloat16, device="cuda"), 1, 0)
+    st.finalize()
+    assert st.status().sumsq_total == 8.0 and st.status().skip == 0
+    rng = np.random.default_rng(21)
+    sizes = [0, 1, 0, 7, 4096]
+    ps = [_draw(max(n, 1), "bf16", rng) for n in sizes]
+    P = [U.to_dev(p[:n], torch.bfloat16) for (p, _), n in zip(ps, sizes)]
+    G = [U.to_dev(g[:n], torch.bfloat16) for (_, g), n in zip(ps, sizes)]
+    k = len(sizes)
+    pt = (ctypes.c_void_p * k)(*[t.data_ptr() for t in P])
+    gt = (ctypes.c_void_p * k)(*[t.data_ptr() for t in G])
+    nt = (ctypes.c_int64 * k)(*sizes)
+    _lib.check(U.lib().lomo_fused_update_multi(pt, gt, nt, k, _lib.BF16, _lib.MATH_F64,
+                                               0.05, 0.0, 0.0, 0, None, U.stream()), "multi")
+    for t, (p0, g0), n in zip(P, ps, sizes):
+        assert np.array_equal(t.double().cpu().numpy(), _expected(p0[:n], g0[:n], "bf16"))
+    ss = (ctypes.c_int * k)(*range(k))
+    st2 = U.State(k)
+    st2.begin()
+    _lib.check(U.lib().lomo_probe_multi(gt, nt, ss, k, _lib.BF16, _lib.ACCUM_F64, st2.ptr,
+                                        U.stream()), "probe multi")
+    got = st2.slots(k)
+    for j, (g, n) in enumerate(zip(G, sizes)):
+        assert got[j] == float((g.double() ** 2).sum())
+    peers = torch.tensor([P[-1].data_ptr()], dtype=torch.int64, device="cuda")
+    assert U.lib().lomo_fused_rs_update(P[-1].data_ptr(), peers.data_ptr(), 1, 0, 0, _lib.BF16,
+                                        _lib.MATH_F32, 0.05, 0.0, 0.0, 0, None,
+                                        U.stream()) == 0
+
+    class M(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.w = torch.nn.Parameter(torch.ones(4, device="cuda"))
+            self.empty = torch.nn.Parameter(torch.zeros(0, device="cuda"))
+
+        def loss(self, x):
+            return (self.w * x).sum() + self.empty.sum()
+
+    m = M()
+    opt = LOMO(m, lr=0.5, clip_grad_norm=10.0)
+    x = torch.full((4,), 2.0, device="cuda")
+    opt.step(lambda: m.loss(x), 0.5)
+    assert torch.equal(m.w, torch.zeros(4, device="cuda"))  # 1 - 0.5 * 2
