@@ -197,3 +197,18 @@ def test_clip_by_value_kat_and_validation():
     for t in (0.0, -1.0):
         with pytest.raises(ConfigError):
             clip_by_value(torch.zeros(2), t)
+
+
+def test_step_batch_form_needs_a_model_loss():
+    """step(batch, lr) maps (inputs, targets) to model.loss (optim.py:57-60);
+    an optimizer whose model has no .loss raises TypeError, a closure passes
+    through unchanged."""
+    from types import SimpleNamespace
+
+    from paper_2306_09782_b200.lomo import _as_closure
+    f = lambda: 1.0  # noqa: E731
+    assert _as_closure(SimpleNamespace(), f) is f
+    with pytest.raises(TypeError):
+        _as_closure(SimpleNamespace(_model=object()), (1, 2))
+    m = SimpleNamespace(loss=lambda x, t: x + t)
+    assert _as_closure(SimpleNamespace(_model=m), (1, 2))() == 3
