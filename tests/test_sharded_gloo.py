@@ -30,13 +30,16 @@ def _free_port():
     return p
 
 
+CLIP_V = 0.01  # value-clip threshold of the "value" mode (small enough to bind)
+
+
 def _batches(step, world):
     g = torch.Generator().manual_seed(100 + step)
     d = torch.randint(0, CFG["vocab"], (2 * world, 9), generator=g)
     return d[:, :-1], d[:, 1:]
 
 
-def _reference(steps, world, max_norm, lr, inf_step=None, fused_proj=False):
+def _reference(steps, world, max_norm, lr, inf_step=None, fused_proj=False, clip_value=None):
     from paper_2306_09782_b200.workloads import Llama
     model = Llama(CFG, dtype=torch.float64, device="cpu", seed=0, fused_proj=fused_proj)
     outcomes = []
@@ -55,7 +58,8 @@ def _reference(steps, world, max_norm, lr, inf_step=None, fused_proj=False):
             n = math.sqrt(sq)
             coef = min(1.0, max_norm / n) if (max_norm and n > 0) else 1.0
             for p in ps:
-                p.copy_(p - lr * (p.grad * coef))
+                g = p.grad.clamp(-clip_value, clip_value) if clip_value else p.grad * coef
+                p.copy_(p - lr * g)
                 p.grad = None
         outcomes.append("apply")
     return {n: p.detach().clone() for n, p in model.named_parameters()}, outcomes
@@ -88,9 +92,11 @@ def _run(rank, world, port, mode, q):
         torch.manual_seed(1234 + rank)  # ranks start different: broadcast must fix it
         model = Llama(CFG, dtype=torch.float64, device="cpu", seed=rank, fused_proj=fused_proj)
         lr = 0.05
-        max_norm = 0.5 if mode != "plain" else None
+        max_norm = 0.5 if mode not in ("plain", "value") else None
         stab = None
-        if mode == "norm":
+        if mode == "value":  # single pass, the clip applied to the reduced (mean) gradient
+            stab = Stabilizer(ClipMode.by_value(CLIP_V))
+        elif mode == "norm":
             stab = Stabilizer(ClipMode.by_global_norm(max_norm))
         elif mode in ("norm_scaler", "skip"):
             stab = Stabilizer(ClipMode.by_global_norm(max_norm), LossScaler(2.0 ** 8, 2))
@@ -122,7 +128,7 @@ def _run(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["plain", "norm", "norm_scaler", "skip", "norm_scaler_copy",
+@pytest.mark.parametrize("mode", ["plain", "value", "norm", "norm_scaler", "skip", "norm_scaler_copy",
                                   "norm_replay", "norm_scaler_replay", "skip_replay",
                                   "norm_scaler_keep", "skip_keep", "norm_scaler_fp",
                                   "norm_scaler_fp_keep"])
@@ -149,9 +155,10 @@ def test_sharded_lomo_matches_full_batch_reference(mode):
     mode = mode.removesuffix("_copy").removesuffix("_replay").removesuffix("_keep")
     fused_proj = mode.endswith("_fp")
     mode = mode.removesuffix("_fp")
-    max_norm = 0.5 if mode != "plain" else None
+    max_norm = 0.5 if mode not in ("plain", "value") else None
     want, want_out = _reference(3, world, max_norm, 0.05, inf_step=1 if mode == "skip" else None,
-                                fused_proj=fused_proj)
+                                fused_proj=fused_proj,
+                                clip_value=CLIP_V if mode == "value" else None)
     for rank, released, outcomes, got in res:
         assert all(released), "layer buckets must be released after construction (ZeRO-3)"
         assert outcomes == want_out, (rank, outcomes, want_out)
