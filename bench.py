@@ -446,8 +446,37 @@ def bench_update(args, rank, world):
                          "where the gradient's producer runs just before each K1"}
     del P, G
     torch.cuda.empty_cache()
+    # SURVEY 8(d) C2's fp16 + scaler variant: fp16 p and g (g scaled by 2^10),
+    # pass 2's flags -- unscale, clip coefficient, skip, lr from the state
+    fp16 = None
+    if args.dtype == "bf16":
+        P16, G16 = make_update_workload(rank, world, "fp16")
+        for g in G16:
+            g.mul_(1024.0)
+        st16 = torch.zeros(_lib.state_bytes(len(P16)), dtype=torch.uint8, device="cuda")
+        _lib.check(lib.lomo_state_init(st16.data_ptr(), len(P16), 1024.0, 16, 1.0, 2.0 ** 24,
+                                       1.0, 1.0, stream), "init")
+        _lib.check(lib.lomo_set_lr(st16.data_ptr(), 0.05, stream), "lomo_set_lr")
+        d16 = HookDispatcher(lib, st16.data_ptr(), _lib.MATH_F32)
+        d16.configure(flags=_lib.USE_SKIP | _lib.USE_SCALE | _lib.USE_COEF | _lib.LR_FROM_STATE,
+                      chain=True)
+        for _ in range(2):
+            run_update_pass(d16, P16, G16, _lib.F16, stream)
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(args.steps):
+            run_update_pass(d16, P16, G16, _lib.F16, stream)
+        end.record()
+        torch.cuda.synchronize()
+        f16_ms = start.elapsed_time(end) / args.steps
+        fp16 = {"gbs": round(BYTES_PER_ELEM * elems / (f16_ms * 1e-3) / 1e9, 1),
+                "ms_per_pass": round(f16_ms, 4),
+                "what": "fp16 parameters and gradients (scaled by 2^10), K1 with "
+                        "USE_SKIP|USE_SCALE|USE_COEF|LR_FROM_STATE, chained"}
+        del P16, G16, st16
+        torch.cuda.empty_cache()
     return {"gbs": gbs, "ms": ms / args.steps, "probe": probe, "f64_math": f64,
-            "flags_pass": flags_pass, "unchained": unchained,
+            "flags_pass": flags_pass, "unchained": unchained, "fp16_scaled": fp16,
             "graphed_gbs": BYTES_PER_ELEM * elems / (upd_graph_ms * 1e-3) / 1e9,
             "host_ms": host_ms, "host_enqueue": host_enqueue,
             "elems_per_rank": elems, "total_elems": total_elems,
@@ -1699,6 +1728,9 @@ def main():
                                              frac=round(up["flags_pass"]["gbs"] / peak, 4)),
             "update_pass_unchained": dict(up["unchained"],
                                           frac=round(up["unchained"]["gbs"] / peak, 4)),
+            "update_pass_fp16_scaled": (dict(up["fp16_scaled"],
+                                             frac=round(up["fp16_scaled"]["gbs"] / peak, 4))
+                                        if up["fp16_scaled"] else None),
             "f64_math_update_pass": dict(up["f64_math"],
                                          frac=round(up["f64_math"]["gbs"] / peak, 4)),
             "gpu_launches": up["launches"], "clocks": up["clocks"]}
