@@ -9,18 +9,23 @@
 // K3a lomo_finalize_norm       N, clip coef, skip, LossScaler.on_overflow
 //     reference: stabilize.py:201-213, 94-127, 155-159.
 // K3b lomo_scaler_on_clean     LossScaler.on_clean (stabilize.py:123-127, :228-229)
+// K4  lomo_fused_rs_update / _probe(_keep), lomo_fused_mc_*: the sharded
+//     mode's reduce-scatter fused with K1 / K2 over peer memory (CUDA-IPC P2P
+//     loads, or NVLS multimem.ld_reduce).
 //
 // Design notes:
 //  * Each launch processes ONE tensor as it arrives from autograd (the LOMO
 //    contract: a gradient is consumed the moment it exists, tape.py:387-405).
 //  * 128-bit LDG/STG: g is read through the non-coherent path with
 //    L1::no_allocate (read exactly once), p is read and written with
-//    streaming hints; every CTA owns one contiguous, equally sized chunk of
-//    the tensor so all CTAs finish together (no grid-stride tail).
-//  * Grid = min(work, #SM x resident CTAs/SM) (queried once per device).
+//    streaming hints.  K1: one 256-vector tile per CTA, grid = ceil(n/tile),
+//    the block scheduler balances the tiles; K2: 16 KB tiles, 6 CTAs/SM.
+//  * PDL between launches; LOMO_CHAINED launches (a K1 / K2 right after one
+//    on other tensors) run before griddepcontrol.wait and wait at their end.
 //  * Determinism: K2 reduces per thread (fixed element order), per warp
-//    (xor shuffles), per CTA (fixed warp order) and across CTAs by a
-//    last-CTA finish over scratch[] in index order -- no float atomics.
+//    (xor shuffles), per CTA (fixed warp order) into its own partial slot;
+//    K3a sums each slot's partials in CTA order, then the slots in delivery
+//    order -- no float atomics.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
