@@ -2,7 +2,7 @@
 K3a) exactly as pass 1's hooks issue them -- the command the K2 ncu captures
 under profiles/ were taken from.
 
-    python tools/probe_pass.py [--passes 3] [--dtype bf16]
+    python tools/probe_pass.py [--passes 3] [--dtype bf16] [--unchained]
 """
 import argparse
 import sys
@@ -20,6 +20,7 @@ from paper_2306_09782_b200.dispatch import HookDispatcher  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--passes", type=int, default=3)
 ap.add_argument("--dtype", default="bf16")
+ap.add_argument("--unchained", action="store_true")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 lib = _lib.load()
@@ -30,7 +31,7 @@ st = torch.zeros(_lib.state_bytes(len(G)), dtype=torch.uint8, device="cuda")
 _lib.check(lib.lomo_state_init(st.data_ptr(), len(G), 1024.0, 16, 1.0, 2.0 ** 24, 1.0, 1.0, s),
            "init")
 disp = HookDispatcher(lib, st.data_ptr(), _lib.MATH_F32)
-disp.configure(flags=_lib.USE_SCALE)
+disp.configure(flags=_lib.USE_SCALE, chain=not a.unchained)  # as the bench's probe pass
 for _ in range(a.passes):
     lib.lomo_begin_step(st.data_ptr(), None, 0, s)
     for i in range(len(G) - 1, -1, -1):
