@@ -146,7 +146,10 @@ __device__ __forceinline__ double to_m<double, __half>(__half v) {
 }
 template <>
 __device__ __forceinline__ double to_m<double, __nv_bfloat16>(__nv_bfloat16 v) {
-  return (double)__bfloat162float(v);  // exact
+  // exact.  (Integer widening for normals/zeros with a conversion fallback
+  // measured 0.54 of peak over the f64-math pass against 0.85 for this --
+  // the per-element branches cost more than the F2F pipe.)
+  return (double)__bfloat162float(v);
 }
 
 // Round-to-nearest-even store, overflow to +-inf (tensor.py:30-38 for f16;

@@ -798,3 +798,25 @@ def test_chained_k1_stress_many_short_launches():
             d.flush(U.stream())
     torch.cuda.synchronize()
     assert all(torch.equal(a, b) for a, b in zip(P, Q))
+
+
+@pytest.mark.parametrize("prec", ["half", "bf16"])
+def test_f64_math_widening_special_values(prec):
+    """f64 math widens 16-bit storage by integer ops for normals and zeros
+    and by conversion for the rest: every class -- +-0, subnormals, the
+    smallest/largest normals, inf, NaN -- in p and g gives the oracle's bits."""
+    dt = U.TORCH_DT[prec]
+    info = torch.finfo(dt)
+    sub = info.tiny / 4
+    vals = [0.0, -0.0, sub, -sub, info.tiny, -info.tiny, info.max, -info.max, 1.0, -1.5,
+            float("inf"), float("-inf"), 3.0e-3, -7.25e-2]
+    rng = np.random.default_rng(5)
+    p0 = O.round_to(np.array([vals[i % len(vals)] for i in range(4099)]), prec)
+    g0 = O.round_to(np.array([vals[(7 * i + 3) % len(vals)] for i in range(4099)]), prec)
+    p0[::97] = np.nan
+    p, g = U.to_dev(p0, dt), U.to_dev(g0, dt)
+    U.fused_update(p, g, math="f64", lr=0.5)
+    got = p.double().cpu().numpy()
+    want = _expected(p0, g0, prec, lr=0.5)
+    same = (got == want) | (np.isnan(got) & np.isnan(want))
+    assert same.all(), np.flatnonzero(~same)[:10]
