@@ -170,6 +170,12 @@ int lomo_fused_update_multi(void* const* p_list, const void* const* g_list,
 
 /* Set state->lr (a one-thread kernel; launch it outside a captured graph). */
 int lomo_set_lr(void* state, double lr, void* stream);
+/* Restore the LossScaler's live state from a checkpoint (stabilize.py:94-127:
+ * scale -- a power of two -- and clean_steps) and the applied / skipped step
+ * counters; 1/scale, the fp32 scale and the pass-2 record follow.  The scale
+ * is ignored for a state block initialised without a scaler. */
+int lomo_set_scaler_state(void* state, double scale, int clean_steps, int steps_applied,
+                          int steps_skipped, void* stream);
 
 /* ---- K2: probe (two-pass pass 1) --------------------------------------- */
 /* sumsq[slot] = sum((g * inv_scale)^2) (deterministic: fixed-order f64 tree);

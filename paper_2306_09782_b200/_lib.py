@@ -53,6 +53,7 @@ EXPORTS = (
     "lomo_fused_rs_update",
     "lomo_fused_rs_probe",
     "lomo_set_lr",
+    "lomo_set_scaler_state",
     "lomo_update_coefs",
     "lomo_gemm_update_dev",
     "lomo_gemm_probe",
@@ -166,6 +167,7 @@ _SIGS = {
                                     _u32, _vp, _vp]),
     "lomo_fused_rs_probe": (_i32, [_vp, _i32, _i64, _i64, _i32, _i32, _u32, _vp, _vp]),
     "lomo_set_lr": (_i32, [_vp, _dbl, _vp]),
+    "lomo_set_scaler_state": (_i32, [_vp, _dbl, _i32, _i32, _i32, _vp]),
     "lomo_update_coefs": (_i32, [_vp, _dbl, _u32, _vp, _vp]),
     "lomo_gemm_update_dev": (_i32, [_vp, _vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp,
                                     ctypes.c_size_t, _vp]),

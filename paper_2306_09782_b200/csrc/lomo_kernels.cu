@@ -1271,6 +1271,25 @@ __global__ void k_set_lr(void* state, double lr) {
   }
 }
 
+// LossScaler state restored from a checkpoint (stabilize.py:94-127's live
+// fields): scale, its reciprocal and fp32 copy, the clean-step counter and
+// the applied/skipped step counts; the pass-2 record is republished.
+__global__ void k_set_scaler(void* state, double scale, int clean_steps, int applied,
+                             int skipped) {
+  pdl_wait();
+  if (threadIdx.x != 0) return;
+  lomo_state* st = hdr(state);
+  if (st->has_scaler) {
+    st->scale = scale;
+    st->inv_scale = 1.0 / (scale * st->grad_div);
+    st->scale_f32 = (float)scale;
+    st->clean_steps = clean_steps;
+  }
+  st->steps_applied = applied;
+  st->steps_skipped = skipped;
+  publish_rec(st);
+}
+
 __global__ void k_update_coefs(const void* state, double wd, unsigned flags, float* out) {
   pdl_wait();
   if (threadIdx.x != 0) return;
@@ -1758,6 +1777,16 @@ int lomo_probe(const void* g, int64_t n, int dtype, int slot, unsigned flags, vo
 int lomo_set_lr(void* state, double lr, void* stream) {
   if (state == nullptr) return LOMO_E_ARG;
   k_set_lr<<<1, 32, 0, (cudaStream_t)stream>>>(state, lr);
+  return (int)cudaGetLastError();
+}
+
+int lomo_set_scaler_state(void* state, double scale, int clean_steps, int steps_applied,
+                          int steps_skipped, void* stream) {
+  if (state == nullptr || !(scale > 0.0) || clean_steps < 0 || steps_applied < 0 ||
+      steps_skipped < 0)
+    return LOMO_E_ARG;
+  k_set_scaler<<<1, 32, 0, (cudaStream_t)stream>>>(state, scale, clean_steps, steps_applied,
+                                                   steps_skipped);
   return (int)cudaGetLastError();
 }
 

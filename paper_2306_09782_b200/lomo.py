@@ -40,7 +40,8 @@ from .engine import CudaEngine, dtype_code
 from .errors import (ConfigError, NonFiniteLossError, ScaleUnderflowError, ShapeError,
                      TapeStateError)
 from .replay import ReplayStash
-from .stabilize import ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome
+from .stabilize import (ClipKind, ClipMode, LossScaler, Stabilizer, StepOutcome,
+                        is_power_of_two)
 
 _PROBE = 1
 _UPDATE = 2
@@ -223,6 +224,33 @@ class _Protocol:
 
     def _after_update(self) -> None:
         pass
+
+    def state_dict(self) -> dict:
+        """The optimizer's whole state (LOMO keeps no per-parameter state,
+        optim.py:115-116): the loss scaler's live fields and the step
+        counters, read from the device (one sync)."""
+        st = self.engine.read_status()
+        self._mirror_scaler(st)
+        return {"scale": float(st.scale) if self.has_scaler else None,
+                "clean_steps": int(st.clean_steps), "steps_applied": int(st.steps_applied),
+                "steps_skipped": int(st.steps_skipped)}
+
+    def load_state_dict(self, sd: dict) -> None:
+        """Restore :meth:`state_dict` (resume from a checkpoint): the device
+        state machine and the user's LossScaler object continue from it."""
+        scale = sd.get("scale")
+        if self.has_scaler:
+            if scale is None:
+                raise ConfigError("state_dict has no loss scale for a scaled optimizer")
+            if not is_power_of_two(float(scale)):
+                raise ConfigError(f"scale must be a positive power of two, got {scale}")
+        _lib.check(self.engine.lib.lomo_set_scaler_state(
+            self.engine.ptr, float(scale) if scale else 1.0, int(sd.get("clean_steps", 0)),
+            int(sd.get("steps_applied", 0)), int(sd.get("steps_skipped", 0)),
+            self.engine.stream()), "lomo_set_scaler_state")
+        if self.has_scaler:
+            self.scaler.scale = float(scale)
+            self.scaler.clean_steps = int(sd.get("clean_steps", 0))
 
     def _mirror_scaler(self, st) -> None:
         """The user's LossScaler object reads as the reference's: the device

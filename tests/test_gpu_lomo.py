@@ -572,3 +572,47 @@ def test_reference_constructor_form():
         assert torch.equal(x, y)
     with pytest.raises(Exception):
         LOMO(a, Stabilizer(), stabilizer=Stabilizer())
+
+
+def test_state_dict_resume_equals_uninterrupted_run():
+    """LOMO.state_dict / load_state_dict (the optimizer's only state: the
+    loss scaler's scale and clean-step count, and the step counters): a run
+    checkpointed after 5 steps and resumed in a fresh optimizer on a copy
+    of the weights equals the uninterrupted run bit for bit -- scales,
+    outcomes (growth and overflow skips) and parameters."""
+    from paper_2306_09782_b200.workloads import Llama
+    cfg = dict(hidden=64, layers=2, heads=4, ffn=128, vocab=128)
+    g = torch.Generator(device="cuda").manual_seed(8)
+    batches = [torch.randint(0, 128, (2, 33), device="cuda", generator=g) for _ in range(10)]
+    mk = lambda m: LOMO(m, lr=0.01, clip_grad_norm=1.0,  # noqa: E731
+                        loss_scale=LossScaler(2.0 ** 21, growth_interval=2, max_scale=2.0 ** 24))
+    a = Llama(cfg, dtype=torch.float16, device="cuda", seed=0)
+    oa = mk(a)
+    trace_a = []
+    for d in batches:
+        oa.step((d[:, :-1], d[:, 1:]), 0.01)
+        trace_a.append((oa.last_outcome, oa.scaler.scale))
+    b = Llama(cfg, dtype=torch.float16, device="cuda", seed=0)
+    ob = mk(b)
+    trace_b = []
+    for d in batches[:5]:
+        ob.step((d[:, :-1], d[:, 1:]), 0.01)
+        trace_b.append((ob.last_outcome, ob.scaler.scale))
+    sd = ob.state_dict()
+    ob.remove_hooks()
+    c = Llama(cfg, dtype=torch.float16, device="cuda", seed=0)
+    with torch.no_grad():
+        for x, y in zip(c.parameters(), b.parameters()):
+            x.copy_(y)
+    oc = mk(c)
+    oc.load_state_dict(sd)
+    assert (oc.scaler.scale, oc.scaler.clean_steps) == (sd["scale"], sd["clean_steps"])
+    for d in batches[5:]:
+        oc.step((d[:, :-1], d[:, 1:]), 0.01)
+        trace_b.append((oc.last_outcome, oc.scaler.scale))
+    assert trace_a == trace_b
+    assert {o for o, _ in trace_a} == {StepOutcome.APPLIED, StepOutcome.SKIPPED_OVERFLOW}
+    for x, y in zip(a.parameters(), c.parameters()):
+        assert torch.equal(x, y)
+    st = oc.read_status()
+    assert st.steps_applied + st.steps_skipped == 10
